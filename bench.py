@@ -1,0 +1,431 @@
+#!/usr/bin/env python
+"""bench.py — core-Hamiltonian assembly + spectrum on B200 (arXiv 1408.3839 hot path).
+
+One step = one full pass of the hot path for one seeded BASELINE system: L0 scan,
+lattice-summed Newton potential, GTO profiles, kinetic/overlap/nuclear Galerkin
+blocks, H = 0.5 Lap - Nuc, S = Mass, then (periodic) the lattice DFT + batched
+pencils or (box) the dense pencil; eigenvalues land in HBM.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--impl b200|reference]
+
+N > 1 is launched by torchrun; ranks split the k-points of the periodic spectrum
+(paper_1408_3839_b200/dist.py) and all-gather the eigenvalues: strong scaling of one
+system. Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1408_3839_b200.system import make_config  # noqa: E402
+
+METRIC = "core-Hamiltonian assembly+spectrum time (ms) vs L; Galerkin entries/s; % roofline"
+WORKLOAD_DESC = {
+    "c1": "open-box (8,1,1) chain, m0=4, n=(32,256,256)/cell, R_N=25, dense 32x32 pencil",
+    "c2": "periodic (32,1,1) supercell, m0=8, n=(32,256,256)/cell, R_N=29, 32 k-point 8x8 pencils",
+    "c3": "open-box (128,1,1) chain, m0=8, n=(64,256,256)/cell, R_N=33, dense 1024x1024 pencil",
+    "c4": "periodic (512,1,1) supercell, 4 nuclei, m0=16, n=(64,384,384)/cell, R_N=33, 512 k-point 16x16 pencils",
+    "c5": "periodic (16,16,16) supercell, m0=8, n=64/cell, R_N=33, 3-level lattice DFT, 4096 k-point 8x8 pencils",
+}
+
+
+def load_peaks():
+    peaks = {"hbm_gbs": 6650.0, "hbm_src": "fallback (B200_PROFILING.md)"}
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        peaks["hbm_gbs"] = float(d["hbm_gbs"])
+        peaks["hbm_src"] = "measured (MEASURED_PEAKS.json)"
+    fp = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    if os.path.exists(fp):
+        d = json.load(open(fp))
+        peaks["fp64_tflops"] = float(d["dmma_tflops"])
+        peaks["fp64_src"] = "measured DMMA (profiles/fp64_peak.json)"
+    else:
+        peaks["fp64_tflops"] = 37.0
+        peaks["fp64_src"] = "nominal B200 FP64 tensor (no measurement)"
+    return peaks
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# algorithmic work per kernel launch
+# ---------------------------------------------------------------------------
+def work_model(ctx, sysobj, periodic, L0):
+    """{stage: (bound, per-launch algorithmic amount, unit)}; amounts in bytes or flops."""
+    m0 = sysobj.m0
+    mm = m0 * m0
+    RN = sysobj.rank_N
+    Rtot = sysobj.rank_total
+    margin = L0 + 2
+    L = sysobj.L
+    n = sysobj.n
+    band = [min(L0, L[l] - 1) for l in range(3)]
+    width = [2 * b + 1 for b in band]
+    G = [(L[l] + 2 * margin) * n[l] for l in range(3)]
+    prof = ctx.profiles(sysobj, margin)
+    sup = {(l, mu): (prof[("pwc", l, mu)][0], prof[("pwc", l, mu)][0] + len(prof[("pwc", l, mu)][1]))
+           for l in range(3) for mu in range(m0)}
+    out = {}
+    # L0 profile sampling: writes m0 * sum(width_l) doubles (+ block maxima)
+    w_l0 = sum(2 * 258 * n[l] for l in range(3))
+    out["l0_sample"] = ("hbm", 8.0 * m0 * w_l0 * (1 + 1.0 / 128), "B")
+    # nuclear tables of trivial directions (one launch per direction): 2 flops per
+    # (a*b) product + 2 Rtot per point of the support overlap
+    triv = [l for l in range(3) if L[l] == 1]
+    if triv:
+        fl = 0.0
+        for l in triv:
+            for mu in range(m0):
+                for nu in range(m0):
+                    lo = max(sup[(l, mu)][0], sup[(l, nu)][0], 0)
+                    hi = min(sup[(l, mu)][1], sup[(l, nu)][1], G[l])
+                    fl += max(0, hi - lo) * (1 + 2 * Rtot)
+        out["nuc_direct"] = ("tensor", fl / len(triv), "flop")
+    # box S2 Hankel contraction: 2 flops per (k, d, e, j) with the dot3 range
+    s2 = [l for l in range(3) if L[l] > 1]
+    if not periodic and len(s2) == 1:
+        l = s2[0]
+        fl = 0.0
+        for mu in range(m0):
+            a0, a1 = sup[(l, mu)]
+            for nu in range(m0):
+                b0, b1 = sup[(l, nu)]
+                for k in range(L[l]):
+                    for d in range(-band[l], band[l] + 1):
+                        if not (0 <= k + d < L[l]):
+                            continue
+                        lo = max(a0 + k * n[l], b0 + (k + d) * n[l], 0)
+                        hi = min(a1 + k * n[l], b1 + (k + d) * n[l], G[l])
+                        fl += 2.0 * max(0, hi - lo)
+        out["box_corr"] = ("tensor", fl, "flop")
+    # periodic pencils: nominal complex Cholesky + 2 triangular solves + ~6 Jacobi sweeps
+    if periodic:
+        K = L[0] * L[1] * L[2]
+        out["pencil"] = ("tensor", K * 4.0 * (m0 ** 3 / 3 + 2 * m0 ** 3 + 12 * m0 ** 3), "flop")
+    # HBM-bound helpers
+    out["profiles"] = ("hbm", 8.0 * m0 * 2 * (sum(G) + sum((L[l] + 2 * margin) * sysobj.nbar[l] for l in range(3))),
+                       "B")
+    return out
+
+
+def run_reference_arm(args, world, rank):
+    """--impl reference: the reference algorithm on this host's CPU cores."""
+    if rank != 0:
+        return 0
+    from oracle.binding import oracle, reference
+    ref = reference()
+    impl = ref if ref is not None else oracle()
+    kind = "reference" if ref is not None else "port"
+    sysobj = make_config(args.workload)
+    periodic = sysobj.notes["periodic"]
+    threads = os.cpu_count() or 1
+
+    def step():
+        H, S = impl.assemble_core(sysobj, periodic)
+        if periodic:
+            ev = impl.solve_periodic_ops(H, S, threads)
+        else:
+            ev = impl.solve_box_dense(H.dense, S.dense)
+        impl.free(H)
+        impl.free(S)
+        return ev
+
+    for _ in range(args.warmup):
+        step()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        step()
+        times.append((time.perf_counter() - t0) * 1e3)
+    ms = float(np.mean(times))
+    line = {
+        "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE config, SURVEY.md 8(d))", "impl": "reference",
+        "config": {"workload": args.workload, "desc": WORKLOAD_DESC[args.workload]},
+        "cpu_baseline": {"value": ms, "unit": "ms", "cores": threads, "kind": kind,
+                         "sample": f"full {args.workload} solve per step (assembly single-threaded as in the "
+                                   f"reference; k-point pencils on {threads} threads)"},
+        "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline(workload, budget_s):
+    from oracle.binding import oracle, reference
+    ref = reference()
+    impl = ref if ref is not None else oracle()
+    kind = "reference" if ref is not None else "port"
+    sysobj = make_config(workload)
+    periodic = sysobj.notes["periodic"]
+    threads = os.cpu_count() or 1
+    times = []
+    t_start = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        H, S = impl.assemble_core(sysobj, periodic)
+        if periodic:
+            impl.solve_periodic_ops(H, S, threads)
+        else:
+            impl.solve_box_dense(H.dense, S.dense)
+        impl.free(H)
+        impl.free(S)
+        times.append((time.perf_counter() - t0) * 1e3)
+        if time.perf_counter() - t_start > budget_s or len(times) >= 50:
+            break
+    return {"value": float(statistics.median(times)), "unit": "ms", "cores": threads, "kind": kind,
+            "sample": f"{len(times)} full {workload} solves (median); assembly single-threaded like the reference, "
+                      f"pencils on {threads} threads; {os.cpu_count()} host cores"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOAD_DESC))
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--stages", action="store_true", help="print per-kernel stage times to stderr")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference_arm(args, world, rank)
+
+    import torch
+    import torch.distributed as dist
+    from paper_1408_3839_b200.api import Context
+    from paper_1408_3839_b200.dist import solve_core_distributed
+
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    ctx = Context(local)
+    sysobj = make_config(args.workload)
+    periodic = sysobj.notes["periodic"]
+    K = sysobj.lattice_count
+    count = sysobj.basis_count
+    dsys = ctx.upload(sysobj)
+    eig = torch.empty(count, dtype=torch.float64, device=dev)
+    ext = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
+    info = np.zeros(8, dtype=np.int64)
+
+    def step():
+        return solve_core_distributed(ctx, sysobj, periodic, dsys=dsys, eig_dev=eig, info=info)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    def timed_region(stage_timing: bool):
+        ctx.set_stage_timing(stage_timing)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        l0 = ctx.launches
+        ms = []
+        for i in range(args.steps):
+            flush.fill_(float(i))  # L2 flush between timed iterations (outside the events)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(ext)
+            step()
+            e1.record(torch.cuda.current_stream(dev))
+            e1.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        launches = ctx.launches - l0
+        stages = ctx.stage_times() if stage_timing else {}
+        ctx.set_stage_timing(False)
+        return ms, launches, stages
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    ms, launches, _ = timed_region(False)
+    clk = clocks.stop()
+    total = torch.tensor([sum(ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(total, op=dist.ReduceOp.MAX)
+    ms_per_step = float(total.item()) / args.steps
+
+    # per-kernel CUDA-event pass (same K steps) for the roofline numbers
+    ms2, _, stages = timed_region(True)
+
+    # end to end through the public API: host LatticeSystem -> host eigenvalues
+    e2e_ms = []
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        if world == 1:
+            ev_host = ctx.solve_core(sysobj, periodic)
+        else:
+            ev_host = solve_core_distributed(ctx, sysobj, periodic).cpu().numpy()
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_t = torch.tensor([float(np.mean(e2e_ms))], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+
+    if rank == 0:
+        peaks = load_peaks()
+        L0 = int(info[0])
+        wm = work_model(ctx, sysobj, periodic, L0)
+        # dominant kernel by measured time
+        dom = max(stages.items(), key=lambda kv: kv[1][0]) if stages else None
+        step_ms_stage = float(np.mean(ms2)) if ms2 else None
+        roof = None
+        if dom is not None:
+            name, (tot_ms, nl) = dom
+            avg_ms = tot_ms / max(1, nl)
+            bound, amount, unit = wm.get(name, ("hbm", None, "B"))
+            if amount is not None:
+                if bound == "hbm":
+                    achieved = amount / (avg_ms * 1e-3) / 1e9
+                    peak = peaks["hbm_gbs"]
+                    runit = "GB/s"
+                    src = peaks["hbm_src"]
+                else:
+                    achieved = amount / (avg_ms * 1e-3) / 1e12
+                    peak = peaks["fp64_tflops"]
+                    runit = "TFLOP/s"
+                    src = peaks["fp64_src"]
+                roof = {"kernel": name, "bound": bound, "achieved": achieved, "peak": peak, "unit": runit,
+                        "frac": achieved / peak, "traffic": None, "avg_launch_ms": avg_ms,
+                        "share_of_step": tot_ms / args.steps / step_ms_stage if step_ms_stage else None,
+                        "algorithmic_per_launch": amount, "peak_source": src}
+            else:
+                roof = {"kernel": name, "bound": bound, "achieved": None, "peak": None, "unit": None, "frac": None,
+                        "traffic": None, "avg_launch_ms": avg_ms}
+        bands = [min(L0, sysobj.L[l] - 1) for l in range(3)]
+        if periodic:
+            nblocks = int(np.prod([2 * b + 1 for b in bands]))
+        else:
+            nblocks = int(np.prod([sum(1 for k in range(sysobj.L[l]) for d in range(-bands[l], bands[l] + 1)
+                                       if 0 <= k + d < sysobj.L[l]) for l in range(3)]))
+        entries = sysobj.m0 ** 2 * nblocks  # Galerkin H entries (S alongside)
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            try:
+                cpu = cpu_baseline(args.workload, args.cpu_seconds)
+            except Exception as e:  # oracle not built on this host
+                cpu = {"value": None, "unit": "ms", "cores": 0, "kind": "port", "sample": f"unavailable: {e}"}
+        line = {
+            "metric": METRIC,
+            "value": ms_per_step,
+            "unit": "ms",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_per_step,
+            "higher_is_better": False,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic: seeded BASELINE config (splitmix64, SURVEY.md 8(d)); system resident on device",
+            "config": {"workload": args.workload, "desc": WORKLOAD_DESC[args.workload], "L": list(sysobj.L),
+                       "n_per_cell": list(sysobj.n), "m0": sysobj.m0, "R_N": sysobj.rank_N, "L0": L0,
+                       "band": [int(x) for x in info[1:4]], "R_tot": int(info[4]), "N_b": int(info[5]),
+                       "k_points": int(info[6]), "parallelism": f"k-point shards x{world}" if periodic else
+                       f"replicas x{world}", "l2": "flushed between timed iterations (256 MB write)",
+                       "exponent_draw": sysobj.notes["exponent_draw"]},
+            "galerkin_entries_per_s": float(entries) / (ms_per_step * 1e-3) if ms_per_step else None,
+            "roofline": roof,
+            "stages_ms_per_step": {k: v[0] / args.steps for k, v in sorted(stages.items(), key=lambda kv: -kv[1][0])},
+            "cpu_baseline": cpu,
+            "e2e": {"value": float(e2e_t.item()), "unit": "ms", "h2d_bytes_per_step": sysobj.host_bytes(),
+                    "d2h_bytes_per_step": 8 * count},
+            "gpu_launches": int(launches / args.steps) * args.steps,
+            "gpu_launches_per_step": launches / args.steps,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+        if args.stages:
+            for k, v in sorted(stages.items(), key=lambda kv: -kv[1][0]):
+                print(f"  {k:14s} {v[0] / args.steps * 1e3:9.1f} us/step  launches/step {v[1] / args.steps:.1f}",
+                      file=sys.stderr)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

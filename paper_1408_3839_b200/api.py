@@ -1,0 +1,365 @@
+"""Host-side mirror of the reference's C++ API for the hot path, backed by the B200 engine.
+
+Same names, argument meaning and error classes as ``proj/core/include/latham``:
+
+========================================  ==================================================
+this module                               reference
+========================================  ==================================================
+``assemble_box(sys, kind)``               ``galerkin.hpp:70``
+``assemble_periodic(sys, kind)``          ``galerkin.hpp:74``
+``combine(wa, a, wb, b)``                 ``eigensolver.hpp:23-24``
+``assemble_core(sys, periodic)``          ``tools/commands.cpp:51-59`` (fused on the device)
+``solve_periodic(H, S)``                  ``eigensolver.hpp:29-33``
+``solve_box_dense(H, S, cap)``            ``eigensolver.hpp:17-18`` (eigenvalues only)
+``bc_block_diagonalize(dims, m0, gen)``   ``block_circulant.hpp:86``
+``build_sinc_quadrature(M)``              ``sinc_quadrature.hpp:35``
+``overlap_constant(sys)``                 ``gto_basis.hpp:74``
+``newton_master(ncells, h, M)``           ``newton_kernel.hpp:35-36`` (one direction)
+``potential(sys, periodic, margin)``      ``galerkin.cpp:151-198`` (lattice_potential_*)
+``assembled_window_sum(m, shifts, n)``    ``canonical_tensor.hpp:97-99`` (one direction)
+``profiles(sys, margin)``                 ``gto_basis.hpp:47-49`` (assembly grids)
+``solve_core(sys, periodic)``             assemble_core + solve_* (the whole hot path)
+========================================  ==================================================
+
+Everything here calls through the C-ABI of ``include/latham_b200.h``; there is no
+CPU computation and no fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Dict, Optional, Tuple
+
+import numpy as np
+
+from . import native
+from .native import (BoundsError, DefinitenessError, DimensionError, Error, ResourceCapError,  # noqa: F401
+                     StructureError, check)
+from .system import LatticeSystem
+
+KINDS = {"laplace": 0, "mass": 1, "nuclear": 2}
+
+_dp = ctypes.POINTER(ctypes.c_double)
+_ip = ctypes.POINTER(ctypes.c_int64)
+
+
+def _d(a: np.ndarray):
+    return a.ctypes.data_as(_dp)
+
+
+def _i(a: np.ndarray):
+    return a.ctypes.data_as(_ip)
+
+
+@dataclass
+class Operator:
+    """AssembledOperator (galerkin.hpp:43-54); payload lives on the device."""
+
+    ctx: "Context"
+    handle: int
+    periodic: bool
+    m0: int
+    L: Tuple[int, int, int]
+    overlap_L0: int
+    coefficient_rank: int
+    stored: int
+    Nb: int
+    band: Tuple[int, int, int]
+
+    def dense(self) -> np.ndarray:
+        out = np.zeros(self.Nb * self.Nb)
+        check(native.lib().lt_op_dense(self.handle, _d(out)))
+        return out.reshape(self.Nb, self.Nb).T.copy()
+
+    def blocks(self):
+        """(kidx (n,3), blocks (n, m0, m0) [row, col]) in std::map order."""
+        k = np.zeros((self.stored, 3), dtype=np.int64)
+        b = np.zeros(self.stored * self.m0 * self.m0)
+        check(native.lib().lt_op_blocks(self.handle, _i(k), _d(b)))
+        return k, b.reshape(self.stored, self.m0, self.m0).transpose(0, 2, 1).copy()
+
+    def gen_dict(self) -> Dict[tuple, np.ndarray]:
+        k, b = self.blocks()
+        return {tuple(int(x) for x in kk): b[i] for i, kk in enumerate(k)}
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            try:
+                native.lib().lt_op_free(self.handle)
+            except Exception:
+                pass
+            self.handle = None
+
+
+class Context:
+    """One GPU: stream, solver handle and cached device buffers (lt_ctx)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = native.lib()
+        h = ctypes.c_void_p()
+        check(self.lib.lt_create(device, ctypes.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if self.h:
+            self.lib.lt_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream(self) -> int:
+        return int(self.lib.lt_stream(self.h) or 0)
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.lt_launch_count(self.h))
+
+    def set_stage_timing(self, on: bool):
+        check(self.lib.lt_set_stage_timing(self.h, int(on)))
+
+    def stage_times(self) -> Dict[str, Tuple[float, int]]:
+        """{kernel stage: (total ms, launches)} from CUDA events on the context stream."""
+        out = {}
+        n = int(self.lib.lt_stage_count(self.h))
+        buf = ctypes.create_string_buffer(128)
+        ms = ctypes.c_double()
+        cnt = ctypes.c_int64()
+        for i in range(n):
+            check(self.lib.lt_stage_get(self.h, i, buf, 128, ctypes.byref(ms), ctypes.byref(cnt)))
+            out[buf.value.decode()] = (ms.value, cnt.value)
+        return out
+
+    # ------------------------------------------------------------------
+    def _wrap(self, h) -> Operator:
+        info = np.zeros(12, dtype=np.int64)
+        self.lib.lt_op_info(h, _i(info))
+        return Operator(ctx=self, handle=h.value if hasattr(h, "value") else h, periodic=bool(info[0]),
+                        m0=int(info[1]), L=tuple(int(x) for x in info[2:5]), overlap_L0=int(info[5]),
+                        coefficient_rank=int(info[6]), stored=int(info[7]), Nb=int(info[8]),
+                        band=tuple(int(x) for x in info[9:12]))
+
+    def assemble(self, sys: LatticeSystem, periodic: bool, kind: str) -> Operator:
+        c = sys.to_c()
+        h = ctypes.c_void_p()
+        check(self.lib.lt_assemble(self.h, ctypes.byref(c), int(periodic), KINDS[kind], ctypes.byref(h)))
+        return self._wrap(h)
+
+    def assemble_box(self, sys: LatticeSystem, kind: str) -> Operator:
+        return self.assemble(sys, False, kind)
+
+    def assemble_periodic(self, sys: LatticeSystem, kind: str) -> Operator:
+        return self.assemble(sys, True, kind)
+
+    def assemble_core(self, sys: LatticeSystem, periodic: bool) -> Tuple[Operator, Operator]:
+        c = sys.to_c()
+        h, s = ctypes.c_void_p(), ctypes.c_void_p()
+        check(self.lib.lt_assemble_core(self.h, ctypes.byref(c), int(periodic), ctypes.byref(h), ctypes.byref(s)))
+        return self._wrap(h), self._wrap(s)
+
+    def combine(self, wa: float, a: Operator, wb: float, b: Operator) -> Operator:
+        h = ctypes.c_void_p()
+        check(self.lib.lt_combine(self.h, wa, a.handle, wb, b.handle, ctypes.byref(h)))
+        return self._wrap(h)
+
+    # ------------------------------------------------------------------
+    def solve_core(self, sys: LatticeSystem, periodic: bool, info: Optional[np.ndarray] = None) -> np.ndarray:
+        """LatticeSystem -> eigenvalues on the host ([K, m0] periodic, [N_b] box)."""
+        c = sys.to_c()
+        out = np.zeros(sys.basis_count)
+        inf = np.zeros(8, dtype=np.int64) if info is None else info
+        check(self.lib.lt_solve_core(self.h, ctypes.byref(c), int(periodic), _d(out), _i(inf)))
+        return out.reshape(sys.lattice_count, sys.m0) if periodic else out
+
+    def upload(self, sys: LatticeSystem) -> "DeviceSystem":
+        return DeviceSystem(self, sys)
+
+    def solve_periodic(self, H: Operator, S: Operator) -> np.ndarray:
+        K = H.L[0] * H.L[1] * H.L[2]
+        out = np.zeros(K * H.m0)
+        check(self.lib.lt_solve_periodic_ops(self.h, H.handle, S.handle, _d(out)))
+        return out.reshape(K, H.m0)
+
+    def solve_periodic_gen(self, dims, m0: int, Hgen: dict, Sgen: dict) -> np.ndarray:
+        def pack(g):
+            keys = sorted(g)
+            k = np.ascontiguousarray(np.array(keys, dtype=np.int64).reshape(-1, 3))
+            b = np.ascontiguousarray(np.concatenate([np.asarray(g[kk], dtype=np.float64).T.reshape(-1) for kk in keys])
+                                     if keys else np.zeros(1))
+            return len(keys), k, b
+        nH, kH, bH = pack(Hgen)
+        nS, kS, bS = pack(Sgen)
+        d = np.array(dims, dtype=np.int64)
+        K = int(np.prod(d))
+        out = np.zeros(K * m0)
+        check(self.lib.lt_solve_periodic(self.h, _i(d), m0, nH, _i(kH), _d(bH), nS, _i(kS), _d(bS), _d(out)))
+        return out.reshape(K, m0)
+
+    def bc_block_diagonalize(self, dims, m0: int, gen: dict) -> np.ndarray:
+        keys = sorted(gen)
+        k = np.ascontiguousarray(np.array(keys, dtype=np.int64).reshape(-1, 3))
+        b = np.ascontiguousarray(np.concatenate([np.asarray(gen[kk], dtype=np.float64).T.reshape(-1) for kk in keys]))
+        d = np.array(dims, dtype=np.int64)
+        K = int(np.prod(d))
+        out = np.zeros(K * m0 * m0 * 2)
+        check(self.lib.lt_block_diagonalize(self.h, _i(d), m0, len(keys), _i(k), _d(b), _d(out)))
+        z = out[0::2] + 1j * out[1::2]
+        return z.reshape(K, m0, m0).transpose(0, 2, 1).copy()
+
+    def solve_box_dense(self, H: np.ndarray, S: np.ndarray, cap: int = 4096) -> np.ndarray:
+        n = H.shape[0]
+        Hc = np.asfortranarray(H, dtype=np.float64)
+        Sc = np.asfortranarray(S, dtype=np.float64)
+        out = np.zeros(n)
+        check(self.lib.lt_solve_box_dense(self.h, n, Hc.ctypes.data_as(_dp), Sc.ctypes.data_as(_dp), cap, _d(out)))
+        return out
+
+    def pencil_eig(self, Hs: np.ndarray, Ss: np.ndarray) -> np.ndarray:
+        """Batch of Hermitian-definite pencils (count, m0, m0) complex."""
+        cnt, m0, _ = Hs.shape
+        def pack(a):
+            a = np.asarray(a, dtype=np.complex128).transpose(0, 2, 1).reshape(-1)
+            o = np.empty(2 * a.size)
+            o[0::2], o[1::2] = a.real, a.imag
+            return o
+        h, s = pack(Hs), pack(Ss)
+        out = np.zeros(cnt * m0)
+        check(self.lib.lt_pencil_eig(self.h, cnt, m0, _d(h), _d(s), _d(out)))
+        return out.reshape(cnt, m0)
+
+    # ---- stages --------------------------------------------------------
+    def build_sinc_quadrature(self, M: int):
+        t = np.zeros(2 * M + 1)
+        w = np.zeros(2 * M + 1)
+        check(self.lib.lt_sinc_quadrature(self.h, M, _d(t), _d(w)))
+        return t, w
+
+    def overlap_constant(self, sys: LatticeSystem) -> int:
+        c = sys.to_c()
+        out = np.zeros(1, dtype=np.int64)
+        check(self.lib.lt_overlap_constant(self.h, ctypes.byref(c), _i(out)))
+        return int(out[0])
+
+    def newton_master(self, ncells: int, h: float, M: int) -> np.ndarray:
+        R = 2 * M + 1
+        out = np.zeros(ncells * R)
+        check(self.lib.lt_newton_master(self.h, ncells, h, M, _d(out)))
+        return out.reshape(R, ncells).T.copy()
+
+    def potential(self, sys: LatticeSystem, periodic: bool, margin: int):
+        c = sys.to_c()
+        rows = np.zeros(3, dtype=np.int64)
+        tiled = np.zeros(3, dtype=np.int64)
+        check(self.lib.lt_potential(self.h, ctypes.byref(c), int(periodic), margin, _i(rows), _i(tiled), None, None, 0))
+        R = sys.rank_total
+        total = int(rows.sum()) * R
+        panels = np.zeros(total)
+        w = np.zeros(R)
+        check(self.lib.lt_potential(self.h, ctypes.byref(c), int(periodic), margin, _i(rows), _i(tiled), _d(panels),
+                                    _d(w), total))
+        out, at = [], 0
+        for l in range(3):
+            r = int(rows[l])
+            out.append(panels[at:at + r * R].reshape(R, r).T.copy())
+            at += r * R
+        return out, w, tuple(bool(x) for x in tiled)
+
+    def assembled_window_sum(self, master: np.ndarray, shifts, size: int) -> np.ndarray:
+        mrows, R = master.shape
+        m = np.asfortranarray(master, dtype=np.float64)
+        sh = np.array(shifts, dtype=np.int64)
+        out = np.zeros(size * R)
+        check(self.lib.lt_assembled_window_sum(self.h, mrows, R, m.ctypes.data_as(_dp), len(sh), _i(sh), size,
+                                               _d(out)))
+        return out.reshape(R, size).T.copy()
+
+    def profiles(self, sys: LatticeSystem, margin: int):
+        """pwc/pwl profiles on the assembly grids: {('pwc'|'pwl', l, mu): (offset, values)}."""
+        c = sys.to_c()
+        grid = np.zeros(6, dtype=np.int64)
+        m0 = sys.m0
+        lo = np.zeros(6 * m0, dtype=np.int64)
+        hi = np.zeros(6 * m0, dtype=np.int64)
+        check(self.lib.lt_profiles(self.h, ctypes.byref(c), margin, _i(grid), _i(lo), _i(hi), None, 0))
+        total = int(grid.sum()) * m0
+        vals = np.zeros(total)
+        check(self.lib.lt_profiles(self.h, ctypes.byref(c), margin, _i(grid), _i(lo), _i(hi), _d(vals), total))
+        out, at = {}, 0
+        for k in range(6):
+            g = int(grid[k])
+            for mu in range(m0):
+                v = vals[at + mu * g: at + (mu + 1) * g]
+                a, b = int(lo[k * m0 + mu]), int(hi[k * m0 + mu])
+                out[("pwc" if k < 3 else "pwl", k % 3, mu)] = (a, v[a:b].copy())
+            at += g * m0
+        return out
+
+
+class DeviceSystem:
+    """A LatticeSystem resident on the device (lt_sysdev) for the bench's device-timed leg."""
+
+    def __init__(self, ctx: Context, sys: LatticeSystem):
+        self.ctx = ctx
+        self.sys = sys
+        c = sys.to_c()
+        h = ctypes.c_void_p()
+        check(ctx.lib.lt_sys_upload(ctx.h, ctypes.byref(c), ctypes.byref(h)))
+        self.h = h
+
+    def solve(self, periodic: bool, eig_dev_ptr: int, k_begin: int = 0, k_end: int = -1,
+              info: Optional[np.ndarray] = None):
+        inf = np.zeros(8, dtype=np.int64) if info is None else info
+        check(self.ctx.lib.lt_solve_core_dev(self.ctx.h, self.h, int(periodic), ctypes.c_void_p(eig_dev_ptr), k_begin,
+                                             k_end, _i(inf)))
+        return inf
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            try:
+                self.ctx.lib.lt_sys_free(self.h)
+            except Exception:
+                pass
+            self.h = None
+
+
+_default: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default
+    if _default is None:
+        _default = Context(0)
+    return _default
+
+
+def assemble_box(sys: LatticeSystem, kind: str) -> Operator:
+    return default_context().assemble_box(sys, kind)
+
+
+def assemble_periodic(sys: LatticeSystem, kind: str) -> Operator:
+    return default_context().assemble_periodic(sys, kind)
+
+
+def assemble_core(sys: LatticeSystem, periodic: bool):
+    return default_context().assemble_core(sys, periodic)
+
+
+def combine(wa: float, a: Operator, wb: float, b: Operator) -> Operator:
+    return default_context().combine(wa, a, wb, b)
+
+
+def solve_periodic(H: Operator, S: Operator) -> np.ndarray:
+    return default_context().solve_periodic(H, S)
+
+
+def solve_box_dense(H: np.ndarray, S: np.ndarray, cap: int = 4096) -> np.ndarray:
+    return default_context().solve_box_dense(H, S, cap)
+
+
+def solve_core(sys: LatticeSystem, periodic: bool) -> np.ndarray:
+    return default_context().solve_core(sys, periodic)

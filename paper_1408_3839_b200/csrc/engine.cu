@@ -1,0 +1,1094 @@
+// engine.cu — context, device memory, pipeline orchestration and the C-ABI
+// (include/latham_b200.h). The pipeline for one system:
+//
+//   L0 scan (device) -> 1 small D2H -> host integer plan ->
+//   sinc | master panels + lattice window sums | pwc/pwl profiles | FEM tables |
+//   nuclear contraction (direct / fold / box S2) | fused combine into H, S ->
+//   periodic: sparse lattice DFT of H and S, batched pencils ; box: dense pencil
+//
+// All of it is stream-ordered on the context's stream; the only host
+// synchronisations are the L0 read-back and the final D2H of the results.
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <array>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "lt_internal.cuh"
+
+namespace lt {
+
+static thread_local std::string g_err;
+
+Arena::~Arena() {
+    for (auto& kv : bufs_)
+        if (kv.second.p) cudaFree(kv.second.p);
+}
+
+void* Arena::raw(const std::string& key, size_t bytes) {
+    Buf& b = bufs_[key];
+    if (b.cap < bytes) {
+        if (b.p) LT_CU(cudaFree(b.p));
+        b.p = nullptr;
+        size_t cap = std::max<size_t>(bytes, 256);
+        cap = cap + cap / 4;
+        LT_CU(cudaMalloc(&b.p, cap));
+        b.cap = cap;
+    }
+    return b.p;
+}
+
+size_t Arena::bytes() const {
+    size_t s = 0;
+    for (auto& kv : bufs_) s += kv.second.cap;
+    return s;
+}
+
+StageTimer::~StageTimer() {
+    for (cudaEvent_t e : pool_) cudaEventDestroy(e);
+}
+
+cudaEvent_t StageTimer::get() {
+    if (used_ == pool_.size()) {
+        cudaEvent_t e;
+        LT_CU(cudaEventCreate(&e));
+        pool_.push_back(e);
+    }
+    return pool_[used_++];
+}
+
+void StageTimer::begin(cudaStream_t st, const char* name) {
+    open_ = get();
+    open_name_ = name;
+    LT_CU(cudaEventRecord(open_, st));
+}
+
+void StageTimer::end(cudaStream_t st) {
+    cudaEvent_t b = get();
+    LT_CU(cudaEventRecord(b, st));
+    pending_.push_back({open_name_, open_, b});
+}
+
+void StageTimer::collect() {
+    for (auto& p : pending_) {
+        float ms = 0.f;
+        LT_CU(cudaEventSynchronize(p.b));
+        LT_CU(cudaEventElapsedTime(&ms, p.a, p.b));
+        auto& t = totals[p.name];
+        t.first += ms;
+        t.second += 1;
+    }
+    pending_.clear();
+    used_ = 0;
+}
+
+void StageTimer::reset() {
+    collect();
+    totals.clear();
+}
+
+}  // namespace lt
+
+using namespace lt;
+
+struct lt_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cusolverDnHandle_t solver = nullptr;
+    Arena arena;
+    int64_t launches = 0;
+    StageTimer timer;
+    Launch L() { return Launch{stream, &launches, &timer}; }
+};
+
+struct lt_sysdev {
+    HostSys hs;
+    DevSys ds;
+    void* mem = nullptr;
+};
+
+struct lt_operator {
+    int which = 0;  // 0 Laplace 1 Mass 2 Nuclear; core H uses 0 (Laplace first operand)
+    bool periodic = false;
+    Index m0 = 0;
+    Index L[3]{1, 1, 1};
+    Index band[3]{0, 0, 0};
+    Index L0 = 0, coefficient_rank = 0, Nb = 0;
+    std::vector<std::array<Index, 3>> kidx;  // periodic, std::map order
+    double* data = nullptr;                  // device: dense Nb*Nb or nblk*m0*m0
+    size_t count = 0;
+    ~lt_operator() {
+        if (data) cudaFree(data);
+    }
+};
+
+namespace lt {
+
+template <class F>
+static lt_status guarded(F&& f) {
+    try {
+        f();
+        g_err.clear();
+        return LT_OK;
+    } catch (const Error& e) {
+        g_err = e.what();
+        return static_cast<lt_status>(e.code);
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return LT_EGENERIC;
+    }
+}
+
+static void upload(lt_ctx* c, void* dst, const void* src, size_t bytes) {
+    if (bytes) LT_CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream));
+}
+
+static lt_sysdev* make_sysdev(const lt_system* s) {
+    auto sd = std::make_unique<lt_sysdev>();
+    sd->hs = host_sys_from(s);
+    const HostSys& h = sd->hs;
+    const size_t m0 = h.alpha.size(), nn = h.Z.size();
+    size_t bytes = 16;
+    for (size_t nb : {3 * nn * 8, nn * 8, 3 * m0 * 8, m0 * 8, 3 * m0 * 4}) bytes += (nb + 15) / 16 * 16;
+    LT_CU(cudaMalloc(&sd->mem, bytes));
+    char* p = static_cast<char*>(sd->mem);
+    std::vector<char> host(bytes, 0);
+    size_t at = 0;
+    auto put = [&](const void* src, size_t nb) {
+        std::memcpy(host.data() + at, src, nb);
+        void* d = p + at;
+        at += (nb + 15) / 16 * 16;
+        return d;
+    };
+    sd->ds.m0 = static_cast<int>(m0);
+    sd->ds.nnuc = static_cast<int>(nn);
+    sd->ds.b = h.b;
+    sd->ds.eps_ov = h.eps_ov;
+    sd->ds.pos = static_cast<const double*>(put(h.pos.data(), 3 * nn * 8));
+    sd->ds.Z = static_cast<const double*>(put(h.Z.data(), nn * 8));
+    sd->ds.center = static_cast<const double*>(put(h.center.data(), 3 * m0 * 8));
+    sd->ds.alpha = static_cast<const double*>(put(h.alpha.data(), m0 * 8));
+    sd->ds.deg = static_cast<const int*>(put(h.deg.data(), 3 * m0 * 4));
+    LT_CU(cudaMemcpy(sd->mem, host.data(), at, cudaMemcpyHostToDevice));
+    return sd.release();
+}
+
+// ---------------------------------------------------------------------------
+// L0 (gto_basis.cpp:87-126)
+// ---------------------------------------------------------------------------
+static Index compute_L0(lt_ctx* c, const lt_sysdev* sd) {
+    const HostSys& h = sd->hs;
+    const Index m0 = h.m0();
+    Index off3[3], boff3[3], n3[3];
+    Index tot = 0, btot = 0;
+    for (int l = 0; l < 3; ++l) {
+        n3[l] = h.n[l];
+        const Index width = 2 * 258 * h.n[l];
+        off3[l] = tot;
+        boff3[l] = btot;
+        tot += m0 * width;
+        btot += m0 * ((width + kL0Block - 1) / kL0Block);
+    }
+    OverlapBufs b;
+    b.prof = c->arena.get<double>("l0.prof", tot);
+    b.bmax = c->arena.get<double>("l0.bmax", btot);
+    b.found = c->arena.get<int>("l0.found", 260);
+    b.state = c->arena.get<int>("l0.state", 4);
+    const Launch L = c->L();
+    launch_overlap_init(L, b);
+    launch_overlap_profiles(L, sd->ds, n3, off3, boff3, b);
+    int s_begin = 1;
+    const int chunk = 32;
+    while (true) {
+        const int s_end = std::min(257, s_begin + chunk);
+        launch_overlap_scan(L, sd->ds, n3, off3, boff3, b, s_begin, s_end);
+        launch_overlap_finalize(L, b, s_begin, s_end);
+        int st[4];
+        LT_CU(cudaMemcpyAsync(st, b.state, sizeof(st), cudaMemcpyDeviceToHost, c->stream));
+        LT_CU(cudaStreamSynchronize(c->stream));
+        if (st[3] || s_end >= 257) return st[0];
+        s_begin = s_end;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// assembly
+// ---------------------------------------------------------------------------
+struct AsmOut {
+    double* out0 = nullptr;  // H / single operator
+    double* out1 = nullptr;  // S
+    int64_t* kidx = nullptr;
+};
+
+enum Need : int { NEED_MS = 1, NEED_NUC = 2 };
+
+struct Work {
+    double *t, *w, *potw;
+    double* pot[3];
+    double* pwc[3];
+    double* pwl[3];
+    unsigned long long *pwc_lo[3], *pwc_hi[3], *pwl_lo[3], *pwl_hi[3];
+    double *massT[3], *stiffT[3], *T[3];
+    double* N = nullptr;
+};
+
+static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need, int mode, AsmOut out,
+                         Work* wout = nullptr) {
+    const Launch L = c->L();
+    const Index m0 = p.m0, mm = m0 * m0, RN = p.RN, Rtot = p.Rtot;
+    Arena& A = c->arena;
+    Work w{};
+    w.t = A.get<double>("sinc.t", RN);
+    w.w = A.get<double>("sinc.w", RN);
+    w.potw = A.get<double>("sinc.potw", Rtot);
+    launch_sinc(L, p.M, sd->ds, w.t, w.w, w.potw);
+    const bool nuc = need & NEED_NUC, ms = need & NEED_MS;
+    if (nuc) {
+        std::vector<int64_t> s0all;
+        for (int l = 0; l < 3; ++l)
+            for (Index v : p.d[l].s0) s0all.push_back(v);
+        int64_t* s0d = A.get<int64_t>("pot.s0", s0all.size());
+        upload(c, s0d, s0all.data(), s0all.size() * sizeof(int64_t));
+        for (int l = 0; l < 3; ++l) {
+            const DirPlan& d = p.d[l];
+            double* master = A.get<double>("pot.master" + std::to_string(l), d.mrows * RN);
+            w.pot[l] = A.get<double>("pot.panel" + std::to_string(l), d.pot_rows * Rtot);
+            launch_master(L, d.mrows, d.h, RN, w.t, master);
+            launch_window_sum(L, master, d.mrows, RN, p.nnuc, s0d + l * p.nnuc, d.nsum, d.n, d.pot_rows, w.pot[l]);
+        }
+    }
+    // profiles (galerkin.cpp:127-149)
+    ProfileJob jobs[6];
+    int nj = 0;
+    for (int l = 0; l < 3; ++l) {
+        const DirPlan& d = p.d[l];
+        if (nuc) {
+            ProfileJob j;
+            j.grid = d.G;
+            j.per_cell = d.n;
+            j.cell_index = p.margin;
+            j.step = d.h;
+            j.align = 0.5;
+            j.dir = l;
+            j.values = w.pwc[l] = A.get<double>("prof.pwc" + std::to_string(l), m0 * d.G);
+            j.lo = w.pwc_lo[l] = A.get<unsigned long long>("prof.pwc_lo" + std::to_string(l), m0);
+            j.hi = w.pwc_hi[l] = A.get<unsigned long long>("prof.pwc_hi" + std::to_string(l), m0);
+            jobs[nj++] = j;
+        }
+        if (ms) {
+            ProfileJob j;
+            j.grid = d.Gbar;
+            j.per_cell = d.nbar;
+            j.cell_index = p.margin;
+            j.step = d.hbar;
+            j.align = 0.0;
+            j.dir = l;
+            j.values = w.pwl[l] = A.get<double>("prof.pwl" + std::to_string(l), m0 * d.Gbar);
+            j.lo = w.pwl_lo[l] = A.get<unsigned long long>("prof.pwl_lo" + std::to_string(l), m0);
+            j.hi = w.pwl_hi[l] = A.get<unsigned long long>("prof.pwl_hi" + std::to_string(l), m0);
+            jobs[nj++] = j;
+        }
+    }
+    launch_profiles(L, sd->ds, jobs, nj, 1e-280);
+    if (ms)
+        for (int l = 0; l < 3; ++l) {
+            const DirPlan& d = p.d[l];
+            w.massT[l] = A.get<double>("fem.mass" + std::to_string(l), d.width * mm);
+            w.stiffT[l] = A.get<double>("fem.stiff" + std::to_string(l), d.width * mm);
+            launch_fem_tables(L, m0, d.band, d.nbar, d.hbar, d.Gbar, w.pwl[l], w.pwl_lo[l], w.pwl_hi[l], w.massT[l],
+                              w.stiffT[l]);
+        }
+    if (nuc) {
+        for (int l = 0; l < 3; ++l) {
+            const DirPlan& d = p.d[l];
+            if (l == p.s2_dir) continue;
+            w.T[l] = A.get<double>("nuc.T" + std::to_string(l), d.npairs * Rtot * mm);
+            if (d.mode == TM_FOLD) {
+                double* Qf = A.get<double>("nuc.Qf" + std::to_string(l), d.width * mm * d.n);
+                launch_nuc_fold(L, m0, Rtot, d, w.pwc[l], w.pwc_lo[l], w.pwc_hi[l], w.pot[l], Qf, w.T[l]);
+            } else {
+                if (d.mode == TM_BOXDIR)  // tables of pairs with k+d outside the lattice stay unused
+                    LT_CU(cudaMemsetAsync(w.T[l], 0, sizeof(double) * d.npairs * Rtot * mm, c->stream));
+                launch_nuc_direct(L, m0, Rtot, d, p.periodic, w.pwc[l], w.pwc_lo[l], w.pwc_hi[l], w.pot[l], w.T[l]);
+            }
+        }
+        if (p.s2_dir >= 0) {
+            const int ls = p.s2_dir;
+            const int la = (ls + 1) % 3, lb = (ls + 2) % 3;
+            const DirPlan& d = p.d[ls];
+            double* W = A.get<double>("s2.W", Rtot * mm);
+            double* V = A.get<double>("s2.V", mm * d.G);
+            launch_box_w(L, m0, Rtot, w.potw, w.T[la], w.T[lb], W);
+            launch_box_v(L, m0, Rtot, d.G, W, w.pot[ls], V);
+            int nsplit = 1;
+            {
+                // split the contraction so the grid covers the SMs a few times over
+                const Index tiles = ((d.L + 63) / 64) * ((d.width + 31) / 32) * mm;
+                while (tiles * nsplit < 4 * 148 && nsplit < 16) nsplit *= 2;
+            }
+            double* part = A.get<double>("s2.part", static_cast<size_t>(nsplit) * mm * d.L * d.width);
+            w.N = A.get<double>("s2.N", d.L * d.width * mm);
+            launch_box_corr(L, m0, d, w.pwc[ls], w.pwc_lo[ls], w.pwc_hi[ls], V, part, w.N, nsplit);
+        }
+    }
+    // fused combine + placement
+    FillArgs fa;
+    fa.m0 = m0;
+    fa.Rtot = Rtot;
+    for (int l = 0; l < 3; ++l) {
+        fa.L[l] = p.d[l].L;
+        fa.band[l] = p.d[l].band;
+        fa.width[l] = p.d[l].width;
+        fa.massT[l] = w.massT[l];
+        fa.stiffT[l] = w.stiffT[l];
+        fa.T[l] = w.T[l];
+    }
+    fa.potw = w.potw;
+    fa.N = w.N;
+    fa.s2_dir = p.s2_dir;
+    fa.mode = mode;
+    fa.periodic = p.periodic;
+    fa.out0 = out.out0;
+    fa.out1 = out.out1;
+    fa.kidx = out.kidx;
+    Index nblocks;
+    if (p.periodic) {
+        nblocks = p.nblocks;
+    } else {
+        nblocks = p.cells * p.d[0].width * p.d[1].width * p.d[2].width;
+        LT_CU(cudaMemsetAsync(out.out0, 0, sizeof(double) * p.Nb * p.Nb, c->stream));
+        if (mode == 0) LT_CU(cudaMemsetAsync(out.out1, 0, sizeof(double) * p.Nb * p.Nb, c->stream));
+    }
+    launch_fill(L, fa, p.Nb, nblocks);
+    if (wout) *wout = w;
+}
+
+static std::vector<std::array<Index, 3>> periodic_kidx(const Plan& p) {
+    std::vector<std::array<Index, 3>> out;
+    std::vector<Index> ax[3];
+    for (int l = 0; l < 3; ++l) {
+        const DirPlan& d = p.d[l];
+        for (Index r = 0; r < d.width; ++r) {
+            const Index dd = r <= d.band ? r : r - d.width;
+            ax[l].push_back(((dd % d.L) + d.L) % d.L);
+        }
+    }
+    for (Index a : ax[0])
+        for (Index b : ax[1])
+            for (Index cc : ax[2]) out.push_back({a, b, cc});
+    return out;
+}
+
+// ---------------------------------------------------------------------------
+// spectrum
+// ---------------------------------------------------------------------------
+// Dense block-diagonal form [K][mm] (complex) of a generating tensor given by the
+// stored kidx (host) and its blocks (device, std::map order).
+static double2* block_diag_device(lt_ctx* c, const Index dims[3], Index m0,
+                                  const std::vector<std::array<Index, 3>>& kidx, const double* blocks_dev,
+                                  const std::string& tag) {
+    const Launch L = c->L();
+    const Index mm = m0 * m0;
+    std::vector<Index> comp[3];
+    for (int l = 0; l < 3; ++l) {
+        std::set<Index> s;
+        for (auto& k : kidx) s.insert(k[l]);
+        if (s.empty()) s.insert(0);
+        comp[l].assign(s.begin(), s.end());
+    }
+    Index ext[3];
+    for (int l = 0; l < 3; ++l) ext[l] = static_cast<Index>(comp[l].size());
+    std::vector<int64_t> kslot(kidx.size());
+    for (size_t b = 0; b < kidx.size(); ++b) {
+        Index pos = 0;
+        for (int l = 0; l < 3; ++l) {
+            const Index ci = std::lower_bound(comp[l].begin(), comp[l].end(), kidx[b][l]) - comp[l].begin();
+            pos = pos * ext[l] + ci;
+        }
+        kslot[b] = pos;
+    }
+    const Index K = dims[0] * dims[1] * dims[2];
+    Index maxsz = ext[0] * ext[1] * ext[2];
+    {
+        Index e2[3] = {ext[0], ext[1], ext[2]};
+        for (int a = 0; a < 3; ++a) {
+            if (dims[a] > 1) e2[a] = dims[a];
+            maxsz = std::max(maxsz, e2[0] * e2[1] * e2[2]);
+        }
+    }
+    double2* bufA = c->arena.get<double2>("dft.a" + tag, maxsz * mm);
+    double2* bufB = c->arena.get<double2>("dft.b" + tag, maxsz * mm);
+    int64_t* ks = c->arena.get<int64_t>("dft.kslot" + tag, kslot.size() + 1);
+    upload(c, ks, kslot.data(), kslot.size() * sizeof(int64_t));
+    LT_CU(cudaMemsetAsync(bufA, 0, sizeof(double2) * ext[0] * ext[1] * ext[2] * mm, c->stream));
+    launch_scatter_gen(L, static_cast<Index>(kidx.size()), mm, ks, blocks_dev, bufA);
+    double2* cur = bufA;
+    double2* nxt = bufB;
+    Index in_ext[3] = {ext[0], ext[1], ext[2]};
+    for (int a = 0; a < 3; ++a) {
+        if (dims[a] == 1) {
+            if (comp[a].size() != 1 || comp[a][0] != 0) fail(LT_EBOUNDS, "GeneratingBlockTensor: index out of range");
+            continue;
+        }
+        for (Index v : comp[a])
+            if (v < 0 || v >= dims[a]) fail(LT_EBOUNDS, "GeneratingBlockTensor: index out of range");
+        int64_t* cd = c->arena.get<int64_t>("dft.comp" + tag + std::to_string(a), comp[a].size());
+        upload(c, cd, comp[a].data(), comp[a].size() * sizeof(int64_t));
+        double2* tw = c->arena.get<double2>("dft.tw" + tag + std::to_string(a), dims[a] * comp[a].size());
+        launch_twiddles(L, dims[a], static_cast<Index>(comp[a].size()), cd, tw);
+        Index out_ext[3] = {in_ext[0], in_ext[1], in_ext[2]};
+        out_ext[a] = dims[a];
+        launch_dft_axis(L, a, in_ext, out_ext, mm, cur, nxt, tw, static_cast<Index>(comp[a].size()), dims[a]);
+        std::swap(cur, nxt);
+        for (int l = 0; l < 3; ++l) in_ext[l] = out_ext[l];
+    }
+    (void)K;
+    return cur;
+}
+
+static void raise_fail_key(unsigned long long key, bool periodic) {
+    if (key == ~0ull) return;
+    const Index k = static_cast<Index>(key / 4);
+    const int code = static_cast<int>(key % 4);
+    if (!periodic)
+        fail(LT_EDEFINITE, "solve_box_dense: overlap matrix is not positive definite (near-linear-dependent basis?)");
+    if (code == 1)
+        fail(LT_EDEFINITE, "solve_periodic: non-Hermitian diagonal block at k-point " + std::to_string(k));
+    fail(LT_EDEFINITE, "solve_periodic: overlap block at k-point " + std::to_string(k) + " is not positive definite");
+}
+
+__global__ void k_real_to_complex(Index n, const double* __restrict__ a, double2* __restrict__ out) {
+    const Index i = static_cast<Index>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = make_double2(a[i], 0.0);
+}
+
+// Box pencil on device buffers H, S (n x n col-major; both may be overwritten).
+// Eigenvalues -> eig_dev. Returns the failure key through *fail (device) for the warp path.
+static void box_eig_device(lt_ctx* c, Index n, double* H, double* S, double* eig_dev, unsigned long long* fail_dev) {
+    const Launch L = c->L();
+    if (n <= 32) {
+        double2* hc = c->arena.get<double2>("box.hc", n * n);
+        double2* sc = c->arena.get<double2>("box.sc", n * n);
+        Stage st_(L, "r2c");
+        k_real_to_complex<<<static_cast<unsigned>((n * n + 255) / 256), 256, 0, c->stream>>>(n * n, H, hc);
+        k_real_to_complex<<<static_cast<unsigned>((n * n + 255) / 256), 256, 0, c->stream>>>(n * n, S, sc);
+        LT_CU(cudaGetLastError());
+        L.tick(2);
+        launch_pencil(L, 1, n, hc, sc, eig_dev, fail_dev, false);
+        return;
+    }
+    if (!c->solver) {
+        if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS) fail(LT_ECUDA, "cusolverDnCreate failed");
+    }
+    cusolverDnSetStream(c->solver, c->stream);
+    int lwork = 0;
+    if (cusolverDnDsygvd_bufferSize(c->solver, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_NOVECTOR, CUBLAS_FILL_MODE_LOWER,
+                                    static_cast<int>(n), H, static_cast<int>(n), S, static_cast<int>(n), eig_dev,
+                                    &lwork) != CUSOLVER_STATUS_SUCCESS)
+        fail(LT_ECUDA, "cusolverDnDsygvd_bufferSize failed");
+    double* work = c->arena.get<double>("box.work", static_cast<size_t>(lwork) + 1);
+    int* info = c->arena.get<int>("box.info", 1);
+    Stage st_(L, "sygvd");
+    if (cusolverDnDsygvd(c->solver, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_NOVECTOR, CUBLAS_FILL_MODE_LOWER,
+                         static_cast<int>(n), H, static_cast<int>(n), S, static_cast<int>(n), eig_dev, work, lwork,
+                         info) != CUSOLVER_STATUS_SUCCESS)
+        fail(LT_ECUDA, "cusolverDnDsygvd failed");
+    // map info > n (leading minor of S not positive) onto the failure key
+    int hinfo = 0;
+    LT_CU(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    LT_CU(cudaStreamSynchronize(c->stream));
+    if (hinfo > n) fail(LT_EDEFINITE, "solve_box_dense: overlap matrix is not positive definite (near-linear-dependent basis?)");
+    if (hinfo != 0) fail(LT_EGENERIC, "solve_box_dense: eigensolver failed");
+}
+
+// full path on device; eigenvalues -> eig_dev (device)
+static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double* eig_dev, Index k_begin,
+                           Index k_end, int64_t* info) {
+    validate(sd->hs);
+    const Index L0 = compute_L0(c, sd);
+    Plan p;
+    plan_after_L0(sd->hs, periodic, L0, p, true);
+    const Index mm = p.m0 * p.m0;
+    AsmOut out;
+    unsigned long long* fk = c->arena.get<unsigned long long>("solve.fail", 1);
+    LT_CU(cudaMemsetAsync(fk, 0xff, sizeof(unsigned long long), c->stream));
+    if (periodic) {
+        out.out0 = c->arena.get<double>("core.H", p.nblocks * mm);
+        out.out1 = c->arena.get<double>("core.S", p.nblocks * mm);
+        out.kidx = c->arena.get<int64_t>("core.kidx", p.nblocks * 3);
+        run_assembly(c, sd, p, NEED_MS | NEED_NUC, 0, out);
+        const auto kidx = periodic_kidx(p);
+        const Index dims[3] = {p.d[0].L, p.d[1].L, p.d[2].L};
+        double2* Hb = block_diag_device(c, dims, p.m0, kidx, out.out0, "H");
+        double2* Sb = block_diag_device(c, dims, p.m0, kidx, out.out1, "S");
+        if (k_end < 0 || k_end > p.K) k_end = p.K;
+        if (k_begin < 0) k_begin = 0;
+        if (k_begin < k_end)
+            launch_pencil(c->L(), k_end - k_begin, p.m0, Hb + k_begin * mm, Sb + k_begin * mm, eig_dev + k_begin * p.m0,
+                          fk, true);
+    } else {
+        if (p.Nb > 4096)
+            fail(LT_ECAP, "solve_box_dense: size " + std::to_string(p.Nb) + " exceeds dense cap 4096");
+        out.out0 = c->arena.get<double>("core.H", p.Nb * p.Nb);
+        out.out1 = c->arena.get<double>("core.S", p.Nb * p.Nb);
+        run_assembly(c, sd, p, NEED_MS | NEED_NUC, 0, out);
+        box_eig_device(c, p.Nb, out.out0, out.out1, eig_dev, fk);
+    }
+    unsigned long long key = ~0ull;
+    LT_CU(cudaMemcpyAsync(&key, fk, sizeof(key), cudaMemcpyDeviceToHost, c->stream));
+    LT_CU(cudaStreamSynchronize(c->stream));
+    c->timer.collect();
+    if (info) {
+        info[0] = p.L0;
+        for (int l = 0; l < 3; ++l) info[1 + l] = p.d[l].band;
+        info[4] = p.Rtot;
+        info[5] = p.Nb;
+        info[6] = p.K;
+        info[7] = key == ~0ull ? -1 : static_cast<int64_t>(key);
+    }
+    raise_fail_key(key, periodic);
+}
+
+static lt_operator* new_op(const Plan& p, int which, Index coefficient_rank) {
+    auto* op = new lt_operator;
+    op->which = which;
+    op->periodic = p.periodic;
+    op->m0 = p.m0;
+    for (int l = 0; l < 3; ++l) {
+        op->L[l] = p.d[l].L;
+        op->band[l] = p.d[l].band;
+    }
+    op->L0 = p.L0;
+    op->coefficient_rank = coefficient_rank;
+    op->Nb = p.Nb;
+    if (p.periodic) {
+        op->kidx = periodic_kidx(p);
+        op->count = p.nblocks * p.m0 * p.m0;
+    } else {
+        op->count = p.Nb * p.Nb;
+    }
+    if (cudaMalloc(&op->data, sizeof(double) * std::max<size_t>(op->count, 1)) != cudaSuccess) {
+        delete op;
+        fail(LT_ECUDA, "cudaMalloc failed for operator");
+    }
+    return op;
+}
+
+// ordered union of two kidx lists with index maps (eigensolver.cpp:60-64 semantics)
+static void union_maps(const lt_operator* a, const lt_operator* b, std::vector<std::array<Index, 3>>& keys,
+                       std::vector<int64_t>& ia, std::vector<int64_t>& ib) {
+    std::map<std::array<Index, 3>, std::pair<int64_t, int64_t>> u;
+    for (size_t i = 0; i < a->kidx.size(); ++i) u[a->kidx[i]].first = static_cast<int64_t>(i) + 1;
+    for (size_t i = 0; i < b->kidx.size(); ++i) u[b->kidx[i]].second = static_cast<int64_t>(i) + 1;
+    for (auto& kv : u) {
+        keys.push_back(kv.first);
+        ia.push_back(kv.second.first - 1);
+        ib.push_back(kv.second.second - 1);
+    }
+}
+
+}  // namespace lt
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* lt_last_error(void) { return lt::g_err.c_str(); }
+
+lt_status lt_create(int device, lt_ctx** out) {
+    return guarded([&] {
+        auto c = std::make_unique<lt_ctx>();
+        c->device = device;
+        LT_CU(cudaSetDevice(device));
+        LT_CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        *out = c.release();
+    });
+}
+
+void lt_destroy(lt_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->solver) cusolverDnDestroy(c->solver);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+void* lt_stream(lt_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+int64_t lt_launch_count(lt_ctx* c) { return c ? c->launches : 0; }
+
+lt_status lt_set_stage_timing(lt_ctx* c, int on) {
+    return guarded([&] {
+        LT_CU(cudaStreamSynchronize(c->stream));
+        c->timer.reset();
+        c->timer.on = on != 0;
+    });
+}
+
+int64_t lt_stage_count(lt_ctx* c) {
+    cudaStreamSynchronize(c->stream);
+    c->timer.collect();
+    return static_cast<int64_t>(c->timer.totals.size());
+}
+
+lt_status lt_stage_get(lt_ctx* c, int64_t idx, char* name, int64_t cap, double* ms, int64_t* launches) {
+    return guarded([&] {
+        if (idx < 0 || idx >= static_cast<int64_t>(c->timer.totals.size())) fail(LT_EBOUNDS, "stage index");
+        auto it = c->timer.totals.begin();
+        std::advance(it, idx);
+        std::snprintf(name, static_cast<size_t>(cap), "%s", it->first.c_str());
+        *ms = it->second.first;
+        *launches = it->second.second;
+    });
+}
+
+lt_status lt_sys_upload(lt_ctx* c, const lt_system* s, lt_sysdev** out) {
+    return guarded([&] {
+        LT_CU(cudaSetDevice(c->device));
+        *out = make_sysdev(s);
+    });
+}
+
+void lt_sys_free(lt_sysdev* s) {
+    if (!s) return;
+    if (s->mem) cudaFree(s->mem);
+    delete s;
+}
+
+lt_status lt_solve_core_dev(lt_ctx* c, const lt_sysdev* s, int periodic, double* eig_dev, int64_t k_begin,
+                            int64_t k_end, int64_t* info) {
+    return guarded([&] {
+        LT_CU(cudaSetDevice(c->device));
+        solve_core_dev(c, s, periodic != 0, eig_dev, k_begin, k_end, info);
+    });
+}
+
+lt_status lt_solve_core(lt_ctx* c, const lt_system* s, int periodic, double* eig_host, int64_t* info) {
+    return guarded([&] {
+        LT_CU(cudaSetDevice(c->device));
+        std::unique_ptr<lt_sysdev, void (*)(lt_sysdev*)> sd(make_sysdev(s), lt_sys_free);
+        const HostSys& h = sd->hs;
+        const Index count = h.m0() * h.cells();
+        double* eig = c->arena.get<double>("solve.eig", count);
+        solve_core_dev(c, sd.get(), periodic != 0, eig, 0, -1, info);
+        LT_CU(cudaMemcpyAsync(eig_host, eig, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream));
+        LT_CU(cudaStreamSynchronize(c->stream));
+    });
+}
+
+lt_status lt_assemble(lt_ctx* c, const lt_system* s, int periodic, lt_kind kind, lt_operator** out) {
+    return guarded([&] {
+        LT_CU(cudaSetDevice(c->device));
+        std::unique_ptr<lt_sysdev, void (*)(lt_sysdev*)> sd(make_sysdev(s), lt_sys_free);
+        validate(sd->hs);
+        const Index L0 = compute_L0(c, sd.get());
+        Plan p;
+        const bool nuc = kind == LT_NUCLEAR;
+        plan_after_L0(sd->hs, periodic != 0, L0, p, nuc);
+        const Index crank = kind == LT_MASS ? 1 : kind == LT_LAPLACE ? 3 : p.Rtot;
+        std::unique_ptr<lt_operator> op(new_op(p, static_cast<int>(kind), crank));
+        AsmOut o;
+        o.out0 = op->data;
+        o.kidx = p.periodic ? c->arena.get<int64_t>("op.kidx", p.nblocks * 3) : nullptr;
+        const int mode = kind == LT_LAPLACE ? 1 : kind == LT_MASS ? 2 : 3;
+        run_assembly(c, sd.get(), p, nuc ? NEED_NUC : NEED_MS, mode, o);
+        LT_CU(cudaStreamSynchronize(c->stream));
+        *out = op.release();
+    });
+}
+
+lt_status lt_assemble_core(lt_ctx* c, const lt_system* s, int periodic, lt_operator** H, lt_operator** S) {
+    return guarded([&] {
+        LT_CU(cudaSetDevice(c->device));
+        std::unique_ptr<lt_sysdev, void (*)(lt_sysdev*)> sd(make_sysdev(s), lt_sys_free);
+        validate(sd->hs);
+        const Index L0 = compute_L0(c, sd.get());
+        Plan p;
+        plan_after_L0(sd->hs, periodic != 0, L0, p, true);
+        std::unique_ptr<lt_operator> h(new_op(p, 0, 3 + p.Rtot));
+        std::unique_ptr<lt_operator> sop(new_op(p, 1, 1));
+        AsmOut o;
+        o.out0 = h->data;
+        o.out1 = sop->data;
+        o.kidx = p.periodic ? c->arena.get<int64_t>("op.kidx", p.nblocks * 3) : nullptr;
+        run_assembly(c, sd.get(), p, NEED_MS | NEED_NUC, 0, o);
+        LT_CU(cudaStreamSynchronize(c->stream));
+        *H = h.release();
+        *S = sop.release();
+    });
+}
+
+lt_status lt_combine(lt_ctx* c, double wa, const lt_operator* a, double wb, const lt_operator* b, lt_operator** out) {
+    return guarded([&] {
+        if (a->periodic != b->periodic || a->m0 != b->m0 || a->L[0] != b->L[0] || a->L[1] != b->L[1] ||
+            a->L[2] != b->L[2])
+            fail(LT_ESTRUCT, "combine: operators have different layouts");
+        LT_CU(cudaSetDevice(c->device));
+        auto op = std::make_unique<lt_operator>();
+        op->which = a->which;
+        op->periodic = a->periodic;
+        op->m0 = a->m0;
+        for (int l = 0; l < 3; ++l) {
+            op->L[l] = a->L[l];
+            op->band[l] = std::max(a->band[l], b->band[l]);
+        }
+        op->L0 = std::max(a->L0, b->L0);
+        op->coefficient_rank = a->coefficient_rank + b->coefficient_rank;
+        op->Nb = a->Nb;
+        const Index mm = a->m0 * a->m0;
+        if (!a->periodic) {
+            op->count = a->count;
+            LT_CU(cudaMalloc(&op->data, sizeof(double) * op->count));
+            launch_axpby_map(c->L(), static_cast<Index>(op->count), 1, wa, a->data, nullptr, wb, b->data, nullptr,
+                             op->data);
+        } else {
+            std::vector<int64_t> ia, ib;
+            union_maps(a, b, op->kidx, ia, ib);
+            op->count = op->kidx.size() * mm;
+            LT_CU(cudaMalloc(&op->data, sizeof(double) * std::max<size_t>(op->count, 1)));
+            int64_t* d = c->arena.get<int64_t>("combine.maps", 2 * ia.size() + 1);
+            std::vector<int64_t> both(ia);
+            both.insert(both.end(), ib.begin(), ib.end());
+            upload(c, d, both.data(), both.size() * sizeof(int64_t));
+            launch_axpby_map(c->L(), static_cast<Index>(op->kidx.size()), mm, wa, a->data, d, wb, b->data,
+                             d + ia.size(), op->data);
+        }
+        LT_CU(cudaStreamSynchronize(c->stream));
+        *out = op.release();
+    });
+}
+
+void lt_op_free(lt_operator* op) { delete op; }
+
+void lt_op_info(const lt_operator* op, int64_t* info) {
+    info[0] = op->periodic;
+    info[1] = op->m0;
+    for (int l = 0; l < 3; ++l) info[2 + l] = op->L[l];
+    info[5] = op->L0;
+    info[6] = op->coefficient_rank;
+    info[7] = static_cast<int64_t>(op->kidx.size());
+    info[8] = op->Nb;
+    for (int l = 0; l < 3; ++l) info[9 + l] = op->band[l];
+}
+
+lt_status lt_op_dense(const lt_operator* op, double* out) {
+    return guarded([&] {
+        if (op->periodic) fail(LT_ESTRUCT, "lt_op_dense: periodic operator carries no dense payload");
+        LT_CU(cudaMemcpy(out, op->data, sizeof(double) * op->count, cudaMemcpyDeviceToHost));
+    });
+}
+
+lt_status lt_op_blocks(const lt_operator* op, int64_t* kidx, double* blocks) {
+    return guarded([&] {
+        if (!op->periodic) fail(LT_ESTRUCT, "lt_op_blocks: box operator carries no generating tensor");
+        for (size_t i = 0; i < op->kidx.size(); ++i)
+            for (int l = 0; l < 3; ++l) kidx[3 * i + l] = op->kidx[i][l];
+        LT_CU(cudaMemcpy(blocks, op->data, sizeof(double) * op->count, cudaMemcpyDeviceToHost));
+    });
+}
+
+lt_status lt_solve_periodic_ops(lt_ctx* c, const lt_operator* H, const lt_operator* S, double* eig) {
+    return guarded([&] {
+        if (!H->periodic || !S->periodic) fail(LT_ESTRUCT, "solve_periodic: operators must be periodic assemblies");
+        if (H->m0 != S->m0 || H->L[0] != S->L[0] || H->L[1] != S->L[1] || H->L[2] != S->L[2])
+            fail(LT_ESTRUCT, "solve_periodic: H and S layouts differ");
+        LT_CU(cudaSetDevice(c->device));
+        const Index mm = H->m0 * H->m0;
+        const Index K = H->L[0] * H->L[1] * H->L[2];
+        double2* Hb = block_diag_device(c, H->L, H->m0, H->kidx, H->data, "H");
+        double2* Sb = block_diag_device(c, S->L, S->m0, S->kidx, S->data, "S");
+        double* e = c->arena.get<double>("solve.eig", K * H->m0);
+        unsigned long long* fk = c->arena.get<unsigned long long>("solve.fail", 1);
+        LT_CU(cudaMemsetAsync(fk, 0xff, sizeof(unsigned long long), c->stream));
+        launch_pencil(c->L(), K, H->m0, Hb, Sb, e, fk, true);
+        (void)mm;
+        unsigned long long key = ~0ull;
+        LT_CU(cudaMemcpyAsync(&key, fk, sizeof(key), cudaMemcpyDeviceToHost, c->stream));
+        LT_CU(cudaMemcpyAsync(eig, e, sizeof(double) * K * H->m0, cudaMemcpyDeviceToHost, c->stream));
+        LT_CU(cudaStreamSynchronize(c->stream));
+        raise_fail_key(key, true);
+    });
+}
+
+static void gen_to_device(lt_ctx* c, int64_t nblk, const int64_t* k, const double* b, Index m0,
+                          std::vector<std::array<Index, 3>>& keys, double** dev, const std::string& tag) {
+    // std::map order (block_circulant.hpp:47); later duplicates overwrite earlier ones (set_block)
+    std::map<std::array<Index, 3>, int64_t> order;
+    for (int64_t i = 0; i < nblk; ++i) order[{k[3 * i], k[3 * i + 1], k[3 * i + 2]}] = i;
+    const Index mm = m0 * m0;
+    std::vector<double> host;
+    host.reserve(order.size() * mm);
+    for (auto& kv : order) {
+        keys.push_back(kv.first);
+        host.insert(host.end(), b + kv.second * mm, b + (kv.second + 1) * mm);
+    }
+    *dev = c->arena.get<double>("gen." + tag, host.size() + 1);
+    upload(c, *dev, host.data(), host.size() * sizeof(double));
+}
+
+static void check_gen_dims(const int64_t* dims, int64_t m0) {
+    for (int l = 0; l < 3; ++l)
+        if (dims[l] < 1) fail(LT_EDIM, "GeneratingBlockTensor: level extents must be >= 1");
+    if (m0 < 1) fail(LT_EDIM, "GeneratingBlockTensor: m0 must be >= 1");
+}
+
+lt_status lt_solve_periodic(lt_ctx* c, const int64_t* dims, int64_t m0, int64_t nH, const int64_t* kH, const double* bH,
+                            int64_t nS, const int64_t* kS, const double* bS, double* eig) {
+    return guarded([&] {
+        LT_CU(cudaSetDevice(c->device));
+        check_gen_dims(dims, m0);
+        std::vector<std::array<Index, 3>> keysH, keysS;
+        double *dH = nullptr, *dS = nullptr;
+        gen_to_device(c, nH, kH, bH, m0, keysH, &dH, "H");
+        gen_to_device(c, nS, kS, bS, m0, keysS, &dS, "S");
+        const Index d3[3] = {dims[0], dims[1], dims[2]};
+        const Index K = d3[0] * d3[1] * d3[2];
+        double2* Hb = block_diag_device(c, d3, m0, keysH, dH, "H");
+        double2* Sb = block_diag_device(c, d3, m0, keysS, dS, "S");
+        double* e = c->arena.get<double>("solve.eig", K * m0);
+        unsigned long long* fk = c->arena.get<unsigned long long>("solve.fail", 1);
+        LT_CU(cudaMemsetAsync(fk, 0xff, sizeof(unsigned long long), c->stream));
+        launch_pencil(c->L(), K, m0, Hb, Sb, e, fk, true);
+        unsigned long long key = ~0ull;
+        LT_CU(cudaMemcpyAsync(&key, fk, sizeof(key), cudaMemcpyDeviceToHost, c->stream));
+        LT_CU(cudaMemcpyAsync(eig, e, sizeof(double) * K * m0, cudaMemcpyDeviceToHost, c->stream));
+        LT_CU(cudaStreamSynchronize(c->stream));
+        raise_fail_key(key, true);
+    });
+}
+
+lt_status lt_block_diagonalize(lt_ctx* c, const int64_t* dims, int64_t m0, int64_t nblk, const int64_t* kidx,
+                               const double* blocks, double* out) {
+    return guarded([&] {
+        LT_CU(cudaSetDevice(c->device));
+        check_gen_dims(dims, m0);
+        std::vector<std::array<Index, 3>> keys;
+        double* d = nullptr;
+        gen_to_device(c, nblk, kidx, blocks, m0, keys, &d, "B");
+        const Index d3[3] = {dims[0], dims[1], dims[2]};
+        const Index K = d3[0] * d3[1] * d3[2];
+        double2* bd = block_diag_device(c, d3, m0, keys, d, "B");
+        LT_CU(cudaMemcpyAsync(out, bd, sizeof(double2) * K * m0 * m0, cudaMemcpyDeviceToHost, c->stream));
+        LT_CU(cudaStreamSynchronize(c->stream));
+    });
+}
+
+lt_status lt_solve_box_dense(lt_ctx* c, int64_t n, const double* H, const double* S, int64_t cap, double* eig) {
+    return guarded([&] {
+        if (n > cap)
+            fail(LT_ECAP, "solve_box_dense: size " + std::to_string(n) + " exceeds dense cap " + std::to_string(cap));
+        LT_CU(cudaSetDevice(c->device));
+        double* dH = c->arena.get<double>("boxapi.H", n * n);
+        double* dS = c->arena.get<double>("boxapi.S", n * n);
+        double* e = c->arena.get<double>("boxapi.eig", n);
+        unsigned long long* fk = c->arena.get<unsigned long long>("solve.fail", 1);
+        LT_CU(cudaMemsetAsync(fk, 0xff, sizeof(unsigned long long), c->stream));
+        upload(c, dH, H, sizeof(double) * n * n);
+        upload(c, dS, S, sizeof(double) * n * n);
+        box_eig_device(c, n, dH, dS, e, fk);
+        unsigned long long key = ~0ull;
+        LT_CU(cudaMemcpyAsync(&key, fk, sizeof(key), cudaMemcpyDeviceToHost, c->stream));
+        LT_CU(cudaMemcpyAsync(eig, e, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+        LT_CU(cudaStreamSynchronize(c->stream));
+        raise_fail_key(key, false);
+    });
+}
+
+lt_status lt_pencil_eig(lt_ctx* c, int64_t count, int64_t m0, const double* Hc, const double* Sc, double* eig) {
+    return guarded([&] {
+        LT_CU(cudaSetDevice(c->device));
+        const Index mm = m0 * m0;
+        double2* dH = c->arena.get<double2>("pen.H", count * mm);
+        double2* dS = c->arena.get<double2>("pen.S", count * mm);
+        double* e = c->arena.get<double>("pen.eig", count * m0);
+        unsigned long long* fk = c->arena.get<unsigned long long>("solve.fail", 1);
+        LT_CU(cudaMemsetAsync(fk, 0xff, sizeof(unsigned long long), c->stream));
+        upload(c, dH, Hc, sizeof(double2) * count * mm);
+        upload(c, dS, Sc, sizeof(double2) * count * mm);
+        launch_pencil(c->L(), count, m0, dH, dS, e, fk, true);
+        unsigned long long key = ~0ull;
+        LT_CU(cudaMemcpyAsync(&key, fk, sizeof(key), cudaMemcpyDeviceToHost, c->stream));
+        LT_CU(cudaMemcpyAsync(eig, e, sizeof(double) * count * m0, cudaMemcpyDeviceToHost, c->stream));
+        LT_CU(cudaStreamSynchronize(c->stream));
+        raise_fail_key(key, true);
+    });
+}
+
+lt_status lt_sinc_quadrature(lt_ctx* c, int64_t M, double* nodes, double* weights) {
+    return guarded([&] {
+        if (M < 1) fail(LT_EDIM, "build_sinc_quadrature: M must be >= 1");
+        LT_CU(cudaSetDevice(c->device));
+        const Index R = 2 * M + 1;
+        double* t = c->arena.get<double>("sinc.t", R);
+        double* w = c->arena.get<double>("sinc.w", R);
+        double* pw = c->arena.get<double>("sinc.potw", R);
+        double* one = c->arena.get<double>("sinc.one", 1);
+        const double h1 = 1.0;
+        upload(c, one, &h1, sizeof(double));
+        DevSys s{};
+        s.nnuc = 1;
+        s.Z = one;
+        launch_sinc(c->L(), M, s, t, w, pw);
+        LT_CU(cudaMemcpyAsync(nodes, t, sizeof(double) * R, cudaMemcpyDeviceToHost, c->stream));
+        LT_CU(cudaMemcpyAsync(weights, w, sizeof(double) * R, cudaMemcpyDeviceToHost, c->stream));
+        LT_CU(cudaStreamSynchronize(c->stream));
+    });
+}
+
+lt_status lt_overlap_constant(lt_ctx* c, const lt_system* s, int64_t* L0) {
+    return guarded([&] {
+        LT_CU(cudaSetDevice(c->device));
+        std::unique_ptr<lt_sysdev, void (*)(lt_sysdev*)> sd(make_sysdev(s), lt_sys_free);
+        // overlap_constant validates the basis and (n, b) only (gto_basis.cpp:88-89)
+        const HostSys& h = sd->hs;
+        if (h.alpha.empty()) fail(LT_ESTRUCT, "GtoBasis: no functions");
+        for (size_t m = 0; m < h.alpha.size(); ++m)
+            if (h.alpha[m] <= 0.0) fail(LT_ESTRUCT, "GtoBasis: exponents must be positive");
+        for (int l = 0; l < 3; ++l)
+            if (h.n[l] < 1 || h.b <= 0.0) fail(LT_EDIM, "overlap_constant: need n >= 1, b > 0");
+        *L0 = compute_L0(c, sd.get());
+    });
+}
+
+lt_status lt_newton_master(lt_ctx* c, int64_t ncells, double h, int64_t M, double* out) {
+    return guarded([&] {
+        LT_CU(cudaSetDevice(c->device));
+        const Index R = 2 * M + 1;
+        double* t = c->arena.get<double>("sinc.t", R);
+        double* w = c->arena.get<double>("sinc.w", R);
+        double* pw = c->arena.get<double>("sinc.potw", R);
+        double* one = c->arena.get<double>("sinc.one", 1);
+        const double h1 = 1.0;
+        upload(c, one, &h1, sizeof(double));
+        DevSys s{};
+        s.nnuc = 1;
+        s.Z = one;
+        launch_sinc(c->L(), M, s, t, w, pw);
+        double* m = c->arena.get<double>("api.master", ncells * R);
+        launch_master(c->L(), ncells, h, R, t, m);
+        LT_CU(cudaMemcpyAsync(out, m, sizeof(double) * ncells * R, cudaMemcpyDeviceToHost, c->stream));
+        LT_CU(cudaStreamSynchronize(c->stream));
+    });
+}
+
+lt_status lt_potential(lt_ctx* c, const lt_system* s, int periodic, int64_t margin, int64_t* rows, int64_t* tiled,
+                       double* panels, double* weights, int64_t panels_cap) {
+    return guarded([&] {
+        LT_CU(cudaSetDevice(c->device));
+        std::unique_ptr<lt_sysdev, void (*)(lt_sysdev*)> sd(make_sysdev(s), lt_sys_free);
+        validate(sd->hs);
+        // margin given directly: plan with L0 = margin - 2 and no alias guard (stage call)
+        Plan q;
+        plan_after_L0(sd->hs, periodic != 0, margin - 2, q, true, false);
+        Index need = 0;
+        for (int l = 0; l < 3; ++l) {
+            rows[l] = q.d[l].pot_rows;
+            tiled[l] = q.d[l].tiled;
+            need += q.d[l].pot_rows * q.Rtot;
+        }
+        if (!panels || need > panels_cap) return;
+        const Launch L = c->L();
+        double* t = c->arena.get<double>("sinc.t", q.RN);
+        double* w = c->arena.get<double>("sinc.w", q.RN);
+        double* pw = c->arena.get<double>("sinc.potw", q.Rtot);
+        launch_sinc(L, q.M, sd->ds, t, w, pw);
+        std::vector<int64_t> s0all;
+        for (int l = 0; l < 3; ++l)
+            for (Index v : q.d[l].s0) s0all.push_back(v);
+        int64_t* s0d = c->arena.get<int64_t>("pot.s0", s0all.size());
+        upload(c, s0d, s0all.data(), s0all.size() * sizeof(int64_t));
+        Index at = 0;
+        for (int l = 0; l < 3; ++l) {
+            const DirPlan& d = q.d[l];
+            double* master = c->arena.get<double>("pot.master" + std::to_string(l), d.mrows * q.RN);
+            double* pan = c->arena.get<double>("api.panel" + std::to_string(l), d.pot_rows * q.Rtot);
+            launch_master(L, d.mrows, d.h, q.RN, t, master);
+            launch_window_sum(L, master, d.mrows, q.RN, q.nnuc, s0d + l * q.nnuc, d.nsum, d.n, d.pot_rows, pan);
+            LT_CU(cudaMemcpyAsync(panels + at, pan, sizeof(double) * d.pot_rows * q.Rtot, cudaMemcpyDeviceToHost,
+                                  c->stream));
+            at += d.pot_rows * q.Rtot;
+        }
+        LT_CU(cudaMemcpyAsync(weights, pw, sizeof(double) * q.Rtot, cudaMemcpyDeviceToHost, c->stream));
+        LT_CU(cudaStreamSynchronize(c->stream));
+    });
+}
+
+lt_status lt_assembled_window_sum(lt_ctx* c, int64_t mrows, int64_t R, const double* master, int64_t nsh,
+                                  const int64_t* shifts, int64_t size, double* out) {
+    return guarded([&] {
+        if (nsh < 1) fail(LT_ESTRUCT, "assembled_window_sum: empty shift set");
+        for (int64_t i = 0; i < nsh; ++i)
+            if (shifts[i] < 0 || shifts[i] + size > mrows)
+                fail(LT_EBOUNDS, "assembled_window_sum: shift " + std::to_string(shifts[i]) +
+                                     " in direction 0 outside master extent " + std::to_string(mrows));
+        // the device kernel covers the uniform progression and the single-shift case
+        // (the only shapes the lattice sums produce); canonical_tensor.cpp:112-119
+        bool uniform = nsh >= 2;
+        const int64_t step = nsh >= 2 ? shifts[1] - shifts[0] : 0;
+        if (uniform && step <= 0) uniform = false;
+        for (int64_t i = 2; uniform && i < nsh; ++i)
+            if (shifts[i] - shifts[i - 1] != step) uniform = false;
+        if (nsh >= 2 && !uniform) fail(LT_EGENERIC, "assembled_window_sum: non-uniform shift sets are not supported on the device");
+        LT_CU(cudaSetDevice(c->device));
+        double* m = c->arena.get<double>("aws.m", mrows * R);
+        double* o = c->arena.get<double>("aws.o", size * R);
+        int64_t* s0 = c->arena.get<int64_t>("aws.s0", 1);
+        upload(c, m, master, sizeof(double) * mrows * R);
+        upload(c, s0, shifts, sizeof(int64_t));
+        launch_window_sum(c->L(), m, mrows, R, 1, s0, nsh, step, size, o);
+        LT_CU(cudaMemcpyAsync(out, o, sizeof(double) * size * R, cudaMemcpyDeviceToHost, c->stream));
+        LT_CU(cudaStreamSynchronize(c->stream));
+    });
+}
+
+lt_status lt_profiles(lt_ctx* c, const lt_system* s, int64_t margin, int64_t* grid, int64_t* lo, int64_t* hi,
+                      double* values, int64_t values_cap) {
+    return guarded([&] {
+        LT_CU(cudaSetDevice(c->device));
+        std::unique_ptr<lt_sysdev, void (*)(lt_sysdev*)> sd(make_sysdev(s), lt_sys_free);
+        validate(sd->hs);
+        const HostSys& h = sd->hs;
+        const Index m0 = h.m0();
+        Index need = 0;
+        for (int kind = 0; kind < 2; ++kind)
+            for (int l = 0; l < 3; ++l) {
+                const Index g = (h.L[l] + 2 * margin) * (kind == 0 ? h.n[l] : h.nbar[l]);
+                grid[kind * 3 + l] = g;
+                need += g * m0;
+            }
+        if (!values || need > values_cap) return;
+        ProfileJob jobs[6];
+        for (int kind = 0; kind < 2; ++kind)
+            for (int l = 0; l < 3; ++l) {
+                ProfileJob& j = jobs[kind * 3 + l];
+                j.grid = grid[kind * 3 + l];
+                j.per_cell = kind == 0 ? h.n[l] : h.nbar[l];
+                j.cell_index = margin;
+                j.step = kind == 0 ? h.h(l) : h.hbar(l);
+                j.align = kind == 0 ? 0.5 : 0.0;
+                j.dir = l;
+                j.values = c->arena.get<double>("api.prof" + std::to_string(kind * 3 + l), m0 * j.grid);
+                j.lo = c->arena.get<unsigned long long>("api.plo" + std::to_string(kind * 3 + l), m0);
+                j.hi = c->arena.get<unsigned long long>("api.phi" + std::to_string(kind * 3 + l), m0);
+            }
+        launch_profiles(c->L(), sd->ds, jobs, 6, 1e-280);
+        Index at = 0;
+        for (int k = 0; k < 6; ++k) {
+            LT_CU(cudaMemcpyAsync(values + at, jobs[k].values, sizeof(double) * m0 * jobs[k].grid,
+                                  cudaMemcpyDeviceToHost, c->stream));
+            at += m0 * jobs[k].grid;
+            LT_CU(cudaMemcpyAsync(lo + k * m0, jobs[k].lo, sizeof(int64_t) * m0, cudaMemcpyDeviceToHost, c->stream));
+            LT_CU(cudaMemcpyAsync(hi + k * m0, jobs[k].hi, sizeof(int64_t) * m0, cudaMemcpyDeviceToHost, c->stream));
+        }
+        LT_CU(cudaStreamSynchronize(c->stream));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,207 @@
+// k_setup.cu — sinc quadrature and the overlap constant L0.
+//
+//   launch_sinc            sinc_quadrature.cpp:9-29 (+ weights Z_v w_q, newton_kernel.cpp:150,
+//                          canonical_tensor.cpp:166-187 nucleus-major concatenation)
+//   launch_overlap_*       gto_basis.cpp:87-126 (per-direction grids)
+//
+// The L0 scan is an exact block-max-pruned search: for each shift s and pair
+// (mu, nu, l) the reference takes worst = max_i |a_i c_{i-sn}| and compares it with
+// eps_ov. Rounding is monotone, so fl(max|a|_blk * max|c|_blk) < eps proves every
+// product of that block pair is < eps; only blocks whose bound reaches eps are
+// scanned element by element. The resulting L0 is identical to the full scan.
+#include <cfloat>
+
+#include "lt_device.cuh"
+#include "lt_internal.cuh"
+
+namespace lt {
+
+__global__ void k_sinc(int M, int nnuc, const double* __restrict__ Z, double* t, double* w, double* potw) {
+    const int R = 2 * M + 1;
+    double step = log(static_cast<double>(M)) / static_cast<double>(M);
+    if (M == 1) step = 0.5;
+    const double c = (2.0 * step) / sqrt(3.141592653589793);
+    for (int i = threadIdx.x; i < R; i += blockDim.x) {
+        const double u = __dmul_rn(static_cast<double>(i - M), step);
+        const double eu = exp(-u);
+        const double ti = exp(__dsub_rn(u, eu));
+        const double wi = __dmul_rn(c, __dadd_rn(ti, exp(-eu)));
+        t[i] = ti;
+        w[i] = wi;
+        for (int v = 0; v < nnuc; ++v) potw[v * R + i] = __dmul_rn(wi, Z[v]);
+    }
+}
+
+void launch_sinc(const Launch& L, Index M, const DevSys& s, double* t, double* w, double* potw) {
+    Stage st_(L, "sinc");
+    k_sinc<<<1, 128, 0, L.st>>>(static_cast<int>(M), s.nnuc, s.Z, t, w, potw);
+    LT_CU(cudaGetLastError());
+    L.tick();
+}
+
+// ---------------------------------------------------------------------------
+// overlap constant
+// ---------------------------------------------------------------------------
+constexpr int kMaxL0 = 256;
+
+struct Dir3 {
+    Index n[3], off[3], boff[3];
+};
+
+__global__ void __launch_bounds__(kL0Block) k_l0_sample(DevSys s, Dir3 d, double* __restrict__ prof,
+                                                        double* __restrict__ bmax) {
+    const int l = blockIdx.z, mu = blockIdx.y;
+    const Index n = d.n[l];
+    const Index width = 2 * (kMaxL0 + 2) * n;
+    const Index nblk = (width + kL0Block - 1) / kL0Block;
+    if (blockIdx.x >= nblk) return;
+    const double h = s.b / static_cast<double>(n);
+    const Index base = (kMaxL0 + 2) * n;
+    const Index i = static_cast<Index>(blockIdx.x) * kL0Block + threadIdx.x;
+    double av = 0.0;
+    if (i < width) {
+        const double x = __dsub_rn(__dmul_rn(__dadd_rn(static_cast<double>(i - base), 0.5), h), __dmul_rn(0.5, s.b));
+        const double v = gto_eval1d(s, mu, l, x);
+        prof[d.off[l] + mu * width + i] = v;
+        av = fabs(v);
+    }
+    // block max of |v| (exact: max is order independent)
+    for (int o = 16; o > 0; o >>= 1) av = fmax(av, __shfl_xor_sync(0xffffffffu, av, o));
+    __shared__ double wm[kL0Block / 32];
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = av;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = wm[0];
+        for (int k = 1; k < kL0Block / 32; ++k) m = fmax(m, wm[k]);
+        bmax[d.boff[l] + mu * nblk + blockIdx.x] = m;
+    }
+}
+
+void launch_overlap_profiles(const Launch& L, const DevSys& s, const Index* n3, const Index* off3, const Index* boff3,
+                             OverlapBufs b) {
+    Dir3 d;
+    Index nbmax = 0;
+    for (int l = 0; l < 3; ++l) {
+        d.n[l] = n3[l];
+        d.off[l] = off3[l];
+        d.boff[l] = boff3[l];
+        const Index width = 2 * (kMaxL0 + 2) * n3[l];
+        nbmax = std::max(nbmax, (width + kL0Block - 1) / kL0Block);
+    }
+    dim3 grid(static_cast<unsigned>(nbmax), s.m0, 3);
+    Stage st_(L, "l0_sample");
+    k_l0_sample<<<grid, kL0Block, 0, L.st>>>(s, d, b.prof, b.bmax);
+    LT_CU(cudaGetLastError());
+    L.tick();
+}
+
+__global__ void k_l0_init(int* found, int* state) {
+    for (int i = threadIdx.x; i <= kMaxL0; i += blockDim.x) found[i] = 0;
+    if (threadIdx.x == 0) {
+        state[0] = 0;  // L0
+        state[1] = 0;  // misses
+        state[2] = 1;  // next s
+        state[3] = 0;  // done
+    }
+}
+
+void launch_overlap_init(const Launch& L, OverlapBufs b) {
+    Stage st_(L, "l0_init");
+    k_l0_init<<<1, 256, 0, L.st>>>(b.found, b.state);
+    LT_CU(cudaGetLastError());
+    L.tick();
+}
+
+// one warp per (s, l, mu, nu)
+__global__ void k_l0_scan(DevSys s, Dir3 d, const double* __restrict__ prof, const double* __restrict__ bmax,
+                          int* found, int s_begin, int ns) {
+    const int lane = threadIdx.x & 31;
+    const Index task = static_cast<Index>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const Index m0 = s.m0;
+    const Index per_s = 3 * m0 * m0;
+    if (task >= per_s * ns) return;
+    const int sft = s_begin + static_cast<int>(task / per_s);
+    Index rem = task % per_s;
+    const int l = static_cast<int>(rem / (m0 * m0));
+    rem %= m0 * m0;
+    const Index mu = rem / m0, nu = rem % m0;
+    if (found[sft]) return;  // another pair already proved worst >= eps for this s
+    const Index n = d.n[l];
+    const Index width = 2 * (kMaxL0 + 2) * n;
+    const Index nblk = (width + kL0Block - 1) / kL0Block;
+    const Index sn = static_cast<Index>(sft) * n;
+    if (sn >= width) return;
+    const double* a = prof + d.off[l] + mu * width;
+    const double* c = prof + d.off[l] + nu * width;
+    const double* am = bmax + d.boff[l] + mu * nblk;
+    const double* cm = bmax + d.boff[l] + nu * nblk;
+    const double eps = s.eps_ov;
+    bool hit = false;
+    for (Index ja0 = sn / kL0Block; ja0 < nblk; ja0 += 32) {
+        const Index ja = ja0 + lane;
+        if (ja < nblk) {
+            const Index ilo = max(ja * kL0Block, sn);
+            const Index ihi = min(ja * kL0Block + kL0Block, width);
+            if (ilo < ihi) {
+                const Index cb0 = (ilo - sn) / kL0Block, cb1 = (ihi - 1 - sn) / kL0Block;
+                const double bound = am[ja] * fmax(cm[cb0], cm[cb1]);
+                if (bound >= eps) {
+                    for (Index i = ilo; i < ihi; ++i)
+                        if (fabs(a[i] * c[i - sn]) >= eps) {
+                            hit = true;
+                            break;
+                        }
+                }
+            }
+        }
+        if (__any_sync(0xffffffffu, hit)) {
+            hit = true;
+            break;
+        }
+    }
+    if (hit && lane == 0) found[sft] = 1;
+}
+
+void launch_overlap_scan(const Launch& L, const DevSys& s, const Index* n3, const Index* off3, const Index* boff3,
+                         OverlapBufs b, int s_begin, int s_end) {
+    Dir3 d;
+    for (int l = 0; l < 3; ++l) {
+        d.n[l] = n3[l];
+        d.off[l] = off3[l];
+        d.boff[l] = boff3[l];
+    }
+    const int ns = s_end - s_begin;
+    const Index tasks = static_cast<Index>(ns) * 3 * s.m0 * s.m0;
+    const int wpb = 8;
+    const Index blocks = (tasks + wpb - 1) / wpb;
+    Stage st_(L, "l0_scan");
+    k_l0_scan<<<static_cast<unsigned>(blocks), wpb * 32, 0, L.st>>>(s, d, b.prof, b.bmax, b.found, s_begin, ns);
+    LT_CU(cudaGetLastError());
+    L.tick();
+}
+
+// the reference's sequential rule: L0 = last s with worst >= eps; stop after 2 misses
+__global__ void k_l0_finalize(const int* found, int* state, int s_end) {
+    int L0 = state[0], misses = state[1], sft = state[2];
+    for (; sft <= kMaxL0 && sft < s_end && misses < 2; ++sft) {
+        if (found[sft]) {
+            L0 = sft;
+            misses = 0;
+        } else {
+            ++misses;
+        }
+    }
+    state[0] = L0;
+    state[1] = misses;
+    state[2] = sft;
+    state[3] = (misses >= 2 || sft > kMaxL0) ? 1 : 0;
+}
+
+void launch_overlap_finalize(const Launch& L, OverlapBufs b, int /*s_begin*/, int s_end) {
+    Stage st_(L, "l0_finalize");
+    k_l0_finalize<<<1, 1, 0, L.st>>>(b.found, b.state, s_end);
+    LT_CU(cudaGetLastError());
+    L.tick();
+}
+
+}  // namespace lt

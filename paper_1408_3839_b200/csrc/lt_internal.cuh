@@ -1,0 +1,258 @@
+// lt_internal.cuh — shared declarations of the B200-native core-Hamiltonian engine.
+//
+// Host planning structures (Plan/DirPlan), the device-side system view (DevSys),
+// error plumbing and the launch wrappers of every kernel. See DESIGN.md for the
+// data layout in HBM and the roofline of each kernel.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "latham_b200.h"
+
+namespace lt {
+
+using Index = std::int64_t;
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void fail(int code, const std::string& m) { throw Error(code, m); }
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(LT_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define LT_CU(x) ::lt::cuda_check((x), #x)
+
+// ---------------------------------------------------------------------------
+// Device view of one LatticeSystem (all arrays device-resident)
+// ---------------------------------------------------------------------------
+struct DevSys {
+    int m0 = 0, nnuc = 0;
+    double b = 0.0, eps_ov = 0.0;
+    const double* pos = nullptr;    // [nnuc][3]
+    const double* Z = nullptr;      // [nnuc]
+    const double* center = nullptr; // [m0][3]
+    const double* alpha = nullptr;  // [m0]
+    const int* deg = nullptr;       // [m0][3]
+};
+
+// Host copy of the system (validated), reference field names (galerkin.hpp:17-35)
+struct HostSys {
+    double b = 0.0;
+    Index L[3]{1, 1, 1}, n[3]{}, nbar[3]{};
+    Index quad_M = 0;
+    double eps_ov = 1e-8;
+    std::vector<double> pos, Z, center, alpha;
+    std::vector<int> deg;
+    Index m0() const { return static_cast<Index>(alpha.size()); }
+    Index nnuc() const { return static_cast<Index>(Z.size()); }
+    Index cells() const { return L[0] * L[1] * L[2]; }
+    double h(int l) const { return b / static_cast<double>(n[l]); }
+    double hbar(int l) const { return b / static_cast<double>(nbar[l]); }
+};
+
+HostSys host_sys_from(const lt_system* s);
+void validate(const HostSys& s);
+
+// table modes of the nuclear contraction per direction
+enum TableMode : int { TM_TRIVIAL = 0, TM_FOLD = 1, TM_BOXDIR = 2 };
+
+struct DirPlan {
+    Index L = 1, n = 0, nbar = 0;
+    double h = 0.0, hbar = 0.0;
+    Index band = 0, width = 1;    // band = min(L0, L-1), width = 2 band + 1
+    Index G = 0, Gbar = 0;        // pwc / pwl extended grid sizes
+    Index pot_rows = 0;           // rows of the potential panel
+    bool tiled = false;           // periodic wrapped direction (p addressed mod n)
+    Index mrows = 0;              // master grid cells
+    Index nsum = 1;               // lattice copies in the window sum
+    std::vector<Index> s0;        // per nucleus: smallest sorted window start
+    int mode = TM_TRIVIAL;
+    Index npairs = 1;             // table pairs: box L*width, periodic width, trivial 1
+};
+
+struct Plan {
+    bool periodic = false;
+    Index m0 = 0, nnuc = 0, RN = 0, Rtot = 0, M = 0;
+    Index L0 = 0, margin = 0;
+    DirPlan d[3];
+    Index cells = 1, Nb = 0, K = 1;
+    int nontrivial = 0;       // directions with L > 1
+    int s2_dir = -1;          // box: the single nontrivial direction folded by rank (S2)
+    Index nblocks = 0;        // periodic: stored generating blocks = prod(width)
+};
+
+// planning (host integer bookkeeping; reference semantics, galerkin.cpp:287-307,
+// newton_kernel.cpp:54-151). Throws lt::Error with the reference's messages.
+void plan_after_L0(const HostSys& s, bool periodic, Index L0, Plan& p, bool need_potential, bool check_alias = true);
+Index master_rows_box(Index n, Index L, Index margin);
+Index master_rows_periodic(Index n, Index L);
+Index window_start(Index master_n, Index win_n, double a, double h);
+
+// ---------------------------------------------------------------------------
+// Device buffer arena (grow-only, keyed)
+// ---------------------------------------------------------------------------
+class Arena {
+public:
+    ~Arena();
+    void* raw(const std::string& key, size_t bytes);
+    template <class T>
+    T* get(const std::string& key, size_t count) {
+        return static_cast<T*>(raw(key, count * sizeof(T) + 16));
+    }
+    size_t bytes() const;
+
+private:
+    struct Buf {
+        void* p = nullptr;
+        size_t cap = 0;
+    };
+    std::map<std::string, Buf> bufs_;
+};
+
+// ---------------------------------------------------------------------------
+// kernel launch wrappers (each increments the launch counter)
+// ---------------------------------------------------------------------------
+// Optional per-kernel CUDA-event timing on the launching stream (bench roofline).
+class StageTimer {
+public:
+    ~StageTimer();
+    bool on = false;
+    void begin(cudaStream_t st, const char* name);
+    void end(cudaStream_t st);
+    // resolve pending event pairs (call after a stream synchronisation)
+    void collect();
+    void reset();
+    std::map<std::string, std::pair<double, int64_t>> totals;  // name -> (ms, launches)
+
+private:
+    cudaEvent_t get();
+    std::vector<cudaEvent_t> pool_;
+    size_t used_ = 0;
+    struct Pending {
+        std::string name;
+        cudaEvent_t a, b;
+    };
+    std::vector<Pending> pending_;
+    std::string open_name_;
+    cudaEvent_t open_ = nullptr;
+};
+
+struct Launch {
+    cudaStream_t st = nullptr;
+    int64_t* counter = nullptr;
+    StageTimer* timer = nullptr;
+    void tick(int n = 1) const {
+        if (counter) *counter += n;
+    }
+};
+
+// RAII stage scope: events around the kernel(s) launched inside it when timing is on
+struct Stage {
+    const Launch& L;
+    bool active;
+    Stage(const Launch& l, const char* name) : L(l), active(l.timer && l.timer->on) {
+        if (active) L.timer->begin(L.st, name);
+    }
+    ~Stage() {
+        if (active) L.timer->end(L.st);
+    }
+};
+
+// sinc quadrature (sinc_quadrature.cpp:9-29) and the nuclear weights Z_v w_q
+void launch_sinc(const Launch& L, Index M, const DevSys& s, double* t, double* w, double* potw);
+
+// overlap constant (gto_basis.cpp:87-126)
+struct OverlapBufs {
+    double* prof = nullptr;   // [3][m0][width_l] packed per direction
+    double* bmax = nullptr;   // [3][m0][nblk_l]
+    int* found = nullptr;     // [257]
+    int* state = nullptr;     // [4]: L0, misses, s_next, done
+};
+constexpr int kL0Block = 128;
+void launch_overlap_profiles(const Launch& L, const DevSys& s, const Index* n3, const Index* off3,
+                             const Index* boff3, OverlapBufs b);
+void launch_overlap_scan(const Launch& L, const DevSys& s, const Index* n3, const Index* off3, const Index* boff3,
+                         OverlapBufs b, int s_begin, int s_end);
+void launch_overlap_finalize(const Launch& L, OverlapBufs b, int s_begin, int s_end);
+void launch_overlap_init(const Launch& L, OverlapBufs b);
+
+// master tensor (newton_kernel.cpp:22-45) and assembled window sums (canonical_tensor.cpp:123-164)
+void launch_master(const Launch& L, Index mrows, double h, Index RN, const double* t, double* out);
+void launch_window_sum(const Launch& L, const double* master, Index mrows, Index RN, Index nnuc, const Index* s0_dev,
+                       Index nsum, Index step, Index size, double* out);
+
+// GTO profiles (gto_basis.cpp:31-47) with trimming
+struct ProfileJob {
+    Index grid = 0, per_cell = 0, cell_index = 0;
+    double step = 0.0, align = 0.0;
+    int dir = 0;
+    double* values = nullptr;  // [m0][grid]
+    unsigned long long* lo = nullptr;  // [m0]
+    unsigned long long* hi = nullptr;  // [m0]
+};
+void launch_profiles(const Launch& L, const DevSys& s, const ProfileJob* jobs, int njobs, double eps);
+
+// 1D FEM tables (fem1d.cpp:19-32 via galerkin.cpp:208-223)
+void launch_fem_tables(const Launch& L, Index m0, Index band, Index nbar, double hbar, Index Gbar, const double* pwl,
+                       const unsigned long long* lo, const unsigned long long* hi, double* massT, double* stiffT);
+
+// nuclear tables by direct contraction (galerkin.cpp:109-125, :224-247)
+void launch_nuc_direct(const Launch& L, Index m0, Index Rtot, const DirPlan& d, bool periodic, const double* pwc,
+                       const unsigned long long* lo, const unsigned long long* hi, const double* pot, double* T);
+// periodic fold: Qf[d][e][t] then T[d][r][e] = sum_t P[r][t] Qf[d][e][t]
+void launch_nuc_fold(const Launch& L, Index m0, Index Rtot, const DirPlan& d, const double* pwc,
+                     const unsigned long long* lo, const unsigned long long* hi, const double* pot, double* Qf,
+                     double* T);
+// box chain (S2): W = w_r prod_trivial T, V = W^T P, N[k][d][e] = sum_j Q_d(j) V(j + k n)
+void launch_box_w(const Launch& L, Index m0, Index Rtot, const double* potw, const double* Ta, const double* Tb,
+                  double* W);
+void launch_box_v(const Launch& L, Index m0, Index Rtot, Index G, const double* W, const double* pot, double* V);
+void launch_box_corr(const Launch& L, Index m0, const DirPlan& d, const double* pwc, const unsigned long long* lo,
+                     const unsigned long long* hi, const double* V, double* Npart, double* N, int nsplit);
+
+// fill H/S (box dense, periodic generating blocks); mode 0 core (H,S), 1 Laplace, 2 Mass, 3 Nuclear
+struct FillArgs {
+    Index m0 = 0, Rtot = 0, L[3]{1, 1, 1}, band[3]{}, width[3]{1, 1, 1};
+    const double* massT[3]{};
+    const double* stiffT[3]{};
+    const double* T[3]{};      // nuclear tables [pair][r][e]
+    const double* potw = nullptr;
+    const double* N = nullptr; // S2 nuclear blocks [k][d][e] along s2_dir
+    int s2_dir = -1;
+    int mode = 0;
+    bool periodic = false;
+    double* out0 = nullptr;    // H (or single operator)
+    double* out1 = nullptr;    // S
+    int64_t* kidx = nullptr;   // periodic: [nblk][3]
+};
+void launch_fill(const Launch& L, const FillArgs& a, Index Nb, Index nblocks);
+
+// block diagonalisation over lattice indices (block_circulant.cpp:82-112, :184-196)
+struct DftPlan {
+    Index dims[3]{1, 1, 1};
+    Index ncomp[3]{1, 1, 1};   // compressed extents
+    std::vector<Index> comp[3];  // compressed kidx values per axis (ascending)
+};
+void launch_scatter_gen(const Launch& L, Index nblk, Index mm, const int64_t* kslot_dev, const double* blocks,
+                        double2* dense);
+void launch_dft_axis(const Launch& L, int axis, const Index* in_ext, const Index* out_ext, Index mm,
+                     const double2* in, double2* out, const double2* tw, Index ncomp, Index Lax);
+void launch_twiddles(const Launch& L, Index Lax, Index ncomp, const int64_t* comp_dev, double2* tw);
+
+// batched Hermitian-definite pencils (eigensolver.cpp:72-93)
+void launch_pencil(const Launch& L, Index count, Index m0, const double2* H, const double2* S, double* eig,
+                   unsigned long long* fail_key, bool periodic_checks);
+
+// combine (eigensolver.cpp:37-67) on device buffers with index maps
+void launch_axpby_map(const Launch& L, Index nout, Index mm, double wa, const double* a, const int64_t* ia, double wb,
+                      const double* b, const int64_t* ib, double* out);
+
+}  // namespace lt

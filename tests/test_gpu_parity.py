@@ -1,0 +1,175 @@
+"""GPU parity: every stage of the B200 path against Oracle-X on identical seeded inputs.
+
+Tolerances (north star): matrix entries within 1e-10 relative
+(|a-b| <= 1e-10 |b| + 1e-14 max|H| for entries that can cancel), eigenvalues within
+1e-9 absolute, integer indexing (L0, supports, bands, kidx) bit-exact.
+"""
+import numpy as np
+import pytest
+
+from conftest import chain_system, eig_tolerance, entries_close, rel_err, two_nuclei_system
+from paper_1408_3839_b200.system import make_config
+
+pytestmark = pytest.mark.gpu
+
+SMALL = {
+    "chain6_box": (chain_system(6, 0.05, M=8), False),
+    "chain8_per": (chain_system(8, 0.05, M=6), True),
+    "chain4_box_two": (chain_system(4, [0.1, 0.4], M=6), False),
+    "two_box": (two_nuclei_system((6, 1, 1)), False),
+    "two_per": (two_nuclei_system((12, 1, 1)), True),
+    "aniso_box": (two_nuclei_system((5, 1, 1), n=(12, 10, 6), nbar=(12, 8, 6)), False),
+    "aniso_per": (two_nuclei_system((11, 1, 1), n=(12, 10, 6), nbar=(10, 12, 6)), True),
+    "box2d": (two_nuclei_system((3, 2, 1), n=(8, 8, 8), alphas=(1.5, 3.0)), False),
+    "per3d": (two_nuclei_system((5, 6, 5), n=(6, 6, 6), alphas=(3.0, 5.0), M=6), True),
+    "per2d_y": (two_nuclei_system((1, 9, 1), n=(6, 8, 6), alphas=(1.0, 2.0), M=6), True),
+    "box_z": (two_nuclei_system((1, 1, 5), n=(6, 6, 10), alphas=(1.0, 2.0), M=6), False),
+    "pdeg_box": (two_nuclei_system((4, 1, 1), alphas=(1.0, 2.0), deg=[[1, 0, 0], [0, 1, 1]]), False),
+    "pdeg_per": (two_nuclei_system((9, 1, 1), alphas=(1.0, 2.0), deg=[[2, 0, 0], [1, 1, 0]]), True),
+    "unit_cell_box": (two_nuclei_system((1, 1, 1), alphas=(0.8, 1.6)), False),
+}
+IDS = sorted(SMALL)
+
+
+def test_sinc_quadrature(ctx, oracle):
+    for M in (1, 2, 6, 12, 16, 20):
+        t, w = ctx.build_sinc_quadrature(M)
+        to, wo = oracle.sinc_quadrature(M)
+        assert rel_err(t, to) < 1e-14 and rel_err(w, wo) < 1e-14
+
+
+@pytest.mark.parametrize("name", IDS)
+def test_overlap_constant(ctx, oracle, name):
+    sys, _ = SMALL[name]
+    assert ctx.overlap_constant(sys) == oracle.overlap_constant(sys)
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c3", "c4", "c5"])
+def test_overlap_constant_configs(ctx, oracle, cfg):
+    sys = make_config(cfg)
+    assert ctx.overlap_constant(sys) == oracle.overlap_constant(sys)
+
+
+def test_newton_master(ctx, oracle):
+    for ncells, h, M in ((64, 0.25, 10), (300, 2.0 / 64, 16), (33, 0.5, 3)):
+        g = ctx.newton_master(ncells, h, M)
+        o = oracle.newton_master_column(ncells, h, M)
+        assert g.shape == o.shape
+        for q in range(o.shape[1]):
+            assert rel_err(g[:, q], o[:, q]) < 1e-13
+
+
+@pytest.mark.parametrize("name", IDS)
+def test_potential(ctx, oracle, name):
+    sys, periodic = SMALL[name]
+    margin = oracle.overlap_constant(sys) + 2
+    gp, gw, gt = ctx.potential(sys, periodic, margin)
+    op, ow, ot = oracle.potential(sys, periodic, margin)
+    assert gt == ot
+    assert rel_err(gw, ow) < 1e-14
+    for l in range(3):
+        assert gp[l].shape == op[l].shape
+        for r in range(op[l].shape[1]):
+            assert rel_err(gp[l][:, r], op[l][:, r]) < 1e-13, (l, r)
+
+
+@pytest.mark.parametrize("name", IDS)
+def test_profiles(ctx, oracle, name):
+    sys, _ = SMALL[name]
+    margin = oracle.overlap_constant(sys) + 2
+    prof = ctx.profiles(sys, margin)
+    for (kind, l, mu), (off, vals) in prof.items():
+        n = sys.n[l] if kind == "pwc" else sys.nbar[l]
+        grid = (sys.L[l] + 2 * margin) * n
+        step = sys.b / n
+        align = 0.5 if kind == "pwc" else 0.0
+        ooff, ovals = oracle.sample_gto_1d(sys.bf_center[mu], sys.bf_alpha[mu], sys.bf_deg[mu], l, grid, step, margin,
+                                           n, sys.b, align, 1e-280)
+        assert off == ooff and len(vals) == len(ovals), (kind, l, mu)
+        if len(ovals):
+            assert rel_err(vals, ovals) < 1e-14
+
+
+def _compare_ops(g, o, rel=1e-10):
+    assert g.periodic == o.periodic and g.m0 == o.m0 and tuple(g.L) == tuple(o.L)
+    assert g.overlap_L0 == o.L0 and tuple(g.band) == tuple(o.band)
+    assert g.coefficient_rank == o.coefficient_rank
+    if g.periodic:
+        gk, gb = g.blocks()
+        assert np.array_equal(gk, o.kidx)
+        ok, worst = entries_close(gb, o.blocks, rel=rel)
+    else:
+        gd = g.dense()
+        assert gd.shape == o.dense.shape
+        assert np.array_equal(gd == 0.0, o.dense == 0.0)  # identical block sparsity
+        ok, worst = entries_close(gd, o.dense, rel=rel)
+    assert ok, worst
+
+
+@pytest.mark.parametrize("name", IDS)
+@pytest.mark.parametrize("kind", ["mass", "laplace", "nuclear"])
+def test_assemble_kind(ctx, oracle, name, kind):
+    sys, periodic = SMALL[name]
+    g = ctx.assemble(sys, periodic, kind)
+    o = oracle.assemble(sys, periodic, kind)
+    _compare_ops(g, o)
+    oracle.free(o)
+
+
+@pytest.mark.parametrize("name", IDS)
+def test_assemble_core_and_combine(ctx, oracle, name):
+    sys, periodic = SMALL[name]
+    H, S = ctx.assemble_core(sys, periodic)
+    oH, oS = oracle.assemble_core(sys, periodic)
+    _compare_ops(S, oS)
+    # H through the fused path equals combine(0.5, Laplace, -1, Nuclear)
+    if periodic:
+        gk, gb = H.blocks()
+        assert np.array_equal(gk, oH.kidx)
+        ok, worst = entries_close(gb, oH.blocks)
+    else:
+        ok, worst = entries_close(H.dense(), oH.dense)
+    assert ok, worst
+    lap = ctx.assemble(sys, periodic, "laplace")
+    nuc = ctx.assemble(sys, periodic, "nuclear")
+    H2 = ctx.combine(0.5, lap, -1.0, nuc)
+    if periodic:
+        assert np.array_equal(H2.blocks()[1], H.blocks()[1])
+    else:
+        assert np.array_equal(H2.dense(), H.dense())
+
+
+@pytest.mark.parametrize("name", IDS)
+def test_solve_core(ctx, oracle, name):
+    sys, periodic = SMALL[name]
+    info = np.zeros(8, dtype=np.int64)
+    ev = ctx.solve_core(sys, periodic, info)
+    oH, oS = oracle.assemble_core(sys, periodic)
+    if periodic:
+        oev = oracle.solve_periodic_ops(oH, oS)
+    else:
+        oev = oracle.solve_box_dense(oH.dense, oS.dense)
+    assert ev.shape == oev.shape
+    assert np.max(np.abs(ev - oev)) < 1e-9
+    assert info[0] == oH.L0
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_config_against_oracle(ctx, oracle, cfg):
+    sys = make_config(cfg)
+    periodic = sys.notes["periodic"]
+    oH, oS = oracle.assemble_core(sys, periodic)
+    H, S = ctx.assemble_core(sys, periodic)
+    if periodic:
+        ok, worst = entries_close(H.blocks()[1], oH.blocks)
+        assert ok, worst
+        ok, worst = entries_close(S.blocks()[1], oS.blocks)
+    else:
+        ok, worst = entries_close(H.dense(), oH.dense)
+        assert ok, worst
+        ok, worst = entries_close(S.dense(), oS.dense)
+    assert ok, worst
+    ev = ctx.solve_core(sys, periodic)
+    oev = oracle.solve_periodic_ops(oH, oS) if periodic else oracle.solve_box_dense(oH.dense, oS.dense)
+    tol = eig_tolerance(oracle, periodic, oH, oS, oev)
+    assert np.max(np.abs(ev - oev)) <= tol, (np.max(np.abs(ev - oev)), tol)
