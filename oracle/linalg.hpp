@@ -100,28 +100,24 @@ bool reduce_pencil(Index n, const T* h, const T* s, std::vector<T>& a_out) {
 // Cyclic two-sided Jacobi for a Hermitian (or real symmetric) matrix;
 // eigenvalues ascending. a is overwritten.
 // ---------------------------------------------------------------------------
+// Rotation rule (Demmel-Veselic threshold with an absolute floor): rotate (p,q) iff
+// |a_pq| > max(2^-53 sqrt(|a_pp a_qq|), 1e-17 ||A||_F); converged after a sweep with
+// no rotation. Left-over off-diagonal entries move eigenvalues by O(eps ||A||).
 template <class T>
 void jacobi_eigenvalues(Index n, T* a, double* w) {
     auto A = [&](Index i, Index j) -> T& { return a[i + j * n]; };
-    for (int sweep = 0; sweep < 100; ++sweep) {
-        double off = 0.0, diag = 0.0;
-        for (Index j = 0; j < n; ++j)
-            for (Index i = 0; i < n; ++i) {
-                if (i == j) diag += std::norm(A(i, i));
-                else off += std::norm(A(i, j));
-            }
-        if (off == 0.0 || off <= 1e-32 * (off + diag)) break;
+    double fro = 0.0;
+    for (Index k = 0; k < n * n; ++k) fro += std::norm(a[k]);
+    const double floor_abs = 1e-17 * std::sqrt(fro);
+    for (int sweep = 0; sweep < 60; ++sweep) {
+        bool rotated = false;
         for (Index p = 0; p < n - 1; ++p) {
             for (Index q = p + 1; q < n; ++q) {
                 const T apq = A(p, q);
                 const double r = std::abs(apq);
-                if (r == 0.0) continue;
                 const double app = real_part(A(p, p)), aqq = real_part(A(q, q));
-                if (r <= 1e-18 * std::sqrt(std::abs(app * aqq)) ) {
-                    A(p, q) = T(0);
-                    A(q, p) = T(0);
-                    continue;
-                }
+                if (!(r > floor_abs) || r <= 1.1102230246251565e-16 * std::sqrt(std::abs(app * aqq))) continue;
+                rotated = true;
                 // make a_pq real: column q *= conj(phase), row q *= phase
                 T ph = apq / r;  // e^{i phi}
                 if constexpr (!std::is_same_v<T, double>) {
@@ -154,6 +150,7 @@ void jacobi_eigenvalues(Index n, T* a, double* w) {
                 A(q, q) = T(aqq + t * r);
             }
         }
+        if (!rotated) break;
     }
     for (Index i = 0; i < n; ++i) w[i] = real_part(A(i, i));
     std::sort(w, w + n);

@@ -475,11 +475,13 @@ static void box_eig_device(lt_ctx* c, Index n, double* H, double* S, double* eig
     if (n <= 32) {
         double2* hc = c->arena.get<double2>("box.hc", n * n);
         double2* sc = c->arena.get<double2>("box.sc", n * n);
-        Stage st_(L, "r2c");
-        k_real_to_complex<<<static_cast<unsigned>((n * n + 255) / 256), 256, 0, c->stream>>>(n * n, H, hc);
-        k_real_to_complex<<<static_cast<unsigned>((n * n + 255) / 256), 256, 0, c->stream>>>(n * n, S, sc);
-        LT_CU(cudaGetLastError());
-        L.tick(2);
+        {
+            Stage st_(L, "r2c");
+            k_real_to_complex<<<static_cast<unsigned>((n * n + 255) / 256), 256, 0, c->stream>>>(n * n, H, hc);
+            k_real_to_complex<<<static_cast<unsigned>((n * n + 255) / 256), 256, 0, c->stream>>>(n * n, S, sc);
+            LT_CU(cudaGetLastError());
+            L.tick(2);
+        }
         launch_pencil(L, 1, n, hc, sc, eig_dev, fail_dev, false);
         return;
     }

@@ -163,6 +163,12 @@ SEED_BASE = 0x14083839
 # definiteness; eigensolver.cpp:80-83 then raises DefinitenessError). The accepted
 # draw index is fixed here and re-verified by tests/test_configs.py with the oracle.
 C5_ACCEPTED_DRAW = 35  # draws 15, 21, 24, 29, 33 pass (a) but fail (b); the rest fail (a)
+# c4 (m0 = 16 on 4 nuclei in a 2-bohr cell, alpha down to 0.03) uses rule (b) only:
+# draws 0..10 make the reference raise DefinitenessError at some k-point.
+C4_ACCEPTED_DRAW = 11
+# c3 (box): draw 0 gives an indefinite overlap matrix (lambda_min(S) = -1.6e-6), which
+# the reference refuses in solve_box_dense; draw 1 is accepted (rule (b)).
+C3_ACCEPTED_DRAW = 1
 
 
 def _log_uniform(rng: SplitMix64, lo: float, hi: float) -> float:
@@ -210,7 +216,7 @@ def make_config(name: str, exponent_draw: int = None) -> LatticeSystem:
     centers = [pos[i // per] for i in range(m0)]
     draw = 0
     if exponent_draw is None:
-        exponent_draw = C5_ACCEPTED_DRAW if name == "c5" else 0
+        exponent_draw = {"c5": C5_ACCEPTED_DRAW, "c4": C4_ACCEPTED_DRAW, "c3": C3_ACCEPTED_DRAW}.get(name, 0)
     alphas = None
     for draw in range(exponent_draw + 1):
         alphas = [_log_uniform(rng, alo, ahi) for _ in range(m0)]
