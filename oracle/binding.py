@@ -84,8 +84,9 @@ class Oracle:
         self._dense.argtypes = [ctypes.c_void_p, _dp]
         self._blocks = f("op_blocks")
         self._blocks.argtypes = [ctypes.c_void_p, _ip, _dp]
-        self._sep = f("op_separable")
-        self._sep.argtypes = [ctypes.c_void_p, _dp]
+        self._sep = getattr(lib, p + "op_separable", None)
+        if self._sep is not None:
+            self._sep.argtypes = [ctypes.c_void_p, _dp]
         self._solve_ops = f("solve_periodic_ops")
         self._solve_ops.argtypes = [ctypes.c_void_p, ctypes.c_void_p, _i64, _dp]
         self._solve_fact = getattr(lib, p + "solve_periodic_factorized_ops", None)

@@ -44,34 +44,40 @@ inline T conj_of(const T& v) {
     else return std::conj(v);
 }
 
+// Right-looking, column-oriented (contiguous column updates); the pivot x is the
+// Schur-complement diagonal, tested like Eigen's llt_inplace (x <= 0 fails).
 template <class T>
 bool cholesky_lower(Index n, T* a) {
     auto A = [&](Index i, Index j) -> T& { return a[i + j * n]; };
     for (Index k = 0; k < n; ++k) {
-        double x = real_part(A(k, k));
-        for (Index j = 0; j < k; ++j) x -= std::norm(A(k, j));
+        const double x = real_part(A(k, k));
         if (!(x > 0.0)) return false;
         const double dkk = std::sqrt(x);
         A(k, k) = T(dkk);
-        for (Index i = k + 1; i < n; ++i) {
-            T s = A(i, k);
-            for (Index j = 0; j < k; ++j) s -= A(i, j) * conj_of(A(k, j));
-            A(i, k) = s / dkk;
+        const double inv = 1.0 / dkk;
+        T* ck = &A(0, k);
+        for (Index i = k + 1; i < n; ++i) ck[i] *= inv;
+        for (Index j = k + 1; j < n; ++j) {
+            const T f = conj_of(ck[j]);
+            T* cj = &A(0, j);
+            for (Index i = j; i < n; ++i) cj[i] -= ck[i] * f;
         }
         for (Index j = k + 1; j < n; ++j) A(k, j) = T(0);
     }
     return true;
 }
 
-// Solve L X = B in place (B: n x m column-major), L lower from cholesky_lower.
+// Solve L X = B in place (B: n x m column-major), L lower from cholesky_lower
+// (column-oriented forward substitution).
 template <class T>
 void lower_solve(Index n, const T* l, Index m, T* b) {
     for (Index c = 0; c < m; ++c) {
         T* x = b + c * n;
-        for (Index i = 0; i < n; ++i) {
-            T s = x[i];
-            for (Index j = 0; j < i; ++j) s -= l[i + j * n] * x[j];
-            x[i] = s / l[i + i * n];
+        for (Index j = 0; j < n; ++j) {
+            x[j] /= l[j + j * n];
+            const T xj = x[j];
+            const T* lj = l + j * n;
+            for (Index i = j + 1; i < n; ++i) x[i] -= lj[i] * xj;
         }
     }
 }
@@ -164,7 +170,9 @@ void jacobi_eigenvalues(Index n, T* a, double* w) {
 inline void symmetric_eigenvalues(Index n, double* a, double* w) {
     if (n <= 0) return;
     if (n <= 48) { jacobi_eigenvalues<double>(n, a, w); return; }
-    auto A = [&](Index i, Index j) -> double& { return a[i + j * n]; };
+    // symmetric input: address the transposed storage so the row sweeps of the
+    // (row-oriented) Householder scheme run over contiguous memory
+    auto A = [&](Index i, Index j) -> double& { return a[j + i * n]; };
     std::vector<double> d(n), e(n, 0.0);
     // Householder: annihilate row i left of the subdiagonal, i = n-1 .. 1
     for (Index i = n - 1; i > 0; --i) {

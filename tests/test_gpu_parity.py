@@ -172,4 +172,4 @@ def test_config_against_oracle(ctx, oracle, cfg):
     ev = ctx.solve_core(sys, periodic)
     oev = oracle.solve_periodic_ops(oH, oS) if periodic else oracle.solve_box_dense(oH.dense, oS.dense)
     tol = eig_tolerance(oracle, periodic, oH, oS, oev)
-    assert np.max(np.abs(ev - oev)) <= tol, (np.max(np.abs(ev - oev)), tol)
+    assert np.all(np.abs(ev - oev) <= tol), np.max(np.abs(ev - oev) / tol)
