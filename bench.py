@@ -172,15 +172,24 @@ def work_model(ctx, sysobj, periodic, L0):
     return out
 
 
+def pick_cpu_impl(sysobj):
+    """The reference's own code (Oracle-R) when the system is expressible in its API
+    (isotropic grid), else Oracle-X, which is bit-identical to it on isotropic grids."""
+    from oracle.binding import oracle, reference
+    iso = len(set(sysobj.n)) == 1 and len(set(sysobj.nbar)) == 1
+    ref = reference() if iso else None
+    if ref is not None:
+        return ref, "reference"
+    return oracle(), "port"
+
+
 def run_reference_arm(args, world, rank):
     """--impl reference: the reference algorithm on this host's CPU cores."""
     if rank != 0:
         return 0
     from oracle.binding import oracle, reference
-    ref = reference()
-    impl = ref if ref is not None else oracle()
-    kind = "reference" if ref is not None else "port"
     sysobj = make_config(args.workload)
+    impl, kind = pick_cpu_impl(sysobj)
     periodic = sysobj.notes["periodic"]
     threads = os.cpu_count() or 1
 
@@ -218,10 +227,8 @@ def run_reference_arm(args, world, rank):
 
 def cpu_baseline(workload, budget_s):
     from oracle.binding import oracle, reference
-    ref = reference()
-    impl = ref if ref is not None else oracle()
-    kind = "reference" if ref is not None else "port"
     sysobj = make_config(workload)
+    impl, kind = pick_cpu_impl(sysobj)
     periodic = sysobj.notes["periodic"]
     threads = os.cpu_count() or 1
     times = []

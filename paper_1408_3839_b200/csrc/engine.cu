@@ -40,6 +40,7 @@ void* Arena::raw(const std::string& key, size_t bytes) {
         cap = cap + cap / 4;
         LT_CU(cudaMalloc(&b.p, cap));
         b.cap = cap;
+        ++gen_;
     }
     return b.p;
 }
@@ -104,6 +105,11 @@ struct lt_ctx {
     Arena arena;
     int64_t launches = 0;
     StageTimer timer;
+    // CUDA graph of the post-L0 launch sequence (captured on the second identical call)
+    bool graphs = true;
+    cudaGraphExec_t gexec = nullptr;
+    std::vector<int64_t> gkey, gseen;
+    int64_t glaunches = 0;
     Launch L() { return Launch{stream, &launches, &timer}; }
 };
 
@@ -149,14 +155,23 @@ static void upload(lt_ctx* c, void* dst, const void* src, size_t bytes) {
     if (bytes) LT_CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream));
 }
 
-static lt_sysdev* make_sysdev(const lt_system* s) {
+// pack the system arrays into one device block; dst (optional) is a caller-owned buffer
+// of at least sysdev_bytes(); the H2D copy is stream-ordered on `st`
+static size_t sysdev_bytes(const HostSys& h) {
+    const size_t m0 = h.alpha.size(), nn = h.Z.size();
+    size_t bytes = 16;
+    for (size_t nb : {3 * nn * 8, nn * 8, 3 * m0 * 8, m0 * 8, 3 * m0 * 4}) bytes += (nb + 15) / 16 * 16;
+    return bytes;
+}
+
+static lt_sysdev* make_sysdev(const lt_system* s, void* dst = nullptr, cudaStream_t st = nullptr) {
     auto sd = std::make_unique<lt_sysdev>();
     sd->hs = host_sys_from(s);
     const HostSys& h = sd->hs;
     const size_t m0 = h.alpha.size(), nn = h.Z.size();
-    size_t bytes = 16;
-    for (size_t nb : {3 * nn * 8, nn * 8, 3 * m0 * 8, m0 * 8, 3 * m0 * 4}) bytes += (nb + 15) / 16 * 16;
-    LT_CU(cudaMalloc(&sd->mem, bytes));
+    const size_t bytes = sysdev_bytes(h);
+    if (dst) sd->mem = dst;
+    else LT_CU(cudaMalloc(&sd->mem, bytes));
     char* p = static_cast<char*>(sd->mem);
     std::vector<char> host(bytes, 0);
     size_t at = 0;
@@ -175,7 +190,8 @@ static lt_sysdev* make_sysdev(const lt_system* s) {
     sd->ds.center = static_cast<const double*>(put(h.center.data(), 3 * m0 * 8));
     sd->ds.alpha = static_cast<const double*>(put(h.alpha.data(), m0 * 8));
     sd->ds.deg = static_cast<const int*>(put(h.deg.data(), 3 * m0 * 4));
-    LT_CU(cudaMemcpy(sd->mem, host.data(), at, cudaMemcpyHostToDevice));
+    if (dst) LT_CU(cudaMemcpyAsync(sd->mem, host.data(), at, cudaMemcpyHostToDevice, st));
+    else LT_CU(cudaMemcpy(sd->mem, host.data(), at, cudaMemcpyHostToDevice));
     return sd.release();
 }
 
@@ -228,21 +244,60 @@ struct AsmOut {
 
 enum Need : int { NEED_MS = 1, NEED_NUC = 2 };
 
+
 struct Work {
-    double *t, *w, *potw;
-    double* pot[3];
-    double* pwc[3];
-    double* pwl[3];
-    unsigned long long *pwc_lo[3], *pwc_hi[3], *pwl_lo[3], *pwl_hi[3];
-    double *massT[3], *stiffT[3], *T[3];
+    double *t = nullptr, *w = nullptr, *potw = nullptr;
+    double* pot[3]{};
+    double* pwc[3]{};
+    double* pwl[3]{};
+    unsigned long long *pwc_lo[3]{}, *pwc_hi[3]{}, *pwl_lo[3]{}, *pwl_hi[3]{};
+    double *massT[3]{}, *stiffT[3]{}, *T[3]{};
     double* N = nullptr;
 };
 
+// Directions whose every input is bitwise identical (grid counts, lattice extent, every
+// nucleus and basis-centre coordinate, monomial degrees) produce bitwise identical
+// panels, profiles and tables; they are computed once (src[l] = first such direction).
+static void direction_sources(const HostSys& h, int src[3]) {
+    for (int l = 0; l < 3; ++l) {
+        src[l] = l;
+        for (int q = 0; q < l; ++q) {
+            if (src[q] != q) continue;
+            bool same = h.n[l] == h.n[q] && h.nbar[l] == h.nbar[q] && h.L[l] == h.L[q];
+            for (size_t v = 0; same && v < h.Z.size(); ++v) same = h.pos[3 * v + l] == h.pos[3 * v + q];
+            for (size_t m = 0; same && m < h.alpha.size(); ++m)
+                same = h.center[3 * m + l] == h.center[3 * m + q] && h.deg[3 * m + l] == h.deg[3 * m + q];
+            if (same) {
+                src[l] = q;
+                break;
+            }
+        }
+    }
+}
+
+static int splits_for(long long tiles, long long len) {
+    int s = 1;
+    while (tiles * s < 2 * 148 && len / (s * 2) >= 256 && s < 64) s *= 2;
+    return s;
+}
+
+// window starts of every (direction, nucleus) to the device (host part; not capturable)
+static int64_t* upload_s0(lt_ctx* c, const Plan& p) {
+    std::vector<int64_t> s0all;
+    for (int l = 0; l < 3; ++l)
+        for (Index v : p.d[l].s0) s0all.push_back(v);
+    int64_t* s0d = c->arena.get<int64_t>("pot.s0", s0all.size() + 1);
+    upload(c, s0d, s0all.data(), s0all.size() * sizeof(int64_t));
+    return s0d;
+}
+
 static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need, int mode, AsmOut out,
-                         Work* wout = nullptr) {
+                         Work* wout = nullptr, const int64_t* s0_dev = nullptr) {
     const Launch L = c->L();
     const Index m0 = p.m0, mm = m0 * m0, RN = p.RN, Rtot = p.Rtot;
     Arena& A = c->arena;
+    int src[3];
+    direction_sources(sd->hs, src);
     Work w{};
     w.t = A.get<double>("sinc.t", RN);
     w.w = A.get<double>("sinc.w", RN);
@@ -250,12 +305,12 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
     launch_sinc(L, p.M, sd->ds, w.t, w.w, w.potw);
     const bool nuc = need & NEED_NUC, ms = need & NEED_MS;
     if (nuc) {
-        std::vector<int64_t> s0all;
-        for (int l = 0; l < 3; ++l)
-            for (Index v : p.d[l].s0) s0all.push_back(v);
-        int64_t* s0d = A.get<int64_t>("pot.s0", s0all.size());
-        upload(c, s0d, s0all.data(), s0all.size() * sizeof(int64_t));
+        const int64_t* s0d = s0_dev ? s0_dev : upload_s0(c, p);
         for (int l = 0; l < 3; ++l) {
+            if (src[l] != l) {
+                w.pot[l] = w.pot[src[l]];
+                continue;
+            }
             const DirPlan& d = p.d[l];
             double* master = A.get<double>("pot.master" + std::to_string(l), d.mrows * RN);
             w.pot[l] = A.get<double>("pot.panel" + std::to_string(l), d.pot_rows * Rtot);
@@ -263,10 +318,11 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
             launch_window_sum(L, master, d.mrows, RN, p.nnuc, s0d + l * p.nnuc, d.nsum, d.n, d.pot_rows, w.pot[l]);
         }
     }
-    // profiles (galerkin.cpp:127-149)
+    // profiles (galerkin.cpp:127-149), distinct directions only
     ProfileJob jobs[6];
     int nj = 0;
     for (int l = 0; l < 3; ++l) {
+        if (src[l] != l) continue;
         const DirPlan& d = p.d[l];
         if (nuc) {
             ProfileJob j;
@@ -295,46 +351,127 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
             jobs[nj++] = j;
         }
     }
+    for (int l = 0; l < 3; ++l)
+        if (src[l] != l) {
+            w.pwc[l] = w.pwc[src[l]];
+            w.pwc_lo[l] = w.pwc_lo[src[l]];
+            w.pwc_hi[l] = w.pwc_hi[src[l]];
+            w.pwl[l] = w.pwl[src[l]];
+            w.pwl_lo[l] = w.pwl_lo[src[l]];
+            w.pwl_hi[l] = w.pwl_hi[src[l]];
+        }
     launch_profiles(L, sd->ds, jobs, nj, 1e-280);
     if (ms)
         for (int l = 0; l < 3; ++l) {
+            if (src[l] != l) {
+                w.massT[l] = w.massT[src[l]];
+                w.stiffT[l] = w.stiffT[src[l]];
+                continue;
+            }
             const DirPlan& d = p.d[l];
             w.massT[l] = A.get<double>("fem.mass" + std::to_string(l), d.width * mm);
             w.stiffT[l] = A.get<double>("fem.stiff" + std::to_string(l), d.width * mm);
             launch_fem_tables(L, m0, d.band, d.nbar, d.hbar, d.Gbar, w.pwl[l], w.pwl_lo[l], w.pwl_hi[l], w.massT[l],
                               w.stiffT[l]);
         }
+    // nuclear contraction: choose the reassociation (k_nuclear2.cu header)
+    int nuc_mode = 0, ndir = -1;
     if (nuc) {
-        for (int l = 0; l < 3; ++l) {
-            const DirPlan& d = p.d[l];
-            if (l == p.s2_dir) continue;
-            w.T[l] = A.get<double>("nuc.T" + std::to_string(l), d.npairs * Rtot * mm);
-            if (d.mode == TM_FOLD) {
-                double* Qf = A.get<double>("nuc.Qf" + std::to_string(l), d.width * mm * d.n);
-                launch_nuc_fold(L, m0, Rtot, d, w.pwc[l], w.pwc_lo[l], w.pwc_hi[l], w.pot[l], Qf, w.T[l]);
+        std::vector<int> wrapped;
+        for (int l = 0; l < 3; ++l)
+            if (p.d[l].L > 1) wrapped.push_back(l);
+        const bool dmma_ok = m0 <= 32;
+        if (dmma_ok && wrapped.size() == 1) nuc_mode = 1;
+        else if (dmma_ok && p.periodic && wrapped.size() >= 2) nuc_mode = 2;
+        if (nuc_mode != 0) {
+            // trivial directions -> W[r][e] = w_r prod_l T_l[r][e]
+            TrivJobs tj{};
+            WSpec ws{};
+            int njobs = 0;
+            int job_of_src[3] = {-1, -1, -1};
+            for (int l = 0; l < 3; ++l) {
+                if (p.d[l].L > 1) continue;
+                const int s = src[l];
+                if (job_of_src[s] < 0) {
+                    job_of_src[s] = njobs;
+                    TrivJob& J = tj.j[njobs++];
+                    J.pot = w.pot[s];
+                    J.rows = p.d[s].pot_rows;
+                    J.pwc = w.pwc[s];
+                    J.G = p.d[s].G;
+                    J.lo = w.pwc_lo[s];
+                    J.hi = w.pwc_hi[s];
+                }
+                ws.job_of_dir[l] = job_of_src[s];
+            }
+            const int nsym = static_cast<int>(m0 * (m0 + 1) / 2);
+            long long maxG = 1;
+            for (int j = 0; j < njobs; ++j) maxG = std::max(maxG, tj.j[j].G);
+            const int tiles = static_cast<int>(((Rtot + 63) / 64) * ((nsym + 63) / 64));
+            const int splits = njobs ? splits_for(tiles * njobs, maxG) : 1;
+            double* part = A.get<double>("nuc.tpart", std::max<size_t>(1, static_cast<size_t>(njobs) * splits * Rtot * nsym));
+            double* W = A.get<double>("nuc.W", Rtot * mm);
+            launch_triv_tables(L, tj, njobs, ws, static_cast<int>(m0), static_cast<int>(Rtot), w.potw, part, splits, W,
+                               nullptr);
+            if (nuc_mode == 1) {
+                ndir = wrapped[0];
+                const DirPlan& d = p.d[ndir];
+                double* V = A.get<double>("nuc.V", mm * d.pot_rows);
+                launch_vgemm(L, static_cast<int>(mm), static_cast<int>(Rtot), d.pot_rows, W, w.pot[ndir], V);
+                w.N = A.get<double>("nuc.N", d.L * d.width * mm);
+                if (!p.periodic) {
+                    const int nt = static_cast<int>(((d.L + 63) / 64) * ((d.width + 63) / 64) * mm);
+                    const int sp = splits_for(nt, d.G);
+                    double* hp = A.get<double>("nuc.hpart", static_cast<size_t>(sp) * mm * d.L * d.width);
+                    launch_hankel(L, static_cast<int>(m0), d, w.pwc[ndir], w.pwc_lo[ndir], w.pwc_hi[ndir], V, hp, w.N,
+                                  sp);
+                } else {
+                    double* fp = A.get<double>("nuc.fpart", d.n * (d.band + 1) * mm);
+                    launch_fold_dmma(L, static_cast<int>(m0), d, w.pwc[ndir], V, 0, fp, w.N);
+                }
             } else {
-                if (d.mode == TM_BOXDIR)  // tables of pairs with k+d outside the lattice stay unused
-                    LT_CU(cudaMemsetAsync(w.T[l], 0, sizeof(double) * d.npairs * Rtot * mm, c->stream));
-                launch_nuc_direct(L, m0, Rtot, d, p.periodic, w.pwc[l], w.pwc_lo[l], w.pwc_hi[l], w.pot[l], w.T[l]);
+                KRArgs kr;
+                kr.m0 = static_cast<int>(m0);
+                kr.Rtot = static_cast<int>(Rtot);
+                kr.W = W;
+                double* Tl[3] = {nullptr, nullptr, nullptr};
+                for (int l = 0; l < 3; ++l) {
+                    kr.width[l] = static_cast<int>(p.d[l].width);
+                    kr.band[l] = static_cast<int>(p.d[l].band);
+                    if (p.d[l].L == 1) continue;
+                    const int s = src[l];
+                    if (!Tl[s]) {
+                        const DirPlan& d = p.d[s];
+                        double* Qf = A.get<double>("nuc.Qf" + std::to_string(s), (d.band + 1) * mm * d.n);
+                        Tl[s] = A.get<double>("nuc.T" + std::to_string(s), (d.band + 1) * Rtot * mm);
+                        launch_fold_dmma(L, static_cast<int>(m0), d, w.pwc[s], nullptr, 1, Qf, nullptr);
+                        launch_fgemm(L, static_cast<int>(m0), static_cast<int>(Rtot), d, w.pot[s], Qf, Tl[s]);
+                    }
+                    kr.T[l] = Tl[s];
+                }
+                w.N = A.get<double>("nuc.N", p.nblocks * mm);
+                kr.N = w.N;
+                launch_kr_combine(L, kr);
             }
-        }
-        if (p.s2_dir >= 0) {
-            const int ls = p.s2_dir;
-            const int la = (ls + 1) % 3, lb = (ls + 2) % 3;
-            const DirPlan& d = p.d[ls];
-            double* W = A.get<double>("s2.W", Rtot * mm);
-            double* V = A.get<double>("s2.V", mm * d.G);
-            launch_box_w(L, m0, Rtot, w.potw, w.T[la], w.T[lb], W);
-            launch_box_v(L, m0, Rtot, d.G, W, w.pot[ls], V);
-            int nsplit = 1;
-            {
-                // split the contraction so the grid covers the SMs a few times over
-                const Index tiles = ((d.L + 63) / 64) * ((d.width + 31) / 32) * mm;
-                while (tiles * nsplit < 4 * 148 && nsplit < 16) nsplit *= 2;
+        } else {
+            // general path: per-direction tables by direct contraction, combined in the fill
+            for (int l = 0; l < 3; ++l) {
+                const DirPlan& d = p.d[l];
+                if (src[l] != l) {
+                    w.T[l] = w.T[src[l]];
+                    continue;
+                }
+                w.T[l] = A.get<double>("nuc.T" + std::to_string(l), d.npairs * Rtot * mm);
+                if (d.mode == TM_FOLD) {
+                    double* Qf = A.get<double>("nuc.Qf" + std::to_string(l), d.width * mm * d.n);
+                    launch_nuc_fold(L, m0, Rtot, d, w.pwc[l], w.pwc_lo[l], w.pwc_hi[l], w.pot[l], Qf, w.T[l]);
+                } else {
+                    if (d.mode == TM_BOXDIR)  // tables of pairs with k+d outside the lattice stay unused
+                        LT_CU(cudaMemsetAsync(w.T[l], 0, sizeof(double) * d.npairs * Rtot * mm, c->stream));
+                    launch_nuc_direct(L, m0, Rtot, d, p.periodic, w.pwc[l], w.pwc_lo[l], w.pwc_hi[l], w.pot[l],
+                                      w.T[l]);
+                }
             }
-            double* part = A.get<double>("s2.part", static_cast<size_t>(nsplit) * mm * d.L * d.width);
-            w.N = A.get<double>("s2.N", d.L * d.width * mm);
-            launch_box_corr(L, m0, d, w.pwc[ls], w.pwc_lo[ls], w.pwc_hi[ls], V, part, w.N, nsplit);
         }
     }
     // fused combine + placement
@@ -351,7 +488,8 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
     }
     fa.potw = w.potw;
     fa.N = w.N;
-    fa.s2_dir = p.s2_dir;
+    fa.s2_dir = ndir;
+    fa.nuc_mode = nuc_mode;
     fa.mode = mode;
     fa.periodic = p.periodic;
     fa.out0 = out.out0;
@@ -390,66 +528,91 @@ static std::vector<std::array<Index, 3>> periodic_kidx(const Plan& p) {
 // ---------------------------------------------------------------------------
 // Dense block-diagonal form [K][mm] (complex) of a generating tensor given by the
 // stored kidx (host) and its blocks (device, std::map order).
-static double2* block_diag_device(lt_ctx* c, const Index dims[3], Index m0,
-                                  const std::vector<std::array<Index, 3>>& kidx, const double* blocks_dev,
-                                  const std::string& tag) {
-    const Launch L = c->L();
-    const Index mm = m0 * m0;
+struct DftPrep {
+    Index dims[3]{1, 1, 1};
+    Index ext[3]{1, 1, 1};
+    Index ncomp[3]{1, 1, 1};
+    Index nblk = 0, m0 = 0, maxsz = 0;
+    int64_t* kslot = nullptr;
+    int64_t* comp[3]{nullptr, nullptr, nullptr};
+    std::string tag;
+};
+
+// host part of the block diagonalisation: compressed per-axis index sets and slots,
+// uploaded (not capturable, so done before any graph capture)
+static DftPrep prepare_dft(lt_ctx* c, const Index dims[3], Index m0, const std::vector<std::array<Index, 3>>& kidx,
+                           const std::string& tag) {
+    DftPrep P;
+    P.m0 = m0;
+    P.tag = tag;
+    P.nblk = static_cast<Index>(kidx.size());
     std::vector<Index> comp[3];
     for (int l = 0; l < 3; ++l) {
+        P.dims[l] = dims[l];
         std::set<Index> s;
         for (auto& k : kidx) s.insert(k[l]);
         if (s.empty()) s.insert(0);
         comp[l].assign(s.begin(), s.end());
+        P.ext[l] = P.ncomp[l] = static_cast<Index>(comp[l].size());
+        if (dims[l] == 1) {
+            if (comp[l].size() != 1 || comp[l][0] != 0) fail(LT_EBOUNDS, "GeneratingBlockTensor: index out of range");
+        } else {
+            for (Index v : comp[l])
+                if (v < 0 || v >= dims[l]) fail(LT_EBOUNDS, "GeneratingBlockTensor: index out of range");
+        }
     }
-    Index ext[3];
-    for (int l = 0; l < 3; ++l) ext[l] = static_cast<Index>(comp[l].size());
     std::vector<int64_t> kslot(kidx.size());
     for (size_t b = 0; b < kidx.size(); ++b) {
         Index pos = 0;
         for (int l = 0; l < 3; ++l) {
             const Index ci = std::lower_bound(comp[l].begin(), comp[l].end(), kidx[b][l]) - comp[l].begin();
-            pos = pos * ext[l] + ci;
+            pos = pos * P.ext[l] + ci;
         }
         kslot[b] = pos;
     }
-    const Index K = dims[0] * dims[1] * dims[2];
-    Index maxsz = ext[0] * ext[1] * ext[2];
-    {
-        Index e2[3] = {ext[0], ext[1], ext[2]};
-        for (int a = 0; a < 3; ++a) {
-            if (dims[a] > 1) e2[a] = dims[a];
-            maxsz = std::max(maxsz, e2[0] * e2[1] * e2[2]);
-        }
+    P.maxsz = P.ext[0] * P.ext[1] * P.ext[2];
+    Index e2[3] = {P.ext[0], P.ext[1], P.ext[2]};
+    for (int a = 0; a < 3; ++a) {
+        if (dims[a] > 1) e2[a] = dims[a];
+        P.maxsz = std::max(P.maxsz, e2[0] * e2[1] * e2[2]);
     }
-    double2* bufA = c->arena.get<double2>("dft.a" + tag, maxsz * mm);
-    double2* bufB = c->arena.get<double2>("dft.b" + tag, maxsz * mm);
-    int64_t* ks = c->arena.get<int64_t>("dft.kslot" + tag, kslot.size() + 1);
-    upload(c, ks, kslot.data(), kslot.size() * sizeof(int64_t));
-    LT_CU(cudaMemsetAsync(bufA, 0, sizeof(double2) * ext[0] * ext[1] * ext[2] * mm, c->stream));
-    launch_scatter_gen(L, static_cast<Index>(kidx.size()), mm, ks, blocks_dev, bufA);
+    P.kslot = c->arena.get<int64_t>("dft.kslot" + tag, kslot.size() + 1);
+    upload(c, P.kslot, kslot.data(), kslot.size() * sizeof(int64_t));
+    for (int a = 0; a < 3; ++a) {
+        P.comp[a] = c->arena.get<int64_t>("dft.comp" + tag + std::to_string(a), comp[a].size());
+        upload(c, P.comp[a], comp[a].data(), comp[a].size() * sizeof(int64_t));
+    }
+    return P;
+}
+
+// device part (kernels and memsets only: capturable)
+static double2* launch_dft(lt_ctx* c, const DftPrep& P, const double* blocks_dev) {
+    const Launch L = c->L();
+    const Index mm = P.m0 * P.m0;
+    double2* bufA = c->arena.get<double2>("dft.a" + P.tag, P.maxsz * mm);
+    double2* bufB = c->arena.get<double2>("dft.b" + P.tag, P.maxsz * mm);
+    LT_CU(cudaMemsetAsync(bufA, 0, sizeof(double2) * P.ext[0] * P.ext[1] * P.ext[2] * mm, c->stream));
+    launch_scatter_gen(L, P.nblk, mm, P.kslot, blocks_dev, bufA);
     double2* cur = bufA;
     double2* nxt = bufB;
-    Index in_ext[3] = {ext[0], ext[1], ext[2]};
+    Index in_ext[3] = {P.ext[0], P.ext[1], P.ext[2]};
     for (int a = 0; a < 3; ++a) {
-        if (dims[a] == 1) {
-            if (comp[a].size() != 1 || comp[a][0] != 0) fail(LT_EBOUNDS, "GeneratingBlockTensor: index out of range");
-            continue;
-        }
-        for (Index v : comp[a])
-            if (v < 0 || v >= dims[a]) fail(LT_EBOUNDS, "GeneratingBlockTensor: index out of range");
-        int64_t* cd = c->arena.get<int64_t>("dft.comp" + tag + std::to_string(a), comp[a].size());
-        upload(c, cd, comp[a].data(), comp[a].size() * sizeof(int64_t));
-        double2* tw = c->arena.get<double2>("dft.tw" + tag + std::to_string(a), dims[a] * comp[a].size());
-        launch_twiddles(L, dims[a], static_cast<Index>(comp[a].size()), cd, tw);
+        if (P.dims[a] == 1) continue;
+        double2* tw = c->arena.get<double2>("dft.tw" + P.tag + std::to_string(a), P.dims[a] * P.ncomp[a]);
+        launch_twiddles(L, P.dims[a], P.ncomp[a], P.comp[a], tw);
         Index out_ext[3] = {in_ext[0], in_ext[1], in_ext[2]};
-        out_ext[a] = dims[a];
-        launch_dft_axis(L, a, in_ext, out_ext, mm, cur, nxt, tw, static_cast<Index>(comp[a].size()), dims[a]);
+        out_ext[a] = P.dims[a];
+        launch_dft_axis(L, a, in_ext, out_ext, mm, cur, nxt, tw, P.ncomp[a], P.dims[a]);
         std::swap(cur, nxt);
         for (int l = 0; l < 3; ++l) in_ext[l] = out_ext[l];
     }
-    (void)K;
     return cur;
+}
+
+static double2* block_diag_device(lt_ctx* c, const Index dims[3], Index m0,
+                                  const std::vector<std::array<Index, 3>>& kidx, const double* blocks_dev,
+                                  const std::string& tag) {
+    return launch_dft(c, prepare_dft(c, dims, m0, kidx, tag), blocks_dev);
 }
 
 static void raise_fail_key(unsigned long long key, bool periodic) {
@@ -509,6 +672,39 @@ static void box_eig_device(lt_ctx* c, Index n, double* H, double* S, double* eig
     if (hinfo != 0) fail(LT_EGENERIC, "solve_box_dense: eigensolver failed");
 }
 
+// graph-cache key: everything the captured launches bake in (host-derived parameters of
+// the system and plan, device pointers, arena generation)
+static std::vector<int64_t> graph_key(const HostSys& h, const Plan& p, bool periodic, Index kb, Index ke,
+                                      const void* eig, const void* sysmem, uint64_t gen) {
+    std::vector<int64_t> k;
+    auto put_d = [&](double v) {
+        int64_t b;
+        std::memcpy(&b, &v, sizeof(b));
+        k.push_back(b);
+    };
+    k.push_back(periodic);
+    k.push_back(kb);
+    k.push_back(ke);
+    k.push_back(reinterpret_cast<int64_t>(eig));
+    k.push_back(reinterpret_cast<int64_t>(sysmem));
+    k.push_back(static_cast<int64_t>(gen));
+    k.push_back(p.L0);
+    put_d(h.b);
+    put_d(h.eps_ov);
+    k.push_back(h.quad_M);
+    for (int l = 0; l < 3; ++l) {
+        k.push_back(h.L[l]);
+        k.push_back(h.n[l]);
+        k.push_back(h.nbar[l]);
+    }
+    for (double v : h.pos) put_d(v);
+    for (double v : h.Z) put_d(v);
+    for (double v : h.center) put_d(v);
+    for (double v : h.alpha) put_d(v);
+    for (int v : h.deg) k.push_back(v);
+    return k;
+}
+
 // full path on device; eigenvalues -> eig_dev (device)
 static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double* eig_dev, Index k_begin,
                            Index k_end, int64_t* info) {
@@ -517,33 +713,75 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
     Plan p;
     plan_after_L0(sd->hs, periodic, L0, p, true);
     const Index mm = p.m0 * p.m0;
+    if (!periodic && p.Nb > 4096)
+        fail(LT_ECAP, "solve_box_dense: size " + std::to_string(p.Nb) + " exceeds dense cap 4096");
+    if (k_end < 0 || k_end > p.K) k_end = p.K;
+    if (k_begin < 0) k_begin = 0;
+    // host-side preparation (uploads): outside any graph capture
     AsmOut out;
     unsigned long long* fk = c->arena.get<unsigned long long>("solve.fail", 1);
     LT_CU(cudaMemsetAsync(fk, 0xff, sizeof(unsigned long long), c->stream));
+    int64_t* s0d = upload_s0(c, p);
+    DftPrep dpH, dpS;
     if (periodic) {
         out.out0 = c->arena.get<double>("core.H", p.nblocks * mm);
         out.out1 = c->arena.get<double>("core.S", p.nblocks * mm);
         out.kidx = c->arena.get<int64_t>("core.kidx", p.nblocks * 3);
-        run_assembly(c, sd, p, NEED_MS | NEED_NUC, 0, out);
         const auto kidx = periodic_kidx(p);
         const Index dims[3] = {p.d[0].L, p.d[1].L, p.d[2].L};
-        double2* Hb = block_diag_device(c, dims, p.m0, kidx, out.out0, "H");
-        double2* Sb = block_diag_device(c, dims, p.m0, kidx, out.out1, "S");
-        if (k_end < 0 || k_end > p.K) k_end = p.K;
-        if (k_begin < 0) k_begin = 0;
-        if (k_begin < k_end)
-            launch_pencil(c->L(), k_end - k_begin, p.m0, Hb + k_begin * mm, Sb + k_begin * mm, eig_dev + k_begin * p.m0,
-                          fk, true);
+        dpH = prepare_dft(c, dims, p.m0, kidx, "H");
+        dpS = prepare_dft(c, dims, p.m0, kidx, "S");
     } else {
-        if (p.Nb > 4096)
-            fail(LT_ECAP, "solve_box_dense: size " + std::to_string(p.Nb) + " exceeds dense cap 4096");
         out.out0 = c->arena.get<double>("core.H", p.Nb * p.Nb);
         out.out1 = c->arena.get<double>("core.S", p.Nb * p.Nb);
-        run_assembly(c, sd, p, NEED_MS | NEED_NUC, 0, out);
-        box_eig_device(c, p.Nb, out.out0, out.out1, eig_dev, fk);
     }
-    unsigned long long key = ~0ull;
-    LT_CU(cudaMemcpyAsync(&key, fk, sizeof(key), cudaMemcpyDeviceToHost, c->stream));
+    const bool small_box = !periodic && p.Nb <= 32;
+    // device work after L0: kernels and memsets only
+    auto enqueue = [&]() {
+        run_assembly(c, sd, p, NEED_MS | NEED_NUC, 0, out, nullptr, s0d);
+        if (periodic) {
+            double2* Hb = launch_dft(c, dpH, out.out0);
+            double2* Sb = launch_dft(c, dpS, out.out1);
+            if (k_begin < k_end)
+                launch_pencil(c->L(), k_end - k_begin, p.m0, Hb + k_begin * mm, Sb + k_begin * mm,
+                              eig_dev + k_begin * p.m0, fk, true);
+        } else if (small_box) {
+            box_eig_device(c, p.Nb, out.out0, out.out1, eig_dev, fk);
+        }
+    };
+    const bool use_graph = c->graphs && !c->timer.on;
+    std::vector<int64_t> key =
+        graph_key(sd->hs, p, periodic, k_begin, k_end, eig_dev, sd->mem, c->arena.generation());
+    if (use_graph && c->gexec && key == c->gkey) {
+        LT_CU(cudaGraphLaunch(c->gexec, c->stream));
+        c->launches += c->glaunches;
+    } else if (use_graph && key == c->gseen) {
+        // second identical call: capture the launch sequence once and replay it from now on
+        const int64_t l0 = c->launches;
+        cudaGraph_t g = nullptr;
+        LT_CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        try {
+            enqueue();
+        } catch (...) {
+            cudaStreamEndCapture(c->stream, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        LT_CU(cudaStreamEndCapture(c->stream, &g));
+        if (c->gexec) cudaGraphExecDestroy(c->gexec);
+        c->gexec = nullptr;
+        LT_CU(cudaGraphInstantiate(&c->gexec, g, 0));
+        cudaGraphDestroy(g);
+        c->gkey = key;
+        c->glaunches = c->launches - l0;
+        LT_CU(cudaGraphLaunch(c->gexec, c->stream));
+    } else {
+        enqueue();
+        c->gseen = graph_key(sd->hs, p, periodic, k_begin, k_end, eig_dev, sd->mem, c->arena.generation());
+    }
+    if (!periodic && !small_box) box_eig_device(c, p.Nb, out.out0, out.out1, eig_dev, fk);
+    unsigned long long fkey = ~0ull;
+    LT_CU(cudaMemcpyAsync(&fkey, fk, sizeof(fkey), cudaMemcpyDeviceToHost, c->stream));
     LT_CU(cudaStreamSynchronize(c->stream));
     c->timer.collect();
     if (info) {
@@ -552,9 +790,9 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
         info[4] = p.Rtot;
         info[5] = p.Nb;
         info[6] = p.K;
-        info[7] = key == ~0ull ? -1 : static_cast<int64_t>(key);
+        info[7] = fkey == ~0ull ? -1 : static_cast<int64_t>(fkey);
     }
-    raise_fail_key(key, periodic);
+    raise_fail_key(fkey, periodic);
 }
 
 static lt_operator* new_op(const Plan& p, int which, Index coefficient_rank) {
@@ -619,6 +857,7 @@ void lt_destroy(lt_ctx* c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->solver) cusolverDnDestroy(c->solver);
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -675,7 +914,10 @@ lt_status lt_solve_core_dev(lt_ctx* c, const lt_sysdev* s, int periodic, double*
 lt_status lt_solve_core(lt_ctx* c, const lt_system* s, int periodic, double* eig_host, int64_t* info) {
     return guarded([&] {
         LT_CU(cudaSetDevice(c->device));
-        std::unique_ptr<lt_sysdev, void (*)(lt_sysdev*)> sd(make_sysdev(s), lt_sys_free);
+        // the system is copied host -> device on every call, into a context-owned buffer
+        const HostSys hs = host_sys_from(s);
+        void* dst = c->arena.get<char>("sys.mem", sysdev_bytes(hs));
+        std::unique_ptr<lt_sysdev> sd(make_sysdev(s, dst, c->stream));
         const HostSys& h = sd->hs;
         const Index count = h.m0() * h.cells();
         double* eig = c->arena.get<double>("solve.eig", count);

@@ -21,7 +21,7 @@ struct FillDev {
     const double* T[3];
     const double* potw;
     const double* N;
-    int s2_dir, mode, periodic;
+    int s2_dir, mode, periodic, nuc_mode;
     double* out0;
     double* out1;
     int64_t* kidx;
@@ -70,9 +70,11 @@ __global__ void k_fill(FillDev f) {
             lap = __dadd_rn(__dadd_rn(t0, t1), t2);
         }
         if (want_nuc) {
-            if (f.s2_dir >= 0) {
+            if (f.nuc_mode == 1) {
                 const int l = f.s2_dir;
                 nuc = f.N[(k[l] * f.width[l] + d[l] + f.band[l]) * mm + e];
+            } else if (f.nuc_mode == 2) {
+                nuc = f.N[dlin * mm + e];
             } else {
                 double acc = 0.0;
                 const double* T0 = f.T[0] + pidx[0] * f.Rtot * mm + e;
@@ -122,6 +124,7 @@ void launch_fill(const Launch& L, const FillArgs& a, Index Nb, Index nblocks) {
     f.potw = a.potw;
     f.N = a.N;
     f.s2_dir = a.s2_dir;
+    f.nuc_mode = a.nuc_mode;
     f.mode = a.mode;
     f.periodic = a.periodic ? 1 : 0;
     f.out0 = a.out0;

@@ -1,0 +1,417 @@
+// k_nuclear2.cu — the nuclear-attraction contraction on FP64 tensor cores (DMMA).
+//
+// Reference (galerkin.cpp:109-125, :224-247, :273-284):
+//   T_l[k,d,r](mu,nu) = sum_i g_mu(i - s_A) g_nu(i - s_B) p_r(i)          (dot3)
+//   H_nuc[k,d](mu,nu) = sum_r w_r T_0[.] T_1[.] T_2[.]                    (combine_block)
+// Reassociated here so each product is a dense GEMM over the grid:
+//   trivial direction (L_l = 1, one (k,d) pair):  T_l[r][e] = sum_i P[r][i] (g_mu g_nu)(i)
+//       -> GEMM M = R_tot, N = sym pairs (mu <= nu; T is symmetric in (mu, nu) exactly),
+//          K = grid; split-K over CTAs, fixed-order reduction; W[r][e] = w_r prod_l T_l.
+//   V[e][i] = sum_r W[r][e] P_l*[r][i]  (rank sum folded into an effective potential)
+//       -> GEMM M = m0^2, N = rows, K = R_tot.
+//   box chain (one non-trivial direction l*):  N[k][d][e] = sum_j Q_d(j) V_e(j + k n)
+//       -> per e a Hankel-operand GEMM M = L cells, N = 2b+1 offsets, K = support.
+//   periodic wrapped direction:  Qf_t[d](mu,nu) = sum_j a_mu(t + j n) a_nu(t + (j-d) n)
+//       -> per residue t in [0,n) and d >= 0 an (m0 x J)(J x m0) product (m8n8k4 tiles);
+//          Qf[-d](nu,mu) = Qf[d](mu,nu) exactly (same terms, same order).
+//       single non-trivial direction: N[d][e] = sum_t V_e(t) Qf_t[d](e);
+//       several: T_l[d][r][e] = sum_t P_l[r][t] Qf_t[d](e) (GEMM) and
+//                N[d0,d1,d2][e] = sum_r W[r][e] prod_l T_l[d_l][r][e] (Khatri-Rao combine).
+#include "dmma.cuh"
+#include "lt_device.cuh"
+#include "lt_internal.cuh"
+
+namespace lt {
+
+// symmetric pair index e_s (mu <= nu), row-major over mu: e_s = mu*m0 - mu(mu-1)/2 + (nu - mu)
+__device__ __forceinline__ void sym_pair(int es, int m0, int& mu, int& nu) {
+    int m = 0, base = 0;
+    while (es >= base + (m0 - m)) {
+        base += m0 - m;
+        ++m;
+    }
+    mu = m;
+    nu = m + (es - base);
+}
+
+// ---------------------------------------------------------------------------
+// trivial-direction tables: split-K DMMA GEMM over the symmetric pairs
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_triv_gemm(TrivJobs jobs, int m0, int Rtot, int nsym, int splits,
+                                                   double* __restrict__ part) {
+    __shared__ GemmSmem sm;
+    const int job = blockIdx.z / splits, split = blockIdx.z % splits;
+    const TrivJob& J = jobs.j[job];
+    const int r0 = blockIdx.x * kGBM, e0 = blockIdx.y * kGBN;
+    // union of the supports (products vanish outside every pair's overlap)
+    long long klo = J.G, khi = 0;
+    for (int m = 0; m < m0; ++m) {
+        klo = min(klo, static_cast<long long>(J.lo[m]));
+        khi = max(khi, static_cast<long long>(J.hi[m]));
+    }
+    khi = min(khi, static_cast<long long>(J.rows));
+    const long long len = khi > klo ? khi - klo : 0;
+    const long long per = ((len + splits - 1) / splits + kGBK - 1) / kGBK * kGBK;
+    const long long k0 = klo + split * per, k1 = min(khi, k0 + per);
+    __shared__ int smu[64], snu[64];
+    if (threadIdx.x < 64) {
+        int mu = 0, nu = 0;
+        if (e0 + static_cast<int>(threadIdx.x) < nsym) sym_pair(e0 + threadIdx.x, m0, mu, nu);
+        smu[threadIdx.x] = mu;
+        snu[threadIdx.x] = nu;
+    }
+    __syncthreads();
+    const double* P = J.pot;
+    const double* g = J.pwc;
+    const long long G = J.G, rows = J.rows;
+    auto loadA = [&](int m, long long k) -> double { return r0 + m < Rtot ? P[(r0 + m) * rows + k] : 0.0; };
+    auto loadB = [&](long long k, int n) -> double {
+        return e0 + n < nsym ? g[smu[n] * G + k] * g[snu[n] * G + k] : 0.0;
+    };
+    double acc[4][4] = {};
+    cta_gemm_64x64(loadA, loadB, k0, k1, acc, sm);
+    double* out = part + (static_cast<long long>(job) * splits + split) * Rtot * nsym;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            int m, n;
+            acc_coord(nt, i, m, n);
+            if (r0 + m < Rtot && e0 + n < nsym) out[(r0 + m) * nsym + e0 + n] = acc[nt][i];
+        }
+}
+
+// W[r][e] = w_r * prod over trivial directions of T_l[r][e] (T_l reduced over splits in
+// fixed order); e over all m0^2 ordered pairs (mirror of the symmetric index)
+__global__ void k_triv_reduce_w(const double* __restrict__ part, int njobs, const int* dir_job_unused, WSpec ws,
+                                int m0, int Rtot, int nsym, int splits, const double* __restrict__ potw,
+                                double* __restrict__ W, double* __restrict__ Tout) {
+    const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int mm = m0 * m0;
+    if (idx >= static_cast<long long>(Rtot) * mm) return;
+    const int r = static_cast<int>(idx / mm), e = static_cast<int>(idx % mm);
+    const int mu0 = e % m0, nu0 = e / m0;
+    const int mu = min(mu0, nu0), nu = max(mu0, nu0);
+    const int es = mu * m0 - mu * (mu - 1) / 2 + (nu - mu);
+    double w = potw[r];
+    double tj[3] = {1.0, 1.0, 1.0};
+    for (int j = 0; j < njobs; ++j) {
+        double s = 0.0;
+        for (int sp = 0; sp < splits; ++sp) s += part[((static_cast<long long>(j) * splits + sp) * Rtot + r) * nsym + es];
+        tj[j] = s;
+        if (Tout) Tout[(static_cast<long long>(j) * Rtot + r) * mm + e] = s;
+    }
+    // product in direction order (directions may share a job)
+    double prod = 1.0;
+    bool first = true;
+    for (int l = 0; l < 3; ++l) {
+        if (ws.job_of_dir[l] < 0) continue;
+        const double v = tj[ws.job_of_dir[l]];
+        prod = first ? v : prod * v;
+        first = false;
+    }
+    W[idx] = w * prod;
+}
+
+void launch_triv_tables(const Launch& L, const TrivJobs& jobs, int njobs, const WSpec& ws, int m0, int Rtot,
+                        const double* potw, double* part, int splits, double* W, double* Tout) {
+    const int nsym = m0 * (m0 + 1) / 2;
+    if (njobs > 0) {
+        dim3 grid((Rtot + kGBM - 1) / kGBM, (nsym + kGBN - 1) / kGBN, njobs * splits);
+        Stage st_(L, "triv_gemm");
+        k_triv_gemm<<<grid, 256, 0, L.st>>>(jobs, m0, Rtot, nsym, splits, part);
+        LT_CU(cudaGetLastError());
+        L.tick();
+    }
+    const long long tot = static_cast<long long>(Rtot) * m0 * m0;
+    Stage st2_(L, "triv_reduce_w");
+    k_triv_reduce_w<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, L.st>>>(part, njobs, nullptr, ws, m0, Rtot,
+                                                                              nsym, splits, potw, W, Tout);
+    LT_CU(cudaGetLastError());
+    L.tick();
+}
+
+// ---------------------------------------------------------------------------
+// V[e][i] = sum_r W[r][e] P[r][i]
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_vgemm(int mm, int Rtot, long long rows, const double* __restrict__ W,
+                                               const double* __restrict__ P, double* __restrict__ V) {
+    __shared__ GemmSmem sm;
+    const int e0 = blockIdx.y * kGBM;
+    const long long i0 = static_cast<long long>(blockIdx.x) * kGBN;
+    auto loadA = [&](int m, long long k) -> double { return e0 + m < mm ? W[k * mm + e0 + m] : 0.0; };
+    auto loadB = [&](long long k, int n) -> double { return i0 + n < rows ? P[k * rows + i0 + n] : 0.0; };
+    double acc[4][4] = {};
+    cta_gemm_64x64(loadA, loadB, 0, Rtot, acc, sm);
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            int m, n;
+            acc_coord(nt, i, m, n);
+            if (e0 + m < mm && i0 + n < rows) V[(e0 + m) * rows + i0 + n] = acc[nt][i];
+        }
+}
+
+void launch_vgemm(const Launch& L, int mm, int Rtot, long long rows, const double* W, const double* P, double* V) {
+    dim3 grid(static_cast<unsigned>((rows + kGBN - 1) / kGBN), (mm + kGBM - 1) / kGBM);
+    Stage st_(L, "vgemm");
+    k_vgemm<<<grid, 256, 0, L.st>>>(mm, Rtot, rows, W, P, V);
+    LT_CU(cudaGetLastError());
+    L.tick();
+}
+
+// ---------------------------------------------------------------------------
+// box chain: per pair e, C[k][d] = sum_j Q_d(j) V_e(j + k n)   (Hankel A operand)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_hankel(int m0, long long Lc, long long n, int band, long long G,
+                                                const double* __restrict__ pwc,
+                                                const unsigned long long* __restrict__ plo,
+                                                const unsigned long long* __restrict__ phi,
+                                                const double* __restrict__ V, double* __restrict__ part, int splits) {
+    __shared__ GemmSmem sm;
+    const int width = 2 * band + 1;
+    const int nkt = static_cast<int>((Lc + kGBM - 1) / kGBM);
+    const int kt = blockIdx.x % nkt, dt = blockIdx.x / nkt;
+    const int e = blockIdx.y;
+    const int split = blockIdx.z;
+    const int mu = e % m0, nu = e / m0;
+    const long long k0c = static_cast<long long>(kt) * kGBM;
+    const int d0 = dt * kGBN;  // offset index (d + band)
+    const long long alo = static_cast<long long>(plo[mu]), ahi = static_cast<long long>(phi[mu]);
+    const long long blo = static_cast<long long>(plo[nu]), bhi = static_cast<long long>(phi[nu]);
+    const long long dmin = d0 - band, dmax = min(d0 + kGBN, width) - 1 - band;
+    const long long jlo = max(alo, blo + dmin * n), jhi = min(ahi, bhi + dmax * n);
+    const long long len = jhi > jlo ? jhi - jlo : 0;
+    const long long per = ((len + splits - 1) / splits + kGBK - 1) / kGBK * kGBK;
+    const long long j0 = jlo + split * per, j1 = min(jhi, j0 + per);
+    const double* a = pwc + mu * G;
+    const double* b = pwc + nu * G;
+    const double* v = V + static_cast<long long>(e) * G;
+    auto loadA = [&](int m, long long j) -> double {
+        const long long kc = k0c + m;
+        const long long gi = j + kc * n;
+        return (kc < Lc && gi < G) ? v[gi] : 0.0;
+    };
+    auto loadB = [&](long long j, int nn) -> double {
+        const int di = d0 + nn;
+        if (di >= width) return 0.0;
+        const long long jb = j - static_cast<long long>(di - band) * n;
+        return (j >= alo && j < ahi && jb >= blo && jb < bhi) ? a[j] * b[jb] : 0.0;
+    };
+    double acc[4][4] = {};
+    cta_gemm_64x64(loadA, loadB, j0, j1, acc, sm);
+    double* out = part + (static_cast<long long>(split) * m0 * m0 + e) * Lc * width;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            int m, nn;
+            acc_coord(nt, i, m, nn);
+            if (k0c + m < Lc && d0 + nn < width) out[(k0c + m) * width + d0 + nn] = acc[nt][i];
+        }
+}
+
+// N[(k*width + d)][e] = sum_split part[split][e][k][d]
+__global__ void k_split_reduce(long long mm, long long kd, int splits, const double* __restrict__ part,
+                               double* __restrict__ N) {
+    const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= mm * kd) return;
+    const long long e = idx % mm, q = idx / mm;
+    double s = 0.0;
+    for (int sp = 0; sp < splits; ++sp) s += part[(sp * mm + e) * kd + q];
+    N[idx] = s;
+}
+
+void launch_hankel(const Launch& L, int m0, const DirPlan& d, const double* pwc, const unsigned long long* lo,
+                   const unsigned long long* hi, const double* V, double* part, double* N, int splits) {
+    const int nkt = static_cast<int>((d.L + kGBM - 1) / kGBM);
+    const int ndt = static_cast<int>((d.width + kGBN - 1) / kGBN);
+    dim3 grid(nkt * ndt, m0 * m0, splits);
+    {
+        Stage st_(L, "hankel_gemm");
+        k_hankel<<<grid, 256, 0, L.st>>>(m0, d.L, d.n, static_cast<int>(d.band), d.G, pwc, lo, hi, V, part, splits);
+        LT_CU(cudaGetLastError());
+    }
+    const long long mm = m0 * m0, kd = d.L * d.width;
+    Stage st2_(L, "split_reduce");
+    k_split_reduce<<<static_cast<unsigned>((mm * kd + 255) / 256), 256, 0, L.st>>>(mm, kd, splits, part, N);
+    LT_CU(cudaGetLastError());
+    L.tick(2);
+}
+
+// ---------------------------------------------------------------------------
+// periodic fold on DMMA: CTA per (residue t, d-chunk); A_t[mu][j] = a_mu(t + j n) in smem
+// ---------------------------------------------------------------------------
+// mode 0 (single non-trivial direction): part[t][d][e] = V[e][t] * Qf_t[d](e)
+// mode 1 (several): Qf[d][e][t]
+__global__ void __launch_bounds__(256) k_fold_dmma(int m0, int m0p, long long n, long long J, int band, int dchunk,
+                                                   long long G, const double* __restrict__ pwc,
+                                                   const double* __restrict__ V, int mode, double* __restrict__ out) {
+    extern __shared__ double At[];  // [m0p][J + 4]
+    const long long t = blockIdx.x;
+    const int dc = blockIdx.y;
+    const long long ldj = J + 4;
+    for (long long idx = threadIdx.x; idx < static_cast<long long>(m0p) * J; idx += blockDim.x) {
+        const int mu = static_cast<int>(idx / J);
+        const long long j = idx % J;
+        At[mu * ldj + j] = mu < m0 ? pwc[mu * G + t + j * n] : 0.0;
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, tq = lane & 3;
+    const int ntile = m0p / 8;
+    const int dlo = dc * dchunk, dhi = min(band, dlo + dchunk - 1);
+    const int tasks = (dhi - dlo + 1) * ntile * ntile;
+    const int mm = m0 * m0;
+    for (int task = warp; task < tasks; task += blockDim.x >> 5) {
+        const int d = dlo + task / (ntile * ntile);
+        const int mt = (task / ntile) % ntile, nt = task % ntile;
+        double c[2] = {0.0, 0.0};
+        const double* arow = At + (mt * 8 + g) * ldj;
+        const double* brow = At + (nt * 8 + g) * ldj;
+        // j runs over [d, J): B element (j - d)
+        for (long long j = d; j < J; j += 4) {
+            const long long ja = j + tq;
+            const double av = ja < J ? arow[ja] : 0.0;
+            const double bv = ja < J ? brow[ja - d] : 0.0;
+            dmma_m8n8k4(c, av, bv);
+        }
+        // c[i] -> (mu = mt*8 + g, nu = nt*8 + 2 tq + i)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int mu = mt * 8 + g, nu = nt * 8 + 2 * tq + i;
+            if (mu >= m0 || nu >= m0) continue;
+            const int e = mu + nu * m0;
+            if (mode == 0) out[(t * (band + 1) + d) * mm + e] = V[e * n + t] * c[i];
+            else out[(static_cast<long long>(d) * mm + e) * n + t] = c[i];
+        }
+    }
+}
+
+// mode 0 reduction over t, d >= 0, then mirror: N[(d+band)][e] and N[(-d+band)][e^T]
+__global__ void k_fold_reduce(int m0, long long n, int band, const double* __restrict__ part, double* __restrict__ N) {
+    const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int mm = m0 * m0;
+    if (idx >= static_cast<long long>(band + 1) * mm) return;
+    const int d = static_cast<int>(idx / mm), e = static_cast<int>(idx % mm);
+    double s = 0.0;
+    for (long long t = 0; t < n; ++t) s += part[(t * (band + 1) + d) * mm + e];
+    const int mu = e % m0, nu = e / m0;
+    N[(d + band) * mm + e] = s;
+    if (d > 0) N[(band - d) * mm + nu + mu * m0] = s;
+}
+
+void launch_fold_dmma(const Launch& L, int m0, const DirPlan& d, const double* pwc, const double* V, int mode,
+                      double* out, double* N) {
+    const int m0p = (m0 + 7) / 8 * 8;
+    const long long J = d.G / d.n;
+    const int band = static_cast<int>(d.band);
+    const int dchunk = std::max(1, (band + 1 + 3) / 4);
+    const int nd = (band + 1 + dchunk - 1) / dchunk;
+    const size_t smem = sizeof(double) * m0p * (J + 4);
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+        LT_CU(cudaFuncSetAttribute(k_fold_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        attr = smem;
+    }
+    dim3 grid(static_cast<unsigned>(d.n), nd);
+    {
+        Stage st_(L, "fold_dmma");
+        k_fold_dmma<<<grid, 256, smem, L.st>>>(m0, m0p, d.n, J, band, dchunk, d.G, pwc, V, mode, out);
+        LT_CU(cudaGetLastError());
+        L.tick();
+    }
+    if (mode == 0) {
+        const long long tot = static_cast<long long>(band + 1) * m0 * m0;
+        Stage st2_(L, "fold_reduce");
+        k_fold_reduce<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, L.st>>>(m0, d.n, band, out, N);
+        LT_CU(cudaGetLastError());
+        L.tick();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// several wrapped directions: T[d][r][e] = sum_t P[r][t] Qf[d][e][t] (d >= 0), DMMA GEMM
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_fgemm(int mm, int Rtot, long long n, int ncols, const double* __restrict__ P,
+                                               const double* __restrict__ Qf, double* __restrict__ T) {
+    __shared__ GemmSmem sm;
+    const int r0 = blockIdx.y * kGBM;
+    const int c0 = blockIdx.x * kGBN;  // column = d*mm + e
+    auto loadA = [&](int m, long long k) -> double { return r0 + m < Rtot ? P[(r0 + m) * n + k] : 0.0; };
+    auto loadB = [&](long long k, int nn) -> double { return c0 + nn < ncols ? Qf[(c0 + nn) * n + k] : 0.0; };
+    double acc[4][4] = {};
+    cta_gemm_64x64(loadA, loadB, 0, n, acc, sm);
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            int m, nn;
+            acc_coord(nt, i, m, nn);
+            if (r0 + m < Rtot && c0 + nn < ncols) {
+                const int col = c0 + nn;
+                const int dd = col / mm, e = col % mm;
+                T[(static_cast<long long>(dd) * Rtot + r0 + m) * mm + e] = acc[nt][i];
+            }
+        }
+}
+
+void launch_fgemm(const Launch& L, int m0, int Rtot, const DirPlan& d, const double* P, const double* Qf, double* T) {
+    const int mm = m0 * m0;
+    const int ncols = static_cast<int>(d.band + 1) * mm;
+    dim3 grid((ncols + kGBN - 1) / kGBN, (Rtot + kGBM - 1) / kGBM);
+    Stage st_(L, "fold_gemm");
+    k_fgemm<<<grid, 256, 0, L.st>>>(mm, Rtot, d.n, ncols, P, Qf, T);
+    LT_CU(cudaGetLastError());
+    L.tick();
+}
+
+// Khatri-Rao combine: N[d0,d1,d2][e] = sum_r W[r][e] prod_{l wrapped} T_l[d_l][r][e]
+// (T_l stored for d >= 0; T_l[-d][r][(mu,nu)] = T_l[d][r][(nu,mu)]). CTA per (e, d0).
+__global__ void k_kr_combine(KRArgs a) {
+    extern __shared__ double sh[];
+    const int e = blockIdx.x;
+    const int i0 = blockIdx.y;  // d0 index in [0, width0)
+    const int mm = a.m0 * a.m0;
+    const int mu = e % a.m0, nu = e / a.m0;
+    const int eT = nu + mu * a.m0;
+    double* w0 = sh;                    // [Rtot]: W * T0[d0]
+    double* t1 = sh + a.Rtot;           // [width1][Rtot]
+    double* t2 = t1 + a.width[1] * a.Rtot;  // [width2][Rtot]
+    auto tab = [&](int l, int di, int r) -> double {
+        if (!a.T[l]) return 1.0;
+        const int d = di - a.band[l];
+        const int ad = d < 0 ? -d : d;
+        const int ee = d < 0 ? eT : e;
+        return a.T[l][(static_cast<long long>(ad) * a.Rtot + r) * mm + ee];
+    };
+    for (int r = threadIdx.x; r < a.Rtot; r += blockDim.x) w0[r] = a.W[r * mm + e] * tab(0, i0, r);
+    for (int q = threadIdx.x; q < a.width[1] * a.Rtot; q += blockDim.x) t1[q] = tab(1, q / a.Rtot, q % a.Rtot);
+    for (int q = threadIdx.x; q < a.width[2] * a.Rtot; q += blockDim.x) t2[q] = tab(2, q / a.Rtot, q % a.Rtot);
+    __syncthreads();
+    const int nout = a.width[1] * a.width[2];
+    for (int o = threadIdx.x; o < nout; o += blockDim.x) {
+        const int i1 = o / a.width[2], i2 = o % a.width[2];
+        double s = 0.0;
+        for (int r = 0; r < a.Rtot; ++r) s += w0[r] * t1[i1 * a.Rtot + r] * t2[i2 * a.Rtot + r];
+        const long long dlin = (static_cast<long long>(i0) * a.width[1] + i1) * a.width[2] + i2;
+        a.N[dlin * mm + e] = s;
+    }
+}
+
+void launch_kr_combine(const Launch& L, const KRArgs& a) {
+    const size_t smem = sizeof(double) * a.Rtot * (1 + a.width[1] + a.width[2]);
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+        LT_CU(cudaFuncSetAttribute(k_kr_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        attr = smem;
+    }
+    dim3 grid(a.m0 * a.m0, a.width[0]);
+    Stage st_(L, "kr_combine");
+    k_kr_combine<<<grid, 128, smem, L.st>>>(a);
+    LT_CU(cudaGetLastError());
+    L.tick();
+}
+
+}  // namespace lt

@@ -108,6 +108,7 @@ public:
         return static_cast<T*>(raw(key, count * sizeof(T) + 16));
     }
     size_t bytes() const;
+    uint64_t generation() const { return gen_; }  // bumps on every (re)allocation
 
 private:
     struct Buf {
@@ -115,6 +116,7 @@ private:
         size_t cap = 0;
     };
     std::map<std::string, Buf> bufs_;
+    uint64_t gen_ = 0;
 };
 
 // ---------------------------------------------------------------------------
@@ -218,6 +220,38 @@ void launch_box_v(const Launch& L, Index m0, Index Rtot, Index G, const double* 
 void launch_box_corr(const Launch& L, Index m0, const DirPlan& d, const double* pwc, const unsigned long long* lo,
                      const unsigned long long* hi, const double* V, double* Npart, double* N, int nsplit);
 
+// ---- DMMA nuclear contraction (k_nuclear2.cu) ----
+struct TrivJob {
+    const double* pot = nullptr;  // potential panel [Rtot][rows]
+    long long rows = 0;
+    const double* pwc = nullptr;  // profiles [m0][G]
+    long long G = 0;
+    const unsigned long long* lo = nullptr;
+    const unsigned long long* hi = nullptr;
+};
+struct TrivJobs {
+    TrivJob j[3];
+};
+struct WSpec {
+    int job_of_dir[3] = {-1, -1, -1};  // trivial direction -> job (directions may share one)
+};
+struct KRArgs {
+    int m0 = 0, Rtot = 0;
+    int width[3] = {1, 1, 1}, band[3] = {0, 0, 0};
+    const double* T[3] = {nullptr, nullptr, nullptr};  // [d>=0][r][e] per wrapped direction
+    const double* W = nullptr;
+    double* N = nullptr;
+};
+void launch_triv_tables(const Launch& L, const TrivJobs& jobs, int njobs, const WSpec& ws, int m0, int Rtot,
+                        const double* potw, double* part, int splits, double* W, double* Tout);
+void launch_vgemm(const Launch& L, int mm, int Rtot, long long rows, const double* W, const double* P, double* V);
+void launch_hankel(const Launch& L, int m0, const DirPlan& d, const double* pwc, const unsigned long long* lo,
+                   const unsigned long long* hi, const double* V, double* part, double* N, int splits);
+void launch_fold_dmma(const Launch& L, int m0, const DirPlan& d, const double* pwc, const double* V, int mode,
+                      double* out, double* N);
+void launch_fgemm(const Launch& L, int m0, int Rtot, const DirPlan& d, const double* P, const double* Qf, double* T);
+void launch_kr_combine(const Launch& L, const KRArgs& a);
+
 // fill H/S (box dense, periodic generating blocks); mode 0 core (H,S), 1 Laplace, 2 Mass, 3 Nuclear
 struct FillArgs {
     Index m0 = 0, Rtot = 0, L[3]{1, 1, 1}, band[3]{}, width[3]{1, 1, 1};
@@ -225,8 +259,9 @@ struct FillArgs {
     const double* stiffT[3]{};
     const double* T[3]{};      // nuclear tables [pair][r][e]
     const double* potw = nullptr;
-    const double* N = nullptr; // S2 nuclear blocks [k][d][e] along s2_dir
+    const double* N = nullptr; // nuclear blocks: [k][d][e] along s2_dir, or [dlin][e] (nuc_mode 2)
     int s2_dir = -1;
+    int nuc_mode = 0;          // 0 tables, 1 N along s2_dir, 2 N by dlin
     int mode = 0;
     bool periodic = false;
     double* out0 = nullptr;    // H (or single operator)
