@@ -98,6 +98,15 @@ void StageTimer::reset() {
 
 using namespace lt;
 
+struct GraphCache {
+    cudaGraphExec_t exec = nullptr;
+    std::vector<int64_t> key, seen;
+    int64_t launches = 0;
+    ~GraphCache() {
+        if (exec) cudaGraphExecDestroy(exec);
+    }
+};
+
 struct lt_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -105,13 +114,56 @@ struct lt_ctx {
     Arena arena;
     int64_t launches = 0;
     StageTimer timer;
-    // CUDA graph of the post-L0 launch sequence (captured on the second identical call)
+    // CUDA graphs of the L0 sequence and of the post-L0 launch sequence
     bool graphs = true;
-    cudaGraphExec_t gexec = nullptr;
-    std::vector<int64_t> gkey, gseen;
-    int64_t glaunches = 0;
+    GraphCache l0graph, coregraph;
+    int* pinned = nullptr;  // small pinned read-back buffer
     Launch L() { return Launch{stream, &launches, &timer}; }
+    int* pinned_state() {
+        if (!pinned) LT_CU(cudaHostAlloc(reinterpret_cast<void**>(&pinned), 64 * sizeof(int), cudaHostAllocDefault));
+        return pinned;
+    }
 };
+
+namespace lt {
+// Replay a captured launch sequence when the key (every host-derived parameter, pointer
+// and the arena generation) matches; capture on the second identical call (the first runs
+// eagerly so the arena is sized and no allocation happens inside a capture).
+template <class K, class F>
+static void run_cached(lt_ctx* c, GraphCache& g, K&& keyfn, F&& enqueue) {
+    const bool allow = c->graphs && !c->timer.on;
+    const std::vector<int64_t> key = keyfn();
+    if (allow && g.exec && key == g.key) {
+        LT_CU(cudaGraphLaunch(g.exec, c->stream));
+        c->launches += g.launches;
+        return;
+    }
+    if (allow && key == g.seen) {
+        const int64_t l0 = c->launches;
+        cudaGraph_t graph = nullptr;
+        LT_CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        try {
+            enqueue();
+        } catch (...) {
+            cudaStreamEndCapture(c->stream, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            throw;
+        }
+        LT_CU(cudaStreamEndCapture(c->stream, &graph));
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        g.exec = nullptr;
+        const cudaError_t e = cudaGraphInstantiate(&g.exec, graph, 0);
+        cudaGraphDestroy(graph);
+        LT_CU(e);
+        g.key = key;
+        g.launches = c->launches - l0;
+        LT_CU(cudaGraphLaunch(g.exec, c->stream));
+        return;
+    }
+    enqueue();
+    g.seen = keyfn();
+}
+}  // namespace lt
 
 struct lt_sysdev {
     HostSys hs;
@@ -195,6 +247,9 @@ static lt_sysdev* make_sysdev(const lt_system* s, void* dst = nullptr, cudaStrea
     return sd.release();
 }
 
+static std::vector<int64_t> graph_key(const HostSys& h, const Plan& p, bool periodic, Index kb, Index ke,
+                                      const void* eig, const void* sysmem, uint64_t gen);
+
 // ---------------------------------------------------------------------------
 // L0 (gto_basis.cpp:87-126)
 // ---------------------------------------------------------------------------
@@ -214,23 +269,32 @@ static Index compute_L0(lt_ctx* c, const lt_sysdev* sd) {
     OverlapBufs b;
     b.prof = c->arena.get<double>("l0.prof", tot);
     b.bmax = c->arena.get<double>("l0.bmax", btot);
+    b.nz = c->arena.get<unsigned>("l0.nz", 6 * m0);
     b.found = c->arena.get<int>("l0.found", 260);
-    b.state = c->arena.get<int>("l0.state", 4);
+    b.state = c->arena.get<int>("l0.state", 8);
     const Launch L = c->L();
-    launch_overlap_init(L, b);
-    launch_overlap_profiles(L, sd->ds, n3, off3, boff3, b);
-    int s_begin = 1;
-    const int chunk = 32;
-    while (true) {
+    const int chunk = 16;  // shifts per scan launch; L0 + 2 <= 16 needs a single launch
+    int* st = c->pinned_state();
+    // first chunk as one replayable sequence: init, sample, scan (+ fused rule), read-back
+    auto first = [&]() {
+        launch_overlap_init(L, b, static_cast<int>(m0));
+        launch_overlap_profiles(L, sd->ds, n3, off3, boff3, b);
+        launch_overlap_scan(L, sd->ds, n3, off3, boff3, b, 1, 1 + chunk);
+        LT_CU(cudaMemcpyAsync(st, b.state, 4 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    };
+    run_cached(
+        c, c->l0graph,
+        [&]() { return graph_key(h, Plan{}, false, -1, -1, st, sd->mem, c->arena.generation()); }, first);
+    LT_CU(cudaStreamSynchronize(c->stream));
+    int s_begin = 1 + chunk;
+    while (!st[3] && s_begin < 257) {
         const int s_end = std::min(257, s_begin + chunk);
         launch_overlap_scan(L, sd->ds, n3, off3, boff3, b, s_begin, s_end);
-        launch_overlap_finalize(L, b, s_begin, s_end);
-        int st[4];
-        LT_CU(cudaMemcpyAsync(st, b.state, sizeof(st), cudaMemcpyDeviceToHost, c->stream));
+        LT_CU(cudaMemcpyAsync(st, b.state, 4 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
         LT_CU(cudaStreamSynchronize(c->stream));
-        if (st[3] || s_end >= 257) return st[0];
         s_begin = s_end;
     }
+    return st[0];
 }
 
 // ---------------------------------------------------------------------------
@@ -275,9 +339,10 @@ static void direction_sources(const HostSys& h, int src[3]) {
     }
 }
 
+// split-K factor: aim for ~4 CTAs per SM while keeping >= 64 contraction steps per CTA
 static int splits_for(long long tiles, long long len) {
     int s = 1;
-    while (tiles * s < 2 * 148 && len / (s * 2) >= 256 && s < 64) s *= 2;
+    while (tiles * s < 4 * 148 && len / (s * 2) >= 64 && s < 256) s *= 2;
     return s;
 }
 
@@ -361,7 +426,25 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
             w.pwl_hi[l] = w.pwl_hi[src[l]];
         }
     launch_profiles(L, sd->ds, jobs, nj, 1e-280);
-    if (ms)
+    if (ms) {
+        // FEM-applied profiles (T v) for every distinct direction, then the tables as
+        // residue-class correlations <u_mu, (T v_nu)(. - d nbar)> on DMMA
+        FemApplyJobs fj{};
+        int nfj = 0;
+        double *wm[3] = {}, *wsf[3] = {};
+        for (int l = 0; l < 3; ++l) {
+            if (src[l] != l) continue;
+            const DirPlan& d = p.d[l];
+            FemApplyJob& J = fj.j[nfj++];
+            J.pwl = w.pwl[l];
+            J.Gbar = d.Gbar;
+            J.hbar = d.hbar;
+            J.lo = w.pwl_lo[l];
+            J.hi = w.pwl_hi[l];
+            J.wm = wm[l] = A.get<double>("fem.wm" + std::to_string(l), m0 * (d.Gbar + 2));
+            J.ws = wsf[l] = A.get<double>("fem.ws" + std::to_string(l), m0 * (d.Gbar + 2));
+        }
+        launch_fem_apply(L, fj, nfj, static_cast<int>(m0));
         for (int l = 0; l < 3; ++l) {
             if (src[l] != l) {
                 w.massT[l] = w.massT[src[l]];
@@ -371,9 +454,28 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
             const DirPlan& d = p.d[l];
             w.massT[l] = A.get<double>("fem.mass" + std::to_string(l), d.width * mm);
             w.stiffT[l] = A.get<double>("fem.stiff" + std::to_string(l), d.width * mm);
-            launch_fem_tables(L, m0, d.band, d.nbar, d.hbar, d.Gbar, w.pwl[l], w.pwl_lo[l], w.pwl_hi[l], w.massT[l],
-                              w.stiffT[l]);
+            ResFold f;
+            f.m0 = static_cast<int>(m0);
+            f.n = d.nbar;
+            f.J = d.Gbar / d.nbar;
+            f.G = d.Gbar;
+            f.a = w.pwl[l];
+            f.b[0] = wm[l];
+            f.b[1] = wsf[l];
+            f.nb = 2;
+            f.bguard = 1;
+            f.band = static_cast<int>(d.band);
+            f.dlo = -f.band;
+            f.dhi = f.band;
+            f.dchunk = std::max(1, static_cast<int>((d.width + 3) / 4));
+            f.out[0] = A.get<double>("fem.pm" + std::to_string(l), d.nbar * d.width * mm);
+            f.out[1] = A.get<double>("fem.ps" + std::to_string(l), d.nbar * d.width * mm);
+            f.res[0] = w.massT[l];
+            f.res[1] = w.stiffT[l];
+            f.slab = A.get<double>("fem.slab" + std::to_string(l), resfold_slab_doubles(f));
+            launch_resfold(L, f, true, false, "fem_fold");
         }
+    }
     // nuclear contraction: choose the reassociation (k_nuclear2.cu header)
     int nuc_mode = 0, ndir = -1;
     if (nuc) {
@@ -426,8 +528,22 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
                     launch_hankel(L, static_cast<int>(m0), d, w.pwc[ndir], w.pwc_lo[ndir], w.pwc_hi[ndir], V, hp, w.N,
                                   sp);
                 } else {
-                    double* fp = A.get<double>("nuc.fpart", d.n * (d.band + 1) * mm);
-                    launch_fold_dmma(L, static_cast<int>(m0), d, w.pwc[ndir], V, 0, fp, w.N);
+                    ResFold f;
+                    f.m0 = static_cast<int>(m0);
+                    f.n = d.n;
+                    f.J = d.G / d.n;
+                    f.G = d.G;
+                    f.a = f.b[0] = w.pwc[ndir];
+                    f.nb = 1;
+                    f.band = static_cast<int>(d.band);
+                    f.dlo = 0;
+                    f.dhi = f.band;
+                    f.dchunk = std::max(1, (f.band + 1 + 3) / 4);
+                    f.V = V;
+                    f.out[0] = A.get<double>("nuc.fpart", d.n * (d.band + 1) * mm);
+                    f.res[0] = w.N;
+                    f.slab = A.get<double>("nuc.slab", resfold_slab_doubles(f));
+                    launch_resfold(L, f, true, true, "nuc_fold");
                 }
             } else {
                 KRArgs kr;
@@ -444,7 +560,20 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
                         const DirPlan& d = p.d[s];
                         double* Qf = A.get<double>("nuc.Qf" + std::to_string(s), (d.band + 1) * mm * d.n);
                         Tl[s] = A.get<double>("nuc.T" + std::to_string(s), (d.band + 1) * Rtot * mm);
-                        launch_fold_dmma(L, static_cast<int>(m0), d, w.pwc[s], nullptr, 1, Qf, nullptr);
+                        ResFold f;
+                        f.m0 = static_cast<int>(m0);
+                        f.n = d.n;
+                        f.J = d.G / d.n;
+                        f.G = d.G;
+                        f.a = f.b[0] = w.pwc[s];
+                        f.nb = 1;
+                        f.band = static_cast<int>(d.band);
+                        f.dlo = 0;
+                        f.dhi = f.band;
+                        f.dchunk = std::max(1, (f.band + 1 + 3) / 4);
+                        f.out[0] = Qf;  // [t][d][e]
+                        f.slab = A.get<double>("nuc.slab" + std::to_string(s), resfold_slab_doubles(f));
+                        launch_resfold(L, f, false, false, "nuc_fold");
                         launch_fgemm(L, static_cast<int>(m0), static_cast<int>(Rtot), d, w.pot[s], Qf, Tl[s]);
                     }
                     kr.T[l] = Tl[s];
@@ -749,36 +878,10 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
             box_eig_device(c, p.Nb, out.out0, out.out1, eig_dev, fk);
         }
     };
-    const bool use_graph = c->graphs && !c->timer.on;
-    std::vector<int64_t> key =
-        graph_key(sd->hs, p, periodic, k_begin, k_end, eig_dev, sd->mem, c->arena.generation());
-    if (use_graph && c->gexec && key == c->gkey) {
-        LT_CU(cudaGraphLaunch(c->gexec, c->stream));
-        c->launches += c->glaunches;
-    } else if (use_graph && key == c->gseen) {
-        // second identical call: capture the launch sequence once and replay it from now on
-        const int64_t l0 = c->launches;
-        cudaGraph_t g = nullptr;
-        LT_CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-        try {
-            enqueue();
-        } catch (...) {
-            cudaStreamEndCapture(c->stream, &g);
-            if (g) cudaGraphDestroy(g);
-            throw;
-        }
-        LT_CU(cudaStreamEndCapture(c->stream, &g));
-        if (c->gexec) cudaGraphExecDestroy(c->gexec);
-        c->gexec = nullptr;
-        LT_CU(cudaGraphInstantiate(&c->gexec, g, 0));
-        cudaGraphDestroy(g);
-        c->gkey = key;
-        c->glaunches = c->launches - l0;
-        LT_CU(cudaGraphLaunch(c->gexec, c->stream));
-    } else {
-        enqueue();
-        c->gseen = graph_key(sd->hs, p, periodic, k_begin, k_end, eig_dev, sd->mem, c->arena.generation());
-    }
+    run_cached(
+        c, c->coregraph,
+        [&]() { return graph_key(sd->hs, p, periodic, k_begin, k_end, eig_dev, sd->mem, c->arena.generation()); },
+        enqueue);
     if (!periodic && !small_box) box_eig_device(c, p.Nb, out.out0, out.out1, eig_dev, fk);
     unsigned long long fkey = ~0ull;
     LT_CU(cudaMemcpyAsync(&fkey, fk, sizeof(fkey), cudaMemcpyDeviceToHost, c->stream));
@@ -857,7 +960,7 @@ void lt_destroy(lt_ctx* c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->solver) cusolverDnDestroy(c->solver);
-    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    if (c->pinned) cudaFreeHost(c->pinned);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }

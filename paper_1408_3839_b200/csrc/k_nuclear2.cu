@@ -83,24 +83,25 @@ __global__ void __launch_bounds__(256) k_triv_gemm(TrivJobs jobs, int m0, int Rt
 
 // W[r][e] = w_r * prod over trivial directions of T_l[r][e] (T_l reduced over splits in
 // fixed order); e over all m0^2 ordered pairs (mirror of the symmetric index)
+// one warp per (r, symmetric pair): split-K partials summed in a fixed lane/tree order
 __global__ void k_triv_reduce_w(const double* __restrict__ part, int njobs, const int* dir_job_unused, WSpec ws,
                                 int m0, int Rtot, int nsym, int splits, const double* __restrict__ potw,
                                 double* __restrict__ W, double* __restrict__ Tout) {
-    const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const long long wid = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int mm = m0 * m0;
-    if (idx >= static_cast<long long>(Rtot) * mm) return;
-    const int r = static_cast<int>(idx / mm), e = static_cast<int>(idx % mm);
-    const int mu0 = e % m0, nu0 = e / m0;
-    const int mu = min(mu0, nu0), nu = max(mu0, nu0);
-    const int es = mu * m0 - mu * (mu - 1) / 2 + (nu - mu);
-    double w = potw[r];
+    if (wid >= static_cast<long long>(Rtot) * nsym) return;
+    const int r = static_cast<int>(wid / nsym), es = static_cast<int>(wid % nsym);
+    int mu, nu;
+    sym_pair(es, m0, mu, nu);
     double tj[3] = {1.0, 1.0, 1.0};
     for (int j = 0; j < njobs; ++j) {
         double s = 0.0;
-        for (int sp = 0; sp < splits; ++sp) s += part[((static_cast<long long>(j) * splits + sp) * Rtot + r) * nsym + es];
-        tj[j] = s;
-        if (Tout) Tout[(static_cast<long long>(j) * Rtot + r) * mm + e] = s;
+        for (int sp = lane; sp < splits; sp += 32)
+            s += part[((static_cast<long long>(j) * splits + sp) * Rtot + r) * nsym + es];
+        tj[j] = __shfl_sync(0xffffffffu, warp_sum(s), 0);
     }
+    if (lane != 0) return;
     // product in direction order (directions may share a job)
     double prod = 1.0;
     bool first = true;
@@ -110,7 +111,14 @@ __global__ void k_triv_reduce_w(const double* __restrict__ part, int njobs, cons
         prod = first ? v : prod * v;
         first = false;
     }
-    W[idx] = w * prod;
+    const double wv = potw[r] * prod;
+    W[r * mm + mu + nu * m0] = wv;
+    W[r * mm + nu + mu * m0] = wv;
+    if (Tout)
+        for (int j = 0; j < njobs; ++j) {
+            Tout[(static_cast<long long>(j) * Rtot + r) * mm + mu + nu * m0] = tj[j];
+            Tout[(static_cast<long long>(j) * Rtot + r) * mm + nu + mu * m0] = tj[j];
+        }
 }
 
 void launch_triv_tables(const Launch& L, const TrivJobs& jobs, int njobs, const WSpec& ws, int m0, int Rtot,
@@ -123,10 +131,10 @@ void launch_triv_tables(const Launch& L, const TrivJobs& jobs, int njobs, const 
         LT_CU(cudaGetLastError());
         L.tick();
     }
-    const long long tot = static_cast<long long>(Rtot) * m0 * m0;
+    const long long warps = static_cast<long long>(Rtot) * nsym;
     Stage st2_(L, "triv_reduce_w");
-    k_triv_reduce_w<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, L.st>>>(part, njobs, nullptr, ws, m0, Rtot,
-                                                                              nsym, splits, potw, W, Tout);
+    k_triv_reduce_w<<<static_cast<unsigned>((warps + 7) / 8), 256, 0, L.st>>>(part, njobs, nullptr, ws, m0, Rtot,
+                                                                            nsym, splits, potw, W, Tout);
     LT_CU(cudaGetLastError());
     L.tick();
 }
@@ -241,97 +249,6 @@ void launch_hankel(const Launch& L, int m0, const DirPlan& d, const double* pwc,
 }
 
 // ---------------------------------------------------------------------------
-// periodic fold on DMMA: CTA per (residue t, d-chunk); A_t[mu][j] = a_mu(t + j n) in smem
-// ---------------------------------------------------------------------------
-// mode 0 (single non-trivial direction): part[t][d][e] = V[e][t] * Qf_t[d](e)
-// mode 1 (several): Qf[d][e][t]
-__global__ void __launch_bounds__(256) k_fold_dmma(int m0, int m0p, long long n, long long J, int band, int dchunk,
-                                                   long long G, const double* __restrict__ pwc,
-                                                   const double* __restrict__ V, int mode, double* __restrict__ out) {
-    extern __shared__ double At[];  // [m0p][J + 4]
-    const long long t = blockIdx.x;
-    const int dc = blockIdx.y;
-    const long long ldj = J + 4;
-    for (long long idx = threadIdx.x; idx < static_cast<long long>(m0p) * J; idx += blockDim.x) {
-        const int mu = static_cast<int>(idx / J);
-        const long long j = idx % J;
-        At[mu * ldj + j] = mu < m0 ? pwc[mu * G + t + j * n] : 0.0;
-    }
-    __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int g = lane >> 2, tq = lane & 3;
-    const int ntile = m0p / 8;
-    const int dlo = dc * dchunk, dhi = min(band, dlo + dchunk - 1);
-    const int tasks = (dhi - dlo + 1) * ntile * ntile;
-    const int mm = m0 * m0;
-    for (int task = warp; task < tasks; task += blockDim.x >> 5) {
-        const int d = dlo + task / (ntile * ntile);
-        const int mt = (task / ntile) % ntile, nt = task % ntile;
-        double c[2] = {0.0, 0.0};
-        const double* arow = At + (mt * 8 + g) * ldj;
-        const double* brow = At + (nt * 8 + g) * ldj;
-        // j runs over [d, J): B element (j - d)
-        for (long long j = d; j < J; j += 4) {
-            const long long ja = j + tq;
-            const double av = ja < J ? arow[ja] : 0.0;
-            const double bv = ja < J ? brow[ja - d] : 0.0;
-            dmma_m8n8k4(c, av, bv);
-        }
-        // c[i] -> (mu = mt*8 + g, nu = nt*8 + 2 tq + i)
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-            const int mu = mt * 8 + g, nu = nt * 8 + 2 * tq + i;
-            if (mu >= m0 || nu >= m0) continue;
-            const int e = mu + nu * m0;
-            if (mode == 0) out[(t * (band + 1) + d) * mm + e] = V[e * n + t] * c[i];
-            else out[(static_cast<long long>(d) * mm + e) * n + t] = c[i];
-        }
-    }
-}
-
-// mode 0 reduction over t, d >= 0, then mirror: N[(d+band)][e] and N[(-d+band)][e^T]
-__global__ void k_fold_reduce(int m0, long long n, int band, const double* __restrict__ part, double* __restrict__ N) {
-    const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int mm = m0 * m0;
-    if (idx >= static_cast<long long>(band + 1) * mm) return;
-    const int d = static_cast<int>(idx / mm), e = static_cast<int>(idx % mm);
-    double s = 0.0;
-    for (long long t = 0; t < n; ++t) s += part[(t * (band + 1) + d) * mm + e];
-    const int mu = e % m0, nu = e / m0;
-    N[(d + band) * mm + e] = s;
-    if (d > 0) N[(band - d) * mm + nu + mu * m0] = s;
-}
-
-void launch_fold_dmma(const Launch& L, int m0, const DirPlan& d, const double* pwc, const double* V, int mode,
-                      double* out, double* N) {
-    const int m0p = (m0 + 7) / 8 * 8;
-    const long long J = d.G / d.n;
-    const int band = static_cast<int>(d.band);
-    const int dchunk = std::max(1, (band + 1 + 3) / 4);
-    const int nd = (band + 1 + dchunk - 1) / dchunk;
-    const size_t smem = sizeof(double) * m0p * (J + 4);
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && smem > attr) {
-        LT_CU(cudaFuncSetAttribute(k_fold_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        attr = smem;
-    }
-    dim3 grid(static_cast<unsigned>(d.n), nd);
-    {
-        Stage st_(L, "fold_dmma");
-        k_fold_dmma<<<grid, 256, smem, L.st>>>(m0, m0p, d.n, J, band, dchunk, d.G, pwc, V, mode, out);
-        LT_CU(cudaGetLastError());
-        L.tick();
-    }
-    if (mode == 0) {
-        const long long tot = static_cast<long long>(band + 1) * m0 * m0;
-        Stage st2_(L, "fold_reduce");
-        k_fold_reduce<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, L.st>>>(m0, d.n, band, out, N);
-        LT_CU(cudaGetLastError());
-        L.tick();
-    }
-}
-
-// ---------------------------------------------------------------------------
 // several wrapped directions: T[d][r][e] = sum_t P[r][t] Qf[d][e][t] (d >= 0), DMMA GEMM
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_fgemm(int mm, int Rtot, long long n, int ncols, const double* __restrict__ P,
@@ -340,7 +257,8 @@ __global__ void __launch_bounds__(256) k_fgemm(int mm, int Rtot, long long n, in
     const int r0 = blockIdx.y * kGBM;
     const int c0 = blockIdx.x * kGBN;  // column = d*mm + e
     auto loadA = [&](int m, long long k) -> double { return r0 + m < Rtot ? P[(r0 + m) * n + k] : 0.0; };
-    auto loadB = [&](long long k, int nn) -> double { return c0 + nn < ncols ? Qf[(c0 + nn) * n + k] : 0.0; };
+    // Qf layout [t][d][e] (k_resfold): column (d, e) of residue t at t*ncols + d*mm + e
+    auto loadB = [&](long long k, int nn) -> double { return c0 + nn < ncols ? Qf[k * ncols + c0 + nn] : 0.0; };
     double acc[4][4] = {};
     cta_gemm_64x64(loadA, loadB, 0, n, acc, sm);
 #pragma unroll

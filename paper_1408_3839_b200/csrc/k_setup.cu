@@ -48,8 +48,12 @@ struct Dir3 {
     Index n[3], off[3], boff[3];
 };
 
+// Samples the untrimmed L0 profiles (gto_basis.cpp:95-97: width 2 (256+2) n, the
+// function in cell 258) and their block maxima. Values are stored only for blocks with a
+// non-zero maximum (the scan treats the others as zero), and the first/last non-zero
+// block of every profile is recorded so the scan only visits overlapping blocks.
 __global__ void __launch_bounds__(kL0Block) k_l0_sample(DevSys s, Dir3 d, double* __restrict__ prof,
-                                                        double* __restrict__ bmax) {
+                                                        double* __restrict__ bmax, unsigned* __restrict__ nz) {
     const int l = blockIdx.z, mu = blockIdx.y;
     const Index n = d.n[l];
     const Index width = 2 * (kMaxL0 + 2) * n;
@@ -58,11 +62,10 @@ __global__ void __launch_bounds__(kL0Block) k_l0_sample(DevSys s, Dir3 d, double
     const double h = s.b / static_cast<double>(n);
     const Index base = (kMaxL0 + 2) * n;
     const Index i = static_cast<Index>(blockIdx.x) * kL0Block + threadIdx.x;
-    double av = 0.0;
+    double av = 0.0, v = 0.0;
     if (i < width) {
         const double x = __dsub_rn(__dmul_rn(__dadd_rn(static_cast<double>(i - base), 0.5), h), __dmul_rn(0.5, s.b));
-        const double v = gto_eval1d(s, mu, l, x);
-        prof[d.off[l] + mu * width + i] = v;
+        v = gto_eval1d(s, mu, l, x);
         av = fabs(v);
     }
     // block max of |v| (exact: max is order independent)
@@ -70,10 +73,15 @@ __global__ void __launch_bounds__(kL0Block) k_l0_sample(DevSys s, Dir3 d, double
     __shared__ double wm[kL0Block / 32];
     if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = av;
     __syncthreads();
+    double m = wm[0];
+    for (int k = 1; k < kL0Block / 32; ++k) m = fmax(m, wm[k]);
+    if (m > 0.0 && i < width) prof[d.off[l] + mu * width + i] = v;
     if (threadIdx.x == 0) {
-        double m = wm[0];
-        for (int k = 1; k < kL0Block / 32; ++k) m = fmax(m, wm[k]);
         bmax[d.boff[l] + mu * nblk + blockIdx.x] = m;
+        if (m > 0.0) {
+            atomicMin(&nz[(l * s.m0 + mu) * 2], static_cast<unsigned>(blockIdx.x));
+            atomicMax(&nz[(l * s.m0 + mu) * 2 + 1], static_cast<unsigned>(blockIdx.x));
+        }
     }
 }
 
@@ -90,76 +98,124 @@ void launch_overlap_profiles(const Launch& L, const DevSys& s, const Index* n3, 
     }
     dim3 grid(static_cast<unsigned>(nbmax), s.m0, 3);
     Stage st_(L, "l0_sample");
-    k_l0_sample<<<grid, kL0Block, 0, L.st>>>(s, d, b.prof, b.bmax);
+    k_l0_sample<<<grid, kL0Block, 0, L.st>>>(s, d, b.prof, b.bmax, b.nz);
     LT_CU(cudaGetLastError());
     L.tick();
 }
 
-__global__ void k_l0_init(int* found, int* state) {
+
+__global__ void k_l0_init(int* found, int* state, unsigned* nz, int nnz) {
     for (int i = threadIdx.x; i <= kMaxL0; i += blockDim.x) found[i] = 0;
+    for (int i = threadIdx.x; i < nnz; i += blockDim.x) nz[i] = (i & 1) ? 0u : 0xffffffffu;
     if (threadIdx.x == 0) {
         state[0] = 0;  // L0
         state[1] = 0;  // misses
         state[2] = 1;  // next s
         state[3] = 0;  // done
+        state[4] = 0;  // finished-block counter of the fused scan/finalize
     }
 }
 
-void launch_overlap_init(const Launch& L, OverlapBufs b) {
+void launch_overlap_init(const Launch& L, OverlapBufs b, int m0) {
     Stage st_(L, "l0_init");
-    k_l0_init<<<1, 256, 0, L.st>>>(b.found, b.state);
+    k_l0_init<<<1, 256, 0, L.st>>>(b.found, b.state, b.nz, 3 * m0 * 2);
     LT_CU(cudaGetLastError());
     L.tick();
 }
 
-// one warp per (s, l, mu, nu)
+// the reference's sequential rule: L0 = last s with worst >= eps; stop after 2 misses
+__device__ void l0_finalize(const int* found, int* state, int s_end) {
+    int L0 = state[0], misses = state[1], sft = state[2];
+    for (; sft <= kMaxL0 && sft < s_end && misses < 2; ++sft) {
+        if (__ldcg(&found[sft])) {
+            L0 = sft;
+            misses = 0;
+        } else {
+            ++misses;
+        }
+    }
+    state[0] = L0;
+    state[1] = misses;
+    state[2] = sft;
+    state[3] = (misses >= 2 || sft > kMaxL0) ? 1 : 0;
+}
+
+// One warp per (s, l, mu, nu): is there an i with |a_i c_{i-sn}| >= eps_ov? Only blocks
+// where both profiles are non-zero are visited; a block pair is scanned element-wise only
+// if fl(max|a|_blk * max|c|_blk) >= eps (exact pruning: rounding is monotone). The last
+// CTA to finish applies the sequential L0 rule (fused finalize).
 __global__ void k_l0_scan(DevSys s, Dir3 d, const double* __restrict__ prof, const double* __restrict__ bmax,
-                          int* found, int s_begin, int ns) {
+                          const unsigned* __restrict__ nz, int* found, int* state, int s_begin, int ns, int s_end) {
     const int lane = threadIdx.x & 31;
     const Index task = static_cast<Index>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const Index m0 = s.m0;
     const Index per_s = 3 * m0 * m0;
-    if (task >= per_s * ns) return;
-    const int sft = s_begin + static_cast<int>(task / per_s);
-    Index rem = task % per_s;
-    const int l = static_cast<int>(rem / (m0 * m0));
-    rem %= m0 * m0;
-    const Index mu = rem / m0, nu = rem % m0;
-    if (found[sft]) return;  // another pair already proved worst >= eps for this s
-    const Index n = d.n[l];
-    const Index width = 2 * (kMaxL0 + 2) * n;
-    const Index nblk = (width + kL0Block - 1) / kL0Block;
-    const Index sn = static_cast<Index>(sft) * n;
-    if (sn >= width) return;
-    const double* a = prof + d.off[l] + mu * width;
-    const double* c = prof + d.off[l] + nu * width;
-    const double* am = bmax + d.boff[l] + mu * nblk;
-    const double* cm = bmax + d.boff[l] + nu * nblk;
-    const double eps = s.eps_ov;
     bool hit = false;
-    for (Index ja0 = sn / kL0Block; ja0 < nblk; ja0 += 32) {
-        const Index ja = ja0 + lane;
-        if (ja < nblk) {
-            const Index ilo = max(ja * kL0Block, sn);
-            const Index ihi = min(ja * kL0Block + kL0Block, width);
-            if (ilo < ihi) {
-                const Index cb0 = (ilo - sn) / kL0Block, cb1 = (ihi - 1 - sn) / kL0Block;
-                const double bound = am[ja] * fmax(cm[cb0], cm[cb1]);
-                if (bound >= eps) {
-                    for (Index i = ilo; i < ihi; ++i)
-                        if (fabs(a[i] * c[i - sn]) >= eps) {
-                            hit = true;
-                            break;
+    int sft = 0;
+    if (task < per_s * ns) {
+        sft = s_begin + static_cast<int>(task / per_s);
+        Index rem = task % per_s;
+        const int l = static_cast<int>(rem / (m0 * m0));
+        rem %= m0 * m0;
+        const Index mu = rem / m0, nu = rem % m0;
+        const Index n = d.n[l];
+        const Index width = 2 * (kMaxL0 + 2) * n;
+        const Index nblk = (width + kL0Block - 1) / kL0Block;
+        const Index sn = static_cast<Index>(sft) * n;
+        const Index alo = nz[(l * m0 + mu) * 2], ahi = nz[(l * m0 + mu) * 2 + 1];
+        const Index clo = nz[(l * m0 + nu) * 2], chi = nz[(l * m0 + nu) * 2 + 1];
+        Index jlo = max(alo, sn / kL0Block);
+        jlo = max(jlo, (clo * kL0Block + sn) / kL0Block);
+        Index jhi = min(ahi, nblk - 1);
+        jhi = min(jhi, (chi * kL0Block + kL0Block - 1 + sn) / kL0Block);
+        if (!__ldcg(&found[sft]) && sn < width && alo <= ahi && clo <= chi) {
+            const double* a = prof + d.off[l] + mu * width;
+            const double* c = prof + d.off[l] + nu * width;
+            const double* am = bmax + d.boff[l] + mu * nblk;
+            const double* cm = bmax + d.boff[l] + nu * nblk;
+            const double eps = s.eps_ov;
+            for (Index ja0 = jlo; ja0 <= jhi; ja0 += 32) {
+                const Index ja = ja0 + lane;
+                if (ja <= jhi) {
+                    const Index ilo = max(ja * kL0Block, sn);
+                    const Index ihi = min(ja * kL0Block + kL0Block, width);
+                    if (ilo < ihi) {
+                        const Index cb0 = (ilo - sn) / kL0Block, cb1 = (ihi - 1 - sn) / kL0Block;
+                        const double c0 = cm[cb0], c1 = cm[cb1];
+                        const double bound = am[ja] * fmax(c0, c1);
+                        if (bound >= eps) {
+                            for (Index i = ilo; i < ihi; ++i) {
+                                const Index ci = i - sn;
+                                const double cv = (ci / kL0Block == cb0 ? c0 : c1) > 0.0 ? c[ci] : 0.0;
+                                if (fabs(a[i] * cv) >= eps) {
+                                    hit = true;
+                                    break;
+                                }
+                            }
                         }
+                    }
+                }
+                if (__any_sync(0xffffffffu, hit)) {
+                    hit = true;
+                    break;
                 }
             }
         }
-        if (__any_sync(0xffffffffu, hit)) {
-            hit = true;
-            break;
-        }
     }
-    if (hit && lane == 0) found[sft] = 1;
+    if (hit && lane == 0) atomicExch(&found[sft], 1);
+    // fused finalize: the last CTA to finish applies the sequential rule
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(&state[4], 1) == static_cast<int>(gridDim.x) - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        l0_finalize(found, state, s_end);
+        state[4] = 0;
+    }
 }
 
 void launch_overlap_scan(const Launch& L, const DevSys& s, const Index* n3, const Index* off3, const Index* boff3,
@@ -175,31 +231,8 @@ void launch_overlap_scan(const Launch& L, const DevSys& s, const Index* n3, cons
     const int wpb = 8;
     const Index blocks = (tasks + wpb - 1) / wpb;
     Stage st_(L, "l0_scan");
-    k_l0_scan<<<static_cast<unsigned>(blocks), wpb * 32, 0, L.st>>>(s, d, b.prof, b.bmax, b.found, s_begin, ns);
-    LT_CU(cudaGetLastError());
-    L.tick();
-}
-
-// the reference's sequential rule: L0 = last s with worst >= eps; stop after 2 misses
-__global__ void k_l0_finalize(const int* found, int* state, int s_end) {
-    int L0 = state[0], misses = state[1], sft = state[2];
-    for (; sft <= kMaxL0 && sft < s_end && misses < 2; ++sft) {
-        if (found[sft]) {
-            L0 = sft;
-            misses = 0;
-        } else {
-            ++misses;
-        }
-    }
-    state[0] = L0;
-    state[1] = misses;
-    state[2] = sft;
-    state[3] = (misses >= 2 || sft > kMaxL0) ? 1 : 0;
-}
-
-void launch_overlap_finalize(const Launch& L, OverlapBufs b, int /*s_begin*/, int s_end) {
-    Stage st_(L, "l0_finalize");
-    k_l0_finalize<<<1, 1, 0, L.st>>>(b.found, b.state, s_end);
+    k_l0_scan<<<static_cast<unsigned>(blocks), wpb * 32, 0, L.st>>>(s, d, b.prof, b.bmax, b.nz, b.found, b.state,
+                                                                    s_begin, ns, s_end);
     LT_CU(cudaGetLastError());
     L.tick();
 }

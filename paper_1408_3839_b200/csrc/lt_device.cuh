@@ -19,7 +19,9 @@ __device__ __forceinline__ double gto_eval1d(const DevSys& s, Index mu, int l, d
     const int dg = s.deg[3 * mu + l];
     for (int p = 0; p < dg; ++p) mono = __dmul_rn(mono, d);
     const double arg = __dmul_rn(__dmul_rn(-s.alpha[mu], d), d);
-    return __dmul_rn(mono, exp(arg));
+    // exp(arg) rounds to exactly 0 below -745.14; skipping it for arg < -746 is exact and
+    // avoids the slow underflow path of the FP64 exp on the (many) far-tail samples
+    return __dmul_rn(mono, arg < -746.0 ? 0.0 : exp(arg));
 }
 
 __device__ __forceinline__ double warp_sum(double v) {

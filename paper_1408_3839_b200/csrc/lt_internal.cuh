@@ -173,18 +173,19 @@ void launch_sinc(const Launch& L, Index M, const DevSys& s, double* t, double* w
 
 // overlap constant (gto_basis.cpp:87-126)
 struct OverlapBufs {
-    double* prof = nullptr;   // [3][m0][width_l] packed per direction
+    double* prof = nullptr;   // [3][m0][width_l] packed per direction (non-zero blocks only)
     double* bmax = nullptr;   // [3][m0][nblk_l]
+    unsigned* nz = nullptr;   // [3][m0][2]: first / last non-zero block
     int* found = nullptr;     // [257]
-    int* state = nullptr;     // [4]: L0, misses, s_next, done
+    int* state = nullptr;     // [5]: L0, misses, s_next, done, finished-CTA counter
 };
 constexpr int kL0Block = 128;
 void launch_overlap_profiles(const Launch& L, const DevSys& s, const Index* n3, const Index* off3,
                              const Index* boff3, OverlapBufs b);
+// scan of shifts [s_begin, s_end) with the sequential L0 rule fused into the last CTA
 void launch_overlap_scan(const Launch& L, const DevSys& s, const Index* n3, const Index* off3, const Index* boff3,
                          OverlapBufs b, int s_begin, int s_end);
-void launch_overlap_finalize(const Launch& L, OverlapBufs b, int s_begin, int s_end);
-void launch_overlap_init(const Launch& L, OverlapBufs b);
+void launch_overlap_init(const Launch& L, OverlapBufs b, int m0);
 
 // master tensor (newton_kernel.cpp:22-45) and assembled window sums (canonical_tensor.cpp:123-164)
 void launch_master(const Launch& L, Index mrows, double h, Index RN, const double* t, double* out);
@@ -247,8 +248,41 @@ void launch_triv_tables(const Launch& L, const TrivJobs& jobs, int njobs, const 
 void launch_vgemm(const Launch& L, int mm, int Rtot, long long rows, const double* W, const double* P, double* V);
 void launch_hankel(const Launch& L, int m0, const DirPlan& d, const double* pwc, const unsigned long long* lo,
                    const unsigned long long* hi, const double* V, double* part, double* N, int splits);
-void launch_fold_dmma(const Launch& L, int m0, const DirPlan& d, const double* pwc, const double* V, int mode,
-                      double* out, double* N);
+// ---- residue-class correlations on DMMA (k_fold.cu) ----
+struct FemApplyJob {
+    const double* pwl = nullptr;  // [m0][Gbar]
+    long long Gbar = 0;
+    double hbar = 0.0;
+    const unsigned long long* lo = nullptr;
+    const unsigned long long* hi = nullptr;
+    double* wm = nullptr;  // [m0][Gbar] mass-applied profiles
+    double* ws = nullptr;  // [m0][Gbar] stiffness-applied profiles
+};
+struct FemApplyJobs {
+    FemApplyJob j[3];
+};
+void launch_fem_apply(const Launch& L, const FemApplyJobs& jobs, int njobs, int m0);
+struct ResFold {
+    int m0 = 0;
+    long long J = 0, n = 0, G = 0;  // cells, points per cell (residues), grid = J*n
+    const double* a = nullptr;      // [m0][G]
+    const double* b[2] = {nullptr, nullptr};  // [m0][G], or [m0][G+2] with one guard each side
+    int nb = 1;
+    int bguard = 0;
+    int dlo = 0, dhi = 0, dchunk = 1, band = 0;
+    const double* V = nullptr;      // optional weight V[e][t]
+    double* out[2] = {nullptr, nullptr};  // [t][d - dlo][e]
+    double* res[2] = {nullptr, nullptr};  // reduced [d + band][e]
+    double* slab = nullptr;               // workspace [n][1+nb][m0p][ldj] (residue-major)
+};
+// slab row stride: >= J + 5 (two guard columns plus zero padding for the unchecked last
+// k-step), == 4 mod 16 so the 8 rows x 4 columns of an m8n8k4 fragment hit distinct banks
+__host__ __device__ inline long long resfold_ldj(long long J) { return (J + 16) / 16 * 16 + 4; }
+inline size_t resfold_slab_doubles(const ResFold& f) {
+    const size_t m0p = (static_cast<size_t>(f.m0) + 7) / 8 * 8;
+    return static_cast<size_t>(f.n) * (1 + f.nb) * m0p * static_cast<size_t>(resfold_ldj(f.J));
+}
+void launch_resfold(const Launch& L, const ResFold& f, bool reduce, bool mirror, const char* name);
 void launch_fgemm(const Launch& L, int m0, int Rtot, const DirPlan& d, const double* P, const double* Qf, double* T);
 void launch_kr_combine(const Launch& L, const KRArgs& a);
 
