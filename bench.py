@@ -29,6 +29,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 from paper_1408_3839_b200.system import make_config  # noqa: E402
+from paper_1408_3839_b200.workmodel import roofline, stage_work  # noqa: E402
 
 METRIC = "core-Hamiltonian assembly+spectrum time (ms) vs L; Galerkin entries/s; % roofline"
 WORKLOAD_DESC = {
@@ -109,67 +110,6 @@ class ClockSampler:
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
                 "samples": len(sm)}
-
-
-# ---------------------------------------------------------------------------
-# algorithmic work per kernel launch
-# ---------------------------------------------------------------------------
-def work_model(ctx, sysobj, periodic, L0):
-    """{stage: (bound, per-launch algorithmic amount, unit)}; amounts in bytes or flops."""
-    m0 = sysobj.m0
-    mm = m0 * m0
-    RN = sysobj.rank_N
-    Rtot = sysobj.rank_total
-    margin = L0 + 2
-    L = sysobj.L
-    n = sysobj.n
-    band = [min(L0, L[l] - 1) for l in range(3)]
-    width = [2 * b + 1 for b in band]
-    G = [(L[l] + 2 * margin) * n[l] for l in range(3)]
-    prof = ctx.profiles(sysobj, margin)
-    sup = {(l, mu): (prof[("pwc", l, mu)][0], prof[("pwc", l, mu)][0] + len(prof[("pwc", l, mu)][1]))
-           for l in range(3) for mu in range(m0)}
-    out = {}
-    # L0 profile sampling: writes m0 * sum(width_l) doubles (+ block maxima)
-    w_l0 = sum(2 * 258 * n[l] for l in range(3))
-    out["l0_sample"] = ("hbm", 8.0 * m0 * w_l0 * (1 + 1.0 / 128), "B")
-    # nuclear tables of trivial directions (one launch per direction): 2 flops per
-    # (a*b) product + 2 Rtot per point of the support overlap
-    triv = [l for l in range(3) if L[l] == 1]
-    if triv:
-        fl = 0.0
-        for l in triv:
-            for mu in range(m0):
-                for nu in range(m0):
-                    lo = max(sup[(l, mu)][0], sup[(l, nu)][0], 0)
-                    hi = min(sup[(l, mu)][1], sup[(l, nu)][1], G[l])
-                    fl += max(0, hi - lo) * (1 + 2 * Rtot)
-        out["nuc_direct"] = ("tensor", fl / len(triv), "flop")
-    # box S2 Hankel contraction: 2 flops per (k, d, e, j) with the dot3 range
-    s2 = [l for l in range(3) if L[l] > 1]
-    if not periodic and len(s2) == 1:
-        l = s2[0]
-        fl = 0.0
-        for mu in range(m0):
-            a0, a1 = sup[(l, mu)]
-            for nu in range(m0):
-                b0, b1 = sup[(l, nu)]
-                for k in range(L[l]):
-                    for d in range(-band[l], band[l] + 1):
-                        if not (0 <= k + d < L[l]):
-                            continue
-                        lo = max(a0 + k * n[l], b0 + (k + d) * n[l], 0)
-                        hi = min(a1 + k * n[l], b1 + (k + d) * n[l], G[l])
-                        fl += 2.0 * max(0, hi - lo)
-        out["box_corr"] = ("tensor", fl, "flop")
-    # periodic pencils: nominal complex Cholesky + 2 triangular solves + ~6 Jacobi sweeps
-    if periodic:
-        K = L[0] * L[1] * L[2]
-        out["pencil"] = ("tensor", K * 4.0 * (m0 ** 3 / 3 + 2 * m0 ** 3 + 12 * m0 ** 3), "flop")
-    # HBM-bound helpers
-    out["profiles"] = ("hbm", 8.0 * m0 * 2 * (sum(G) + sum((L[l] + 2 * margin) * sysobj.nbar[l] for l in range(3))),
-                       "B")
-    return out
 
 
 def pick_cpu_impl(sysobj):
@@ -354,33 +294,31 @@ def main():
     if rank == 0:
         peaks = load_peaks()
         L0 = int(info[0])
-        wm = work_model(ctx, sysobj, periodic, L0)
-        # dominant kernel by measured time
-        dom = max(stages.items(), key=lambda kv: kv[1][0]) if stages else None
+        work = stage_work(ctx, sysobj, periodic, L0)
         step_ms_stage = float(np.mean(ms2)) if ms2 else None
+        per_stage, step_frac = roofline(work, stages, args.steps, peaks, ms_per_step)
+        # dominant kernel by measured time; achieved = its algorithmic amount per launch over
+        # its mean launch time (CUDA events on the context stream)
         roof = None
-        if dom is not None:
-            name, (tot_ms, nl) = dom
+        if stages:
+            name, (tot_ms, nl) = max(stages.items(), key=lambda kv: kv[1][0])
             avg_ms = tot_ms / max(1, nl)
-            bound, amount, unit = wm.get(name, ("hbm", None, "B"))
-            if amount is not None:
-                if bound == "hbm":
-                    achieved = amount / (avg_ms * 1e-3) / 1e9
-                    peak = peaks["hbm_gbs"]
-                    runit = "GB/s"
-                    src = peaks["hbm_src"]
-                else:
-                    achieved = amount / (avg_ms * 1e-3) / 1e12
-                    peak = peaks["fp64_tflops"]
-                    runit = "TFLOP/s"
-                    src = peaks["fp64_src"]
-                roof = {"kernel": name, "bound": bound, "achieved": achieved, "peak": peak, "unit": runit,
-                        "frac": achieved / peak, "traffic": None, "avg_launch_ms": avg_ms,
+            st = per_stage[name]
+            if "bound" in st:
+                per_launch = st["algorithmic_per_step"] * args.steps / max(1, nl)
+                hbm = st["bound"] == "hbm"
+                achieved = per_launch / (avg_ms * 1e-3) / (1e9 if hbm else 1e12)
+                peak = st["peak"]
+                roof = {"kernel": name, "bound": st["bound"], "achieved": achieved, "peak": peak,
+                        "unit": "GB/s" if hbm else "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                        "avg_launch_ms": avg_ms, "launches_per_step": nl / args.steps,
                         "share_of_step": tot_ms / args.steps / step_ms_stage if step_ms_stage else None,
-                        "algorithmic_per_launch": amount, "peak_source": src}
+                        "algorithmic_per_launch": per_launch,
+                        "peak_source": peaks["hbm_src"] if hbm else peaks["fp64_src"],
+                        "step_roofline_frac": step_frac}
             else:
-                roof = {"kernel": name, "bound": bound, "achieved": None, "peak": None, "unit": None, "frac": None,
-                        "traffic": None, "avg_launch_ms": avg_ms}
+                roof = {"kernel": name, "bound": None, "achieved": None, "peak": None, "unit": None, "frac": None,
+                        "traffic": None, "avg_launch_ms": avg_ms, "step_roofline_frac": step_frac}
         bands = [min(L0, sysobj.L[l] - 1) for l in range(3)]
         if periodic:
             nblocks = int(np.prod([2 * b + 1 for b in bands]))
@@ -415,7 +353,7 @@ def main():
                        "exponent_draw": sysobj.notes["exponent_draw"]},
             "galerkin_entries_per_s": float(entries) / (ms_per_step * 1e-3) if ms_per_step else None,
             "roofline": roof,
-            "stages_ms_per_step": {k: v[0] / args.steps for k, v in sorted(stages.items(), key=lambda kv: -kv[1][0])},
+            "stages": {k: per_stage[k] for k, _ in sorted(stages.items(), key=lambda kv: -kv[1][0])},
             "cpu_baseline": cpu,
             "e2e": {"value": float(e2e_t.item()), "unit": "ms", "h2d_bytes_per_step": sysobj.host_bytes(),
                     "d2h_bytes_per_step": 8 * count},

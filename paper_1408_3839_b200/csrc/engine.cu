@@ -266,6 +266,18 @@ static Index compute_L0(lt_ctx* c, const lt_sysdev* sd) {
         tot += m0 * width;
         btot += m0 * ((width + kL0Block - 1) / kL0Block);
     }
+    // a direction whose grid, centres and degrees repeat an earlier one has identical
+    // profiles: its scan answers are the same, so it is skipped (found[] is an OR over l)
+    int active[3] = {1, 1, 1};
+    for (int l = 1; l < 3; ++l)
+        for (int q = 0; q < l && active[l]; ++q) {
+            if (!active[q] || h.n[q] != h.n[l]) continue;
+            bool same = true;
+            for (Index mu = 0; mu < m0 && same; ++mu)
+                same = std::memcmp(&h.center[3 * mu + q], &h.center[3 * mu + l], sizeof(double)) == 0 &&
+                       h.deg[3 * mu + q] == h.deg[3 * mu + l];
+            if (same) active[l] = 0;
+        }
     OverlapBufs b;
     b.prof = c->arena.get<double>("l0.prof", tot);
     b.bmax = c->arena.get<double>("l0.bmax", btot);
@@ -278,8 +290,8 @@ static Index compute_L0(lt_ctx* c, const lt_sysdev* sd) {
     // first chunk as one replayable sequence: init, sample, scan (+ fused rule), read-back
     auto first = [&]() {
         launch_overlap_init(L, b, static_cast<int>(m0));
-        launch_overlap_profiles(L, sd->ds, n3, off3, boff3, b);
-        launch_overlap_scan(L, sd->ds, n3, off3, boff3, b, 1, 1 + chunk);
+        launch_overlap_profiles(L, sd->ds, n3, off3, boff3, active, b);
+        launch_overlap_scan(L, sd->ds, n3, off3, boff3, active, b, 1, 1 + chunk);
         LT_CU(cudaMemcpyAsync(st, b.state, 4 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     };
     run_cached(
@@ -289,7 +301,7 @@ static Index compute_L0(lt_ctx* c, const lt_sysdev* sd) {
     int s_begin = 1 + chunk;
     while (!st[3] && s_begin < 257) {
         const int s_end = std::min(257, s_begin + chunk);
-        launch_overlap_scan(L, sd->ds, n3, off3, boff3, b, s_begin, s_end);
+        launch_overlap_scan(L, sd->ds, n3, off3, boff3, active, b, s_begin, s_end);
         LT_CU(cudaMemcpyAsync(st, b.state, 4 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
         LT_CU(cudaStreamSynchronize(c->stream));
         s_begin = s_end;

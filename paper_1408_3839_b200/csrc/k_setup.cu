@@ -46,63 +46,100 @@ constexpr int kMaxL0 = 256;
 
 struct Dir3 {
     Index n[3], off[3], boff[3];
+    int nl;          // active (de-duplicated) directions
+    int dir[3];      // their indices
+    Index tcum[4];   // sample tasks: cumulative m0 * nblk over the active directions
 };
 
+__device__ __forceinline__ double l0_x(Index i, Index base, double h, double b) {
+    return __dsub_rn(__dmul_rn(__dadd_rn(static_cast<double>(i - base), 0.5), h), __dmul_rn(0.5, b));
+}
+
 // Samples the untrimmed L0 profiles (gto_basis.cpp:95-97: width 2 (256+2) n, the
-// function in cell 258) and their block maxima. Values are stored only for blocks with a
-// non-zero maximum (the scan treats the others as zero), and the first/last non-zero
-// block of every profile is recorded so the scan only visits overlapping blocks.
-__global__ void __launch_bounds__(kL0Block) k_l0_sample(DevSys s, Dir3 d, double* __restrict__ prof,
-                                                        double* __restrict__ bmax, unsigned* __restrict__ nz) {
-    const int l = blockIdx.z, mu = blockIdx.y;
-    const Index n = d.n[l];
-    const Index width = 2 * (kMaxL0 + 2) * n;
-    const Index nblk = (width + kL0Block - 1) / kL0Block;
-    if (blockIdx.x >= nblk) return;
-    const double h = s.b / static_cast<double>(n);
-    const Index base = (kMaxL0 + 2) * n;
-    const Index i = static_cast<Index>(blockIdx.x) * kL0Block + threadIdx.x;
-    double av = 0.0, v = 0.0;
-    if (i < width) {
-        const double x = __dsub_rn(__dmul_rn(__dadd_rn(static_cast<double>(i - base), 0.5), h), __dmul_rn(0.5, s.b));
-        v = gto_eval1d(s, mu, l, x);
-        av = fabs(v);
-    }
-    // block max of |v| (exact: max is order independent)
-    for (int o = 16; o > 0; o >>= 1) av = fmax(av, __shfl_xor_sync(0xffffffffu, av, o));
-    __shared__ double wm[kL0Block / 32];
-    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = av;
-    __syncthreads();
-    double m = wm[0];
-    for (int k = 1; k < kL0Block / 32; ++k) m = fmax(m, wm[k]);
-    if (m > 0.0 && i < width) prof[d.off[l] + mu * width + i] = v;
-    if (threadIdx.x == 0) {
-        bmax[d.boff[l] + mu * nblk + blockIdx.x] = m;
+// function in cell 258) and their block maxima. One warp per 128-point block in a
+// grid-stride loop. A block whose nearest point to the centre already has
+// fl(fl(alpha d) d) > 746 is all zeros without evaluation: d = fl(x - c) and the
+// products are monotone in |d|, so every point of it takes gto_eval1d's exact zero
+// shortcut. Values are stored only for blocks with a non-zero maximum (the scan treats
+// the others as zero); the first/last non-zero block of each profile is recorded.
+__global__ void __launch_bounds__(256) k_l0_sample(DevSys s, Dir3 d, double* __restrict__ prof,
+                                                   double* __restrict__ bmax, unsigned* __restrict__ nz) {
+    const int lane = threadIdx.x & 31;
+    const Index nwarps = static_cast<Index>(gridDim.x) * (blockDim.x >> 5);
+    for (Index task = static_cast<Index>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); task < d.tcum[d.nl];
+         task += nwarps) {
+        int k = 0;
+        while (task >= d.tcum[k + 1]) ++k;
+        const int l = d.dir[k];
+        const Index n = d.n[l];
+        const Index width = 2 * (kMaxL0 + 2) * n;
+        const Index nblk = (width + kL0Block - 1) / kL0Block;
+        const Index rem = task - d.tcum[k];
+        const int mu = static_cast<int>(rem / nblk);
+        const Index blk = rem % nblk;
+        const double h = s.b / static_cast<double>(n);
+        const Index base = (kMaxL0 + 2) * n;
+        const Index i0 = blk * kL0Block, i1 = min(i0 + kL0Block, width) - 1;
+        const double c = s.center[3 * mu + l];
+        const double x0 = l0_x(i0, base, h, s.b), x1 = l0_x(i1, base, h, s.b);
+        const double dmin = c < x0 ? __dsub_rn(x0, c) : (c > x1 ? __dsub_rn(c, x1) : 0.0);
+        double* bm = bmax + d.boff[l] + mu * nblk + blk;
+        if (__dmul_rn(__dmul_rn(s.alpha[mu], dmin), dmin) > 746.0) {
+            if (lane == 0) *bm = 0.0;
+            continue;
+        }
+        double v[kL0Block / 32];
+        double av = 0.0;
+#pragma unroll
+        for (int q = 0; q < kL0Block / 32; ++q) {
+            const Index i = i0 + lane + 32 * q;
+            v[q] = i <= i1 ? gto_eval1d(s, mu, l, l0_x(i, base, h, s.b)) : 0.0;
+            av = fmax(av, fabs(v[q]));
+        }
+        const double m = warp_max(av);  // exact: max is order independent
         if (m > 0.0) {
-            atomicMin(&nz[(l * s.m0 + mu) * 2], static_cast<unsigned>(blockIdx.x));
-            atomicMax(&nz[(l * s.m0 + mu) * 2 + 1], static_cast<unsigned>(blockIdx.x));
+            double* out = prof + d.off[l] + mu * width;
+#pragma unroll
+            for (int q = 0; q < kL0Block / 32; ++q)
+                if (i0 + lane + 32 * q <= i1) out[i0 + lane + 32 * q] = v[q];
+        }
+        if (lane == 0) {
+            *bm = m;
+            if (m > 0.0) {
+                atomicMin(&nz[(l * s.m0 + mu) * 2], static_cast<unsigned>(blk));
+                atomicMax(&nz[(l * s.m0 + mu) * 2 + 1], static_cast<unsigned>(blk));
+            }
         }
     }
 }
 
-void launch_overlap_profiles(const Launch& L, const DevSys& s, const Index* n3, const Index* off3, const Index* boff3,
-                             OverlapBufs b) {
-    Dir3 d;
-    Index nbmax = 0;
+static Dir3 make_dir3(const DevSys& s, const Index* n3, const Index* off3, const Index* boff3, const int* active) {
+    Dir3 d{};
+    d.nl = 0;
+    d.tcum[0] = 0;
     for (int l = 0; l < 3; ++l) {
         d.n[l] = n3[l];
         d.off[l] = off3[l];
         d.boff[l] = boff3[l];
+        if (!active[l]) continue;
         const Index width = 2 * (kMaxL0 + 2) * n3[l];
-        nbmax = std::max(nbmax, (width + kL0Block - 1) / kL0Block);
+        d.dir[d.nl] = l;
+        d.tcum[d.nl + 1] = d.tcum[d.nl] + static_cast<Index>(s.m0) * ((width + kL0Block - 1) / kL0Block);
+        ++d.nl;
     }
-    dim3 grid(static_cast<unsigned>(nbmax), s.m0, 3);
+    for (int k = d.nl; k < 3; ++k) d.tcum[k + 1] = d.tcum[k];
+    return d;
+}
+
+void launch_overlap_profiles(const Launch& L, const DevSys& s, const Index* n3, const Index* off3, const Index* boff3,
+                             const int* active, OverlapBufs b) {
+    const Dir3 d = make_dir3(s, n3, off3, boff3, active);
+    const Index blocks = std::min<Index>((d.tcum[d.nl] + 7) / 8, 148 * 8);
     Stage st_(L, "l0_sample");
-    k_l0_sample<<<grid, kL0Block, 0, L.st>>>(s, d, b.prof, b.bmax, b.nz);
+    k_l0_sample<<<static_cast<unsigned>(std::max<Index>(1, blocks)), 256, 0, L.st>>>(s, d, b.prof, b.bmax, b.nz);
     LT_CU(cudaGetLastError());
     L.tick();
 }
-
 
 __global__ void k_l0_init(int* found, int* state, unsigned* nz, int nnz) {
     for (int i = threadIdx.x; i <= kMaxL0; i += blockDim.x) found[i] = 0;
@@ -140,22 +177,24 @@ __device__ void l0_finalize(const int* found, int* state, int s_end) {
     state[3] = (misses >= 2 || sft > kMaxL0) ? 1 : 0;
 }
 
-// One warp per (s, l, mu, nu): is there an i with |a_i c_{i-sn}| >= eps_ov? Only blocks
-// where both profiles are non-zero are visited; a block pair is scanned element-wise only
-// if fl(max|a|_blk * max|c|_blk) >= eps (exact pruning: rounding is monotone). The last
-// CTA to finish applies the sequential L0 rule (fused finalize).
+// One warp per (s, l, mu, nu) over the active directions (a duplicated direction has the
+// same profiles, so its answers are identical): is there an i with |a_i c_{i-sn}| >= eps_ov?
+// Only blocks where both profiles are non-zero are visited; a block pair is scanned
+// element-wise only if fl(max|a|_blk * max|c|_blk) >= eps (exact pruning: rounding is
+// monotone). Lanes test the bounds of 32 blocks at once; each candidate block is then
+// scanned by the whole warp. The last CTA to finish applies the sequential L0 rule.
 __global__ void k_l0_scan(DevSys s, Dir3 d, const double* __restrict__ prof, const double* __restrict__ bmax,
                           const unsigned* __restrict__ nz, int* found, int* state, int s_begin, int ns, int s_end) {
     const int lane = threadIdx.x & 31;
     const Index task = static_cast<Index>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const Index m0 = s.m0;
-    const Index per_s = 3 * m0 * m0;
+    const Index per_s = static_cast<Index>(d.nl) * m0 * m0;
     bool hit = false;
     int sft = 0;
     if (task < per_s * ns) {
         sft = s_begin + static_cast<int>(task / per_s);
         Index rem = task % per_s;
-        const int l = static_cast<int>(rem / (m0 * m0));
+        const int l = d.dir[rem / (m0 * m0)];
         rem %= m0 * m0;
         const Index mu = rem / m0, nu = rem % m0;
         const Index n = d.n[l];
@@ -174,30 +213,32 @@ __global__ void k_l0_scan(DevSys s, Dir3 d, const double* __restrict__ prof, con
             const double* am = bmax + d.boff[l] + mu * nblk;
             const double* cm = bmax + d.boff[l] + nu * nblk;
             const double eps = s.eps_ov;
-            for (Index ja0 = jlo; ja0 <= jhi; ja0 += 32) {
+            for (Index ja0 = jlo; ja0 <= jhi && !hit; ja0 += 32) {
                 const Index ja = ja0 + lane;
+                Index ilo = 0, ihi = 0;
+                bool cand = false;
                 if (ja <= jhi) {
-                    const Index ilo = max(ja * kL0Block, sn);
-                    const Index ihi = min(ja * kL0Block + kL0Block, width);
+                    ilo = max(ja * kL0Block, sn);
+                    ihi = min(ja * kL0Block + kL0Block, width);
                     if (ilo < ihi) {
                         const Index cb0 = (ilo - sn) / kL0Block, cb1 = (ihi - 1 - sn) / kL0Block;
-                        const double c0 = cm[cb0], c1 = cm[cb1];
-                        const double bound = am[ja] * fmax(c0, c1);
-                        if (bound >= eps) {
-                            for (Index i = ilo; i < ihi; ++i) {
-                                const Index ci = i - sn;
-                                const double cv = (ci / kL0Block == cb0 ? c0 : c1) > 0.0 ? c[ci] : 0.0;
-                                if (fabs(a[i] * cv) >= eps) {
-                                    hit = true;
-                                    break;
-                                }
-                            }
-                        }
+                        cand = am[ja] * fmax(cm[cb0], cm[cb1]) >= eps;
                     }
                 }
-                if (__any_sync(0xffffffffu, hit)) {
-                    hit = true;
-                    break;
+                unsigned mask = __ballot_sync(0xffffffffu, cand);
+                while (mask && !hit) {
+                    const int src = __ffs(mask) - 1;
+                    mask &= mask - 1;
+                    const Index blo = __shfl_sync(0xffffffffu, ilo, src), bhi = __shfl_sync(0xffffffffu, ihi, src);
+                    const double amx = am[(blo) / kL0Block];
+                    bool h = false;
+                    for (Index i = blo + lane; i < bhi; i += 32) {
+                        const Index ci = i - sn;
+                        const double av = amx > 0.0 ? a[i] : 0.0;
+                        const double cv = cm[ci / kL0Block] > 0.0 ? c[ci] : 0.0;
+                        h |= fabs(av * cv) >= eps;
+                    }
+                    hit = __any_sync(0xffffffffu, h);
                 }
             }
         }
@@ -219,17 +260,12 @@ __global__ void k_l0_scan(DevSys s, Dir3 d, const double* __restrict__ prof, con
 }
 
 void launch_overlap_scan(const Launch& L, const DevSys& s, const Index* n3, const Index* off3, const Index* boff3,
-                         OverlapBufs b, int s_begin, int s_end) {
-    Dir3 d;
-    for (int l = 0; l < 3; ++l) {
-        d.n[l] = n3[l];
-        d.off[l] = off3[l];
-        d.boff[l] = boff3[l];
-    }
+                         const int* active, OverlapBufs b, int s_begin, int s_end) {
+    const Dir3 d = make_dir3(s, n3, off3, boff3, active);
     const int ns = s_end - s_begin;
-    const Index tasks = static_cast<Index>(ns) * 3 * s.m0 * s.m0;
+    const Index tasks = static_cast<Index>(ns) * d.nl * s.m0 * s.m0;
     const int wpb = 8;
-    const Index blocks = (tasks + wpb - 1) / wpb;
+    const Index blocks = std::max<Index>(1, (tasks + wpb - 1) / wpb);
     Stage st_(L, "l0_scan");
     k_l0_scan<<<static_cast<unsigned>(blocks), wpb * 32, 0, L.st>>>(s, d, b.prof, b.bmax, b.nz, b.found, b.state,
                                                                     s_begin, ns, s_end);
