@@ -18,6 +18,16 @@
 #include "lt_device.cuh"
 #include "lt_internal.cuh"
 
+// Optional phase clocks (tools/pencil_phases.cu): group leader of pencil k records
+// clock64() at phase boundaries into lt_pencil_prof[k][0..7].
+#ifdef LT_PENCIL_PROFILE
+__device__ long long lt_pencil_prof[8192][8];
+#define PPROF(i) \
+    if (t == 0 && k < 8192) lt_pencil_prof[k][i] = clock64();
+#else
+#define PPROF(i)
+#endif
+
 namespace lt {
 
 namespace {
@@ -53,53 +63,90 @@ struct PSmem {
     double2 C[NM][NM + 1];
     double2 v[NM], w[NM];
     double d[NM], e2[NM], e[NM];
-    double red[8];
-    double2 tau;
+    double ix[NM], invd[NM];  // 1 / pivot, 1 / sqrt(pivot)
+    double red[4][32];
     double scal[4];
 };
 
-template <int G, bool MAX>
-__device__ __forceinline__ double greduce(double v, double* red, int t, int slot) {
+// group reduction of NV values at once (one pair of barriers for all of them)
+template <int G, int NV, bool MAX>
+__device__ __forceinline__ void greduce(double (&v)[NV], double (*red)[32], int t, int slot) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const double w = __shfl_xor_sync(0xffffffffu, v, o);
-        v = MAX ? fmax(v, w) : v + w;
-    }
-    if constexpr (G == 32) {
-        return __shfl_sync(0xffffffffu, v, 0);
-    } else {
-        if ((t & 31) == 0) red[t >> 5] = v;
-        gsync<G>(slot);
-        double r = red[0];
+    for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-        for (int w = 1; w < G / 32; ++w) r = MAX ? fmax(r, red[w]) : r + red[w];
+        for (int q = 0; q < NV; ++q) {
+            const double w = __shfl_xor_sync(0xffffffffu, v[q], o);
+            v[q] = MAX ? fmax(v[q], w) : v[q] + w;
+        }
+    if constexpr (G > 32) {
+        if ((t & 31) == 0)
+#pragma unroll
+            for (int q = 0; q < NV; ++q) red[q][t >> 5] = v[q];
         gsync<G>(slot);
-        return r;
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            double r = red[q][0];
+#pragma unroll
+            for (int w = 1; w < G / 32; ++w) r = MAX ? fmax(r, red[q][w]) : r + red[q][w];
+            v[q] = r;
+        }
+        gsync<G>(slot);
     }
 }
 
-// number of eigenvalues of the symmetric tridiagonal (d, e^2) strictly below x
-__device__ __forceinline__ int sturm_count(const double* d, const double* e2, int n, double x, double pivmin) {
-    int cnt = 0;
-    double q = d[0] - x;
-    if (fabs(q) < pivmin) q = -pivmin;
-    cnt += q < 0.0;
-    for (int i = 1; i < n; ++i) {
-        q = (d[i] - x) - e2[i - 1] / q;
-        if (fabs(q) < pivmin) q = -pivmin;
-        cnt += q < 0.0;
+// 1/q: MUFU reciprocal seed + two Newton steps (within an ulp or two of 1/q) instead of
+// the IEEE division subroutine on the dependent chains. Needs DBL_MIN <= |q| < 2^1022
+// (safe_rcp falls back to the IEEE division outside that range).
+__device__ __forceinline__ double fast_rcp(double q) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+    double t = fma(-q, r, 1.0);
+    r = fma(r, t, r);
+    t = fma(-q, r, 1.0);
+    return fma(r, t, r);
+}
+__device__ __forceinline__ double safe_rcp(double q) {
+    const double a = fabs(q);
+    return (a >= 1e-300 && a <= 1e300) ? fast_rcp(q) : 1.0 / q;
+}
+
+// Sturm counts (eigenvalues of the symmetric tridiagonal (d, e^2) strictly below x) at Q
+// shifts at once: Q independent LDL^T pivot chains interleaved for ILP. LAPACK's pivmin
+// guard; the counts are backward stable, so bisection converges to within O(eps ||T||)
+// of the exact eigenvalues.
+template <int Q>
+__device__ __forceinline__ void sturm_counts(const double* d, const double* e2, int n, const double (&x)[Q],
+                                             double pivmin, int (&cnt)[Q]) {
+    double q[Q];
+#pragma unroll
+    for (int j = 0; j < Q; ++j) {
+        q[j] = d[0] - x[j];
+        if (fabs(q[j]) < pivmin) q[j] = -pivmin;
+        cnt[j] = q[j] < 0.0;
     }
-    return cnt;
+    for (int i = 1; i < n; ++i) {
+        const double di = d[i], ei = e2[i - 1];
+#pragma unroll
+        for (int j = 0; j < Q; ++j) {
+            q[j] = (di - x[j]) - ei * fast_rcp(q[j]);
+            if (fabs(q[j]) < pivmin) q[j] = -pivmin;
+            cnt[j] += q[j] < 0.0;
+        }
+    }
 }
 
 }  // namespace
 
-template <int NM, int G>
-__global__ void __launch_bounds__(256) k_pencil(Index count, int m0, const double2* __restrict__ Hb,
+// Threads of a group own matrix entries e = t + G*u (row e % NM, column e / NM); the
+// Householder mat-vec uses TPR = G / NM threads per row.
+template <int NM, int G, int BS>
+__global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double2* __restrict__ Hb,
                                                 const double2* __restrict__ Sb, double* __restrict__ eig,
                                                 unsigned long long* fail_key, int periodic_checks) {
-    constexpr int PPC = (G >= 256) ? 1 : 256 / G;
+    constexpr int PPC = BS / G;                 // pencils per CTA
     constexpr int EPT = (NM * NM + G - 1) / G;  // matrix entries per thread
+    constexpr int TPR = G / NM;                 // mat-vec threads per row
+    static_assert(TPR >= 1 && TPR <= 32 && (TPR & (TPR - 1)) == 0, "row split");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PSmem<NM>* all = reinterpret_cast<PSmem<NM>*>(smem_raw);
     const int slot = threadIdx.x / G;
@@ -107,6 +154,7 @@ __global__ void __launch_bounds__(256) k_pencil(Index count, int m0, const doubl
     const Index k = static_cast<Index>(blockIdx.x) * PPC + slot;
     if (k >= count) return;
     PSmem<NM>& sm = all[slot];
+    PPROF(0);
     auto& A = sm.A;
     auto& B = sm.B;
     auto& C = sm.C;
@@ -127,9 +175,10 @@ __global__ void __launch_bounds__(256) k_pencil(Index count, int m0, const doubl
         }
     }
     gsync<G>(slot);
+    PPROF(1);
     int code = 0;
     if (periodic_checks) {
-        double hmax = 0.0, smax = 0.0, hdev = 0.0, sdev = 0.0;
+        double red4[4] = {0.0, 0.0, 0.0, 0.0};  // hmax, smax, hdev, sdev
         double2 va[EPT], vb[EPT];
 #pragma unroll
         for (int u = 0; u < EPT; ++u) {
@@ -137,19 +186,16 @@ __global__ void __launch_bounds__(256) k_pencil(Index count, int m0, const doubl
             if (e < NM * NM) {
                 const int r = e % NM, c = e / NM;
                 const double2 a = A[r][c], at = A[c][r], b = B[r][c], bt = B[c][r];
-                hmax = fmax(hmax, cabs_(a));
-                smax = fmax(smax, cabs_(b));
-                hdev = fmax(hdev, cabs_(csub(a, cconj(at))));
-                sdev = fmax(sdev, cabs_(csub(b, cconj(bt))));
+                red4[0] = fmax(red4[0], cabs_(a));
+                red4[1] = fmax(red4[1], cabs_(b));
+                red4[2] = fmax(red4[2], cabs_(csub(a, cconj(at))));
+                red4[3] = fmax(red4[3], cabs_(csub(b, cconj(bt))));
                 va[u] = cscale(0.5, cadd(a, cconj(at)));
                 vb[u] = cscale(0.5, cadd(b, cconj(bt)));
             }
         }
-        hmax = greduce<G, true>(hmax, sm.red, t, slot);
-        smax = greduce<G, true>(smax, sm.red, t, slot);
-        hdev = greduce<G, true>(hdev, sm.red, t, slot);
-        sdev = greduce<G, true>(sdev, sm.red, t, slot);
-        if (hdev > 1e-10 * fmax(1.0, hmax) || sdev > 1e-10 * fmax(1.0, smax)) code = 1;
+        greduce<G, 4, true>(red4, sm.red, t, slot);  // its barriers also order the reads above
+        if (red4[2] > 1e-10 * fmax(1.0, red4[0]) || red4[3] > 1e-10 * fmax(1.0, red4[1])) code = 1;
 #pragma unroll
         for (int u = 0; u < EPT; ++u) {
             const int e = t + G * u;
@@ -160,7 +206,11 @@ __global__ void __launch_bounds__(256) k_pencil(Index count, int m0, const doubl
         }
         gsync<G>(slot);
     }
-    // 2. right-looking Cholesky of B (lower triangle)
+    PPROF(2);
+    // 2. right-looking Cholesky S = L L^H, unscaled: step kk subtracts
+    //    B[r][kk] conj(B[c][kk]) / x_kk from the trailing lower triangle and leaves column kk
+    //    unscaled, so one barrier per step suffices (L[r][kk] = B[r][kk] / sqrt(x_kk),
+    //    applied implicitly below). Pivot test as Eigen's LLT: x <= 0 fails.
     if (code == 0) {
         for (int kk = 0; kk < n; ++kk) {
             const double x = B[kk][kk].x;
@@ -168,20 +218,17 @@ __global__ void __launch_bounds__(256) k_pencil(Index count, int m0, const doubl
                 code = 2;
                 break;
             }
-            const double dd = sqrt(x);
-            const double inv = 1.0 / dd;
-            gsync<G>(slot);
-            for (int i = kk + 1 + t; i < n; i += G) B[i][kk] = cscale(inv, B[i][kk]);
-            if (t == 0) B[kk][kk] = make_double2(dd, 0.0);
-            gsync<G>(slot);
+            const double ixk = safe_rcp(x);
 #pragma unroll
             for (int u = 0; u < EPT; ++u) {
                 const int e = t + G * u;
                 if (e < NM * NM) {
                     const int r = e % NM, c = e / NM;
-                    if (c > kk && r >= c && r < n) B[r][c] = csub(B[r][c], cmul(B[r][kk], cconj(B[c][kk])));
+                    if (c > kk && r >= c && r < n)
+                        B[r][c] = csub(B[r][c], cscale(ixk, cmul(B[r][kk], cconj(B[c][kk]))));
                 }
             }
+            if (t == 0) sm.ix[kk] = ixk;
             gsync<G>(slot);
         }
     }
@@ -189,66 +236,58 @@ __global__ void __launch_bounds__(256) k_pencil(Index count, int m0, const doubl
         if (t == 0) atomicMin(fail_key, static_cast<unsigned long long>(k) * 4ull + static_cast<unsigned long long>(code));
         return;
     }
-    // 3. C = L^-1 (thread c owns column c), then A = C H C^H, symmetrised, into A
-    for (int c = t; c < n; c += G) {
-        for (int i = 0; i < n; ++i) {
-            if (i < c) {
-                C[i][c] = make_double2(0.0, 0.0);
-                continue;
+    for (int i = t; i < n; i += G) sm.invd[i] = 1.0 / sqrt(B[i][i].x);
+    PPROF(3);
+    // 3. A = L^-1 H L^-H by two right-looking forward substitutions (one barrier per step):
+    //    Y = L^-1 H in place in A, then Z = L^-1 Y^H in C; A = Z^H, symmetrised.
+    //    With L[r][i] = B[r][i] invd[i]: cur_r -= B[r][i] ix[i] cur_i, then y_r = cur_r invd[r].
+    for (int i = 0; i + 1 < n; ++i) {
+        const double ixi = sm.ix[i];
+#pragma unroll
+        for (int u = 0; u < EPT; ++u) {
+            const int e = t + G * u;
+            if (e < NM * NM) {
+                const int r = e % NM, c = e / NM;
+                if (r > i && r < n && c < n) A[r][c] = csub(A[r][c], cscale(ixi, cmul(B[r][i], A[i][c])));
             }
-            double2 s = make_double2(i == c ? 1.0 : 0.0, 0.0);
-            for (int j = c; j < i; ++j) s = csub(s, cmul(B[i][j], C[j][c]));
-            C[i][c] = cscale(1.0 / B[i][i].x, s);
+        }
+        gsync<G>(slot);
+    }
+    gsync<G>(slot);  // sm.invd visible (n == 1 runs no step above)
+#pragma unroll
+    for (int u = 0; u < EPT; ++u) {
+        const int e = t + G * u;
+        if (e < NM * NM) {
+            const int r = e % NM, c = e / NM;
+            C[r][c] = (r < n && c < n) ? cscale(sm.invd[c], cconj(A[c][r])) : make_double2(0.0, 0.0);
         }
     }
     gsync<G>(slot);
+    for (int i = 0; i + 1 < n; ++i) {
+        const double ixi = sm.ix[i];
+#pragma unroll
+        for (int u = 0; u < EPT; ++u) {
+            const int e = t + G * u;
+            if (e < NM * NM) {
+                const int r = e % NM, c = e / NM;
+                if (r > i && r < n && c < n) C[r][c] = csub(C[r][c], cscale(ixi, cmul(B[r][i], C[i][c])));
+            }
+        }
+        gsync<G>(slot);
+    }
     {
+        // A = Z^H with Z[r][c] = C[r][c] invd[r]; symmetrised: A_sym = (Z + Z^H) / 2
         double2 y[EPT];
 #pragma unroll
         for (int u = 0; u < EPT; ++u) {
             const int e = t + G * u;
             if (e < NM * NM) {
                 const int r = e % NM, c = e / NM;
-                double2 s = make_double2(0.0, 0.0);
-                if (r < n && c < n)
-                    for (int a = 0; a <= r; ++a) s = cadd(s, cmul(C[r][a], A[a][c]));
-                y[u] = s;
+                y[u] = (r < n && c < n)
+                           ? cscale(0.5, cadd(cscale(sm.invd[r], C[r][c]), cconj(cscale(sm.invd[c], C[c][r]))))
+                           : make_double2(0.0, 0.0);
             }
         }
-        gsync<G>(slot);
-#pragma unroll
-        for (int u = 0; u < EPT; ++u) {
-            const int e = t + G * u;
-            if (e < NM * NM) B[e % NM][e / NM] = y[u];  // B := L^-1 H  (L no longer needed)
-        }
-        gsync<G>(slot);
-#pragma unroll
-        for (int u = 0; u < EPT; ++u) {
-            const int e = t + G * u;
-            if (e < NM * NM) {
-                const int r = e % NM, c = e / NM;
-                double2 s = make_double2(0.0, 0.0);
-                if (r < n && c < n)
-                    for (int b = 0; b <= c; ++b) s = cadd(s, cmul(B[r][b], cconj(C[c][b])));
-                y[u] = s;
-            }
-        }
-        gsync<G>(slot);
-#pragma unroll
-        for (int u = 0; u < EPT; ++u) {
-            const int e = t + G * u;
-            if (e < NM * NM) A[e % NM][e / NM] = y[u];
-        }
-        gsync<G>(slot);
-#pragma unroll
-        for (int u = 0; u < EPT; ++u) {
-            const int e = t + G * u;
-            if (e < NM * NM) {
-                const int r = e % NM, c = e / NM;
-                y[u] = cscale(0.5, cadd(A[r][c], cconj(A[c][r])));
-            }
-        }
-        gsync<G>(slot);
 #pragma unroll
         for (int u = 0; u < EPT; ++u) {
             const int e = t + G * u;
@@ -256,13 +295,16 @@ __global__ void __launch_bounds__(256) k_pencil(Index count, int m0, const doubl
         }
         gsync<G>(slot);
     }
+    PPROF(4);
     // 4. Householder tridiagonalisation of the leading n x n block (zhetd2, lower)
+    const int row = t / TPR, part = t % TPR;
     for (int kk = 0; kk + 1 < n; ++kk) {
         const int m = n - kk - 1;  // reflector length (rows kk+1 .. n-1)
         // zlarfg on x = A[kk+1 .. n-1][kk]
-        double xn2 = 0.0;
-        for (int i = kk + 2 + t; i < n; i += G) xn2 += cabs2(A[i][kk]);
-        xn2 = greduce<G, false>(xn2, sm.red, t, slot);
+        double xr[1] = {0.0};
+        for (int i = kk + 2 + t; i < n; i += G) xr[0] += cabs2(A[i][kk]);
+        greduce<G, 1, false>(xr, sm.red, t, slot);
+        const double xn2 = xr[0];
         const double2 x0 = A[kk + 1][kk];
         double beta;
         double2 tau;
@@ -274,25 +316,29 @@ __global__ void __launch_bounds__(256) k_pencil(Index count, int m0, const doubl
         } else {
             const double nrm = sqrt(x0.x * x0.x + x0.y * x0.y + xn2);
             beta = x0.x >= 0.0 ? -nrm : nrm;
-            tau = make_double2((beta - x0.x) / beta, -x0.y / beta);
+            const double ib = safe_rcp(beta);
+            tau = make_double2((beta - x0.x) * ib, -x0.y * ib);
             const double2 den = make_double2(x0.x - beta, x0.y);
-            const double id = 1.0 / (den.x * den.x + den.y * den.y);
+            const double id = safe_rcp(den.x * den.x + den.y * den.y);
             scal = make_double2(den.x * id, -den.y * id);
         }
         // v (index 0 <-> row kk+1)
         for (int i = t; i < m; i += G) sm.v[i] = i == 0 ? make_double2(1.0, 0.0) : cmul(A[kk + 1 + i][kk], scal);
         gsync<G>(slot);
         if (tau.x != 0.0 || tau.y != 0.0) {
-            // y = A22 v, then w = tau y - 1/2 |tau|^2 (v^H y) v
+            // y = A22 v (TPR threads per row), then w = tau y - 1/2 |tau|^2 (v^H y) v
             double2 yi = make_double2(0.0, 0.0);
-            const int i = t;
-            if (i < m) {
-                for (int j = 0; j < m; ++j) yi = cadd(yi, cmul(A[kk + 1 + i][kk + 1 + j], sm.v[j]));
+            if (row < m)
+                for (int j = part; j < m; j += TPR) yi = cadd(yi, cmul(A[kk + 1 + row][kk + 1 + j], sm.v[j]));
+#pragma unroll
+            for (int o = TPR / 2; o > 0; o >>= 1) {
+                yi.x += __shfl_xor_sync(0xffffffffu, yi.x, o);
+                yi.y += __shfl_xor_sync(0xffffffffu, yi.y, o);
             }
-            double part = i < m ? cmulc(sm.v[i], yi).x : 0.0;  // Re(v^H y); v^H A v is real
-            const double vy = greduce<G, false>(part, sm.red, t, slot);
-            const double half = 0.5 * (tau.x * tau.x + tau.y * tau.y) * vy;
-            if (i < m) sm.w[i] = csub(cmul(tau, yi), cscale(half, sm.v[i]));
+            double vr[1] = {(row < m && part == 0) ? cmulc(sm.v[row], yi).x : 0.0};  // Re(v^H y)
+            greduce<G, 1, false>(vr, sm.red, t, slot);
+            const double half = 0.5 * (tau.x * tau.x + tau.y * tau.y) * vr[0];
+            if (row < m && part == 0) sm.w[row] = csub(cmul(tau, yi), cscale(half, sm.v[row]));
             gsync<G>(slot);
             // A22 -= w v^H + v w^H
 #pragma unroll
@@ -333,36 +379,60 @@ __global__ void __launch_bounds__(256) k_pencil(Index count, int m0, const doubl
         sm.scal[2] = 2.2250738585072014e-308 * fmax(1.0, emax);
     }
     gsync<G>(slot);
-    // 5. parallel multisection: P threads per eigenvalue (same warp, contiguous lanes)
+    PPROF(5);
+    // 5. parallel multisection: P threads (contiguous lanes) x Q shifts per thread and
+    //    eigenvalue; the bracket shrinks (P Q + 1)-fold per round.
+    constexpr int Q = 4;
     int P = 1;
     while (P * 2 <= 32 && P * 2 * n <= G) P *= 2;
     const double pivmin = sm.scal[2];
     const int per_round = G / P;  // eigenvalues handled concurrently
+    const double inv_pts = 1.0 / static_cast<double>(P * Q + 1);
     for (int base = 0; base < n; base += per_round) {
-        const int mi = base + t / P;   // eigenvalue index of this thread
+        const int mi = base + t / P;  // eigenvalue index of this thread
         const int sub = t % P;
         const bool active = mi < n;
         double a = sm.scal[0], b = sm.scal[1];
         const unsigned lane = threadIdx.x & 31;
-        const unsigned gmask = (P == 32) ? 0xffffffffu : (((1u << P) - 1u) << (lane & ~static_cast<unsigned>(P - 1)));
+        const int gb = static_cast<int>(lane & ~static_cast<unsigned>(P - 1));
+        const unsigned gmask = (P == 32) ? 0xffffffffu : (((1u << P) - 1u) << gb);
         for (int it = 0; it < 80; ++it) {
-            const double x = a + (b - a) * (static_cast<double>(sub + 1) / static_cast<double>(P + 1));
-            const int cnt = active ? sturm_count(sm.d, sm.e2, n, x, pivmin) : 0;
-            const unsigned bal = __ballot_sync(0xffffffffu, active && cnt > mi) & gmask;
-            // x values of the group are increasing with sub: the first x with count > mi
-            // bounds the eigenvalue above, its predecessor (or a) below. Shuffles are
-            // executed unconditionally by the whole warp (groups may take different cases).
-            const int gb = static_cast<int>(lane & ~static_cast<unsigned>(P - 1));
-            const int j = bal ? (__ffs(bal) - 1 - gb) : P;  // P: none of the points is above
-            const double xb = __shfl_sync(0xffffffffu, x, gb + min(j, P - 1));
-            const double xa = __shfl_sync(0xffffffffu, x, gb + max(min(j, P) - 1, 0));
-            double na, nb;
-            if (j == P) {
-                na = xb;  // last point
-                nb = b;
+            double x[Q];
+            int cnt[Q];
+#pragma unroll
+            for (int j = 0; j < Q; ++j) x[j] = a + (b - a) * (static_cast<double>(sub * Q + j + 1) * inv_pts);
+            if (active) {
+                sturm_counts<Q>(sm.d, sm.e2, n, x, pivmin, cnt);
             } else {
-                nb = xb;
-                na = j > 0 ? xa : a;
+#pragma unroll
+                for (int j = 0; j < Q; ++j) cnt[j] = 0;
+            }
+            // first shift (in group order sub*Q + j, increasing x) whose count exceeds mi
+            int fq = Q;
+#pragma unroll
+            for (int j = Q - 1; j >= 0; --j)
+                if (cnt[j] > mi) fq = j;
+            // candidate bracket if this thread holds the first such shift
+            const double prev_last = __shfl_up_sync(0xffffffffu, x[Q - 1], 1);
+            double clo = (sub > 0) ? prev_last : a, chi = x[0];
+#pragma unroll
+            for (int j = 1; j < Q; ++j)
+                if (fq == j) {
+                    clo = x[j - 1];
+                    chi = x[j];
+                }
+            const unsigned bal = __ballot_sync(0xffffffffu, active && fq < Q) & gmask;
+            const int src = bal ? (__ffs(bal) - 1) : (gb + P - 1);
+            const double slo = __shfl_sync(0xffffffffu, clo, src);
+            const double shi = __shfl_sync(0xffffffffu, chi, src);
+            const double last = __shfl_sync(0xffffffffu, x[Q - 1], gb + P - 1);
+            double na, nb;
+            if (bal) {
+                na = slo;
+                nb = shi;
+            } else {
+                na = last;  // every shift is below the eigenvalue
+                nb = b;
             }
             const bool done = !(nb - na > 2.2e-16 * fmax(fabs(na), fabs(nb))) || (na == a && nb == b);
             a = na;
@@ -371,33 +441,46 @@ __global__ void __launch_bounds__(256) k_pencil(Index count, int m0, const doubl
         }
         if (active && sub == 0) eig[k * m0 + mi] = 0.5 * (a + b);
     }
+    PPROF(6);
 }
 
-template <int NM, int G>
+template <int NM, int G, int BS>
 static void run_pencil(const Launch& L, Index count, Index m0, const double2* H, const double2* S, double* eig,
                        unsigned long long* fail_key, bool checks) {
-    constexpr int PPC = (G >= 256) ? 1 : 256 / G;
+    static_assert(BS % G == 0 && (G <= 32 || G % 32 == 0), "group layout");
+    constexpr int PPC = BS / G;
     const size_t smem = sizeof(PSmem<NM>) * PPC;
     static bool attr = false;
     if (!attr) {
-        LT_CU(cudaFuncSetAttribute(k_pencil<NM, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        LT_CU(cudaFuncSetAttribute(k_pencil<NM, G, BS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
         attr = true;
     }
     const Index blocks = (count + PPC - 1) / PPC;
     Stage st_(L, "pencil");
-    k_pencil<NM, G><<<static_cast<unsigned>(blocks), 256, smem, L.st>>>(count, static_cast<int>(m0), H, S, eig,
-                                                                         fail_key, checks ? 1 : 0);
+    k_pencil<NM, G, BS><<<static_cast<unsigned>(blocks), BS, smem, L.st>>>(count, static_cast<int>(m0), H, S, eig,
+                                                                            fail_key, checks ? 1 : 0);
     LT_CU(cudaGetLastError());
     L.tick();
 }
 
+// Group size per pencil (measured with tools/pencil_phases.cu): more threads per pencil
+// only pay off for m0 <= 8 batches that cannot fill the GPU (16 multisection points per
+// eigenvalue instead of 4); for larger blocks the extra threads lengthen every barrier of
+// the Cholesky/Householder chains more than they shorten the bisection.
 void launch_pencil(const Launch& L, Index count, Index m0, const double2* H, const double2* S, double* eig,
                    unsigned long long* fail_key, bool periodic_checks) {
     if (count <= 0) return;
-    if (m0 <= 8) run_pencil<8, 32>(L, count, m0, H, S, eig, fail_key, periodic_checks);
-    else if (m0 <= 16) run_pencil<16, 64>(L, count, m0, H, S, eig, fail_key, periodic_checks);
-    else if (m0 <= 32) run_pencil<32, 256>(L, count, m0, H, S, eig, fail_key, periodic_checks);
-    else fail(LT_EDIM, "pencil_eig: block size m0 > 32 is not supported by the batched solver");
+    if (m0 <= 8) {
+        if (count <= 1184) run_pencil<8, 128, 256>(L, count, m0, H, S, eig, fail_key, periodic_checks);
+        else run_pencil<8, 32, 256>(L, count, m0, H, S, eig, fail_key, periodic_checks);
+    } else if (m0 <= 16) {
+        run_pencil<16, 64, 256>(L, count, m0, H, S, eig, fail_key, periodic_checks);
+    } else if (m0 <= 32) {
+        run_pencil<32, 256, 256>(L, count, m0, H, S, eig, fail_key, periodic_checks);
+    } else {
+        fail(LT_EDIM, "pencil_eig: block size m0 > 32 is not supported by the batched solver");
+    }
 }
 
 }  // namespace lt

@@ -58,6 +58,18 @@ def test_pencils_random(ctx, oracle, m0):
         assert np.max(np.abs(ev[j] - orc)) < 1e-11 * max(1.0, np.max(np.abs(ref)))
 
 
+@pytest.mark.parametrize("m0,count", [(8, 1300), (12, 700), (24, 160)])
+def test_pencils_large_batch(ctx, m0, count):
+    # batches too large for the latency layout take the throughput layout (fewer
+    # multisection points per eigenvalue); both must agree with scipy
+    rng = np.random.default_rng(7 * m0 + count)
+    H, S = random_pencils(rng, count, m0)
+    ev = ctx.pencil_eig(H, S)
+    for j in range(0, count, 7):
+        ref = sl.eigh(H[j], S[j], eigvals_only=True)
+        assert np.max(np.abs(ev[j] - ref)) < 1e-11 * max(1.0, np.max(np.abs(ref)))
+
+
 def test_pencil_scalar_kat(ctx):
     # test_eigensolver.cpp:28-34 scalar pencil (-0.3, 0.8) -> -0.375
     ev = ctx.pencil_eig(np.array([[[-0.3 + 0j]]]), np.array([[[0.8 + 0j]]]))
