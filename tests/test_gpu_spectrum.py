@@ -58,7 +58,7 @@ def test_pencils_random(ctx, oracle, m0):
         assert np.max(np.abs(ev[j] - orc)) < 1e-11 * max(1.0, np.max(np.abs(ref)))
 
 
-@pytest.mark.parametrize("m0,count", [(8, 1300), (12, 700), (24, 160)])
+@pytest.mark.parametrize("m0,count", [(8, 1300), (12, 700), (24, 160), (6, 1100)])
 def test_pencils_large_batch(ctx, m0, count):
     # batches too large for the latency layout take the throughput layout (fewer
     # multisection points per eigenvalue); both must agree with scipy

@@ -84,7 +84,7 @@ int main() {
     run<16, 64, 256>(512, 16, 5);
     run<16, 256, 256>(512, 16, 5);
     run<32, 256, 256>(1, 32, 5);
-    run<32, 1024, 1024>(1, 32, 5);
+    run<8, 128, 256>(1184, 8, 5);
     run<8, 32, 256>(4096, 8, 5);
     return 0;
 }
