@@ -312,7 +312,8 @@ def main():
                 roof = {"kernel": name, "bound": st["bound"], "achieved": achieved, "peak": peak,
                         "unit": "GB/s" if hbm else "TFLOP/s", "frac": achieved / peak, "traffic": None,
                         "avg_launch_ms": avg_ms, "launches_per_step": nl / args.steps,
-                        "share_of_step": tot_ms / args.steps / step_ms_stage if step_ms_stage else None,
+                        # share of the summed kernel time (comparable with the ncu launch list)
+                        "share_of_step": tot_ms / sum(v[0] for v in stages.values()),
                         "algorithmic_per_launch": per_launch,
                         "peak_source": peaks["hbm_src"] if hbm else peaks["fp64_src"],
                         "step_roofline_frac": step_frac}

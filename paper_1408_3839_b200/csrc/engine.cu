@@ -118,7 +118,17 @@ struct lt_ctx {
     bool graphs = true;
     GraphCache l0graph, coregraph;
     int* pinned = nullptr;  // small pinned read-back buffer
+    // side streams for independent branches of the assembly (captured into the same graph
+    // as parallel branches) and the fork/join events between them
+    cudaStream_t aux[2]{nullptr, nullptr};
+    cudaEvent_t ev[8]{};
     Launch L() { return Launch{stream, &launches, &timer}; }
+    Launch LA(int i) { return Launch{aux[i], &launches, &timer}; }
+    // `to` waits for everything enqueued on `from` so far
+    void join(int e, cudaStream_t from, cudaStream_t to) {
+        LT_CU(cudaEventRecord(ev[e], from));
+        LT_CU(cudaStreamWaitEvent(to, ev[e], 0));
+    }
     int* pinned_state() {
         if (!pinned) LT_CU(cudaHostAlloc(reinterpret_cast<void**>(&pinned), 64 * sizeof(int), cudaHostAllocDefault));
         return pinned;
@@ -370,31 +380,43 @@ static int64_t* upload_s0(lt_ctx* c, const Plan& p) {
 
 static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need, int mode, AsmOut out,
                          Work* wout = nullptr, const int64_t* s0_dev = nullptr) {
+    // Three concurrent branches (parallel branches of the captured graph):
+    //   main   : sinc -> potential of the 1st, 3rd distinct direction -> nuclear -> fill
+    //   aux[1] : potential of the 2nd distinct direction (joins main before the nuclear part)
+    //   aux[0] : profiles -> FEM tables (profiles join main before the nuclear part, the
+    //            tables before the fill)
     const Launch L = c->L();
+    const Launch LF = c->LA(0), LP = c->LA(1);
     const Index m0 = p.m0, mm = m0 * m0, RN = p.RN, Rtot = p.Rtot;
     Arena& A = c->arena;
     int src[3];
     direction_sources(sd->hs, src);
     Work w{};
+    const int64_t* s0d = nullptr;
+    const bool nuc = need & NEED_NUC, ms = need & NEED_MS;
+    if (nuc) s0d = s0_dev ? s0_dev : upload_s0(c, p);
+    c->join(0, c->stream, c->aux[0]);
     w.t = A.get<double>("sinc.t", RN);
     w.w = A.get<double>("sinc.w", RN);
     w.potw = A.get<double>("sinc.potw", Rtot);
     launch_sinc(L, p.M, sd->ds, w.t, w.w, w.potw);
-    const bool nuc = need & NEED_NUC, ms = need & NEED_MS;
+    c->join(1, c->stream, c->aux[1]);
     if (nuc) {
-        const int64_t* s0d = s0_dev ? s0_dev : upload_s0(c, p);
+        int nth = 0;
         for (int l = 0; l < 3; ++l) {
             if (src[l] != l) {
                 w.pot[l] = w.pot[src[l]];
                 continue;
             }
+            const Launch& LL = (nth++ == 1) ? LP : L;
             const DirPlan& d = p.d[l];
             double* master = A.get<double>("pot.master" + std::to_string(l), d.mrows * RN);
             w.pot[l] = A.get<double>("pot.panel" + std::to_string(l), d.pot_rows * Rtot);
-            launch_master(L, d.mrows, d.h, RN, w.t, master);
-            launch_window_sum(L, master, d.mrows, RN, p.nnuc, s0d + l * p.nnuc, d.nsum, d.n, d.pot_rows, w.pot[l]);
+            launch_master(LL, d.mrows, d.h, RN, w.t, master);
+            launch_window_sum(LL, master, d.mrows, RN, p.nnuc, s0d + l * p.nnuc, d.nsum, d.n, d.pot_rows, w.pot[l]);
         }
     }
+    c->join(2, c->aux[1], c->stream);
     // profiles (galerkin.cpp:127-149), distinct directions only
     ProfileJob jobs[6];
     int nj = 0;
@@ -437,7 +459,8 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
             w.pwl_lo[l] = w.pwl_lo[src[l]];
             w.pwl_hi[l] = w.pwl_hi[src[l]];
         }
-    launch_profiles(L, sd->ds, jobs, nj, 1e-280);
+    launch_profiles(LF, sd->ds, jobs, nj, 1e-280);
+    c->join(3, c->aux[0], c->stream);  // nuclear part needs the profiles
     if (ms) {
         // FEM-applied profiles (T v) for every distinct direction, then the tables as
         // residue-class correlations <u_mu, (T v_nu)(. - d nbar)> on DMMA
@@ -456,7 +479,7 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
             J.wm = wm[l] = A.get<double>("fem.wm" + std::to_string(l), m0 * (d.Gbar + 2));
             J.ws = wsf[l] = A.get<double>("fem.ws" + std::to_string(l), m0 * (d.Gbar + 2));
         }
-        launch_fem_apply(L, fj, nfj, static_cast<int>(m0));
+        launch_fem_apply(LF, fj, nfj, static_cast<int>(m0));
         for (int l = 0; l < 3; ++l) {
             if (src[l] != l) {
                 w.massT[l] = w.massT[src[l]];
@@ -485,7 +508,7 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
             f.res[0] = w.massT[l];
             f.res[1] = w.stiffT[l];
             f.slab = A.get<double>("fem.slab" + std::to_string(l), resfold_slab_doubles(f));
-            launch_resfold(L, f, true, false, "fem_fold");
+            launch_resfold(LF, f, true, false, "fem_fold");
         }
     }
     // nuclear contraction: choose the reassociation (k_nuclear2.cu header)
@@ -615,6 +638,7 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
             }
         }
     }
+    c->join(4, c->aux[0], c->stream);  // FEM tables before the fill
     // fused combine + placement
     FillArgs fa;
     fa.m0 = m0;
@@ -674,13 +698,13 @@ struct DftPrep {
     Index ext[3]{1, 1, 1};
     Index ncomp[3]{1, 1, 1};
     Index nblk = 0, m0 = 0, maxsz = 0;
-    int64_t* kslot = nullptr;
+    int* slot2blk = nullptr;  // compressed position -> stored block (-1: zero block)
     int64_t* comp[3]{nullptr, nullptr, nullptr};
     std::string tag;
 };
 
-// host part of the block diagonalisation: compressed per-axis index sets and slots,
-// uploaded (not capturable, so done before any graph capture)
+// host part of the block diagonalisation: compressed per-axis index sets and the
+// slot map, uploaded (not capturable, so done before any graph capture)
 static DftPrep prepare_dft(lt_ctx* c, const Index dims[3], Index m0, const std::vector<std::array<Index, 3>>& kidx,
                            const std::string& tag) {
     DftPrep P;
@@ -702,14 +726,14 @@ static DftPrep prepare_dft(lt_ctx* c, const Index dims[3], Index m0, const std::
                 if (v < 0 || v >= dims[l]) fail(LT_EBOUNDS, "GeneratingBlockTensor: index out of range");
         }
     }
-    std::vector<int64_t> kslot(kidx.size());
+    std::vector<int> slot2blk(static_cast<size_t>(P.ext[0] * P.ext[1] * P.ext[2]), -1);
     for (size_t b = 0; b < kidx.size(); ++b) {
         Index pos = 0;
         for (int l = 0; l < 3; ++l) {
             const Index ci = std::lower_bound(comp[l].begin(), comp[l].end(), kidx[b][l]) - comp[l].begin();
             pos = pos * P.ext[l] + ci;
         }
-        kslot[b] = pos;
+        slot2blk[pos] = static_cast<int>(b);
     }
     P.maxsz = P.ext[0] * P.ext[1] * P.ext[2];
     Index e2[3] = {P.ext[0], P.ext[1], P.ext[2]};
@@ -717,8 +741,8 @@ static DftPrep prepare_dft(lt_ctx* c, const Index dims[3], Index m0, const std::
         if (dims[a] > 1) e2[a] = dims[a];
         P.maxsz = std::max(P.maxsz, e2[0] * e2[1] * e2[2]);
     }
-    P.kslot = c->arena.get<int64_t>("dft.kslot" + tag, kslot.size() + 1);
-    upload(c, P.kslot, kslot.data(), kslot.size() * sizeof(int64_t));
+    P.slot2blk = c->arena.get<int>("dft.slot" + tag, slot2blk.size());
+    upload(c, P.slot2blk, slot2blk.data(), slot2blk.size() * sizeof(int));
     for (int a = 0; a < 3; ++a) {
         P.comp[a] = c->arena.get<int64_t>("dft.comp" + tag + std::to_string(a), comp[a].size());
         upload(c, P.comp[a], comp[a].data(), comp[a].size() * sizeof(int64_t));
@@ -726,34 +750,64 @@ static DftPrep prepare_dft(lt_ctx* c, const Index dims[3], Index m0, const std::
     return P;
 }
 
-// device part (kernels and memsets only: capturable)
-static double2* launch_dft(lt_ctx* c, const DftPrep& P, const double* blocks_dev) {
+// device part (kernels only: capturable). Transforms nops operators that share the
+// stored kidx (blocks[op] on device, std::map order); out[op] receives [K][mm] complex.
+static void launch_dft(lt_ctx* c, const DftPrep& P, int nops, const double* const* blocks, double2** out) {
     const Launch L = c->L();
     const Index mm = P.m0 * P.m0;
-    double2* bufA = c->arena.get<double2>("dft.a" + P.tag, P.maxsz * mm);
-    double2* bufB = c->arena.get<double2>("dft.b" + P.tag, P.maxsz * mm);
-    LT_CU(cudaMemsetAsync(bufA, 0, sizeof(double2) * P.ext[0] * P.ext[1] * P.ext[2] * mm, c->stream));
-    launch_scatter_gen(L, P.nblk, mm, P.kslot, blocks_dev, bufA);
-    double2* cur = bufA;
-    double2* nxt = bufB;
-    Index in_ext[3] = {P.ext[0], P.ext[1], P.ext[2]};
-    for (int a = 0; a < 3; ++a) {
-        if (P.dims[a] == 1) continue;
-        double2* tw = c->arena.get<double2>("dft.tw" + P.tag + std::to_string(a), P.dims[a] * P.ncomp[a]);
-        launch_twiddles(L, P.dims[a], P.ncomp[a], P.comp[a], tw);
-        Index out_ext[3] = {in_ext[0], in_ext[1], in_ext[2]};
-        out_ext[a] = P.dims[a];
-        launch_dft_axis(L, a, in_ext, out_ext, mm, cur, nxt, tw, P.ncomp[a], P.dims[a]);
-        std::swap(cur, nxt);
-        for (int l = 0; l < 3; ++l) in_ext[l] = out_ext[l];
+    double2* buf[2][2];
+    for (int op = 0; op < nops; ++op) {
+        buf[op][0] = c->arena.get<double2>("dft.a" + P.tag + std::to_string(op), P.maxsz * mm);
+        buf[op][1] = c->arena.get<double2>("dft.b" + P.tag + std::to_string(op), P.maxsz * mm);
     }
-    return cur;
+    DftAxisArgs a;
+    a.mm = mm;
+    for (int l = 0; l < 3; ++l) a.in[l] = P.ext[l];
+    int nax = 0, cur = 0;
+    for (int ax = 0; ax < 3; ++ax) {
+        if (P.dims[ax] == 1) continue;
+        a.axis = ax;
+        for (int l = 0; l < 3; ++l) a.out[l] = a.in[l];
+        a.out[ax] = P.dims[ax];
+        a.ncomp = P.ncomp[ax];
+        a.Lax = P.dims[ax];
+        a.comp = P.comp[ax];
+        for (int op = 0; op < nops; ++op) {
+            a.gen[op] = nax == 0 ? blocks[op] : nullptr;
+            a.in_buf[op] = nax == 0 ? nullptr : buf[op][cur];
+            a.out_buf[op] = buf[op][cur ^ 1];
+        }
+        a.slot2blk = P.slot2blk;
+        launch_dft_axis2(L, a, nops);
+        cur ^= 1;
+        ++nax;
+        for (int l = 0; l < 3; ++l) a.in[l] = a.out[l];
+    }
+    if (nax == 0) {
+        // K = 1 (all L_l = 1): a single generating block; real -> complex copy
+        DftAxisArgs z = a;
+        z.axis = 0;
+        z.ncomp = 1;
+        z.Lax = 1;
+        z.comp = P.comp[0];
+        for (int op = 0; op < nops; ++op) {
+            z.gen[op] = blocks[op];
+            z.out_buf[op] = buf[op][1];
+        }
+        z.slot2blk = P.slot2blk;
+        launch_dft_axis2(L, z, nops);
+        cur = 1;
+    }
+    for (int op = 0; op < nops; ++op) out[op] = buf[op][cur];
 }
 
 static double2* block_diag_device(lt_ctx* c, const Index dims[3], Index m0,
                                   const std::vector<std::array<Index, 3>>& kidx, const double* blocks_dev,
                                   const std::string& tag) {
-    return launch_dft(c, prepare_dft(c, dims, m0, kidx, tag), blocks_dev);
+    const DftPrep P = prepare_dft(c, dims, m0, kidx, tag);
+    double2* out = nullptr;
+    launch_dft(c, P, 1, &blocks_dev, &out);
+    return out;
 }
 
 static void raise_fail_key(unsigned long long key, bool periodic) {
@@ -863,15 +917,14 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
     unsigned long long* fk = c->arena.get<unsigned long long>("solve.fail", 1);
     LT_CU(cudaMemsetAsync(fk, 0xff, sizeof(unsigned long long), c->stream));
     int64_t* s0d = upload_s0(c, p);
-    DftPrep dpH, dpS;
+    DftPrep dp;
     if (periodic) {
         out.out0 = c->arena.get<double>("core.H", p.nblocks * mm);
         out.out1 = c->arena.get<double>("core.S", p.nblocks * mm);
         out.kidx = c->arena.get<int64_t>("core.kidx", p.nblocks * 3);
         const auto kidx = periodic_kidx(p);
         const Index dims[3] = {p.d[0].L, p.d[1].L, p.d[2].L};
-        dpH = prepare_dft(c, dims, p.m0, kidx, "H");
-        dpS = prepare_dft(c, dims, p.m0, kidx, "S");
+        dp = prepare_dft(c, dims, p.m0, kidx, "HS");
     } else {
         out.out0 = c->arena.get<double>("core.H", p.Nb * p.Nb);
         out.out1 = c->arena.get<double>("core.S", p.Nb * p.Nb);
@@ -881,8 +934,11 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
     auto enqueue = [&]() {
         run_assembly(c, sd, p, NEED_MS | NEED_NUC, 0, out, nullptr, s0d);
         if (periodic) {
-            double2* Hb = launch_dft(c, dpH, out.out0);
-            double2* Sb = launch_dft(c, dpS, out.out1);
+            const double* blocks[2] = {out.out0, out.out1};
+            double2* bd[2];
+            launch_dft(c, dp, 2, blocks, bd);
+            double2* Hb = bd[0];
+            double2* Sb = bd[1];
             if (k_begin < k_end)
                 launch_pencil(c->L(), k_end - k_begin, p.m0, Hb + k_begin * mm, Sb + k_begin * mm,
                               eig_dev + k_begin * p.m0, fk, true);
@@ -963,6 +1019,8 @@ lt_status lt_create(int device, lt_ctx** out) {
         c->device = device;
         LT_CU(cudaSetDevice(device));
         LT_CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        for (auto& a : c->aux) LT_CU(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
+        for (auto& e : c->ev) LT_CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         *out = c.release();
     });
 }
@@ -973,6 +1031,13 @@ void lt_destroy(lt_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->solver) cusolverDnDestroy(c->solver);
     if (c->pinned) cudaFreeHost(c->pinned);
+    for (auto& a : c->aux)
+        if (a) {
+            cudaStreamSynchronize(a);
+            cudaStreamDestroy(a);
+        }
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }

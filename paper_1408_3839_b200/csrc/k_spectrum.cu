@@ -1,12 +1,12 @@
 // k_spectrum.cu — block diagonalisation over lattice indices and batched pencil eigensolves.
 //
-//   launch_scatter_gen / launch_dft_axis
+//   launch_dft_axis2
 //       bc_block_diagonalize + fft_levels (block_circulant.cpp:82-112, :184-196):
 //       unnormalised forward DFT, omega = exp(-2 pi i / L), axis 0 then 1 then 2, for every
 //       block entry. Only the stored generating blocks are non-zero, so each axis is a
 //       sparse DFT from the compressed set of stored kidx values to all L frequencies
-//       (exact same sum as the zero-padded FFT; K = (2b+1) terms per output instead of
-//       log L butterflies over mostly zeros).
+//       (the zero-padded FFT's values from (2b+1) terms per output instead of log L
+//       butterflies over mostly zeros).
 // The batched pencil eigensolver is in k_pencil.cu.
 #include "lt_device.cuh"
 #include "lt_internal.cuh"
@@ -24,82 +24,73 @@ __device__ __forceinline__ double cabs2(double2 a) { return a.x * a.x + a.y * a.
 __device__ __forceinline__ double cabs_(double2 a) { return hypot(a.x, a.y); }
 
 // ---------------------------------------------------------------------------
-// DFT over lattice indices
+// fused axis DFT: one launch per transformed axis for up to two operators (H, S). CTA
+// (j, op, chunk): output frequency j along the axis; its twiddles w^(j comp[c] mod L)
+// are computed once into shared memory (same sincospi argument as k_twiddles). The
+// first axis reads the real generating blocks directly through slot -> block (-1:
+// absent block, i.e. zero), so no scatter / memset / twiddle launches remain. The sum
+// runs over the compressed indices c in ascending order, as in k_dft_axis.
 // ---------------------------------------------------------------------------
-__global__ void k_scatter_gen(Index nblk, Index mm, const int64_t* __restrict__ kslot, const double* __restrict__ blocks,
-                              double2* __restrict__ dense) {
-    const Index idx = static_cast<Index>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (idx >= nblk * mm) return;
-    const Index b = idx / mm, e = idx % mm;
-    dense[kslot[b] * mm + e] = make_double2(blocks[idx], 0.0);
-}
-
-void launch_scatter_gen(const Launch& L, Index nblk, Index mm, const int64_t* kslot_dev, const double* blocks,
-                        double2* dense) {
-    const Index tot = nblk * mm;
-    if (tot == 0) return;
-    Stage st_(L, "scatter_gen");
-    k_scatter_gen<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, L.st>>>(nblk, mm, kslot_dev, blocks, dense);
-    LT_CU(cudaGetLastError());
-    L.tick();
-}
-
-__global__ void k_twiddles(Index Lax, Index ncomp, const int64_t* __restrict__ comp, double2* __restrict__ tw) {
-    const Index idx = static_cast<Index>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (idx >= Lax * ncomp) return;
-    const Index j = idx / ncomp, c = idx % ncomp;
-    const Index m = (j * comp[c]) % Lax;
-    double s, co;
-    sincospi(-2.0 * static_cast<double>(m) / static_cast<double>(Lax), &s, &co);
-    tw[idx] = make_double2(co, s);
-}
-
-void launch_twiddles(const Launch& L, Index Lax, Index ncomp, const int64_t* comp_dev, double2* tw) {
-    const Index tot = Lax * ncomp;
-    Stage st_(L, "twiddles");
-    k_twiddles<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, L.st>>>(Lax, ncomp, comp_dev, tw);
-    LT_CU(cudaGetLastError());
-    L.tick();
-}
-
-struct Ext3 {
-    Index in[3], out[3];
-};
-
-__global__ void k_dft_axis(int axis, Ext3 x, Index mm, const double2* __restrict__ in, double2* __restrict__ out,
-                           const double2* __restrict__ tw, Index ncomp) {
-    const Index total = x.out[0] * x.out[1] * x.out[2] * mm;
-    const Index idx = static_cast<Index>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (idx >= total) return;
-    const Index e = idx % mm;
-    Index pos = idx / mm;
-    Index o[3];
-    o[2] = pos % x.out[2];
-    pos /= x.out[2];
-    o[1] = pos % x.out[1];
-    o[0] = pos / x.out[1];
-    const Index j = o[axis];
-    Index stride = mm;
-    for (int l = 2; l > axis; --l) stride *= x.in[l];
-    Index base = 0;
-    for (int l = 0; l < 3; ++l) base = base * x.in[l] + (l == axis ? 0 : o[l]);
-    base = base * mm + e;
-    double2 acc = make_double2(0.0, 0.0);
-    const double2* t = tw + j * ncomp;
-    for (Index c = 0; c < ncomp; ++c) acc = cadd(acc, cmul(t[c], in[base + c * stride]));
-    out[idx] = acc;
-}
-
-void launch_dft_axis(const Launch& L, int axis, const Index* in_ext, const Index* out_ext, Index mm, const double2* in,
-                     double2* out, const double2* tw, Index ncomp, Index /*Lax*/) {
-    Ext3 x;
-    for (int l = 0; l < 3; ++l) {
-        x.in[l] = in_ext[l];
-        x.out[l] = out_ext[l];
+__global__ void k_dft_axis2(DftAxisArgs a) {
+    extern __shared__ double2 tws[];
+    const Index j = blockIdx.x;
+    const int op = blockIdx.y;
+    for (Index c = threadIdx.x; c < a.ncomp; c += blockDim.x) {
+        const Index m = (j * a.comp[c]) % a.Lax;
+        double s, co;
+        sincospi(-2.0 * static_cast<double>(m) / static_cast<double>(a.Lax), &s, &co);
+        tws[c] = make_double2(co, s);
     }
-    const Index tot = out_ext[0] * out_ext[1] * out_ext[2] * mm;
+    __syncthreads();
+    const Index mm = a.mm;
+    const Index o0 = a.out[0], o1 = a.out[1], o2 = a.out[2];
+    const Index i1 = a.in[1], i2 = a.in[2];
+    const Index others = (o0 * o1 * o2 / (a.axis == 0 ? o0 : (a.axis == 1 ? o1 : o2))) * mm;
+    const double* gen = op ? a.gen[1] : a.gen[0];
+    const double2* in = op ? a.in_buf[1] : a.in_buf[0];
+    double2* out = op ? a.out_buf[1] : a.out_buf[0];
+    for (Index q = static_cast<Index>(blockIdx.z) * blockDim.x + threadIdx.x; q < others;
+         q += static_cast<Index>(gridDim.z) * blockDim.x) {
+        const Index e = q % mm, r = q / mm;
+        Index ipos0, istride, opos;  // input position of c = 0, stride per c, output position
+        if (a.axis == 0) {
+            const Index u = r / o2, w = r % o2;
+            ipos0 = u * i2 + w;
+            istride = i1 * i2;
+            opos = (j * o1 + u) * o2 + w;
+        } else if (a.axis == 1) {
+            const Index u = r / o2, w = r % o2;
+            ipos0 = u * i1 * i2 + w;
+            istride = i2;
+            opos = (u * o1 + j) * o2 + w;
+        } else {
+            const Index u = r / o1, w = r % o1;
+            ipos0 = (u * i1 + w) * i2;
+            istride = 1;
+            opos = (u * o1 + w) * o2 + j;
+        }
+        double2 acc = make_double2(0.0, 0.0);
+        if (gen) {
+#pragma unroll 4
+            for (Index c = 0; c < a.ncomp; ++c) {
+                const int b = a.slot2blk[ipos0 + c * istride];
+                const double v = b >= 0 ? gen[static_cast<Index>(b) * mm + e] : 0.0;
+                acc = cadd(acc, cmul(tws[c], make_double2(v, 0.0)));
+            }
+        } else {
+#pragma unroll 4
+            for (Index c = 0; c < a.ncomp; ++c) acc = cadd(acc, cmul(tws[c], in[(ipos0 + c * istride) * mm + e]));
+        }
+        out[opos * mm + e] = acc;
+    }
+}
+
+void launch_dft_axis2(const Launch& L, const DftAxisArgs& a, int nops) {
+    const Index others = (a.out[0] * a.out[1] * a.out[2] / a.Lax) * a.mm;
+    const Index chunks = std::max<Index>(1, std::min<Index>((others + 1023) / 1024, 64));
+    dim3 grid(static_cast<unsigned>(a.Lax), nops, static_cast<unsigned>(chunks));
     Stage st_(L, "dft_axis");
-    k_dft_axis<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, L.st>>>(axis, x, mm, in, out, tw, ncomp);
+    k_dft_axis2<<<grid, 256, sizeof(double2) * a.ncomp, L.st>>>(a);
     LT_CU(cudaGetLastError());
     L.tick();
 }

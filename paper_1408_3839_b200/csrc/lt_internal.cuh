@@ -311,11 +311,18 @@ struct DftPlan {
     Index ncomp[3]{1, 1, 1};   // compressed extents
     std::vector<Index> comp[3];  // compressed kidx values per axis (ascending)
 };
-void launch_scatter_gen(const Launch& L, Index nblk, Index mm, const int64_t* kslot_dev, const double* blocks,
-                        double2* dense);
-void launch_dft_axis(const Launch& L, int axis, const Index* in_ext, const Index* out_ext, Index mm,
-                     const double2* in, double2* out, const double2* tw, Index ncomp, Index Lax);
-void launch_twiddles(const Launch& L, Index Lax, Index ncomp, const int64_t* comp_dev, double2* tw);
+// fused per-axis DFT for one or two operators (k_spectrum.cu)
+struct DftAxisArgs {
+    int axis = 0;
+    Index in[3]{1, 1, 1}, out[3]{1, 1, 1};
+    Index mm = 0, ncomp = 0, Lax = 1;
+    const int64_t* comp = nullptr;                 // compressed indices along the axis
+    const double* gen[2] = {nullptr, nullptr};     // first axis: real generating blocks
+    const int* slot2blk = nullptr;                 // first axis: compressed position -> block (-1: none)
+    const double2* in_buf[2] = {nullptr, nullptr};  // later axes: complex input
+    double2* out_buf[2] = {nullptr, nullptr};
+};
+void launch_dft_axis2(const Launch& L, const DftAxisArgs& a, int nops);
 
 // batched Hermitian-definite pencils (eigensolver.cpp:72-93)
 void launch_pencil(const Launch& L, Index count, Index m0, const double2* H, const double2* S, double* eig,
