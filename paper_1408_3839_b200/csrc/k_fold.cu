@@ -117,11 +117,44 @@ __global__ void __launch_bounds__(256) k_resfold(ResFold f) {
     const int m0p = (f.m0 + 7) / 8 * 8;
     const double* As = sh;                // [m0p][ldj]
     const double* Bs = sh + m0p * ldj;    // [NB][m0p][ldj], column j' + 1 for j' in [-1, J]
-    {
-        const long long tot = static_cast<long long>(1 + NB) * m0p * ldj;
+    const long long tot = static_cast<long long>(1 + NB) * m0p * ldj;
+    double* Vs = sh + tot;                // fused weights V[e] for this residue (f.W set)
+    if (f.slab) {
         const double2* srcp = reinterpret_cast<const double2*>(f.slab + t * tot);
         double2* dstp = reinterpret_cast<double2*>(sh);
         for (int idx = threadIdx.x; idx < tot / 2; idx += blockDim.x) dstp[idx] = srcp[idx];
+    } else {
+        // short residue classes: gather the strided rows directly (same values as the slab)
+        const long long gb = f.bguard ? f.G + 2 : f.G;
+        for (long long idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+            const int src = static_cast<int>(idx / (static_cast<long long>(m0p) * ldj));
+            const int mu = static_cast<int>((idx / ldj) % m0p);
+            const long long c = idx % ldj;
+            double v = 0.0;
+            if (mu < f.m0) {
+                if (src == 0) {
+                    if (c < J) v = f.a[mu * f.G + t + c * f.n];
+                } else if (c < J + 2) {
+                    const double* bsrc = src == 2 ? f.b[1] : f.b[0];
+                    const long long gi = t + (c - 1) * f.n;
+                    if (f.bguard) {
+                        if (gi >= -1 && gi <= f.G) v = bsrc[mu * gb + gi + 1];
+                    } else if (gi >= 0 && gi < f.G) {
+                        v = bsrc[mu * gb + gi];
+                    }
+                }
+            }
+            sh[idx] = v;
+        }
+    }
+    if (f.W) {
+        // V[e][t] = sum_r W[r][e] P[r][t] (the rank sum folded into an effective potential)
+        const int mme = f.m0 * f.m0;
+        for (int e = threadIdx.x; e < mme; e += blockDim.x) {
+            double v = 0.0;
+            for (int r = 0; r < f.Rtot; ++r) v = fma(f.W[r * mme + e], f.P[r * f.prow + t], v);
+            Vs[e] = v;
+        }
     }
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -164,7 +197,7 @@ __global__ void __launch_bounds__(256) k_resfold(ResFold f) {
             const int mu = mt * 8 + g, nu = nt * 8 + 2 * tq + i;
             if (mu >= f.m0 || nu >= f.m0) continue;
             const int e = mu + nu * f.m0;
-            const double wgt = f.V ? f.V[e * f.n + t] : 1.0;
+            const double wgt = f.W ? Vs[e] : (f.V ? f.V[e * f.n + t] : 1.0);
             const long long o = (t * nd + (d - f.dlo)) * static_cast<long long>(mm) + e;
             f.out[0][o] = wgt * (c0[0][i] + c1[0][i]);
             if (NB == 2) f.out[1][o] = wgt * (c0[NB - 1][i] + c1[NB - 1][i]);
@@ -199,7 +232,8 @@ __global__ void k_resfold_reduce(ResFold f, int mirror) {
 
 void launch_resfold(const Launch& L, const ResFold& f, bool reduce, bool mirror, const char* name) {
     const int m0p = (f.m0 + 7) / 8 * 8;
-    const size_t smem = sizeof(double) * static_cast<size_t>(m0p) * resfold_ldj(f.J) * (1 + f.nb);
+    const size_t smem = sizeof(double) * (static_cast<size_t>(m0p) * resfold_ldj(f.J) * (1 + f.nb) +
+                                          (f.W ? static_cast<size_t>(f.m0) * f.m0 : 0));
     static size_t attr[2] = {0, 0};
     if (f.nb < 1 || f.nb > 2) fail(LT_EGENERIC, "residue fold: nb must be 1 or 2");
     if (smem > 48 * 1024 && smem > attr[f.nb - 1] && smem <= 227 * 1024) {
@@ -214,7 +248,7 @@ void launch_resfold(const Launch& L, const ResFold& f, bool reduce, bool mirror,
     if (smem > 227 * 1024)
         fail(LT_EGENERIC, "residue fold: one residue class (" + std::to_string(smem) +
                               " bytes) exceeds the 227 KB shared-memory limit");
-    {
+    if (f.slab) {
         Stage st_(L, "fold_prep");
         dim3 gp(static_cast<unsigned>((f.n + 31) / 32), static_cast<unsigned>((resfold_ldj(f.J) + 31) / 32), (1 + f.nb) * m0p);
         k_resfold_prep<<<gp, 256, 0, L.st>>>(f);

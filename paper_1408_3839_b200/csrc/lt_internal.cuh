@@ -274,11 +274,18 @@ struct ResFold {
     const double* V = nullptr;      // optional weight V[e][t]
     double* out[2] = {nullptr, nullptr};  // [t][d - dlo][e]
     double* res[2] = {nullptr, nullptr};  // reduced [d + band][e]
-    double* slab = nullptr;               // workspace [n][1+nb][m0p][ldj] (residue-major)
+    double* slab = nullptr;               // workspace [n][1+nb][m0p][ldj] (residue-major); null: direct gather
+    // fused weight (instead of V): wgt(e, t) = sum_r W[r][e] P[r][t], P rows of length prow
+    const double* W = nullptr;
+    const double* P = nullptr;
+    int Rtot = 0;
+    long long prow = 0;
 };
 // slab row stride: >= J + 5 (two guard columns plus zero padding for the unchecked last
 // k-step), == 4 mod 16 so the 8 rows x 4 columns of an m8n8k4 fragment hit distinct banks
 __host__ __device__ inline long long resfold_ldj(long long J) { return (J + 16) / 16 * 16 + 4; }
+// residue classes this short are gathered directly by the fold (no transpose launch)
+constexpr long long kResfoldDirectJ = 128;
 inline size_t resfold_slab_doubles(const ResFold& f) {
     const size_t m0p = (static_cast<size_t>(f.m0) + 7) / 8 * 8;
     return static_cast<size_t>(f.n) * (1 + f.nb) * m0p * static_cast<size_t>(resfold_ldj(f.J));

@@ -63,3 +63,19 @@ def test_gpu_kpoint_shards_equal_full_solve(ctx, name):
     for b, e in shard_ranges(K, 3):
         dsys.solve(True, part.data_ptr(), b, e)
     assert torch.equal(full, part)
+
+
+def test_gpu_repeated_and_interleaved_solves_identical(ctx):
+    # graph replay, the cached plan tables and the L0 speculation must reproduce a fresh
+    # solve bitwise, including after another system (different L0 and plan) ran in between
+    seq = ["c2", "c5", "c2", "c2", "c1", "c2", "c4", "c4", "c2"]
+    first = {}
+    for name in seq:
+        s, periodic, d = load(name)
+        info = np.zeros(8, dtype=np.int64)
+        ev = ctx.solve_core(s, periodic, info)
+        assert int(info[0]) == int(d["L0"])
+        if name in first:
+            assert np.array_equal(ev, first[name]), name
+        else:
+            first[name] = ev.copy()
