@@ -76,6 +76,10 @@ int64_t lt_launch_count(lt_ctx* ctx);
 lt_status lt_set_stage_timing(lt_ctx* ctx, int on);
 int64_t lt_stage_count(lt_ctx* ctx);
 lt_status lt_stage_get(lt_ctx* ctx, int64_t idx, char* name, int64_t cap, double* ms, int64_t* launches);
+/* per-launch timeline of the last timed solve: stream 0 main, 1-2 side branches; ms from solve start */
+int64_t lt_stage_timeline_count(lt_ctx* ctx);
+lt_status lt_stage_timeline_get(lt_ctx* ctx, int64_t idx, char* name, int64_t cap, int* stream, double* t0,
+                                double* t1);
 
 /* ---- whole path: LatticeSystem -> eigenvalues ------------------------------- *
  * Replaces assemble_core (tools/commands.cpp:51-59: H = combine(0.5, Laplace,

@@ -123,6 +123,20 @@ class Context:
     def set_stage_timing(self, on: bool):
         check(self.lib.lt_set_stage_timing(self.h, int(on)))
 
+    def stage_timeline(self):
+        """[(name, stream, t0_ms, t1_ms)] of the last solve run with stage timing on."""
+        n = int(self.lib.lt_stage_timeline_count(self.h))
+        out = []
+        buf = ctypes.create_string_buffer(128)
+        st = ctypes.c_int()
+        t0 = ctypes.c_double()
+        t1 = ctypes.c_double()
+        for i in range(n):
+            check(self.lib.lt_stage_timeline_get(self.h, i, buf, 128, ctypes.byref(st), ctypes.byref(t0),
+                                                 ctypes.byref(t1)))
+            out.append((buf.value.decode(), st.value, t0.value, t1.value))
+        return out
+
     def stage_times(self) -> Dict[str, Tuple[float, int]]:
         """{kernel stage: (total ms, launches)} from CUDA events on the context stream."""
         out = {}

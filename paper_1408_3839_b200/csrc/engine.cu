@@ -53,6 +53,7 @@ size_t Arena::bytes() const {
 }
 
 StageTimer::~StageTimer() {
+    if (ref_) cudaEventDestroy(ref_);
     for (cudaEvent_t e : pool_) cudaEventDestroy(e);
 }
 
@@ -74,7 +75,14 @@ void StageTimer::begin(cudaStream_t st, const char* name) {
 void StageTimer::end(cudaStream_t st) {
     cudaEvent_t b = get();
     LT_CU(cudaEventRecord(b, st));
-    pending_.push_back({open_name_, open_, b});
+    pending_.push_back({open_name_, open_, b, st, ref_});
+}
+
+void StageTimer::mark_ref(cudaStream_t st) {
+    if (!on) return;
+    if (!ref_) LT_CU(cudaEventCreate(&ref_));
+    LT_CU(cudaEventRecord(ref_, st));
+    timeline.clear();
 }
 
 void StageTimer::collect() {
@@ -85,6 +93,12 @@ void StageTimer::collect() {
         auto& t = totals[p.name];
         t.first += ms;
         t.second += 1;
+        if (p.ref) {
+            float t0 = 0.f, t1 = 0.f;
+            LT_CU(cudaEventElapsedTime(&t0, p.ref, p.a));
+            LT_CU(cudaEventElapsedTime(&t1, p.ref, p.b));
+            timeline.push_back({p.name, p.st, t0, t1});
+        }
     }
     pending_.clear();
     used_ = 0;
@@ -450,10 +464,12 @@ static void direction_sources(const HostSys& h, int src[3]) {
     }
 }
 
-// split-K factor: aim for ~4 CTAs per SM while keeping >= 64 contraction steps per CTA
+// split-K factor: aim for ~4 CTAs per SM while keeping >= 32 contraction steps (two
+// 16-deep tiles) per CTA: these GEMMs are load-latency bound, so more CTAs with fewer
+// dependent tile loads each finish sooner; the fixed-order split reduction absorbs it
 static int splits_for(long long tiles, long long len) {
     int s = 1;
-    while (tiles * s < 4 * 148 && len / (s * 2) >= 64 && s < 256) s *= 2;
+    while (tiles * s < 4 * 148 && len / (s * 2) >= 32 && s < 512) s *= 2;
     return s;
 }
 
@@ -590,15 +606,17 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
             f.nb = 2;
             f.bguard = 1;
             f.band = static_cast<int>(d.band);
-            f.dlo = -f.band;
+            // <u_mu, T v_nu(. - d nbar)> = <T u_mu(. + d nbar), v_nu>: the d < 0 half is the
+            // (mu, nu)-transposed mirror of d > 0 (T symmetric), so only d >= 0 is folded
+            f.dlo = 0;
             f.dhi = f.band;
-            f.dchunk = std::max(1, static_cast<int>((d.width + 3) / 4));
-            f.out[0] = A.get<double>("fem.pm" + std::to_string(l), d.nbar * d.width * mm);
-            f.out[1] = A.get<double>("fem.ps" + std::to_string(l), d.nbar * d.width * mm);
+            f.dchunk = std::max(1, (f.band + 1 + 3) / 4);
+            f.out[0] = A.get<double>("fem.pm" + std::to_string(l), d.nbar * (d.band + 1) * mm);
+            f.out[1] = A.get<double>("fem.ps" + std::to_string(l), d.nbar * (d.band + 1) * mm);
             f.res[0] = w.massT[l];
             f.res[1] = w.stiffT[l];
             f.slab = f.J <= kResfoldDirectJ ? nullptr : A.get<double>("fem.slab" + std::to_string(l), resfold_slab_doubles(f));
-            launch_resfold(LF, f, true, false, "fem_fold");
+            launch_resfold(LF, f, true, true, "fem_fold");
         }
     }
     // nuclear contraction: choose the reassociation (k_nuclear2.cu header)
@@ -993,6 +1011,7 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
                            Index k_end, int64_t* info, double* eig_host = nullptr, bool allow_spec = true) {
     validate(sd->hs);
     c->phase_mark(0);
+    c->timer.mark_ref(c->stream);
     // L0 speculation: L0 is a function of the system alone; when this system's L0 is known
     // from the previous call, the post-L0 graph is launched right behind the L0 graph
     // (no host round trip) and the device-computed L0 is checked after the final sync.
@@ -1209,6 +1228,24 @@ lt_status lt_stage_get(lt_ctx* c, int64_t idx, char* name, int64_t cap, double* 
         std::snprintf(name, static_cast<size_t>(cap), "%s", it->first.c_str());
         *ms = it->second.first;
         *launches = it->second.second;
+    });
+}
+
+int64_t lt_stage_timeline_count(lt_ctx* c) {
+    cudaStreamSynchronize(c->stream);
+    c->timer.collect();
+    return static_cast<int64_t>(c->timer.timeline.size());
+}
+
+lt_status lt_stage_timeline_get(lt_ctx* c, int64_t idx, char* name, int64_t cap, int* stream, double* t0,
+                                double* t1) {
+    return guarded([&] {
+        if (idx < 0 || idx >= static_cast<int64_t>(c->timer.timeline.size())) fail(LT_EBOUNDS, "timeline index");
+        const auto& sp = c->timer.timeline[static_cast<size_t>(idx)];
+        std::snprintf(name, static_cast<size_t>(cap), "%s", sp.name.c_str());
+        *stream = sp.stream == c->stream ? 0 : (sp.stream == c->aux[0] ? 1 : (sp.stream == c->aux[1] ? 2 : 3));
+        *t0 = sp.t0;
+        *t1 = sp.t1;
     });
 }
 

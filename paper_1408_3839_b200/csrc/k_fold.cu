@@ -148,11 +148,30 @@ __global__ void __launch_bounds__(256) k_resfold(ResFold f) {
         }
     }
     if (f.W) {
-        // V[e][t] = sum_r W[r][e] P[r][t] (the rank sum folded into an effective potential)
+        // V[e][t] = sum_r W[r][e] P[r][t] (the rank sum folded into an effective potential):
+        // every thread takes one (e, rank part) with four independent accumulators so the
+        // loads of a part are in flight together; parts are summed in fixed order below
         const int mme = f.m0 * f.m0;
+        const int parts = max(1, static_cast<int>(blockDim.x) / mme);
+        double* Vp = Vs + mme;  // [parts][mme]
+        for (int idx = threadIdx.x; idx < mme * parts; idx += blockDim.x) {
+            const int e = idx % mme, part = idx / mme;
+            const int r0 = (f.Rtot * part) / parts, r1 = (f.Rtot * (part + 1)) / parts;
+            double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+            int r = r0;
+            for (; r + 3 < r1; r += 4) {
+                v0 = fma(f.W[(r + 0) * mme + e], f.P[(r + 0) * f.prow + t], v0);
+                v1 = fma(f.W[(r + 1) * mme + e], f.P[(r + 1) * f.prow + t], v1);
+                v2 = fma(f.W[(r + 2) * mme + e], f.P[(r + 2) * f.prow + t], v2);
+                v3 = fma(f.W[(r + 3) * mme + e], f.P[(r + 3) * f.prow + t], v3);
+            }
+            for (; r < r1; ++r) v0 = fma(f.W[r * mme + e], f.P[r * f.prow + t], v0);
+            Vp[part * mme + e] = (v0 + v1) + (v2 + v3);
+        }
+        __syncthreads();
         for (int e = threadIdx.x; e < mme; e += blockDim.x) {
-            double v = 0.0;
-            for (int r = 0; r < f.Rtot; ++r) v = fma(f.W[r * mme + e], f.P[r * f.prow + t], v);
+            double v = Vp[e];
+            for (int part = 1; part < parts; ++part) v += Vp[part * mme + e];
             Vs[e] = v;
         }
     }
@@ -232,8 +251,10 @@ __global__ void k_resfold_reduce(ResFold f, int mirror) {
 
 void launch_resfold(const Launch& L, const ResFold& f, bool reduce, bool mirror, const char* name) {
     const int m0p = (f.m0 + 7) / 8 * 8;
+    const size_t mme = static_cast<size_t>(f.m0) * f.m0;
+    const size_t vparts = f.W ? std::max<size_t>(1, 256 / mme) : 0;
     const size_t smem = sizeof(double) * (static_cast<size_t>(m0p) * resfold_ldj(f.J) * (1 + f.nb) +
-                                          (f.W ? static_cast<size_t>(f.m0) * f.m0 : 0));
+                                          (f.W ? mme * (1 + vparts) : 0));
     static size_t attr[2] = {0, 0};
     if (f.nb < 1 || f.nb > 2) fail(LT_EGENERIC, "residue fold: nb must be 1 or 2");
     if (smem > 48 * 1024 && smem > attr[f.nb - 1] && smem <= 227 * 1024) {

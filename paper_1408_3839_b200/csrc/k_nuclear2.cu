@@ -43,13 +43,27 @@ __global__ void __launch_bounds__(256) k_triv_gemm(TrivJobs jobs, int m0, int Rt
     const int job = blockIdx.z / splits, split = blockIdx.z % splits;
     const TrivJob& J = jobs.j[job];
     const int r0 = blockIdx.x * kGBM, e0 = blockIdx.y * kGBN;
-    // union of the supports (products vanish outside every pair's overlap)
-    long long klo = J.G, khi = 0;
-    for (int m = 0; m < m0; ++m) {
-        klo = min(klo, static_cast<long long>(J.lo[m]));
-        khi = max(khi, static_cast<long long>(J.hi[m]));
+    // union of the supports (products vanish outside every pair's overlap): one parallel
+    // load per function and a warp reduction instead of a serial chain of m0 loads
+    __shared__ long long sk[2];
+    if (threadIdx.x < 32) {
+        long long lo = J.G, hi = 0;
+        for (int m = threadIdx.x; m < m0; m += 32) {
+            lo = min(lo, static_cast<long long>(J.lo[m]));
+            hi = max(hi, static_cast<long long>(J.hi[m]));
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if (threadIdx.x == 0) {
+            sk[0] = lo;
+            sk[1] = hi;
+        }
     }
-    khi = min(khi, static_cast<long long>(J.rows));
+    __syncthreads();
+    const long long klo = sk[0];
+    const long long khi = min(sk[1], static_cast<long long>(J.rows));
     const long long len = khi > klo ? khi - klo : 0;
     const long long per = ((len + splits - 1) / splits + kGBK - 1) / kGBK * kGBK;
     const long long k0 = klo + split * per, k1 = min(khi, k0 + per);

@@ -133,14 +133,25 @@ public:
     void collect();
     void reset();
     std::map<std::string, std::pair<double, int64_t>> totals;  // name -> (ms, launches)
+    // per-launch timeline relative to the last mark_ref() (stage-timing mode only)
+    struct Span {
+        std::string name;
+        cudaStream_t stream;
+        double t0, t1;
+    };
+    std::vector<Span> timeline;
+    void mark_ref(cudaStream_t st);
 
 private:
     cudaEvent_t get();
     std::vector<cudaEvent_t> pool_;
     size_t used_ = 0;
+    cudaEvent_t ref_ = nullptr;
     struct Pending {
         std::string name;
         cudaEvent_t a, b;
+        cudaStream_t st;
+        cudaEvent_t ref;
     };
     std::vector<Pending> pending_;
     std::string open_name_;
