@@ -1065,14 +1065,38 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
     auto enqueue = [&]() {
         run_assembly(c, sd, p, NEED_MS | NEED_NUC, 0, out, nullptr, s0d);
         if (periodic) {
-            const double* blocks[2] = {out.out0, out.out1};
-            double2* bd[2];
-            launch_dft(c, dp, 2, blocks, bd);
-            double2* Hb = bd[0];
-            double2* Sb = bd[1];
-            if (k_begin < k_end)
-                launch_pencil(c->L(), k_end - k_begin, p.m0, Hb + k_begin * mm, Sb + k_begin * mm,
-                              eig_dev + k_begin * p.m0, fk, true);
+            int wrapped = 0, ax = -1;
+            for (int l = 0; l < 3; ++l)
+                if (dp.dims[l] > 1) {
+                    ++wrapped;
+                    ax = l;
+                }
+            // single wrapped axis and a small transform (K nc m0^2 terms): the lattice DFT is
+            // fused into the pencil load stage (one launch less); larger ones keep the
+            // separate DFT kernel, whose parallelism beats per-pencil sums
+            if (wrapped == 1 && dp.ncomp[ax] <= kPencilDftMax &&
+                (k_end - k_begin) * dp.ncomp[ax] * mm <= (Index(1) << 20)) {
+                PencilDft f;
+                f.nc = static_cast<int>(dp.ncomp[ax]);
+                f.L = dp.dims[ax];
+                f.k0 = k_begin;
+                f.comp = dp.comp[ax];
+                f.blk = dp.slot2blk;
+                f.GH = out.out0;
+                f.GS = out.out1;
+                if (k_begin < k_end)
+                    launch_pencil(c->L(), k_end - k_begin, p.m0, nullptr, nullptr, eig_dev + k_begin * p.m0, fk, true,
+                                  f);
+            } else {
+                const double* blocks[2] = {out.out0, out.out1};
+                double2* bd[2];
+                launch_dft(c, dp, 2, blocks, bd);
+                double2* Hb = bd[0];
+                double2* Sb = bd[1];
+                if (k_begin < k_end)
+                    launch_pencil(c->L(), k_end - k_begin, p.m0, Hb + k_begin * mm, Sb + k_begin * mm,
+                                  eig_dev + k_begin * p.m0, fk, true);
+            }
         } else if (small_box) {
             box_eig_device(c, p.Nb, out.out0, out.out1, eig_dev, fk);
         }

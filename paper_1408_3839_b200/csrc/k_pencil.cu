@@ -58,6 +58,7 @@ __device__ __forceinline__ void gsync(int slot) {
 
 template <int NM>
 struct PSmem {
+    static_assert(kPencilDftMax > 0, "");
     double2 A[NM][NM + 1];
     double2 B[NM][NM + 1];
     double2 C[NM][NM + 1];
@@ -66,6 +67,7 @@ struct PSmem {
     double ix[NM], invd[NM];  // 1 / pivot, 1 / sqrt(pivot)
     double red[4][32];
     double scal[4];
+    double2 tw[kPencilDftMax];  // fused DFT: twiddles of this k-point
 };
 
 // group reduction of NV values at once (one pair of barriers for all of them)
@@ -142,7 +144,7 @@ __device__ __forceinline__ void sturm_counts(const double* d, const double* e2, 
 template <int NM, int G, int BS>
 __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double2* __restrict__ Hb,
                                                 const double2* __restrict__ Sb, double* __restrict__ eig,
-                                                unsigned long long* fail_key, int periodic_checks) {
+                                                unsigned long long* fail_key, int periodic_checks, PencilDft dft) {
     constexpr int PPC = BS / G;                 // pencils per CTA
     constexpr int EPT = (NM * NM + G - 1) / G;  // matrix entries per thread
     constexpr int TPR = G / NM;                 // mat-vec threads per row
@@ -160,14 +162,39 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
     auto& C = sm.C;
     const int n = m0;
     const int mm = m0 * m0;
+    if (dft.nc > 0) {
+        // fused lattice DFT (single wrapped axis): F[k] = sum_c w^(k comp[c] mod L) G[blk[c]],
+        // c ascending, the sum of k_dft_axis2's first axis
+        const Index j = dft.k0 + k;
+        for (int c = t; c < dft.nc; c += G) {
+            const Index mres = (j * dft.comp[c]) % dft.L;
+            double sn, co;
+            sincospi(-2.0 * static_cast<double>(mres) / static_cast<double>(dft.L), &sn, &co);
+            sm.tw[c] = make_double2(co, sn);
+        }
+        gsync<G>(slot);
+    }
 #pragma unroll
     for (int u = 0; u < EPT; ++u) {
         const int e = t + G * u;
         if (e < NM * NM) {
             const int r = e % NM, c = e / NM;
             if (r < m0 && c < m0) {
-                A[r][c] = Hb[k * mm + r + c * m0];
-                B[r][c] = Sb[k * mm + r + c * m0];
+                if (dft.nc > 0) {
+                    double2 ah = make_double2(0.0, 0.0), as = make_double2(0.0, 0.0);
+                    for (int q = 0; q < dft.nc; ++q) {
+                        const Index b = dft.blk[q];
+                        const double vh = b >= 0 ? dft.GH[b * mm + r + c * m0] : 0.0;
+                        const double vs = b >= 0 ? dft.GS[b * mm + r + c * m0] : 0.0;
+                        ah = cadd(ah, cmul(sm.tw[q], make_double2(vh, 0.0)));
+                        as = cadd(as, cmul(sm.tw[q], make_double2(vs, 0.0)));
+                    }
+                    A[r][c] = ah;
+                    B[r][c] = as;
+                } else {
+                    A[r][c] = Hb[k * mm + r + c * m0];
+                    B[r][c] = Sb[k * mm + r + c * m0];
+                }
             } else {
                 A[r][c] = make_double2(0.0, 0.0);
                 B[r][c] = make_double2(r == c ? 1.0 : 0.0, 0.0);
@@ -446,7 +473,7 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
 
 template <int NM, int G, int BS>
 static void run_pencil(const Launch& L, Index count, Index m0, const double2* H, const double2* S, double* eig,
-                       unsigned long long* fail_key, bool checks) {
+                       unsigned long long* fail_key, bool checks, const PencilDft& dft) {
     static_assert(BS % G == 0 && (G <= 32 || G % 32 == 0), "group layout");
     constexpr int PPC = BS / G;
     const size_t smem = sizeof(PSmem<NM>) * PPC;
@@ -459,7 +486,7 @@ static void run_pencil(const Launch& L, Index count, Index m0, const double2* H,
     const Index blocks = (count + PPC - 1) / PPC;
     Stage st_(L, "pencil");
     k_pencil<NM, G, BS><<<static_cast<unsigned>(blocks), BS, smem, L.st>>>(count, static_cast<int>(m0), H, S, eig,
-                                                                            fail_key, checks ? 1 : 0);
+                                                                            fail_key, checks ? 1 : 0, dft);
     LT_CU(cudaGetLastError());
     L.tick();
 }
@@ -469,15 +496,16 @@ static void run_pencil(const Launch& L, Index count, Index m0, const double2* H,
 // eigenvalue instead of 4); for larger blocks the extra threads lengthen every barrier of
 // the Cholesky/Householder chains more than they shorten the bisection.
 void launch_pencil(const Launch& L, Index count, Index m0, const double2* H, const double2* S, double* eig,
-                   unsigned long long* fail_key, bool periodic_checks) {
+                   unsigned long long* fail_key, bool periodic_checks, const PencilDft& dft) {
     if (count <= 0) return;
+    if (dft.nc > kPencilDftMax) fail(LT_EGENERIC, "pencil_eig: fused DFT supports at most 64 stored offsets");
     if (m0 <= 8) {
-        if (count <= 1184) run_pencil<8, 128, 256>(L, count, m0, H, S, eig, fail_key, periodic_checks);
-        else run_pencil<8, 32, 256>(L, count, m0, H, S, eig, fail_key, periodic_checks);
+        if (count <= 1184) run_pencil<8, 128, 256>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft);
+        else run_pencil<8, 32, 256>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft);
     } else if (m0 <= 16) {
-        run_pencil<16, 64, 256>(L, count, m0, H, S, eig, fail_key, periodic_checks);
+        run_pencil<16, 64, 256>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft);
     } else if (m0 <= 32) {
-        run_pencil<32, 256, 256>(L, count, m0, H, S, eig, fail_key, periodic_checks);
+        run_pencil<32, 256, 256>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft);
     } else {
         fail(LT_EDIM, "pencil_eig: block size m0 > 32 is not supported by the batched solver");
     }

@@ -343,8 +343,19 @@ struct DftAxisArgs {
 void launch_dft_axis2(const Launch& L, const DftAxisArgs& a, int nops);
 
 // batched Hermitian-definite pencils (eigensolver.cpp:72-93)
+// fused lattice DFT in the pencil load stage (single wrapped axis): generating blocks
+// GH/GS [nblocks][m0^2] (real), stored offsets comp[c] (ascending kidx) -> block blk[c]
+constexpr int kPencilDftMax = 64;
+struct PencilDft {
+    int nc = 0;  // 0: H, S are the Fourier blocks already
+    Index L = 1, k0 = 0;
+    const int64_t* comp = nullptr;
+    const int* blk = nullptr;
+    const double* GH = nullptr;
+    const double* GS = nullptr;
+};
 void launch_pencil(const Launch& L, Index count, Index m0, const double2* H, const double2* S, double* eig,
-                   unsigned long long* fail_key, bool periodic_checks);
+                   unsigned long long* fail_key, bool periodic_checks, const PencilDft& dft = PencilDft{});
 
 // combine (eigensolver.cpp:37-67) on device buffers with index maps
 void launch_axpby_map(const Launch& L, Index nout, Index mm, double wa, const double* a, const int64_t* ia, double wb,
