@@ -2,7 +2,7 @@
  *
  * The reference (arXiv 1408.3839 C++ reference, "latham") has no plugin or FFI
  * layer: its boundary is the free-function C++ API under
- * proj/core/include/latham/*.hpp. Each entry point below replaces one of those
+ * proj/core/include/latham/ headers. Each entry point below replaces one of those
  * functions (cited file:line); include/latham_b200.hpp wraps them back into the
  * reference's C++ call shapes. Plain pointers and sizes only; no exceptions cross
  * the ABI; every function returns an lt_status whose message is lt_last_error().

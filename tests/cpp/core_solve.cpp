@@ -1,0 +1,71 @@
+// A reference-style client of the C++ mirror (include/latham_b200.hpp): the calls
+// tools/commands.cpp makes for `latham solve` (assemble Laplace / Nuclear / Mass,
+// H = combine(0.5, Lap, -1, Nuc), S = Mass, then the spectrum), plus the fused
+// whole-path entry and the reference's error classes. Prints one line per result:
+//   <tag> <count> <v1> <v2> ...   (%.17g)
+#include <cstdio>
+#include <string>
+
+#include "latham_b200.hpp"
+
+using namespace latham_b200;
+
+static LatticeSystem chain(Index Lx, bool two_nuclei) {
+    LatticeSystem s;
+    s.b = 2.0;
+    s.L = {Lx, 1, 1};
+    s.set_grid(32, 32);
+    s.quad_M = 8;
+    s.nuclei.cell_size = s.b;
+    if (two_nuclei) {
+        s.nuclei.nuclei.push_back({{-0.5, 0.0, 0.0}, 1.0});
+        s.nuclei.nuclei.push_back({{0.5, 0.0, 0.0}, 1.0});
+    } else {
+        s.nuclei.nuclei.push_back({{0.0, 0.0, 0.0}, 1.0});
+    }
+    for (const auto& nu : s.nuclei.nuclei) {
+        s.basis.functions.push_back({nu.position, 1.3, {0, 0, 0}});
+        s.basis.functions.push_back({nu.position, 3.1, {0, 0, 0}});
+    }
+    return s;
+}
+
+static void print(const std::string& tag, const std::vector<double>& v) {
+    std::printf("%s %zu", tag.c_str(), v.size());
+    for (double x : v) std::printf(" %.17g", x);
+    std::printf("\n");
+}
+
+int main() {
+    Context ctx(0);
+    // periodic: reference-shaped calls
+    const LatticeSystem per = chain(16, true);
+    auto lap = assemble_periodic(ctx, per, OperatorKind::Laplace);
+    auto nuc = assemble_periodic(ctx, per, OperatorKind::Nuclear);
+    auto S = assemble_periodic(ctx, per, OperatorKind::Mass);
+    auto H = combine(ctx, 0.5, lap, -1.0, nuc);
+    print("periodic_ops", solve_periodic(ctx, H, S).sorted_all());
+    print("periodic_core", solve_core_periodic(ctx, per).sorted_all());
+    // box
+    const LatticeSystem box = chain(6, false);
+    auto blap = assemble_box(ctx, box, OperatorKind::Laplace);
+    auto bnuc = assemble_box(ctx, box, OperatorKind::Nuclear);
+    auto bS = assemble_box(ctx, box, OperatorKind::Mass);
+    auto bH = combine(ctx, 0.5, blap, -1.0, bnuc);
+    print("box_ops", solve_box_dense(ctx, bH.dense(), bS.dense(), bH.basis_count()).eigenvalues);
+    print("box_core", solve_core_box(ctx, box).eigenvalues);
+    // errors: alias guard (galerkin.cpp:294-302) and the dense cap (eigensolver.cpp:17-19)
+    try {
+        assemble_periodic(ctx, chain(3, true), OperatorKind::Mass);
+        std::printf("error_alias none\n");
+    } catch (const StructureError& e) {
+        std::printf("error_alias StructureError %s\n", e.what());
+    }
+    try {
+        solve_box_dense(ctx, bH.dense(), bS.dense(), bH.basis_count(), 4);
+        std::printf("error_cap none\n");
+    } catch (const ResourceCapError& e) {
+        std::printf("error_cap ResourceCapError %s\n", e.what());
+    }
+    return 0;
+}
