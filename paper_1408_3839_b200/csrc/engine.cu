@@ -58,6 +58,12 @@ StageTimer::~StageTimer() {
 }
 
 cudaEvent_t StageTimer::get() {
+    if (owned) {
+        cudaEvent_t e;
+        LT_CU(cudaEventCreate(&e));
+        owned->push_back(e);
+        return e;
+    }
     if (used_ == pool_.size()) {
         cudaEvent_t e;
         LT_CU(cudaEventCreate(&e));
@@ -66,15 +72,22 @@ cudaEvent_t StageTimer::get() {
     return pool_[used_++];
 }
 
+// while capturing, timing events must be external event-record nodes (a plain record
+// inside a capture only expresses a dependency and cannot be timed afterwards)
+static void record_timing_event(cudaEvent_t e, cudaStream_t st, bool capturing) {
+    if (capturing) LT_CU(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
+    else LT_CU(cudaEventRecord(e, st));
+}
+
 void StageTimer::begin(cudaStream_t st, const char* name) {
     open_ = get();
     open_name_ = name;
-    LT_CU(cudaEventRecord(open_, st));
+    record_timing_event(open_, st, owned != nullptr);
 }
 
 void StageTimer::end(cudaStream_t st) {
     cudaEvent_t b = get();
-    LT_CU(cudaEventRecord(b, st));
+    record_timing_event(b, st, owned != nullptr);
     pending_.push_back({open_name_, open_, b, st, ref_});
 }
 
@@ -117,8 +130,17 @@ struct GraphCache {
     cudaGraphExec_t exec = nullptr;
     std::vector<int64_t> key, seen;
     int64_t launches = 0;
+    // stage-timing events captured as graph nodes (timed graphs only)
+    std::vector<cudaEvent_t> events;
+    std::vector<StageTimer::Pending> timing;
+    void drop_events() {
+        for (cudaEvent_t e : events) cudaEventDestroy(e);
+        events.clear();
+        timing.clear();
+    }
     ~GraphCache() {
         if (exec) cudaGraphExecDestroy(exec);
+        drop_events();
     }
 };
 
@@ -235,37 +257,50 @@ namespace lt {
 // eagerly so the arena is sized and no allocation happens inside a capture).
 template <class K, class F>
 static void run_cached(lt_ctx* c, GraphCache& g, K&& keyfn, F&& enqueue) {
-    const bool allow = c->graphs && !c->timer.on;
-    const std::vector<int64_t> key = keyfn();
+    // stage timing is captured too (event nodes inside the graph), keyed separately, so the
+    // per-stage times come from the same graph execution as the untimed solve
+    const bool allow = c->graphs;
+    std::vector<int64_t> key = keyfn();
+    key.push_back(c->timer.on ? 1 : 0);
     if (allow && g.exec && key == g.key) {
         LT_CU(cudaGraphLaunch(g.exec, c->stream));
         c->launches += g.launches;
+        if (c->timer.on) c->timer.add_pending(g.timing);
         return;
     }
     if (allow && key == g.seen) {
         const int64_t l0 = c->launches;
         cudaGraph_t graph = nullptr;
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        g.exec = nullptr;
+        g.drop_events();
+        const size_t p0 = c->timer.pending_size();
+        c->timer.owned = &g.events;
         LT_CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         try {
             enqueue();
         } catch (...) {
+            c->timer.owned = nullptr;
             cudaStreamEndCapture(c->stream, &graph);
             if (graph) cudaGraphDestroy(graph);
+            c->timer.take_pending(p0);
             throw;
         }
+        c->timer.owned = nullptr;
         LT_CU(cudaStreamEndCapture(c->stream, &graph));
-        if (g.exec) cudaGraphExecDestroy(g.exec);
-        g.exec = nullptr;
+        g.timing = c->timer.take_pending(p0);
         const cudaError_t e = cudaGraphInstantiate(&g.exec, graph, 0);
         cudaGraphDestroy(graph);
         LT_CU(e);
         g.key = key;
         g.launches = c->launches - l0;
         LT_CU(cudaGraphLaunch(g.exec, c->stream));
+        if (c->timer.on) c->timer.add_pending(g.timing);
         return;
     }
     enqueue();
-    g.seen = keyfn();
+    g.seen = keyfn();  // after the eager run: it may have grown the arena (new generation)
+    g.seen.push_back(c->timer.on ? 1 : 0);
 }
 }  // namespace lt
 
@@ -492,7 +527,10 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
     //   aux[0] : profiles -> FEM tables (profiles join main before the nuclear part, the
     //            tables before the fill)
     const Launch L = c->L();
-    const Launch LF = c->LA(0), LP = c->LA(1);
+    // stage-timing mode runs the branches back to back on the main stream, so each stage's
+    // events bracket that kernel alone (concurrent branches would share SMs)
+    const bool serial = c->timer.on;
+    const Launch LF = serial ? L : c->LA(0), LP = serial ? L : c->LA(1);
     const Index m0 = p.m0, mm = m0 * m0, RN = p.RN, Rtot = p.Rtot;
     Arena& A = c->arena;
     int src[3];

@@ -141,18 +141,33 @@ public:
     };
     std::vector<Span> timeline;
     void mark_ref(cudaStream_t st);
-
-private:
-    cudaEvent_t get();
-    std::vector<cudaEvent_t> pool_;
-    size_t used_ = 0;
-    cudaEvent_t ref_ = nullptr;
+    // graph capture with timing on: events come from `owned` (kept alive by the graph) and
+    // the begin/end pairs of the captured launches are replayed into pending_ per launch
     struct Pending {
         std::string name;
         cudaEvent_t a, b;
         cudaStream_t st;
         cudaEvent_t ref;
     };
+    std::vector<cudaEvent_t>* owned = nullptr;
+    size_t pending_size() const { return pending_.size(); }
+    std::vector<Pending> take_pending(size_t from) {
+        std::vector<Pending> out(pending_.begin() + static_cast<std::ptrdiff_t>(from), pending_.end());
+        pending_.resize(from);
+        return out;
+    }
+    void add_pending(const std::vector<Pending>& v) {
+        for (Pending p : v) {
+            p.ref = ref_;
+            pending_.push_back(p);
+        }
+    }
+
+private:
+    cudaEvent_t get();
+    std::vector<cudaEvent_t> pool_;
+    size_t used_ = 0;
+    cudaEvent_t ref_ = nullptr;
     std::vector<Pending> pending_;
     std::string open_name_;
     cudaEvent_t open_ = nullptr;
