@@ -124,6 +124,27 @@ lt_status lt_solve_box_dense(lt_ctx* ctx, int64_t n, const double* H, const doub
 /* batch of Hermitian-definite pencils (eigensolver.cpp:72-93); complex interleaved col-major */
 lt_status lt_pencil_eig(lt_ctx* ctx, int64_t count, int64_t m0, const double* Hc, const double* Sc, double* eig);
 
+/* ---- separable metadata and the factorized Fourier path -------------------------- *
+ * Periodic operators carry their rank metadata (galerkin.cpp:394-423; combine scales level 0
+ * and concatenates, eigensolver.cpp:57-64). Layout of a term list: [t][level l][L_l][m0*m0]
+ * (SeparableTerm::level_blocks, factorized_diag.hpp). */
+int64_t lt_op_separable_count(const lt_operator* op); /* doubles lt_op_separable writes; 0: none */
+lt_status lt_op_separable(const lt_operator* op, double* out);
+/* separable_residual (galerkin.hpp): max |gen_k - expanded_k| over the lattice */
+lt_status lt_separable_residual(lt_ctx* ctx, const lt_operator* op, double* resid);
+/* solve_periodic_factorized (eigensolver.hpp): metadata residual above metadata_tol is a
+ * StructureError; then 1D DFTs per level and per-k Hadamard sums, batched pencils */
+lt_status lt_solve_periodic_factorized(lt_ctx* ctx, const lt_operator* H, const lt_operator* S, double metadata_tol,
+                                       double* eig);
+/* the same from host generating tensors and host term lists (tH / tS terms each) */
+lt_status lt_solve_periodic_factorized_gen(lt_ctx* ctx, const int64_t* dims, int64_t m0, int64_t nH, const int64_t* kH,
+                                           const double* bH, int64_t tH, const double* termsH, int64_t nS,
+                                           const int64_t* kS, const double* bS, int64_t tS, const double* termsS,
+                                           double metadata_tol, double* eig);
+/* factorized_block_diagonalize (factorized_diag.hpp): out = K blocks, complex interleaved */
+lt_status lt_factorized_block_diagonalize(lt_ctx* ctx, int levels, const int64_t* dims, int64_t m0, int64_t nterms,
+                                          const double* terms, double* out);
+
 /* ---- stage entry points for unit parity tests ---------------------------------- */
 lt_status lt_sinc_quadrature(lt_ctx* ctx, int64_t M, double* nodes, double* weights); /* sinc_quadrature.cpp:9-29 */
 lt_status lt_overlap_constant(lt_ctx* ctx, const lt_system* sys, int64_t* L0);         /* gto_basis.cpp:87-126 */

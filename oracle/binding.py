@@ -174,6 +174,24 @@ class Oracle:
         S = self.assemble(sys, periodic, "mass")
         return H, S
 
+    def separable_terms(self, op: Operator):
+        """Rank metadata (galerkin.cpp:394-423): list over terms of [level 0, 1, 2]
+        (L_l, m0, m0) [row, col] block sequences."""
+        L, m0 = op.L, op.m0
+        per = (L[0] + L[1] + L[2]) * m0 * m0
+        out = np.zeros(max(1, op.coefficient_rank * per))
+        self._sep(op._handle, _dptr(out))
+        terms = []
+        for t in range(op.coefficient_rank):
+            at = t * per
+            term = []
+            for l in range(3):
+                n = L[l] * m0 * m0
+                term.append(out[at:at + n].reshape(L[l], m0, m0).transpose(0, 2, 1).copy())
+                at += n
+            terms.append(term)
+        return terms
+
     def free(self, op: Operator):
         if op._handle is not None:
             self._free(op._handle)

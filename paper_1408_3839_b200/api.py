@@ -82,6 +82,14 @@ class Operator:
         k, b = self.blocks()
         return {tuple(int(x) for x in kk): b[i] for i, kk in enumerate(k)}
 
+    def separable(self):
+        """Rank metadata (galerkin.hpp:52): list over terms of [level 0, 1, 2] sequences,
+        each an (L_l, m0, m0) array of [row, col] blocks (SeparableTerm::level_blocks)."""
+        n = int(native.lib().lt_op_separable_count(self.handle))
+        out = np.zeros(max(n, 1))
+        check(native.lib().lt_op_separable(self.handle, _d(out)))
+        return unpack_terms(out[:n], self.L, self.m0)
+
     def __del__(self):
         if getattr(self, "handle", None):
             try:
@@ -89,6 +97,30 @@ class Operator:
             except Exception:
                 pass
             self.handle = None
+
+
+def pack_terms(terms, L, m0) -> np.ndarray:
+    """[t][level][L_l][m0*m0] column-major blocks (the C-ABI term-list layout)."""
+    parts = []
+    for term in terms:
+        for l in range(3):
+            seq = np.asarray(term[l], dtype=np.float64).reshape(L[l], m0, m0)
+            parts.append(np.ascontiguousarray(seq.transpose(0, 2, 1)).reshape(-1))
+    return np.ascontiguousarray(np.concatenate(parts)) if parts else np.zeros(1)
+
+
+def unpack_terms(flat: np.ndarray, L, m0):
+    per = (L[0] + L[1] + L[2]) * m0 * m0
+    out = []
+    for t in range(flat.size // per if per else 0):
+        at = t * per
+        term = []
+        for l in range(3):
+            n = L[l] * m0 * m0
+            term.append(flat[at:at + n].reshape(L[l], m0, m0).transpose(0, 2, 1).copy())
+            at += n
+        out.append(term)
+    return out
 
 
 class Context:
@@ -212,6 +244,49 @@ class Context:
         K = int(np.prod(d))
         out = np.zeros(K * m0)
         check(self.lib.lt_solve_periodic(self.h, _i(d), m0, nH, _i(kH), _d(bH), nS, _i(kS), _d(bS), _d(out)))
+        return out.reshape(K, m0)
+
+    # ---- separable metadata / factorized path --------------------------------
+    def separable_residual(self, op: Operator) -> float:
+        r = ctypes.c_double()
+        check(self.lib.lt_separable_residual(self.h, op.handle, ctypes.byref(r)))
+        return r.value
+
+    def solve_periodic_factorized(self, H: Operator, S: Operator, metadata_tol: float = 1e-10) -> np.ndarray:
+        """solve_periodic_factorized (eigensolver.hpp): [K, m0] eigenvalues."""
+        K = H.L[0] * H.L[1] * H.L[2]
+        out = np.zeros(K * H.m0)
+        check(self.lib.lt_solve_periodic_factorized(self.h, H.handle, S.handle, metadata_tol, _d(out)))
+        return out.reshape(K, H.m0)
+
+    def factorized_block_diagonalize(self, levels: int, dims, m0: int, terms) -> np.ndarray:
+        """factorized_block_diagonalize (factorized_diag.hpp): (K, m0, m0) complex blocks."""
+        d = np.array(dims, dtype=np.int64)
+        K = int(np.prod(d))
+        flat = pack_terms(terms, dims, m0)
+        out = np.zeros(K * m0 * m0 * 2)
+        check(self.lib.lt_factorized_block_diagonalize(self.h, levels, _i(d), m0, len(terms), _d(flat), _d(out)))
+        z = out[0::2] + 1j * out[1::2]
+        return z.reshape(K, m0, m0).transpose(0, 2, 1).copy()
+
+    def solve_periodic_factorized_gen(self, dims, m0: int, Hgen: dict, Sgen: dict, Hterms, Sterms,
+                                      metadata_tol: float = 1e-10) -> np.ndarray:
+        def pack(g):
+            keys = sorted(g)
+            k = np.ascontiguousarray(np.array(keys, dtype=np.int64).reshape(-1, 3))
+            b = np.ascontiguousarray(np.concatenate([np.asarray(g[kk], dtype=np.float64).T.reshape(-1) for kk in keys])
+                                     if keys else np.zeros(1))
+            return len(keys), k, b
+        nH, kH, bH = pack(Hgen)
+        nS, kS, bS = pack(Sgen)
+        d = np.array(dims, dtype=np.int64)
+        K = int(np.prod(d))
+        tH = pack_terms(Hterms, dims, m0)
+        tS = pack_terms(Sterms, dims, m0)
+        out = np.zeros(K * m0)
+        check(self.lib.lt_solve_periodic_factorized_gen(self.h, _i(d), m0, nH, _i(kH), _d(bH), len(Hterms), _d(tH),
+                                                        nS, _i(kS), _d(bS), len(Sterms), _d(tS), metadata_tol,
+                                                        _d(out)))
         return out.reshape(K, m0)
 
     def bc_block_diagonalize(self, dims, m0: int, gen: dict) -> np.ndarray:

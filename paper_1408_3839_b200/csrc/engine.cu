@@ -310,6 +310,22 @@ struct lt_sysdev {
     void* mem = nullptr;
 };
 
+// separable coefficient metadata of a periodic operator (galerkin.hpp:52 `separable`),
+// band-compressed: level l keeps slots s with lattice index kid[l][s]; vals[t][l][s][mm]
+struct SepMeta {
+    Index terms = 0, m0 = 0, S = 1;
+    Index L[3]{1, 1, 1};
+    std::vector<Index> kid[3];
+    double* vals = nullptr;
+    SepMeta() = default;
+    SepMeta(const SepMeta&) = delete;
+    SepMeta& operator=(const SepMeta&) = delete;
+    ~SepMeta() {
+        if (vals) cudaFree(vals);
+    }
+    size_t count() const { return static_cast<size_t>(terms * 3 * S * m0 * m0); }
+};
+
 struct lt_operator {
     int which = 0;  // 0 Laplace 1 Mass 2 Nuclear; core H uses 0 (Laplace first operand)
     bool periodic = false;
@@ -320,6 +336,7 @@ struct lt_operator {
     std::vector<std::array<Index, 3>> kidx;  // periodic, std::map order
     double* data = nullptr;                  // device: dense Nb*Nb or nblk*m0*m0
     size_t count = 0;
+    std::unique_ptr<SepMeta> sep;            // periodic: rank metadata
     ~lt_operator() {
         if (data) cudaFree(data);
     }
@@ -519,8 +536,12 @@ static int64_t* upload_s0(lt_ctx* c, const Plan& p) {
     return s0d;
 }
 
+// flags: AS_GENERAL_NUC forces the per-direction nuclear tables (w.T, the reference's
+// nucT layout) instead of the fused reassociations; AS_NO_FILL stops after the tables.
+enum AsmFlags : unsigned { AS_GENERAL_NUC = 1u, AS_NO_FILL = 2u };
+
 static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need, int mode, AsmOut out,
-                         Work* wout = nullptr, const int64_t* s0_dev = nullptr) {
+                         Work* wout = nullptr, const int64_t* s0_dev = nullptr, unsigned flags = 0) {
     // Three concurrent branches (parallel branches of the captured graph):
     //   main   : sinc -> potential of the 1st, 3rd distinct direction -> nuclear -> fill
     //   aux[1] : potential of the 2nd distinct direction (joins main before the nuclear part)
@@ -663,7 +684,7 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
         std::vector<int> wrapped;
         for (int l = 0; l < 3; ++l)
             if (p.d[l].L > 1) wrapped.push_back(l);
-        const bool dmma_ok = m0 <= 32;
+        const bool dmma_ok = m0 <= 32 && !(flags & AS_GENERAL_NUC);
         if (dmma_ok && wrapped.size() == 1) nuc_mode = 1;
         else if (dmma_ok && p.periodic && wrapped.size() >= 2) nuc_mode = 2;
         if (nuc_mode != 0) {
@@ -791,6 +812,10 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
         }
     }
     c->join(4, c->aux[0], c->stream);  // FEM tables before the fill
+    if (flags & AS_NO_FILL) {
+        if (wout) *wout = w;
+        return;
+    }
     // fused combine + placement
     FillArgs fa;
     fa.m0 = m0;
@@ -1230,6 +1255,198 @@ extern "C" {
 
 const char* lt_last_error(void) { return lt::g_err.c_str(); }
 
+
+// ---------------------------------------------------------------------------
+// separable metadata and the factorized Fourier path (k_sep.cu)
+// ---------------------------------------------------------------------------
+// metadata of one assembly from its per-direction tables (galerkin.cpp:394-423)
+static std::unique_ptr<SepMeta> build_sep(lt_ctx* c, const Plan& p, int kind, const Work& w) {
+    auto m = std::make_unique<SepMeta>();
+    m->m0 = p.m0;
+    m->terms = kind == LT_MASS ? 1 : (kind == LT_LAPLACE ? 3 : p.Rtot);
+    SepBuild b;
+    b.kind = kind;
+    b.mm = p.m0 * p.m0;
+    b.R = p.Rtot;
+    for (int l = 0; l < 3; ++l) {
+        const DirPlan& d = p.d[l];
+        m->L[l] = d.L;
+        m->S = std::max(m->S, d.width);
+        for (Index sl = 0; sl < d.width; ++sl) {
+            const Index dd = sl - d.band;
+            m->kid[l].push_back(((dd % d.L) + d.L) % d.L);
+        }
+        b.nslot[l] = d.width;
+        b.mass[l] = w.massT[l];
+        b.stiff[l] = w.stiffT[l];
+        b.T[l] = w.T[l];
+    }
+    b.S = m->S;
+    b.potw = w.potw;
+    LT_CU(cudaMalloc(&m->vals, sizeof(double) * std::max<size_t>(1, m->count())));
+    LT_CU(cudaMemsetAsync(m->vals, 0, sizeof(double) * m->count(), c->stream));
+    b.out = m->vals;
+    launch_sep_from_tables(c->L(), b, m->terms);
+    return m;
+}
+
+// scaled concatenation a (level 0 times wa) ++ b (level 0 times wb), slot sets united
+// (combine, eigensolver.cpp:57-64)
+static std::unique_ptr<SepMeta> sep_combine(lt_ctx* c, const SepMeta& a, double wa, const SepMeta& b, double wb) {
+    auto m = std::make_unique<SepMeta>();
+    m->m0 = a.m0;
+    m->terms = a.terms + b.terms;
+    std::vector<Index> mapa[3], mapb[3];
+    for (int l = 0; l < 3; ++l) {
+        m->L[l] = a.L[l];
+        m->kid[l] = a.kid[l];
+        for (size_t q = 0; q < a.kid[l].size(); ++q) mapa[l].push_back(static_cast<Index>(q));
+        for (Index k : b.kid[l]) {
+            auto it = std::find(m->kid[l].begin(), m->kid[l].end(), k);
+            if (it == m->kid[l].end()) {
+                mapb[l].push_back(static_cast<Index>(m->kid[l].size()));
+                m->kid[l].push_back(k);
+            } else {
+                mapb[l].push_back(static_cast<Index>(it - m->kid[l].begin()));
+            }
+        }
+        m->S = std::max<Index>(m->S, static_cast<Index>(m->kid[l].size()));
+    }
+    LT_CU(cudaMalloc(&m->vals, sizeof(double) * std::max<size_t>(1, m->count())));
+    LT_CU(cudaMemsetAsync(m->vals, 0, sizeof(double) * m->count(), c->stream));
+    const Index mm = a.m0 * a.m0;
+    for (int side = 0; side < 2; ++side) {
+        const SepMeta& src = side ? b : a;
+        SepCopy cp;
+        cp.mm = mm;
+        cp.Ssrc = src.S;
+        cp.Sdst = m->S;
+        cp.t0 = side ? a.terms : 0;
+        cp.w = side ? wb : wa;
+        cp.src = src.vals;
+        cp.dst = m->vals;
+        for (int l = 0; l < 3; ++l) {
+            const auto& mp = side ? mapb[l] : mapa[l];
+            Index* d = c->arena.get<Index>("sep.map" + std::to_string(side) + std::to_string(l), mp.size() + 1);
+            upload(c, d, mp.data(), mp.size() * sizeof(Index));
+            cp.map[l] = d;
+            cp.nslot[l] = static_cast<Index>(mp.size());
+        }
+        if (src.terms > 0) launch_sep_scale_copy(c->L(), cp, src.terms);
+    }
+    return m;
+}
+
+// metadata given as full level sequences [t][l][L_l][m0*m0] (reference SeparableTerm)
+static std::unique_ptr<SepMeta> sep_from_full(lt_ctx* c, Index m0, const Index L[3], Index terms, const double* full) {
+    auto m = std::make_unique<SepMeta>();
+    m->m0 = m0;
+    m->terms = terms;
+    const Index mm = m0 * m0;
+    for (int l = 0; l < 3; ++l) {
+        m->L[l] = L[l];
+        for (Index k = 0; k < L[l]; ++k) m->kid[l].push_back(k);
+        m->S = std::max(m->S, L[l]);
+    }
+    std::vector<double> host(m->count(), 0.0);
+    const Index per_term = (L[0] + L[1] + L[2]) * mm;
+    for (Index t = 0; t < terms; ++t) {
+        Index off = t * per_term;
+        for (int l = 0; l < 3; ++l)
+            for (Index k = 0; k < L[l]; ++k, off += mm)
+                std::memcpy(&host[static_cast<size_t>(((t * 3 + l) * m->S + k) * mm)], full + off, sizeof(double) * mm);
+    }
+    LT_CU(cudaMalloc(&m->vals, sizeof(double) * std::max<size_t>(1, m->count())));
+    LT_CU(cudaMemcpy(m->vals, host.data(), sizeof(double) * host.size(), cudaMemcpyHostToDevice));
+    return m;
+}
+
+// max over every lattice point of |gen_k - expanded_k| (separable_residual)
+static double sep_residual(lt_ctx* c, const SepMeta& m, const std::vector<std::array<Index, 3>>& kidx,
+                           const double* gen_dev, const std::string& tag) {
+    SepResid r;
+    r.mm = m.m0 * m.m0;
+    r.terms = m.terms;
+    r.S = m.S;
+    for (int l = 0; l < 3; ++l) {
+        r.L[l] = m.L[l];
+        std::vector<int> so(static_cast<size_t>(m.L[l]), -1);
+        for (size_t q = 0; q < m.kid[l].size(); ++q) so[static_cast<size_t>(m.kid[l][q])] = static_cast<int>(q);
+        int* d = c->arena.get<int>("sep.slot" + tag + std::to_string(l), so.size());
+        upload(c, d, so.data(), so.size() * sizeof(int));
+        r.slot_of[l] = d;
+    }
+    const Index K = m.L[0] * m.L[1] * m.L[2];
+    std::vector<int> go(static_cast<size_t>(K), -1);
+    for (size_t b = 0; b < kidx.size(); ++b)
+        go[static_cast<size_t>((kidx[b][0] * m.L[1] + kidx[b][1]) * m.L[2] + kidx[b][2])] = static_cast<int>(b);
+    int* gd = c->arena.get<int>("sep.gen" + tag, go.size());
+    upload(c, gd, go.data(), go.size() * sizeof(int));
+    r.gen_of = gd;
+    r.vals = m.vals;
+    r.gen = gen_dev;
+    r.out = c->arena.get<unsigned long long>("sep.resid" + tag, 1);
+    LT_CU(cudaMemsetAsync(r.out, 0, sizeof(unsigned long long), c->stream));
+    launch_sep_residual(c->L(), r);
+    unsigned long long bits = 0;
+    LT_CU(cudaMemcpyAsync(&bits, r.out, sizeof(bits), cudaMemcpyDeviceToHost, c->stream));
+    LT_CU(cudaStreamSynchronize(c->stream));
+    double v;
+    std::memcpy(&v, &bits, sizeof(v));
+    return v;
+}
+
+// k-point blocks [K][m0*m0] (complex) by per-level 1D DFTs and per-k Hadamard sums
+static double2* sep_fourier(lt_ctx* c, const SepMeta& m, const std::string& tag) {
+    const Index mm = m.m0 * m.m0;
+    const Index Lmax = std::max(m.L[0], std::max(m.L[1], m.L[2]));
+    SepDft d;
+    d.mm = mm;
+    d.S = m.S;
+    d.Lmax = Lmax;
+    d.vals = m.vals;
+    for (int l = 0; l < 3; ++l) {
+        d.L[l] = m.L[l];
+        d.nslot[l] = static_cast<Index>(m.kid[l].size());
+        Index* k = c->arena.get<Index>("sep.kid" + tag + std::to_string(l), m.kid[l].size() + 1);
+        upload(c, k, m.kid[l].data(), m.kid[l].size() * sizeof(Index));
+        d.kid[l] = k;
+    }
+    d.out = c->arena.get<double2>("sep.X" + tag, static_cast<size_t>(m.terms * 3 * Lmax * mm));
+    launch_sep_dft(c->L(), d, m.terms);
+    SepBlocks b;
+    b.mm = mm;
+    b.terms = m.terms;
+    b.Lmax = Lmax;
+    for (int l = 0; l < 3; ++l) b.L[l] = m.L[l];
+    b.X = d.out;
+    b.out = c->arena.get<double2>("sep.F" + tag, static_cast<size_t>(m.L[0] * m.L[1] * m.L[2] * mm));
+    launch_sep_blocks(c->L(), b);
+    return b.out;
+}
+
+// eigenvalues of the factorized pencils (solve_blocks with the factorized blocks)
+static void sep_solve(lt_ctx* c, const SepMeta& H, const SepMeta& S, double* eig) {
+    const Index K = H.L[0] * H.L[1] * H.L[2];
+    double2* Hb = sep_fourier(c, H, "H");
+    double2* Sb = sep_fourier(c, S, "S");
+    double* e = c->arena.get<double>("solve.eig", K * H.m0);
+    unsigned long long* fk = c->arena.get<unsigned long long>("solve.fail", 1);
+    LT_CU(cudaMemsetAsync(fk, 0xff, sizeof(unsigned long long), c->stream));
+    launch_pencil(c->L(), K, H.m0, Hb, Sb, e, fk, true);
+    unsigned long long key = ~0ull;
+    LT_CU(cudaMemcpyAsync(&key, fk, sizeof(key), cudaMemcpyDeviceToHost, c->stream));
+    LT_CU(cudaMemcpyAsync(eig, e, sizeof(double) * K * H.m0, cudaMemcpyDeviceToHost, c->stream));
+    LT_CU(cudaStreamSynchronize(c->stream));
+    raise_fail_key(key, true);
+}
+
+static void sep_check_resid(double resid, double tol) {
+    if (resid > tol)
+        fail(LT_ESTRUCT, "solve_periodic_factorized: factorization residual " + std::to_string(resid) +
+                             " exceeds tolerance");
+}
+
 lt_status lt_create(int device, lt_ctx** out) {
     return guarded([&] {
         auto c = std::make_unique<lt_ctx>();
@@ -1362,7 +1579,12 @@ lt_status lt_assemble(lt_ctx* c, const lt_system* s, int periodic, lt_kind kind,
         o.out0 = op->data;
         o.kidx = p.periodic ? c->arena.get<int64_t>("op.kidx", p.nblocks * 3) : nullptr;
         const int mode = kind == LT_LAPLACE ? 1 : kind == LT_MASS ? 2 : 3;
-        run_assembly(c, sd.get(), p, nuc ? NEED_NUC : NEED_MS, mode, o);
+        // periodic: the per-direction tables are kept (nuclear in the reference's nucT form)
+        // and become the operator's separable metadata
+        Work w{};
+        run_assembly(c, sd.get(), p, nuc ? NEED_NUC : NEED_MS, mode, o, &w, nullptr,
+                     p.periodic && nuc ? AS_GENERAL_NUC : 0u);
+        if (p.periodic) op->sep = build_sep(c, p, static_cast<int>(kind), w);
         LT_CU(cudaStreamSynchronize(c->stream));
         *out = op.release();
     });
@@ -1382,7 +1604,19 @@ lt_status lt_assemble_core(lt_ctx* c, const lt_system* s, int periodic, lt_opera
         o.out0 = h->data;
         o.out1 = sop->data;
         o.kidx = p.periodic ? c->arena.get<int64_t>("op.kidx", p.nblocks * 3) : nullptr;
-        run_assembly(c, sd.get(), p, NEED_MS | NEED_NUC, 0, o);
+        Work w{};
+        run_assembly(c, sd.get(), p, NEED_MS | NEED_NUC, 0, o, &w);
+        if (p.periodic) {
+            // metadata: assemble_core's H = combine(0.5, Laplace, -1, Nuclear) and S = Mass;
+            // the nuclear part needs the per-direction tables of the general contraction
+            Work wn{};
+            run_assembly(c, sd.get(), p, NEED_NUC, 3, AsmOut{}, &wn, nullptr, AS_GENERAL_NUC | AS_NO_FILL);
+            auto lap = build_sep(c, p, LT_LAPLACE, w);
+            auto nucm = build_sep(c, p, LT_NUCLEAR, wn);
+            h->sep = sep_combine(c, *lap, 0.5, *nucm, -1.0);
+            sop->sep = build_sep(c, p, LT_MASS, w);
+            LT_CU(cudaStreamSynchronize(c->stream));
+        }
         LT_CU(cudaStreamSynchronize(c->stream));
         *H = h.release();
         *S = sop.release();
@@ -1423,6 +1657,7 @@ lt_status lt_combine(lt_ctx* c, double wa, const lt_operator* a, double wb, cons
             upload(c, d, both.data(), both.size() * sizeof(int64_t));
             launch_axpby_map(c->L(), static_cast<Index>(op->kidx.size()), mm, wa, a->data, d, wb, b->data,
                              d + ia.size(), op->data);
+            if (a->sep && b->sep) op->sep = sep_combine(c, *a->sep, wa, *b->sep, wb);
         }
         LT_CU(cudaStreamSynchronize(c->stream));
         *out = op.release();
@@ -1756,3 +1991,102 @@ lt_status lt_profiles(lt_ctx* c, const lt_system* s, int64_t margin, int64_t* gr
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// factorized path entry points (eigensolver.hpp solve_periodic_factorized,
+// factorized_diag.hpp factorized_block_diagonalize, galerkin.hpp separable_residual)
+// ---------------------------------------------------------------------------
+int64_t lt_op_separable_count(const lt_operator* op) {
+    if (!op || !op->sep) return 0;
+    return op->sep->terms * (op->L[0] + op->L[1] + op->L[2]) * op->m0 * op->m0;
+}
+
+lt_status lt_op_separable(const lt_operator* op, double* out) {
+    return guarded([&] {
+        if (!op->periodic) fail(LT_ESTRUCT, "separable_residual: box operators carry no metadata");
+        if (!op->sep) fail(LT_ESTRUCT, "separable_residual: no metadata present");
+        const SepMeta& m = *op->sep;
+        const Index mm = m.m0 * m.m0;
+        std::vector<double> v(m.count());
+        LT_CU(cudaMemcpy(v.data(), m.vals, sizeof(double) * v.size(), cudaMemcpyDeviceToHost));
+        const Index per_term = (m.L[0] + m.L[1] + m.L[2]) * mm;
+        std::fill(out, out + m.terms * per_term, 0.0);
+        for (Index t = 0; t < m.terms; ++t) {
+            Index loff = 0;
+            for (int l = 0; l < 3; ++l) {
+                for (size_t q = 0; q < m.kid[l].size(); ++q)
+                    std::memcpy(out + t * per_term + loff + m.kid[l][q] * mm,
+                                &v[static_cast<size_t>(((t * 3 + l) * m.S + static_cast<Index>(q)) * mm)],
+                                sizeof(double) * mm);
+                loff += m.L[l] * mm;
+            }
+        }
+    });
+}
+
+lt_status lt_separable_residual(lt_ctx* c, const lt_operator* op, double* resid) {
+    return guarded([&] {
+        if (!op->periodic) fail(LT_ESTRUCT, "separable_residual: box operators carry no metadata");
+        if (!op->sep) fail(LT_ESTRUCT, "separable_residual: no metadata present");
+        LT_CU(cudaSetDevice(c->device));
+        *resid = sep_residual(c, *op->sep, op->kidx, op->data, "R");
+    });
+}
+
+lt_status lt_solve_periodic_factorized(lt_ctx* c, const lt_operator* H, const lt_operator* S, double metadata_tol,
+                                       double* eig) {
+    return guarded([&] {
+        if (!H->periodic || !S->periodic)
+            fail(LT_ESTRUCT, "solve_periodic_factorized: operators must be periodic assemblies");
+        if (!H->sep || !S->sep || H->sep->terms == 0 || S->sep->terms == 0)
+            fail(LT_ESTRUCT, "solve_periodic_factorized: rank metadata missing");
+        LT_CU(cudaSetDevice(c->device));
+        sep_check_resid(sep_residual(c, *H->sep, H->kidx, H->data, "H"), metadata_tol);
+        sep_check_resid(sep_residual(c, *S->sep, S->kidx, S->data, "S"), metadata_tol);
+        sep_solve(c, *H->sep, *S->sep, eig);
+    });
+}
+
+static void check_levels(int levels, const int64_t* dims, Index nterms) {
+    if (levels < 1 || levels > 3) fail(LT_ESTRUCT, "FactorizedDiagonalizer: levels must be 1, 2 or 3");
+    if (nterms <= 0) fail(LT_ESTRUCT, "FactorizedDiagonalizer: no separable terms");
+    for (int l = levels; l < 3; ++l)
+        if (dims[l] != 1)
+            fail(LT_ESTRUCT, "FactorizedDiagonalizer: level " + std::to_string(l) + " sequence must have 1 blocks");
+}
+
+lt_status lt_factorized_block_diagonalize(lt_ctx* c, int levels, const int64_t* dims, int64_t m0, int64_t nterms,
+                                          const double* terms, double* out) {
+    return guarded([&] {
+        check_levels(levels, dims, nterms);
+        check_gen_dims(dims, m0);
+        LT_CU(cudaSetDevice(c->device));
+        const Index L[3] = {dims[0], dims[1], dims[2]};
+        auto m = sep_from_full(c, m0, L, nterms, terms);
+        double2* F = sep_fourier(c, *m, "B");
+        const Index K = L[0] * L[1] * L[2];
+        LT_CU(cudaMemcpyAsync(out, F, sizeof(double2) * K * m0 * m0, cudaMemcpyDeviceToHost, c->stream));
+        LT_CU(cudaStreamSynchronize(c->stream));
+    });
+}
+
+lt_status lt_solve_periodic_factorized_gen(lt_ctx* c, const int64_t* dims, int64_t m0, int64_t nH, const int64_t* kH,
+                                           const double* bH, int64_t tH, const double* termsH, int64_t nS,
+                                           const int64_t* kS, const double* bS, int64_t tS, const double* termsS,
+                                           double metadata_tol, double* eig) {
+    return guarded([&] {
+        check_gen_dims(dims, m0);
+        if (tH <= 0 || tS <= 0) fail(LT_ESTRUCT, "solve_periodic_factorized: rank metadata missing");
+        LT_CU(cudaSetDevice(c->device));
+        std::vector<std::array<Index, 3>> keysH, keysS;
+        double *dH = nullptr, *dS = nullptr;
+        gen_to_device(c, nH, kH, bH, m0, keysH, &dH, "H");
+        gen_to_device(c, nS, kS, bS, m0, keysS, &dS, "S");
+        const Index L[3] = {dims[0], dims[1], dims[2]};
+        auto mH = sep_from_full(c, m0, L, tH, termsH);
+        auto mS = sep_from_full(c, m0, L, tS, termsS);
+        sep_check_resid(sep_residual(c, *mH, keysH, dH, "H"), metadata_tol);
+        sep_check_resid(sep_residual(c, *mS, keysS, dS, "S"), metadata_tol);
+        sep_solve(c, *mH, *mS, eig);
+    });
+}

@@ -344,6 +344,54 @@ struct DftPlan {
     Index ncomp[3]{1, 1, 1};   // compressed extents
     std::vector<Index> comp[3];  // compressed kidx values per axis (ascending)
 };
+// separable metadata and the factorized Fourier path (k_sep.cu); vals[t][l][s][e]
+struct SepBuild {
+    int kind = 0;  // 0 Laplace, 1 Mass, 2 Nuclear
+    Index mm = 0, S = 0, R = 0;
+    Index nslot[3]{1, 1, 1};
+    const double* mass[3]{};
+    const double* stiff[3]{};
+    const double* T[3]{};  // nuclear per-pair tables [slot][R][mm]
+    const double* potw = nullptr;
+    double* out = nullptr;
+};
+void launch_sep_from_tables(const Launch& L, const SepBuild& b, Index terms);
+struct SepCopy {
+    Index mm = 0, Ssrc = 0, Sdst = 0, t0 = 0;
+    Index nslot[3]{1, 1, 1};
+    const Index* map[3]{};  // device: source slot -> destination slot
+    double w = 1.0;
+    const double* src = nullptr;
+    double* dst = nullptr;
+};
+void launch_sep_scale_copy(const Launch& L, const SepCopy& c, Index terms);
+struct SepDft {
+    Index mm = 0, S = 0, Lmax = 1;
+    Index L[3]{1, 1, 1};
+    Index nslot[3]{1, 1, 1};
+    const Index* kid[3]{};  // device: lattice index of each slot
+    const double* vals = nullptr;
+    double2* out = nullptr;  // [t][l][Lmax][mm]
+};
+void launch_sep_dft(const Launch& L, const SepDft& d, Index terms);
+struct SepBlocks {
+    Index mm = 0, terms = 0, Lmax = 1;
+    Index L[3]{1, 1, 1};
+    const double2* X = nullptr;
+    double2* out = nullptr;  // [K][mm]
+};
+void launch_sep_blocks(const Launch& L, const SepBlocks& b);
+struct SepResid {
+    Index mm = 0, terms = 0, S = 0;
+    Index L[3]{1, 1, 1};
+    const int* slot_of[3]{};  // device: lattice index -> slot (-1 none)
+    const int* gen_of = nullptr;  // device: lattice index -> stored generating block (-1 none)
+    const double* vals = nullptr;
+    const double* gen = nullptr;
+    unsigned long long* out = nullptr;
+};
+void launch_sep_residual(const Launch& L, const SepResid& r);
+
 // fused per-axis DFT for one or two operators (k_spectrum.cu)
 struct DftAxisArgs {
     int axis = 0;

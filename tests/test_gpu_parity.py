@@ -133,10 +133,14 @@ def test_assemble_core_and_combine(ctx, oracle, name):
     lap = ctx.assemble(sys, periodic, "laplace")
     nuc = ctx.assemble(sys, periodic, "nuclear")
     H2 = ctx.combine(0.5, lap, -1.0, nuc)
+    # periodic Nuclear assembles through the per-direction tables (it carries the rank
+    # metadata), the fused H through the reassociated contraction: equal to rounding
     if periodic:
-        assert np.array_equal(H2.blocks()[1], H.blocks()[1])
+        ok, worst = entries_close(H2.blocks()[1], H.blocks()[1])
     else:
-        assert np.array_equal(H2.dense(), H.dense())
+        ok = np.array_equal(H2.dense(), H.dense())
+        worst = None
+    assert ok, worst
 
 
 @pytest.mark.parametrize("name", IDS)
