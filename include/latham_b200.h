@@ -145,6 +145,10 @@ lt_status lt_solve_periodic_factorized_gen(lt_ctx* ctx, const int64_t* dims, int
 lt_status lt_factorized_block_diagonalize(lt_ctx* ctx, int levels, const int64_t* dims, int64_t m0, int64_t nterms,
                                           const double* terms, double* out);
 
+/* box_circulant_defect (galerkin.hpp:76-83): nuclear box matrix minus the dense expansion of
+ * the periodic circulant; rel_fro = ||defect||_F / ||box||_F; defect (optional) N_b*N_b col-major */
+lt_status lt_box_circulant_defect(lt_ctx* ctx, const lt_system* sys, double* rel_fro, double* defect);
+
 /* ---- stage entry points for unit parity tests ---------------------------------- */
 lt_status lt_sinc_quadrature(lt_ctx* ctx, int64_t M, double* nodes, double* weights); /* sinc_quadrature.cpp:9-29 */
 lt_status lt_overlap_constant(lt_ctx* ctx, const lt_system* sys, int64_t* L0);         /* gto_basis.cpp:87-126 */

@@ -311,6 +311,69 @@ inline DenseSpectrum solve_box_dense(Context& ctx, const std::vector<double>& H,
     return d;
 }
 
+/// eigensolver.hpp solve_periodic_factorized: rank metadata validated against the
+/// generating blocks (StructureError above metadata_tol), 1D DFTs per level, per-k sums.
+inline KPointSpectrum solve_periodic_factorized(Context& ctx, const AssembledOperator& H, const AssembledOperator& S,
+                                                double metadata_tol = 1e-10) {
+    const Index K = H.L[0] * H.L[1] * H.L[2];
+    std::vector<double> flat(static_cast<size_t>(K * H.m0));
+    check(lt_solve_periodic_factorized(ctx.get(), H.handle(), S.handle(), metadata_tol, flat.data()));
+    return make_spectrum(H.L, H.m0, flat, "periodic_factorized");
+}
+
+/// galerkin.hpp separable_residual
+inline double separable_residual(Context& ctx, const AssembledOperator& op) {
+    double r = 0.0;
+    check(lt_separable_residual(ctx.get(), op.handle(), &r));
+    return r;
+}
+
+struct DefectReport {  // galerkin.hpp:76-83
+    std::vector<double> defect;  ///< N_b x N_b column-major
+    double relative_fro = 0.0;
+};
+
+/// galerkin.hpp box_circulant_defect
+inline DefectReport box_circulant_defect(Context& ctx, const LatticeSystem& sys) {
+    SystemView v(sys);
+    DefectReport d;
+    d.defect.resize(static_cast<size_t>(sys.basis_count() * sys.basis_count()));
+    check(lt_box_circulant_defect(ctx.get(), v.get(), &d.relative_fro, d.defect.data()));
+    return d;
+}
+
+struct BandStructure {  // spectrum.hpp
+    Index m0 = 0;
+    std::vector<std::vector<double>> bands;  ///< m0 bands, each of length k_count
+    std::vector<double> band_min, band_max;
+};
+
+/// eigensolver.hpp spectral_bands
+inline BandStructure spectral_bands(const KPointSpectrum& spec) {
+    BandStructure bs;
+    bs.m0 = spec.m0;
+    bs.bands.assign(static_cast<size_t>(spec.m0), std::vector<double>(static_cast<size_t>(spec.k_count())));
+    for (Index m = 0; m < spec.m0; ++m) {
+        for (Index j = 0; j < spec.k_count(); ++j)
+            bs.bands[static_cast<size_t>(m)][static_cast<size_t>(j)] =
+                spec.eigenvalues[static_cast<size_t>(j)][static_cast<size_t>(m)];
+        const auto& b = bs.bands[static_cast<size_t>(m)];
+        bs.band_min.push_back(*std::min_element(b.begin(), b.end()));
+        bs.band_max.push_back(*std::max_element(b.begin(), b.end()));
+    }
+    return bs;
+}
+
+/// eigensolver.hpp average_energy_per_cell
+inline double average_energy_per_cell(const std::vector<double>& sorted_eigenvalues, Index cells, Index n_occ) {
+    const Index take = n_occ * cells;
+    if (take < 0 || take > static_cast<Index>(sorted_eigenvalues.size()))
+        throw DimensionError("average_energy_per_cell: occupation exceeds spectrum size");
+    double s = 0.0;
+    for (Index i = 0; i < take; ++i) s += sorted_eigenvalues[static_cast<size_t>(i)];
+    return s / static_cast<double>(cells);
+}
+
 /// tools/commands.cpp:51-59 + solve_periodic, fused on the device.
 inline KPointSpectrum solve_core_periodic(Context& ctx, const LatticeSystem& sys, int64_t* info = nullptr) {
     SystemView v(sys);

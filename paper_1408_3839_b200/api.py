@@ -246,6 +246,17 @@ class Context:
         check(self.lib.lt_solve_periodic(self.h, _i(d), m0, nH, _i(kH), _d(bH), nS, _i(kS), _d(bS), _d(out)))
         return out.reshape(K, m0)
 
+    def box_circulant_defect(self, sys: LatticeSystem, want_defect: bool = False):
+        """box_circulant_defect (galerkin.cpp:445-454): relative Frobenius norm of the box
+        nuclear matrix minus the dense periodic circulant (and the defect matrix)."""
+        c = sys.to_c()
+        r = ctypes.c_double()
+        Nb = sys.basis_count
+        out = np.zeros(Nb * Nb) if want_defect else None
+        check(self.lib.lt_box_circulant_defect(self.h, ctypes.byref(c), ctypes.byref(r),
+                                               _d(out) if want_defect else None))
+        return (r.value, out.reshape(Nb, Nb).T.copy()) if want_defect else r.value
+
     # ---- separable metadata / factorized path --------------------------------
     def separable_residual(self, op: Operator) -> float:
         r = ctypes.c_double()
@@ -452,3 +463,19 @@ def solve_box_dense(H: np.ndarray, S: np.ndarray, cap: int = 4096) -> np.ndarray
 
 def solve_core(sys: LatticeSystem, periodic: bool) -> np.ndarray:
     return default_context().solve_core(sys, periodic)
+
+
+def spectral_bands(eig: np.ndarray):
+    """spectral_bands (eigensolver.cpp:177-190): eig [K, m0] -> (bands [m0, K], band_min, band_max)."""
+    eig = np.asarray(eig, dtype=np.float64)
+    bands = eig.T.copy()
+    return bands, bands.min(axis=1), bands.max(axis=1)
+
+
+def average_energy_per_cell(sorted_eigenvalues, cells: int, n_occ: int) -> float:
+    """average_energy_per_cell (eigensolver.cpp:192-198): sum of the lowest n_occ*cells / cells."""
+    ev = np.asarray(sorted_eigenvalues, dtype=np.float64)
+    take = n_occ * cells
+    if take < 0 or take > ev.size:
+        raise DimensionError("average_energy_per_cell: occupation exceeds spectrum size")
+    return float(np.sum(ev[:take])) / float(cells)

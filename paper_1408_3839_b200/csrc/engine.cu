@@ -2090,3 +2090,49 @@ lt_status lt_solve_periodic_factorized_gen(lt_ctx* c, const int64_t* dims, int64
         sep_solve(c, *mH, *mS, eig);
     });
 }
+
+// box_circulant_defect (galerkin.cpp:445-454): Nuclear assembled both ways, the periodic
+// circulant expanded densely; rel_fro = ||box - per|| / ||box||. defect (optional): Nb*Nb.
+lt_status lt_box_circulant_defect(lt_ctx* c, const lt_system* s, double* rel_fro, double* defect) {
+    return guarded([&] {
+        LT_CU(cudaSetDevice(c->device));
+        lt_operator* bo = nullptr;
+        lt_operator* po = nullptr;
+        lt_status st = lt_assemble(c, s, 0, LT_NUCLEAR, &bo);
+        if (st != LT_OK) fail(static_cast<int>(st), lt_last_error());
+        std::unique_ptr<lt_operator> box(bo);
+        st = lt_assemble(c, s, 1, LT_NUCLEAR, &po);
+        if (st != LT_OK) fail(static_cast<int>(st), lt_last_error());
+        std::unique_ptr<lt_operator> per(po);
+        const Index K = per->L[0] * per->L[1] * per->L[2];
+        std::vector<int> go(static_cast<size_t>(K), -1);
+        for (size_t b = 0; b < per->kidx.size(); ++b)
+            go[static_cast<size_t>((per->kidx[b][0] * per->L[1] + per->kidx[b][1]) * per->L[2] + per->kidx[b][2])] =
+                static_cast<int>(b);
+        StageScope ss(c, 1 << 20);
+        int* gd = c->arena.get<int>("defect.gen", go.size());
+        upload(c, gd, go.data(), go.size() * sizeof(int));
+        CircDefect d;
+        d.Nb = box->Nb;
+        d.m0 = box->m0;
+        for (int l = 0; l < 3; ++l) d.L[l] = per->L[l];
+        d.box = box->data;
+        d.gen = per->data;
+        d.gen_of = gd;
+        d.defect = defect ? c->arena.get<double>("defect.out", d.Nb * d.Nb) : nullptr;
+        const int blocks = static_cast<int>(std::min<Index>(148 * 4, (d.Nb * d.Nb + 255) / 256));
+        d.partial = c->arena.get<double>("defect.part", 2 * blocks);
+        launch_circ_defect(c->L(), d, blocks);
+        std::vector<double> part(static_cast<size_t>(2 * blocks));
+        LT_CU(cudaMemcpyAsync(part.data(), d.partial, sizeof(double) * part.size(), cudaMemcpyDeviceToHost, c->stream));
+        if (defect)
+            LT_CU(cudaMemcpyAsync(defect, d.defect, sizeof(double) * d.Nb * d.Nb, cudaMemcpyDeviceToHost, c->stream));
+        LT_CU(cudaStreamSynchronize(c->stream));
+        double sd = 0.0, sb = 0.0;
+        for (int b = 0; b < blocks; ++b) {
+            sd += part[static_cast<size_t>(2 * b)];
+            sb += part[static_cast<size_t>(2 * b + 1)];
+        }
+        *rel_fro = std::sqrt(sd) / std::sqrt(sb);
+    });
+}

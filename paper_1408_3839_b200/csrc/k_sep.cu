@@ -162,3 +162,59 @@ void launch_sep_residual(const Launch& L, const SepResid& r) {
 }
 
 }  // namespace lt
+
+namespace lt {
+
+// box_circulant_defect (galerkin.cpp:445-454): defect = box - bc_to_dense(periodic) where
+// block (i, j) of the circulant is gen[(m_i - m_j) mod L] (block_circulant.cpp:128-149).
+// Writes the defect (optional) and per-CTA partial sums of defect^2 and box^2; the host
+// adds the partials in CTA order (deterministic).
+__global__ void k_circ_defect(CircDefect d) {
+    __shared__ double s_def[8], s_box[8];
+    const Index nb = d.Nb, m0 = d.m0;
+    double acc_d = 0.0, acc_b = 0.0;
+    for (Index idx = static_cast<Index>(blockIdx.x) * blockDim.x + threadIdx.x; idx < nb * nb;
+         idx += static_cast<Index>(gridDim.x) * blockDim.x) {
+        const Index row = idx % nb, col = idx / nb;  // column-major
+        const Index i = row / m0, j = col / m0, mu = row % m0, nu = col % m0;
+        Index k[3];
+        const Index iv[3] = {i / (d.L[1] * d.L[2]), (i / d.L[2]) % d.L[1], i % d.L[2]};
+        const Index jv[3] = {j / (d.L[1] * d.L[2]), (j / d.L[2]) % d.L[1], j % d.L[2]};
+#pragma unroll
+        for (int l = 0; l < 3; ++l) k[l] = ((iv[l] - jv[l]) % d.L[l] + d.L[l]) % d.L[l];
+        const int b = d.gen_of[(k[0] * d.L[1] + k[1]) * d.L[2] + k[2]];
+        const double per = b >= 0 ? d.gen[static_cast<Index>(b) * m0 * m0 + mu + nu * m0] : 0.0;
+        const double box = d.box[idx];
+        const double df = box - per;
+        if (d.defect) d.defect[idx] = df;
+        acc_d = fma(df, df, acc_d);
+        acc_b = fma(box, box, acc_b);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        acc_d += __shfl_xor_sync(0xffffffffu, acc_d, o);
+        acc_b += __shfl_xor_sync(0xffffffffu, acc_b, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        s_def[threadIdx.x >> 5] = acc_d;
+        s_box[threadIdx.x >> 5] = acc_b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, bsum = 0.0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+            a += s_def[w];
+            bsum += s_box[w];
+        }
+        d.partial[2 * blockIdx.x] = a;
+        d.partial[2 * blockIdx.x + 1] = bsum;
+    }
+}
+
+void launch_circ_defect(const Launch& L, const CircDefect& d, int blocks) {
+    Stage st_(L, "circ_defect");
+    k_circ_defect<<<blocks, 256, 0, L.st>>>(d);
+    LT_CU(cudaGetLastError());
+    L.tick();
+}
+
+}  // namespace lt

@@ -392,6 +392,17 @@ struct SepResid {
 };
 void launch_sep_residual(const Launch& L, const SepResid& r);
 
+struct CircDefect {
+    Index Nb = 0, m0 = 0;
+    Index L[3]{1, 1, 1};
+    const double* box = nullptr;  // dense Nb x Nb, column-major
+    const double* gen = nullptr;  // periodic generating blocks [stored][m0*m0]
+    const int* gen_of = nullptr;  // lattice index -> stored block (-1 none)
+    double* defect = nullptr;     // optional output
+    double* partial = nullptr;    // [blocks][2]: sum defect^2, sum box^2
+};
+void launch_circ_defect(const Launch& L, const CircDefect& d, int blocks);
+
 // fused per-axis DFT for one or two operators (k_spectrum.cu)
 struct DftAxisArgs {
     int axis = 0;

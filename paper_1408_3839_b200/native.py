@@ -75,6 +75,7 @@ def lib():
             "lt_solve_periodic_factorized_gen": ([_vp, _ip, _i64, _i64, _ip, _dp, _i64, _dp, _i64, _ip, _dp, _i64,
                                                   _dp, ctypes.c_double, _dp], ctypes.c_int),
             "lt_factorized_block_diagonalize": ([_vp, ctypes.c_int, _ip, _i64, _i64, _dp, _dp], ctypes.c_int),
+            "lt_box_circulant_defect": ([_vp, _vp, _dp, _dp], ctypes.c_int),
             "lt_stage_timeline_count": ([_vp], _i64),
             "lt_stage_timeline_get": ([_vp, _i64, ctypes.c_char_p, _i64, ctypes.POINTER(ctypes.c_int), _dp, _dp],
                                       ctypes.c_int),
@@ -120,7 +121,7 @@ EXPORTS = (
     "lt_create", "lt_destroy", "lt_last_error", "lt_stream", "lt_launch_count", "lt_set_stage_timing",
     "lt_stage_count", "lt_stage_get", "lt_stage_timeline_count", "lt_stage_timeline_get",
     "lt_op_separable_count", "lt_op_separable", "lt_separable_residual", "lt_solve_periodic_factorized",
-    "lt_solve_periodic_factorized_gen", "lt_factorized_block_diagonalize", "lt_solve_core", "lt_sys_upload",
+    "lt_solve_periodic_factorized_gen", "lt_factorized_block_diagonalize", "lt_box_circulant_defect", "lt_solve_core", "lt_sys_upload",
     "lt_sys_free", "lt_solve_core_dev", "lt_assemble", "lt_assemble_core", "lt_combine", "lt_op_free", "lt_op_info",
     "lt_op_dense", "lt_op_blocks", "lt_solve_periodic_ops", "lt_solve_periodic", "lt_block_diagonalize",
     "lt_solve_box_dense", "lt_pencil_eig", "lt_sinc_quadrature", "lt_overlap_constant", "lt_newton_master",

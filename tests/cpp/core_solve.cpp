@@ -46,6 +46,8 @@ int main() {
     auto H = combine(ctx, 0.5, lap, -1.0, nuc);
     print("periodic_ops", solve_periodic(ctx, H, S).sorted_all());
     print("periodic_core", solve_core_periodic(ctx, per).sorted_all());
+    print("periodic_factorized", solve_periodic_factorized(ctx, H, S).sorted_all());
+    std::printf("residual %.3g\n", separable_residual(ctx, H));
     // box
     const LatticeSystem box = chain(6, false);
     auto blap = assemble_box(ctx, box, OperatorKind::Laplace);

@@ -40,7 +40,7 @@ def chain(Lx, two):
 def test_cpp_client_matches_python_api(tmp_path, ctx):
     out = subprocess.run([build(tmp_path)], check=True, capture_output=True, text=True).stdout.splitlines()
     res = {ln.split()[0]: ln.split()[1:] for ln in out}
-    vals = {k: np.array([float(x) for x in v[1:]]) for k, v in res.items() if not k.startswith("error")}
+    vals = {k: np.array([float(x) for x in v[1:]]) for k, v in res.items() if not k.startswith(("error", "resid"))}
     per = np.sort(ctx.solve_core(chain(16, True), True).reshape(-1))
     box = ctx.solve_core(chain(6, False), False)
     assert np.array_equal(vals["periodic_core"], per)
@@ -48,5 +48,7 @@ def test_cpp_client_matches_python_api(tmp_path, ctx):
     # the separate-operator route (assemble x3, combine, solve) agrees to rounding
     assert np.max(np.abs(vals["periodic_ops"] - per)) < 1e-10 * max(1.0, np.max(np.abs(per)))
     assert np.max(np.abs(vals["box_ops"] - box)) < 1e-10 * max(1.0, np.max(np.abs(box)))
+    assert np.max(np.abs(vals["periodic_factorized"] - per)) < 1e-10 * max(1.0, np.max(np.abs(per)))
+    assert float(res["residual"][0]) < 1e-12
     assert res["error_alias"][0] == "StructureError"
     assert res["error_cap"][0] == "ResourceCapError"

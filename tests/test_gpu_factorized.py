@@ -145,3 +145,26 @@ def test_factorized_requires_metadata(ctx):
     Hb = ctx.assemble(s, False, "mass")
     with pytest.raises(StructureError, match="operators must be periodic assemblies"):
         ctx.solve_periodic_factorized(Hb, Hb)
+
+
+def test_box_circulant_defect(ctx, oracle):
+    # galerkin.cpp:445-454 against the oracle's box and periodic nuclear operators
+    s = chain_system(7, [0.6, 1.7], n=8, nbar=8, M=6, b=4.0)
+    rel, D = ctx.box_circulant_defect(s, want_defect=True)
+    box = oracle.assemble(s, False, "nuclear")
+    per = oracle.assemble(s, True, "nuclear")
+    L, m0 = per.L, per.m0
+    g = per.gen_dict()
+    K = L[0] * L[1] * L[2]
+    dense = np.zeros((K * m0, K * m0))
+    idx = [(a, b, c) for a in range(L[0]) for b in range(L[1]) for c in range(L[2])]
+    for i, mi in enumerate(idx):
+        for j, mj in enumerate(idx):
+            k = tuple((mi[l] - mj[l]) % L[l] for l in range(3))
+            if k in g:
+                dense[i * m0:(i + 1) * m0, j * m0:(j + 1) * m0] = g[k]
+    ref = box.dense - dense
+    assert abs(rel - np.linalg.norm(ref) / np.linalg.norm(box.dense)) <= 1e-9 * rel
+    assert np.max(np.abs(D - ref)) <= 1e-10 * np.max(np.abs(box.dense))
+    oracle.free(box)
+    oracle.free(per)
