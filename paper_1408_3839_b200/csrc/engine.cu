@@ -414,9 +414,11 @@ static std::vector<int64_t> graph_key(const HostSys& h, const Plan& p, bool peri
 // ---------------------------------------------------------------------------
 // L0 (gto_basis.cpp:87-126)
 // ---------------------------------------------------------------------------
-// launch_only: enqueue the first 16-shift chunk (whose fused rule decides L0 <= 14)
-// with its read-back into pinned memory and return -1 without synchronising.
-static Index compute_L0(lt_ctx* c, const lt_sysdev* sd, bool launch_only = false) {
+// launch_only: enqueue the first chunk (whose fused rule decides L0 <= chunk - 2) with its
+// read-back into pinned memory and return -1 without synchronising. spec_L0 >= 0 (with
+// launch_only): the chunk is cut to shifts 1 .. spec_L0 + 2, exactly the shifts the
+// sequential rule needs to confirm that L0; the caller checks done && L0 == spec_L0.
+static Index compute_L0(lt_ctx* c, const lt_sysdev* sd, bool launch_only = false, Index spec_L0 = -1) {
     const HostSys& h = sd->hs;
     const Index m0 = h.m0();
     Index off3[3], boff3[3], n3[3];
@@ -441,6 +443,17 @@ static Index compute_L0(lt_ctx* c, const lt_sysdev* sd, bool launch_only = false
                        h.deg[3 * mu + q] == h.deg[3 * mu + l];
             if (same) active[l] = 0;
         }
+    // directions whose functions are all degree 0 take the exact peak-window search
+    // (k_l0_peak); the others sample the profiles and scan them
+    int act_peak[3] = {0, 0, 0}, act_scan[3] = {0, 0, 0};
+    bool any_peak = false, any_scan = false;
+    for (int l = 0; l < 3; ++l) {
+        if (!active[l]) continue;
+        bool deg0 = true;
+        for (Index mu = 0; mu < m0; ++mu) deg0 = deg0 && h.deg[3 * mu + l] == 0;
+        (deg0 ? act_peak : act_scan)[l] = 1;
+        (deg0 ? any_peak : any_scan) = true;
+    }
     OverlapBufs b;
     b.prof = c->arena.get<double>("l0.prof", tot);
     b.bmax = c->arena.get<double>("l0.bmax", btot);
@@ -448,25 +461,30 @@ static Index compute_L0(lt_ctx* c, const lt_sysdev* sd, bool launch_only = false
     b.found = c->arena.get<int>("l0.found", 260);
     b.state = c->arena.get<int>("l0.state", 8);
     const Launch L = c->L();
-    const int chunk = 16;  // shifts per scan launch; L0 + 2 <= 16 needs a single launch
+    const int chunk = (launch_only && spec_L0 >= 0) ? static_cast<int>(spec_L0) + 2
+                                                    : 16;  // L0 + 2 <= 16 needs one launch
     int* st = c->pinned_state();
     // first chunk as one replayable sequence: init, sample, scan (+ fused rule), read-back
     auto first = [&]() {
         launch_overlap_init(L, b, static_cast<int>(m0));
-        launch_overlap_profiles(L, sd->ds, n3, off3, boff3, active, b);
-        launch_overlap_scan(L, sd->ds, n3, off3, boff3, active, b, 1, 1 + chunk);
+        if (any_scan) {
+            launch_overlap_profiles(L, sd->ds, n3, off3, boff3, act_scan, b);
+            launch_overlap_scan(L, sd->ds, n3, off3, boff3, act_scan, b, 1, 1 + chunk, !any_peak);
+        }
+        if (any_peak) launch_overlap_peak(L, sd->ds, n3, act_peak, b, 1, 1 + chunk, true);
         LT_CU(cudaMemcpyAsync(st, b.state, 4 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     };
     run_cached(
         c, c->l0graph,
-        [&]() { return graph_key(h, Plan{}, false, -1, -1, st, sd->mem, c->arena.generation()); }, first);
+        [&]() { return graph_key(h, Plan{}, false, chunk, -1, st, sd->mem, c->arena.generation()); }, first);
     c->phase_mark(1);
     if (launch_only) return -1;
     LT_CU(cudaStreamSynchronize(c->stream));
     int s_begin = 1 + chunk;
     while (!st[3] && s_begin < 257) {
         const int s_end = std::min(257, s_begin + chunk);
-        launch_overlap_scan(L, sd->ds, n3, off3, boff3, active, b, s_begin, s_end);
+        if (any_scan) launch_overlap_scan(L, sd->ds, n3, off3, boff3, act_scan, b, s_begin, s_end, !any_peak);
+        if (any_peak) launch_overlap_peak(L, sd->ds, n3, act_peak, b, s_begin, s_end, true);
         LT_CU(cudaMemcpyAsync(st, b.state, 4 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
         LT_CU(cudaStreamSynchronize(c->stream));
         s_begin = s_end;
@@ -1084,7 +1102,7 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
                       c->spec_L0 <= 14 && skey == c->spec_key;
     Index L0;
     if (spec) {
-        compute_L0(c, sd, true);
+        compute_L0(c, sd, true, c->spec_L0);
         L0 = c->spec_L0;
     } else {
         L0 = compute_L0(c, sd);

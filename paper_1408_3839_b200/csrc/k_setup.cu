@@ -184,7 +184,8 @@ __device__ void l0_finalize(const int* found, int* state, int s_end) {
 // monotone). Lanes test the bounds of 32 blocks at once; each candidate block is then
 // scanned by the whole warp. The last CTA to finish applies the sequential L0 rule.
 __global__ void k_l0_scan(DevSys s, Dir3 d, const double* __restrict__ prof, const double* __restrict__ bmax,
-                          const unsigned* __restrict__ nz, int* found, int* state, int s_begin, int ns, int s_end) {
+                          const unsigned* __restrict__ nz, int* found, int* state, int s_begin, int ns, int s_end,
+                          int finalize) {
     const int lane = threadIdx.x & 31;
     const Index task = static_cast<Index>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const Index m0 = s.m0;
@@ -244,6 +245,7 @@ __global__ void k_l0_scan(DevSys s, Dir3 d, const double* __restrict__ prof, con
         }
     }
     if (hit && lane == 0) atomicExch(&found[sft], 1);
+    if (!finalize) return;
     // fused finalize: the last CTA to finish applies the sequential rule
     __shared__ bool last;
     __syncthreads();
@@ -260,7 +262,7 @@ __global__ void k_l0_scan(DevSys s, Dir3 d, const double* __restrict__ prof, con
 }
 
 void launch_overlap_scan(const Launch& L, const DevSys& s, const Index* n3, const Index* off3, const Index* boff3,
-                         const int* active, OverlapBufs b, int s_begin, int s_end) {
+                         const int* active, OverlapBufs b, int s_begin, int s_end, bool finalize) {
     const Dir3 d = make_dir3(s, n3, off3, boff3, active);
     const int ns = s_end - s_begin;
     const Index tasks = static_cast<Index>(ns) * d.nl * s.m0 * s.m0;
@@ -268,7 +270,81 @@ void launch_overlap_scan(const Launch& L, const DevSys& s, const Index* n3, cons
     const Index blocks = std::max<Index>(1, (tasks + wpb - 1) / wpb);
     Stage st_(L, "l0_scan");
     k_l0_scan<<<static_cast<unsigned>(blocks), wpb * 32, 0, L.st>>>(s, d, b.prof, b.bmax, b.nz, b.found, b.state,
-                                                                    s_begin, ns, s_end);
+                                                                    s_begin, ns, s_end, finalize ? 1 : 0);
+    LT_CU(cudaGetLastError());
+    L.tick();
+}
+
+// Degree-0 directions: every profile is a sampled Gaussian exp(-alpha (x_i - c)^2) with
+// x_i affine in i, so log|a_i c_{i-sn}| is a concave quadratic in i whose continuous
+// maximiser is i* (x* = (alpha c_mu + beta (c_nu + s b)) / (alpha + beta)). The discrete
+// maximum over the valid range is at round(i*) clipped to the range, so an 8-point window
+// around it, evaluated with the same device arithmetic as the sampled scan, yields the
+// scan's maximum (neighbouring products differ by a relative (alpha+beta) h^2 >> ulp).
+// A window maximum just below eps (relative 1e-12) is re-checked by a full scan of that
+// (s, mu, nu), so the decision equals the exhaustive one. One thread per (s, l, mu, nu);
+// the last CTA applies the sequential rule when `finalize`.
+__global__ void k_l0_peak(DevSys s, Dir3 d, int* found, int* state, int s_begin, int ns, int s_end, int finalize) {
+    const Index task = static_cast<Index>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const Index m0 = s.m0;
+    const Index per_s = static_cast<Index>(d.nl) * m0 * m0;
+    if (task < per_s * ns) {
+        const int sft = s_begin + static_cast<int>(task / per_s);
+        Index rem = task % per_s;
+        const int l = d.dir[rem / (m0 * m0)];
+        rem %= m0 * m0;
+        const int mu = static_cast<int>(rem / m0), nu = static_cast<int>(rem % m0);
+        const Index n = d.n[l];
+        const Index base = (kMaxL0 + 2) * n, width = 2 * base, sn = static_cast<Index>(sft) * n;
+        if (!__ldcg(&found[sft]) && sn < width) {
+            const double h = s.b / static_cast<double>(n);
+            const double al = s.alpha[mu], be = s.alpha[nu];
+            const double xs = (al * s.center[3 * mu + l] + be * (s.center[3 * nu + l] + sft * s.b)) / (al + be);
+            const double is = (xs + 0.5 * s.b) / h + static_cast<double>(base) - 0.5;
+            const Index lo = sn, hi = width - 1;  // j = i - sn >= 0
+            const double isc = fmin(fmax(is, static_cast<double>(lo)), static_cast<double>(hi));
+            Index i0 = static_cast<Index>(floor(isc)) - 3;
+            i0 = max(lo, min(i0, hi - 7));
+            const Index i1 = min(hi, i0 + 7);
+            double best = 0.0;
+            for (Index i = i0; i <= i1; ++i) {
+                const double a = gto_eval1d(s, mu, l, l0_x(i, base, h, s.b));
+                const double c = gto_eval1d(s, nu, l, l0_x(i - sn, base, h, s.b));
+                best = fmax(best, fabs(a * c));
+            }
+            bool hit = best >= s.eps_ov;
+            if (!hit && best >= s.eps_ov * (1.0 - 1e-12))  // at the threshold: exhaustive
+                for (Index i = lo; i <= hi && !hit; ++i)
+                    hit = fabs(gto_eval1d(s, mu, l, l0_x(i, base, h, s.b)) *
+                               gto_eval1d(s, nu, l, l0_x(i - sn, base, h, s.b))) >= s.eps_ov;
+            if (hit) atomicExch(&found[sft], 1);
+        }
+    }
+    if (!finalize) return;
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(&state[4], 1) == static_cast<int>(gridDim.x) - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        l0_finalize(found, state, s_end);
+        state[4] = 0;
+    }
+}
+
+void launch_overlap_peak(const Launch& L, const DevSys& s, const Index* n3, const int* active, OverlapBufs b,
+                         int s_begin, int s_end, bool finalize) {
+    const Index zero3[3] = {0, 0, 0};
+    const Dir3 d = make_dir3(s, n3, zero3, zero3, active);
+    const int ns = s_end - s_begin;
+    const Index tasks = static_cast<Index>(ns) * d.nl * s.m0 * s.m0;
+    const Index blocks = std::max<Index>(1, (tasks + 127) / 128);
+    Stage st_(L, "l0_peak");
+    k_l0_peak<<<static_cast<unsigned>(blocks), 128, 0, L.st>>>(s, d, b.found, b.state, s_begin, ns, s_end,
+                                                              finalize ? 1 : 0);
     LT_CU(cudaGetLastError());
     L.tick();
 }

@@ -211,7 +211,10 @@ void launch_overlap_profiles(const Launch& L, const DevSys& s, const Index* n3, 
                              const Index* boff3, const int* active, OverlapBufs b);
 // scan of shifts [s_begin, s_end) with the sequential L0 rule fused into the last CTA
 void launch_overlap_scan(const Launch& L, const DevSys& s, const Index* n3, const Index* off3, const Index* boff3,
-                         const int* active, OverlapBufs b, int s_begin, int s_end);
+                         const int* active, OverlapBufs b, int s_begin, int s_end, bool finalize);
+// degree-0 directions: exact peak-window search instead of sampling + scanning
+void launch_overlap_peak(const Launch& L, const DevSys& s, const Index* n3, const int* active, OverlapBufs b,
+                         int s_begin, int s_end, bool finalize);
 void launch_overlap_init(const Launch& L, OverlapBufs b, int m0);
 
 // master tensor (newton_kernel.cpp:22-45) and assembled window sums (canonical_tensor.cpp:123-164)
