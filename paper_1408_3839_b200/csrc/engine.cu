@@ -181,7 +181,7 @@ struct lt_ctx {
     // side streams for independent branches of the assembly (captured into the same graph
     // as parallel branches) and the fork/join events between them
     cudaStream_t aux[2]{nullptr, nullptr};
-    cudaEvent_t ev[8]{};
+    cudaEvent_t ev[8]{};  // fork/join points of run_assembly (indices 0-5)
     // pinned staging for the small per-call host<->device copies (system, window starts,
     // DFT index maps, eigenvalue read-back): async copies instead of pageable round trips.
     // Valid between stage_begin() (stream idle) and the end of the API call.
@@ -579,11 +579,16 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
     const bool nuc = need & NEED_NUC, ms = need & NEED_MS;
     if (nuc) s0d = s0_dev ? s0_dev : upload_s0(c, p);
     c->join(0, c->stream, c->aux[0]);
+    c->join(1, c->stream, c->aux[1]);
+    // Trivial-direction panels could be evaluated inside k_triv_gemm (TrivJob.pot = null):
+    // measured slower (erf pairs in the GEMM loader, repeated per N tile), so every panel is
+    // materialised by the master-free window kernels.
+    constexpr bool fused_nuc = false;
     w.t = A.get<double>("sinc.t", RN);
     w.w = A.get<double>("sinc.w", RN);
     w.potw = A.get<double>("sinc.potw", Rtot);
     launch_sinc(L, p.M, sd->ds, w.t, w.w, w.potw);
-    c->join(1, c->stream, c->aux[1]);
+    c->join(5, c->stream, c->aux[1]);  // the side branch's master needs the nodes
     if (nuc) {
         int nth = 0;
         for (int l = 0; l < 3; ++l) {
@@ -591,12 +596,26 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
                 w.pot[l] = w.pot[src[l]];
                 continue;
             }
-            const Launch& LL = (nth++ == 1) ? LP : L;
             const DirPlan& d = p.d[l];
-            double* master = A.get<double>("pot.master" + std::to_string(l), d.mrows * RN);
+            if (fused_nuc && d.L == 1) {  // consumed by k_triv_gemm straight from the master cells
+                w.pot[l] = nullptr;
+                continue;
+            }
+            const Launch& LL = (nth++ == 1) ? LP : L;
             w.pot[l] = A.get<double>("pot.panel" + std::to_string(l), d.pot_rows * Rtot);
-            launch_master(LL, d.mrows, d.h, RN, w.t, master);
-            launch_window_sum(LL, master, d.mrows, RN, p.nnuc, s0d + l * p.nnuc, d.nsum, d.n, d.pot_rows, w.pot[l]);
+            if (d.nsum == 1 && p.nnuc == 1) {
+                // a single window copy of one nucleus: each master cell is read once, so it
+                // is evaluated in the copy kernel instead of being materialised first
+                launch_potential_fused(LL, d.mrows, d.h, p.M, RN, p.nnuc, s0d + l * p.nnuc, d.nsum, d.n,
+                                       d.pot_rows, w.pot[l]);
+            } else {
+                // the master panel once (massively parallel), then the windows read it: a cell
+                // serves every nucleus and, for lattice sums, two running-sum updates
+                double* master = A.get<double>("pot.master" + std::to_string(l), d.mrows * RN);
+                launch_master(LL, d.mrows, d.h, RN, w.t, master);
+                launch_window_sum(LL, master, d.mrows, RN, p.nnuc, s0d + l * p.nnuc, d.nsum, d.n, d.pot_rows,
+                                  w.pot[l]);
+            }
         }
     }
     c->join(2, c->aux[1], c->stream);
@@ -719,6 +738,11 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
                     TrivJob& J = tj.j[njobs++];
                     J.pot = w.pot[s];
                     J.rows = p.d[s].pot_rows;
+                    J.mrows = p.d[s].mrows;
+                    J.h = p.d[s].h;
+                    J.M = static_cast<int>(p.M);
+                    J.RN = static_cast<int>(RN);
+                    J.s0 = s0d + s * p.nnuc;
                     J.pwc = w.pwc[s];
                     J.G = p.d[s].G;
                     J.lo = w.pwc_lo[s];

@@ -68,17 +68,29 @@ __global__ void __launch_bounds__(256) k_triv_gemm(TrivJobs jobs, int m0, int Rt
     const long long per = ((len + splits - 1) / splits + kGBK - 1) / kGBK * kGBK;
     const long long k0 = klo + split * per, k1 = min(khi, k0 + per);
     __shared__ int smu[64], snu[64];
+    __shared__ double tqs[kGBM];    // in-place potential: t_q of each tile row
+    __shared__ long long s0s[kGBM];  // and its window start s0[v]
     if (threadIdx.x < 64) {
         int mu = 0, nu = 0;
         if (e0 + static_cast<int>(threadIdx.x) < nsym) sym_pair(e0 + threadIdx.x, m0, mu, nu);
         smu[threadIdx.x] = mu;
         snu[threadIdx.x] = nu;
+        const int r = r0 + static_cast<int>(threadIdx.x);
+        if (!J.pot && r < Rtot) {
+            tqs[threadIdx.x] = sinc_node(r % J.RN, J.M);
+            s0s[threadIdx.x] = J.s0[r / J.RN];
+        }
     }
     __syncthreads();
     const double* P = J.pot;
     const double* g = J.pwc;
     const long long G = J.G, rows = J.rows;
-    auto loadA = [&](int m, long long k) -> double { return r0 + m < Rtot ? P[(r0 + m) * rows + k] : 0.0; };
+    // A = the potential panel P[r][i], read or (P null) evaluated in place from the master
+    // cells of its window (the panel the window copy would have written, bit for bit)
+    auto loadA = [&](int m, long long k) -> double {
+        if (r0 + m >= Rtot) return 0.0;
+        return P ? P[(r0 + m) * rows + k] : master_cell(s0s[m] + k, J.mrows, J.h, tqs[m]);
+    };
     auto loadB = [&](long long k, int n) -> double {
         return e0 + n < nsym ? g[smu[n] * G + k] * g[snu[n] * G + k] : 0.0;
     };

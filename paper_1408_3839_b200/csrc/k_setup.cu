@@ -24,7 +24,7 @@ __global__ void k_sinc(int M, int nnuc, const double* __restrict__ Z, double* t,
     for (int i = threadIdx.x; i < R; i += blockDim.x) {
         const double u = __dmul_rn(static_cast<double>(i - M), step);
         const double eu = exp(-u);
-        const double ti = exp(__dsub_rn(u, eu));
+        const double ti = sinc_node(i, M);  // exp(u - e^-u), shared with the fused potential
         const double wi = __dmul_rn(c, __dadd_rn(ti, exp(-eu)));
         t[i] = ti;
         w[i] = wi;

@@ -219,6 +219,10 @@ void launch_overlap_init(const Launch& L, OverlapBufs b, int m0);
 
 // master tensor (newton_kernel.cpp:22-45) and assembled window sums (canonical_tensor.cpp:123-164)
 void launch_master(const Launch& L, Index mrows, double h, Index RN, const double* t, double* out);
+void launch_sinc_nodes(const Launch& L, Index M, double* t);
+// window sums with the master cells evaluated in place (no master panel)
+void launch_potential_fused(const Launch& L, Index mrows, double h, Index M, Index RN, Index nnuc, const Index* s0_dev,
+                            Index nsum, Index step, Index size, double* out);
 void launch_window_sum(const Launch& L, const double* master, Index mrows, Index RN, Index nnuc, const Index* s0_dev,
                        Index nsum, Index step, Index size, double* out);
 
@@ -253,8 +257,13 @@ void launch_box_corr(const Launch& L, Index m0, const DirPlan& d, const double* 
 
 // ---- DMMA nuclear contraction (k_nuclear2.cu) ----
 struct TrivJob {
-    const double* pot = nullptr;  // potential panel [Rtot][rows]
+    const double* pot = nullptr;  // potential panel [Rtot][rows]; null: evaluated in place
     long long rows = 0;
+    // in-place potential (pot == null): P[v RN + q][i] = master_cell(s0[v] + i, mrows, h, t_q)
+    long long mrows = 0;
+    double h = 0.0;
+    int M = 0, RN = 0;
+    const Index* s0 = nullptr;
     const double* pwc = nullptr;  // profiles [m0][G]
     long long G = 0;
     const unsigned long long* lo = nullptr;
