@@ -11,6 +11,7 @@
 #include <cusolverDn.h>
 
 #include <algorithm>
+#include <chrono>
 #include <array>
 #include <cstdlib>
 #include <cstring>
@@ -176,7 +177,7 @@ struct lt_ctx {
     StageTimer timer;
     // CUDA graphs of the L0 sequence and of the post-L0 launch sequence
     bool graphs = true;
-    GraphCache l0graph, coregraph;
+    GraphCache l0graph, coregraph, fullgraph;  // fullgraph: L0 + post-L0 under speculation
     int* pinned = nullptr;  // small pinned read-back buffer
     // side streams for independent branches of the assembly (captured into the same graph
     // as parallel branches) and the fork/join events between them
@@ -212,6 +213,22 @@ struct lt_ctx {
     // speculation on L0: the last (system, L0) pair the device computed
     std::vector<int64_t> spec_key;
     Index spec_L0 = -1;
+    // optional host-side timestamps (env LT_HOST_TIMING=1): enter / launched / synced / exit
+    bool host_timing = false;
+    double host_acc[4] = {0, 0, 0, 0};
+    double graph_launch_us = 0.0, key_us = 0.0;
+    int64_t n_replay = 0, n_capture = 0, n_eager = 0;
+    int64_t host_n = 0;
+    std::chrono::steady_clock::time_point host_t[5];
+    void host_mark(int i) {
+        if (host_timing) host_t[i] = std::chrono::steady_clock::now();
+    }
+    void host_collect() {
+        if (!host_timing) return;
+        for (int i = 0; i < 4; ++i)
+            host_acc[i] += std::chrono::duration<double, std::micro>(host_t[i + 1] - host_t[i]).count();
+        ++host_n;
+    }
     // optional phase markers (env LT_PHASE_TIMING=1): events between the graph launches,
     // accumulated into the stage totals as phase_l0 / phase_gap / phase_post
     bool phase_timing = false;
@@ -260,10 +277,17 @@ static void run_cached(lt_ctx* c, GraphCache& g, K&& keyfn, F&& enqueue) {
     // stage timing is captured too (event nodes inside the graph), keyed separately, so the
     // per-stage times come from the same graph execution as the untimed solve
     const bool allow = c->graphs;
+    const auto tk = std::chrono::steady_clock::now();
     std::vector<int64_t> key = keyfn();
+    if (c->host_timing)
+        c->key_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tk).count();
     key.push_back(c->timer.on ? 1 : 0);
     if (allow && g.exec && key == g.key) {
+        const auto t0 = std::chrono::steady_clock::now();
         LT_CU(cudaGraphLaunch(g.exec, c->stream));
+        if (c->host_timing)
+            c->graph_launch_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+        ++c->n_replay;
         c->launches += g.launches;
         if (c->timer.on) c->timer.add_pending(g.timing);
         return;
@@ -296,8 +320,10 @@ static void run_cached(lt_ctx* c, GraphCache& g, K&& keyfn, F&& enqueue) {
         g.launches = c->launches - l0;
         LT_CU(cudaGraphLaunch(g.exec, c->stream));
         if (c->timer.on) c->timer.add_pending(g.timing);
+        ++c->n_capture;
         return;
     }
+    ++c->n_eager;
     enqueue();
     g.seen = keyfn();  // after the eager run: it may have grown the arena (new generation)
     g.seen.push_back(c->timer.on ? 1 : 0);
@@ -414,20 +440,37 @@ static std::vector<int64_t> graph_key(const HostSys& h, const Plan& p, bool peri
 // ---------------------------------------------------------------------------
 // L0 (gto_basis.cpp:87-126)
 // ---------------------------------------------------------------------------
-// launch_only: enqueue the first chunk (whose fused rule decides L0 <= chunk - 2) with its
-// read-back into pinned memory and return -1 without synchronising. spec_L0 >= 0 (with
-// launch_only): the chunk is cut to shifts 1 .. spec_L0 + 2, exactly the shifts the
-// sequential rule needs to confirm that L0; the caller checks done && L0 == spec_L0.
-static Index compute_L0(lt_ctx* c, const lt_sysdev* sd, bool launch_only = false, Index spec_L0 = -1) {
+// L0 work of one system: direction classes, device buffers, and the launches of a shift
+// chunk [s_begin, s_end) (init + per-direction sampling only with the first chunk)
+struct L0Work {
+    const lt_sysdev* sd = nullptr;
+    int m0 = 0;
+    Index n3[3]{}, off3[3]{}, boff3[3]{};
+    int act_peak[3] = {0, 0, 0}, act_scan[3] = {0, 0, 0};
+    bool any_peak = false, any_scan = false;
+    OverlapBufs b;
+    void enqueue(const Launch& L, int s_begin, int s_end, bool first) const {
+        if (first) launch_overlap_init(L, b, m0);
+        if (any_scan) {
+            if (first) launch_overlap_profiles(L, sd->ds, n3, off3, boff3, act_scan, b);
+            launch_overlap_scan(L, sd->ds, n3, off3, boff3, act_scan, b, s_begin, s_end, !any_peak);
+        }
+        if (any_peak) launch_overlap_peak(L, sd->ds, n3, act_peak, b, s_begin, s_end, true);
+    }
+};
+
+static L0Work l0_setup(lt_ctx* c, const lt_sysdev* sd) {
     const HostSys& h = sd->hs;
+    L0Work w;
+    w.sd = sd;
+    w.m0 = static_cast<int>(h.m0());
     const Index m0 = h.m0();
-    Index off3[3], boff3[3], n3[3];
     Index tot = 0, btot = 0;
     for (int l = 0; l < 3; ++l) {
-        n3[l] = h.n[l];
+        w.n3[l] = h.n[l];
         const Index width = 2 * 258 * h.n[l];
-        off3[l] = tot;
-        boff3[l] = btot;
+        w.off3[l] = tot;
+        w.boff3[l] = btot;
         tot += m0 * width;
         btot += m0 * ((width + kL0Block - 1) / kL0Block);
     }
@@ -445,47 +488,42 @@ static Index compute_L0(lt_ctx* c, const lt_sysdev* sd, bool launch_only = false
         }
     // directions whose functions are all degree 0 take the exact peak-window search
     // (k_l0_peak); the others sample the profiles and scan them
-    int act_peak[3] = {0, 0, 0}, act_scan[3] = {0, 0, 0};
-    bool any_peak = false, any_scan = false;
     for (int l = 0; l < 3; ++l) {
         if (!active[l]) continue;
         bool deg0 = true;
         for (Index mu = 0; mu < m0; ++mu) deg0 = deg0 && h.deg[3 * mu + l] == 0;
-        (deg0 ? act_peak : act_scan)[l] = 1;
-        (deg0 ? any_peak : any_scan) = true;
+        (deg0 ? w.act_peak : w.act_scan)[l] = 1;
+        (deg0 ? w.any_peak : w.any_scan) = true;
     }
-    OverlapBufs b;
-    b.prof = c->arena.get<double>("l0.prof", tot);
-    b.bmax = c->arena.get<double>("l0.bmax", btot);
-    b.nz = c->arena.get<unsigned>("l0.nz", 6 * m0);
-    b.found = c->arena.get<int>("l0.found", 260);
-    b.state = c->arena.get<int>("l0.state", 8);
+    w.b.prof = w.any_scan ? c->arena.get<double>("l0.prof", tot) : nullptr;
+    w.b.bmax = w.any_scan ? c->arena.get<double>("l0.bmax", btot) : nullptr;
+    w.b.nz = c->arena.get<unsigned>("l0.nz", 6 * m0);
+    w.b.found = c->arena.get<int>("l0.found", 260);
+    w.b.state = c->arena.get<int>("l0.state", 8);
+    return w;
+}
+
+// L0 with the host reading it: the first 16-shift chunk (it decides L0 <= 14) as a
+// replayable graph ending in the read-back, further chunks only if the rule is not done
+static Index compute_L0(lt_ctx* c, const lt_sysdev* sd) {
+    const L0Work w = l0_setup(c, sd);
     const Launch L = c->L();
-    const int chunk = (launch_only && spec_L0 >= 0) ? static_cast<int>(spec_L0) + 2
-                                                    : 16;  // L0 + 2 <= 16 needs one launch
+    const int chunk = 16;
     int* st = c->pinned_state();
-    // first chunk as one replayable sequence: init, sample, scan (+ fused rule), read-back
-    auto first = [&]() {
-        launch_overlap_init(L, b, static_cast<int>(m0));
-        if (any_scan) {
-            launch_overlap_profiles(L, sd->ds, n3, off3, boff3, act_scan, b);
-            launch_overlap_scan(L, sd->ds, n3, off3, boff3, act_scan, b, 1, 1 + chunk, !any_peak);
-        }
-        if (any_peak) launch_overlap_peak(L, sd->ds, n3, act_peak, b, 1, 1 + chunk, true);
-        LT_CU(cudaMemcpyAsync(st, b.state, 4 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    };
     run_cached(
         c, c->l0graph,
-        [&]() { return graph_key(h, Plan{}, false, chunk, -1, st, sd->mem, c->arena.generation()); }, first);
+        [&]() { return graph_key(sd->hs, Plan{}, false, chunk, -1, st, sd->mem, c->arena.generation()); },
+        [&]() {
+            w.enqueue(L, 1, 1 + chunk, true);
+            LT_CU(cudaMemcpyAsync(st, w.b.state, 4 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        });
     c->phase_mark(1);
-    if (launch_only) return -1;
     LT_CU(cudaStreamSynchronize(c->stream));
     int s_begin = 1 + chunk;
     while (!st[3] && s_begin < 257) {
         const int s_end = std::min(257, s_begin + chunk);
-        if (any_scan) launch_overlap_scan(L, sd->ds, n3, off3, boff3, act_scan, b, s_begin, s_end, !any_peak);
-        if (any_peak) launch_overlap_peak(L, sd->ds, n3, act_peak, b, s_begin, s_end, true);
-        LT_CU(cudaMemcpyAsync(st, b.state, 4 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        w.enqueue(L, s_begin, s_end, false);
+        LT_CU(cudaMemcpyAsync(st, w.b.state, 4 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
         LT_CU(cudaStreamSynchronize(c->stream));
         s_begin = s_end;
     }
@@ -587,8 +625,9 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
     w.t = A.get<double>("sinc.t", RN);
     w.w = A.get<double>("sinc.w", RN);
     w.potw = A.get<double>("sinc.potw", Rtot);
-    launch_sinc(L, p.M, sd->ds, w.t, w.w, w.potw);
-    c->join(5, c->stream, c->aux[1]);  // the side branch's master needs the nodes
+    // nodes and weights Z_v w_q on the side branch: the master kernels evaluate their nodes
+    // in place, the weights are first needed after the join before the nuclear part
+    launch_sinc(LP, p.M, sd->ds, w.t, w.w, w.potw);
     if (nuc) {
         int nth = 0;
         for (int l = 0; l < 3; ++l) {
@@ -612,7 +651,7 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
                 // the master panel once (massively parallel), then the windows read it: a cell
                 // serves every nucleus and, for lattice sums, two running-sum updates
                 double* master = A.get<double>("pot.master" + std::to_string(l), d.mrows * RN);
-                launch_master(LL, d.mrows, d.h, RN, w.t, master);
+                launch_master(LL, d.mrows, d.h, RN, nullptr, master, p.M);
                 launch_window_sum(LL, master, d.mrows, RN, p.nnuc, s0d + l * p.nnuc, d.nsum, d.n, d.pot_rows,
                                   w.pot[l]);
             }
@@ -717,6 +756,8 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
     }
     // nuclear contraction: choose the reassociation (k_nuclear2.cu header)
     int nuc_mode = 0, ndir = -1;
+    const double* npart = nullptr;  // periodic single-direction fold partials (summed in fill)
+    Index npart_res = 0, npart_nd = 0;
     if (nuc) {
         std::vector<int> wrapped;
         for (int l = 0; l < 3; ++l)
@@ -793,7 +834,15 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
                     f.out[0] = A.get<double>("nuc.fpart", d.n * (d.band + 1) * mm);
                     f.res[0] = w.N;
                     f.slab = f.J <= kResfoldDirectJ ? nullptr : A.get<double>("nuc.slab", resfold_slab_doubles(f));
-                    launch_resfold(L, f, true, true, "nuc_fold");
+                    if (f.n <= 32) {
+                        // few residues: the fill sums them (no reduce launch)
+                        launch_resfold(L, f, false, false, "nuc_fold");
+                        npart = f.out[0];
+                        npart_res = f.n;
+                        npart_nd = f.dhi - f.dlo + 1;
+                    } else {
+                        launch_resfold(L, f, true, true, "nuc_fold");
+                    }
                 }
             } else {
                 KRArgs kr;
@@ -872,6 +921,9 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
     }
     fa.potw = w.potw;
     fa.N = w.N;
+    fa.Npart = npart;
+    fa.Nres = npart_res;
+    fa.Nnd = npart_nd;
     fa.s2_dir = ndir;
     fa.nuc_mode = nuc_mode;
     fa.mode = mode;
@@ -1114,6 +1166,7 @@ static std::vector<int64_t> graph_key(const HostSys& h, const Plan& p, bool peri
 // full path on device; eigenvalues -> eig_dev (device)
 static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double* eig_dev, Index k_begin,
                            Index k_end, int64_t* info, double* eig_host = nullptr, bool allow_spec = true) {
+    c->host_mark(0);
     validate(sd->hs);
     c->phase_mark(0);
     c->timer.mark_ref(c->stream);
@@ -1125,9 +1178,13 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
     const bool spec = allow_spec && spec_ok_path && c->graphs && !c->timer.on && c->spec_L0 >= 0 &&
                       c->spec_L0 <= 14 && skey == c->spec_key;
     Index L0;
+    L0Work l0w;
     if (spec) {
-        compute_L0(c, sd, true, c->spec_L0);
+        // L0 runs inside the same graph as the rest (shifts 1 .. L0 + 2, exactly those the
+        // rule needs to confirm the prediction); its state is read back with the results
+        l0w = l0_setup(c, sd);
         L0 = c->spec_L0;
+        c->phase_mark(1);  // no separate L0 phase: it is part of the single graph
     } else {
         L0 = compute_L0(c, sd);
     }
@@ -1153,8 +1210,10 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
     if (k_end < 0 || k_end > p.K) k_end = p.K;
     if (k_begin < 0) k_begin = 0;
     AsmOut out;
-    unsigned long long* fk = c->arena.get<unsigned long long>("solve.fail", 1);
-    LT_CU(cudaMemsetAsync(fk, 0xff, sizeof(unsigned long long), c->stream));
+    // read-back block: L0 state (ints 0-3, written by the L0 finalize) and the pencil
+    // failure key (ints 6-7), fetched with one copy at the end of the graph
+    int* ret = c->arena.get<int>("l0.state", 8);
+    auto* fk = reinterpret_cast<unsigned long long*>(ret + 6);
     if (periodic) {
         out.out0 = c->arena.get<double>("core.H", p.nblocks * mm);
         out.out1 = c->arena.get<double>("core.S", p.nblocks * mm);
@@ -1164,10 +1223,16 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
         out.out1 = c->arena.get<double>("core.S", p.Nb * p.Nb);
     }
     const bool small_box = !periodic && p.Nb <= 32;
+    const bool inline_readback = periodic || small_box;  // no host step after the graph
+    const size_t ebytes = sizeof(double) * (periodic ? p.K * p.m0 : p.Nb);
+    void* epin = eig_host ? c->stage_alloc(ebytes) : nullptr;  // pinned: capturable copy target
+    int* rpin = c->pinned_state();
     const int64_t* s0d = cp.s0d;
     const DftPrep& dp = cp.dp;
-    // device work after L0: kernels and memsets only
+    // device work after L0 (with L0 in front under speculation): kernels and memsets only
     auto enqueue = [&]() {
+        if (spec) l0w.enqueue(c->L(), 1, static_cast<int>(L0) + 3, true);
+        LT_CU(cudaMemsetAsync(fk, 0xff, sizeof(unsigned long long), c->stream));
         run_assembly(c, sd, p, NEED_MS | NEED_NUC, 0, out, nullptr, s0d);
         if (periodic) {
             int wrapped = 0, ax = -1;
@@ -1205,23 +1270,36 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
         } else if (small_box) {
             box_eig_device(c, p.Nb, out.out0, out.out1, eig_dev, fk);
         }
+        if (inline_readback) {
+            LT_CU(cudaMemcpyAsync(rpin, ret, 8 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+            if (epin) LT_CU(cudaMemcpyAsync(epin, eig_dev, ebytes, cudaMemcpyDeviceToHost, c->stream));
+        }
     };
     c->phase_mark(2);
+    c->host_mark(1);
     run_cached(
-        c, c->coregraph,
-        [&]() { return graph_key(sd->hs, p, periodic, k_begin, k_end, eig_dev, sd->mem, c->arena.generation()); },
+        c, spec ? c->fullgraph : c->coregraph,
+        [&]() {
+            auto k = graph_key(sd->hs, p, periodic, k_begin, k_end, eig_dev, sd->mem, c->arena.generation());
+            k.push_back(spec ? 1 : 0);
+            k.push_back(reinterpret_cast<int64_t>(epin));
+            k.push_back(reinterpret_cast<int64_t>(rpin));
+            return k;
+        },
         enqueue);
-    if (!periodic && !small_box) box_eig_device(c, p.Nb, out.out0, out.out1, eig_dev, fk);
+    if (!inline_readback) {
+        box_eig_device(c, p.Nb, out.out0, out.out1, eig_dev, fk);
+        LT_CU(cudaMemcpyAsync(rpin, ret, 8 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        if (epin) LT_CU(cudaMemcpyAsync(epin, eig_dev, ebytes, cudaMemcpyDeviceToHost, c->stream));
+    }
     c->phase_mark(3);
     // one synchronisation for the failure key, the L0 state and (host API) the eigenvalues
-    const size_t ebytes = sizeof(double) * (periodic ? p.K * p.m0 : p.Nb);
-    void* epin = eig_host ? c->stage_alloc(ebytes) : nullptr;
-    if (eig_host) LT_CU(cudaMemcpyAsync(epin ? epin : eig_host, eig_dev, ebytes, cudaMemcpyDeviceToHost, c->stream));
-    auto* fpin = static_cast<unsigned long long*>(c->stage_alloc(sizeof(unsigned long long)));
-    unsigned long long fkey = ~0ull;
-    LT_CU(cudaMemcpyAsync(fpin ? fpin : &fkey, fk, sizeof(fkey), cudaMemcpyDeviceToHost, c->stream));
+    if (eig_host && !epin) LT_CU(cudaMemcpyAsync(eig_host, eig_dev, ebytes, cudaMemcpyDeviceToHost, c->stream));
+    c->host_mark(2);
     LT_CU(cudaStreamSynchronize(c->stream));
-    if (fpin) fkey = *fpin;
+    c->host_mark(3);
+    unsigned long long fkey;
+    std::memcpy(&fkey, rpin + 6, sizeof(fkey));
     cp.epoch = c->prep_epoch;
     cp.gen = c->arena.generation();
     cp.valid = true;
@@ -1247,6 +1325,8 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
         info[6] = p.K;
         info[7] = fkey == ~0ull ? -1 : static_cast<int64_t>(fkey);
     }
+    c->host_mark(4);
+    c->host_collect();
     raise_fail_key(fkey, periodic);
 }
 
@@ -1499,6 +1579,8 @@ lt_status lt_create(int device, lt_ctx** out) {
         for (auto& e : c->ev) LT_CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         const char* pt = std::getenv("LT_PHASE_TIMING");
         c->phase_timing = pt && pt[0] == '1';
+        const char* ht = std::getenv("LT_HOST_TIMING");
+        c->host_timing = ht && ht[0] == '1';
         if (c->phase_timing)
             for (auto& e : c->pev) LT_CU(cudaEventCreate(&e));
         *out = c.release();
@@ -1507,6 +1589,14 @@ lt_status lt_create(int device, lt_ctx** out) {
 
 void lt_destroy(lt_ctx* c) {
     if (!c) return;
+    if (c->host_timing && c->host_n)
+        std::fprintf(stderr,
+                     "host timing over %lld solves (us): prep %.2f launch %.2f (key %.2f, cudaGraphLaunch %.2f) "
+                     "wait %.2f finish %.2f; run_cached replay %lld capture %lld eager %lld\n",
+                     static_cast<long long>(c->host_n), c->host_acc[0] / c->host_n, c->host_acc[1] / c->host_n,
+                     c->key_us / c->host_n, c->graph_launch_us / c->host_n, c->host_acc[2] / c->host_n,
+                     c->host_acc[3] / c->host_n, static_cast<long long>(c->n_replay),
+                     static_cast<long long>(c->n_capture), static_cast<long long>(c->n_eager));
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->solver) cusolverDnDestroy(c->solver);

@@ -21,6 +21,8 @@ struct FillDev {
     const double* T[3];
     const double* potw;
     const double* N;
+    const double* Npart;
+    Index Nres, Nnd;
     int s2_dir, mode, periodic, nuc_mode;
     double* out0;
     double* out1;
@@ -70,7 +72,16 @@ __global__ void k_fill(FillDev f) {
             lap = __dadd_rn(__dadd_rn(t0, t1), t2);
         }
         if (want_nuc) {
-            if (f.nuc_mode == 1) {
+            if (f.nuc_mode == 1 && f.Npart) {
+                // periodic residue-fold partials summed here in t order (d < 0: the
+                // (mu,nu)-transposed mirror of |d|)
+                const int l = f.s2_dir;
+                const Index ad = d[l] < 0 ? -d[l] : d[l];
+                const Index ee = d[l] < 0 ? (e / f.m0) + (e % f.m0) * f.m0 : e;
+                double acc = 0.0;
+                for (Index t = 0; t < f.Nres; ++t) acc += f.Npart[(t * f.Nnd + ad) * mm + ee];
+                nuc = acc;
+            } else if (f.nuc_mode == 1) {
                 const int l = f.s2_dir;
                 nuc = f.N[(k[l] * f.width[l] + d[l] + f.band[l]) * mm + e];
             } else if (f.nuc_mode == 2) {
@@ -123,6 +134,9 @@ void launch_fill(const Launch& L, const FillArgs& a, Index Nb, Index nblocks) {
     }
     f.potw = a.potw;
     f.N = a.N;
+    f.Npart = a.Npart;
+    f.Nres = a.Nres;
+    f.Nnd = a.Nnd;
     f.s2_dir = a.s2_dir;
     f.nuc_mode = a.nuc_mode;
     f.mode = a.mode;

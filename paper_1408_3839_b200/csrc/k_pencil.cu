@@ -404,6 +404,9 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
         sm.scal[0] = lo - wid;
         sm.scal[1] = hi + wid;
         sm.scal[2] = 2.2250738585072014e-308 * fmax(1.0, emax);
+        // absolute tolerance ulp * ||T|| (LAPACK dstebz's default ABSTOL): eigenvalues near
+        // zero stop at the normwise-backward-stable accuracy instead of chasing relative ulps
+        sm.scal[3] = 2.2e-16 * fmax(fabs(lo), fabs(hi));
     }
     gsync<G>(slot);
     PPROF(5);
@@ -413,6 +416,7 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
     int P = 1;
     while (P * 2 <= 32 && P * 2 * n <= G) P *= 2;
     const double pivmin = sm.scal[2];
+    const double atol = sm.scal[3];
     const int per_round = G / P;  // eigenvalues handled concurrently
     const double inv_pts = 1.0 / static_cast<double>(P * Q + 1);
     for (int base = 0; base < n; base += per_round) {
@@ -461,7 +465,7 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
                 na = last;  // every shift is below the eigenvalue
                 nb = b;
             }
-            const bool done = !(nb - na > 2.2e-16 * fmax(fabs(na), fabs(nb))) || (na == a && nb == b);
+            const bool done = !(nb - na > 2.2e-16 * fmax(fabs(na), fabs(nb)) + atol) || (na == a && nb == b);
             a = na;
             b = nb;
             if (__all_sync(0xffffffffu, done || !active)) break;

@@ -18,11 +18,14 @@
 
 namespace lt {
 
-__global__ void k_master(Index mrows, double h, Index RN, const double* __restrict__ t, double* __restrict__ out) {
+// t == null: the node t_q is evaluated in place (sinc_node, k_sinc's arithmetic), so the
+// master does not wait for the sinc kernel
+__global__ void k_master(Index mrows, double h, Index RN, const double* __restrict__ t, int M,
+                         double* __restrict__ out) {
     const Index j = static_cast<Index>(blockIdx.x) * blockDim.x + threadIdx.x;
     const Index q = blockIdx.y;
     if (j >= mrows) return;
-    out[q * mrows + j] = master_cell(j, mrows, h, t[q]);
+    out[q * mrows + j] = master_cell(j, mrows, h, t ? t[q] : sinc_node(static_cast<int>(q), M));
 }
 
 // the sinc nodes alone (k_sinc's t_q), for the master panel of a long lattice sum
@@ -37,10 +40,10 @@ void launch_sinc_nodes(const Launch& L, Index M, double* t) {
     L.tick();
 }
 
-void launch_master(const Launch& L, Index mrows, double h, Index RN, const double* t, double* out) {
+void launch_master(const Launch& L, Index mrows, double h, Index RN, const double* t, double* out, Index M) {
     dim3 grid(static_cast<unsigned>((mrows + 255) / 256), static_cast<unsigned>(RN));
     Stage st_(L, "master");
-    k_master<<<grid, 256, 0, L.st>>>(mrows, h, RN, t, out);
+    k_master<<<grid, 256, 0, L.st>>>(mrows, h, RN, t, static_cast<int>(M), out);
     LT_CU(cudaGetLastError());
     L.tick();
 }
@@ -82,6 +85,26 @@ __global__ void k_window_sum_uniform(Src src, Index RN, Index nnuc, const Index*
     }
 }
 
+// size <= step (the periodic cell window: every residue class holds one output): no
+// running-sum recurrence, so the K-term sum of each output is split over a warp
+// (lane-strided partial sums, then a fixed shuffle tree) instead of one serial chain
+template <class Src>
+__global__ void k_window_sum_short(Src src, Index RN, Index nnuc, const Index* __restrict__ s0v, Index K, Index step,
+                                   Index size, double* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const Index w = (static_cast<Index>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (w >= nnuc * RN * size) return;
+    const Index r = w % size;
+    const Index q = (w / size) % RN;
+    const Index v = w / (size * RN);
+    const double tq = src.tq(q);
+    const Index s0 = s0v[v];
+    double acc = 0.0;
+    for (Index k = lane; k < K; k += 32) acc += src(s0 + r + k * step, q, tq);
+    acc = warp_sum(acc);
+    if (lane == 0) out[(v * RN + q) * size + r] = acc;
+}
+
 // single shift (non-uniform branch with one window): out = 0 + m[s0 + i]
 template <class Src>
 __global__ void k_window_copy(Src src, Index RN, Index nnuc, const Index* __restrict__ s0v, Index size,
@@ -97,7 +120,11 @@ template <class Src>
 static void window_sum(const Launch& L, const Src& src, Index RN, Index nnuc, const Index* s0_dev, Index nsum,
                        Index step, Index size, double* out) {
     Stage st_(L, "window_sum");
-    if (nsum >= 2) {
+    if (nsum >= 32 && size <= step) {
+        const Index warps = nnuc * RN * size;
+        k_window_sum_short<<<static_cast<unsigned>((warps + 7) / 8), 256, 0, L.st>>>(src, RN, nnuc, s0_dev, nsum, step,
+                                                                                     size, out);
+    } else if (nsum >= 2) {
         const Index nres = std::min(step, size);
         const Index threads = nnuc * RN * nres;
         k_window_sum_uniform<<<static_cast<unsigned>((threads + 127) / 128), 128, 0, L.st>>>(src, RN, nnuc, s0_dev,

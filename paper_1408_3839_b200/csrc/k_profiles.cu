@@ -66,6 +66,16 @@ __global__ void k_profile_trim(ProfileJobs jobs) {
     }
 }
 
+// support bounds of every job reset in one launch (lo = all ones, hi = 0): a memset per
+// array would put 2 x njobs serial graph nodes in front of the sampling
+__global__ void k_profile_bounds_init(ProfileJobs jobs, int njobs, Index m0) {
+    for (int k = 0; k < njobs; ++k)
+        for (Index mu = threadIdx.x; mu < m0; mu += blockDim.x) {
+            jobs.j[k].lo[mu] = ~0ull;
+            jobs.j[k].hi[mu] = 0ull;
+        }
+}
+
 void launch_profiles(const Launch& L, const DevSys& s, const ProfileJob* jobs, int njobs, double eps) {
     if (njobs > kMaxProfileJobs) fail(LT_EGENERIC, "launch_profiles: too many jobs");
     ProfileJobs pj{};
@@ -73,17 +83,17 @@ void launch_profiles(const Launch& L, const DevSys& s, const ProfileJob* jobs, i
     for (int k = 0; k < njobs; ++k) {
         pj.j[k] = jobs[k];
         gmax = std::max(gmax, jobs[k].grid);
-        LT_CU(cudaMemsetAsync(jobs[k].lo, 0xff, sizeof(unsigned long long) * s.m0, L.st));
-        LT_CU(cudaMemsetAsync(jobs[k].hi, 0x00, sizeof(unsigned long long) * s.m0, L.st));
     }
     dim3 grid(static_cast<unsigned>((gmax + 255) / 256), s.m0, njobs);
     Stage st_(L, "profiles");
+    k_profile_bounds_init<<<1, 64, 0, L.st>>>(pj, njobs, s.m0);
+    LT_CU(cudaGetLastError());
     k_profile_sample<<<grid, 256, 0, L.st>>>(s, pj, eps);
     LT_CU(cudaGetLastError());
     // trimming depends on the complete bounds: second pass (stream-ordered)
     k_profile_trim<<<grid, 256, 0, L.st>>>(pj);
     LT_CU(cudaGetLastError());
-    L.tick(2);
+    L.tick(3);
 }
 
 // ---------------------------------------------------------------------------

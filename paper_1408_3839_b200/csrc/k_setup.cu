@@ -282,43 +282,55 @@ void launch_overlap_scan(const Launch& L, const DevSys& s, const Index* n3, cons
 // around it, evaluated with the same device arithmetic as the sampled scan, yields the
 // scan's maximum (neighbouring products differ by a relative (alpha+beta) h^2 >> ulp).
 // A window maximum just below eps (relative 1e-12) is re-checked by a full scan of that
-// (s, mu, nu), so the decision equals the exhaustive one. One thread per (s, l, mu, nu);
+// (s, mu, nu), so the decision equals the exhaustive one. Eight lanes per (s, l, mu, nu);
 // the last CTA applies the sequential rule when `finalize`.
 __global__ void k_l0_peak(DevSys s, Dir3 d, int* found, int* state, int s_begin, int ns, int s_end, int finalize) {
-    const Index task = static_cast<Index>(blockIdx.x) * blockDim.x + threadIdx.x;
+    // 8 lanes per (s, l, mu, nu): one window point each, max by shuffles within the group
+    const Index gtid = static_cast<Index>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const Index task = gtid >> 3;
+    const int sub = static_cast<int>(threadIdx.x & 7);
     const Index m0 = s.m0;
     const Index per_s = static_cast<Index>(d.nl) * m0 * m0;
-    if (task < per_s * ns) {
-        const int sft = s_begin + static_cast<int>(task / per_s);
+    bool valid = task < per_s * ns;
+    int sft = 0, l = 0, mu = 0, nu = 0;
+    Index base = 0, sn = 0, lo = 0, hi = -1, i0 = 0;
+    double h = 1.0;
+    if (valid) {
+        sft = s_begin + static_cast<int>(task / per_s);
         Index rem = task % per_s;
-        const int l = d.dir[rem / (m0 * m0)];
+        l = d.dir[rem / (m0 * m0)];
         rem %= m0 * m0;
-        const int mu = static_cast<int>(rem / m0), nu = static_cast<int>(rem % m0);
+        mu = static_cast<int>(rem / m0);
+        nu = static_cast<int>(rem % m0);
         const Index n = d.n[l];
-        const Index base = (kMaxL0 + 2) * n, width = 2 * base, sn = static_cast<Index>(sft) * n;
-        if (!__ldcg(&found[sft]) && sn < width) {
-            const double h = s.b / static_cast<double>(n);
+        base = (kMaxL0 + 2) * n;
+        const Index width = 2 * base;
+        sn = static_cast<Index>(sft) * n;
+        valid = !__ldcg(&found[sft]) && sn < width;
+        if (valid) {
+            h = s.b / static_cast<double>(n);
             const double al = s.alpha[mu], be = s.alpha[nu];
             const double xs = (al * s.center[3 * mu + l] + be * (s.center[3 * nu + l] + sft * s.b)) / (al + be);
             const double is = (xs + 0.5 * s.b) / h + static_cast<double>(base) - 0.5;
-            const Index lo = sn, hi = width - 1;  // j = i - sn >= 0
+            lo = sn;
+            hi = width - 1;  // j = i - sn >= 0
             const double isc = fmin(fmax(is, static_cast<double>(lo)), static_cast<double>(hi));
-            Index i0 = static_cast<Index>(floor(isc)) - 3;
+            i0 = static_cast<Index>(floor(isc)) - 3;
             i0 = max(lo, min(i0, hi - 7));
-            const Index i1 = min(hi, i0 + 7);
-            double best = 0.0;
-            for (Index i = i0; i <= i1; ++i) {
-                const double a = gto_eval1d(s, mu, l, l0_x(i, base, h, s.b));
-                const double c = gto_eval1d(s, nu, l, l0_x(i - sn, base, h, s.b));
-                best = fmax(best, fabs(a * c));
-            }
-            bool hit = best >= s.eps_ov;
-            if (!hit && best >= s.eps_ov * (1.0 - 1e-12))  // at the threshold: exhaustive
-                for (Index i = lo; i <= hi && !hit; ++i)
-                    hit = fabs(gto_eval1d(s, mu, l, l0_x(i, base, h, s.b)) *
-                               gto_eval1d(s, nu, l, l0_x(i - sn, base, h, s.b))) >= s.eps_ov;
-            if (hit) atomicExch(&found[sft], 1);
         }
+    }
+    double p = 0.0;
+    const Index i = i0 + sub;
+    if (valid && i <= hi)
+        p = fabs(gto_eval1d(s, mu, l, l0_x(i, base, h, s.b)) * gto_eval1d(s, nu, l, l0_x(i - sn, base, h, s.b)));
+    for (int o = 4; o > 0; o >>= 1) p = fmax(p, __shfl_xor_sync(0xffffffffu, p, o));
+    if (valid && sub == 0) {
+        bool hit = p >= s.eps_ov;
+        if (!hit && p >= s.eps_ov * (1.0 - 1e-12))  // at the threshold: exhaustive
+            for (Index k = lo; k <= hi && !hit; ++k)
+                hit = fabs(gto_eval1d(s, mu, l, l0_x(k, base, h, s.b)) *
+                           gto_eval1d(s, nu, l, l0_x(k - sn, base, h, s.b))) >= s.eps_ov;
+        if (hit) atomicExch(&found[sft], 1);
     }
     if (!finalize) return;
     __shared__ bool last;
@@ -341,7 +353,7 @@ void launch_overlap_peak(const Launch& L, const DevSys& s, const Index* n3, cons
     const Dir3 d = make_dir3(s, n3, zero3, zero3, active);
     const int ns = s_end - s_begin;
     const Index tasks = static_cast<Index>(ns) * d.nl * s.m0 * s.m0;
-    const Index blocks = std::max<Index>(1, (tasks + 127) / 128);
+    const Index blocks = std::max<Index>(1, (8 * tasks + 127) / 128);
     Stage st_(L, "l0_peak");
     k_l0_peak<<<static_cast<unsigned>(blocks), 128, 0, L.st>>>(s, d, b.found, b.state, s_begin, ns, s_end,
                                                               finalize ? 1 : 0);

@@ -218,7 +218,8 @@ void launch_overlap_peak(const Launch& L, const DevSys& s, const Index* n3, cons
 void launch_overlap_init(const Launch& L, OverlapBufs b, int m0);
 
 // master tensor (newton_kernel.cpp:22-45) and assembled window sums (canonical_tensor.cpp:123-164)
-void launch_master(const Launch& L, Index mrows, double h, Index RN, const double* t, double* out);
+// t == null: nodes evaluated in place from M (no dependency on the sinc kernel)
+void launch_master(const Launch& L, Index mrows, double h, Index RN, const double* t, double* out, Index M = 0);
 void launch_sinc_nodes(const Launch& L, Index M, double* t);
 // window sums with the master cells evaluated in place (no master panel)
 void launch_potential_fused(const Launch& L, Index mrows, double h, Index M, Index RN, Index nnuc, const Index* s0_dev,
@@ -340,6 +341,9 @@ struct FillArgs {
     const double* T[3]{};      // nuclear tables [pair][r][e]
     const double* potw = nullptr;
     const double* N = nullptr; // nuclear blocks: [k][d][e] along s2_dir, or [dlin][e] (nuc_mode 2)
+    // periodic nuc_mode 1 without the reduce launch: N[d][e] = sum_t Npart[t][|d|][e or e^T]
+    const double* Npart = nullptr;
+    Index Nres = 0, Nnd = 0;
     int s2_dir = -1;
     int nuc_mode = 0;          // 0 tables, 1 N along s2_dir, 2 N by dlin
     int mode = 0;

@@ -55,7 +55,7 @@ static void run(int count, int m0, int reps) {
     for (int r = 0; r < reps; ++r) {
         cudaMemset(fk, 0xff, sizeof(unsigned long long));
         cudaEventRecord(e0);
-        lt::k_pencil<NM, G, BS><<<blocks, BS, smem>>>(count, m0, dH, dS, de, fk, 1);
+        lt::k_pencil<NM, G, BS><<<blocks, BS, smem>>>(count, m0, dH, dS, de, fk, 1, lt::PencilDft{});
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms;
