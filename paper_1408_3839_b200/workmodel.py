@@ -71,13 +71,19 @@ def stage_work(ctx, s, periodic: bool, L0: int) -> Dict[str, Tuple[str, float, s
         else:
             out[name] = (bound, float(amount), unit)
 
-    # ---- L0: profiles on the 2*258*n grid (non-zero values written once, read once by the scan)
-    l0_nz = 0
+    # ---- L0
+    # s-type directions take the peak-window search (16 profile evaluations per task,
+    # latency-bound; counted as its 8-byte result reads), p-type ones sample and scan
+    ntask = 0
     for l in uniq:
-        lo, hi = sup[("pwc", l)]
-        l0_nz += int(np.sum(hi - lo))
-    add("l0_sample", "hbm", 8.0 * l0_nz, "B")
-    add("l0_scan", "hbm", 8.0 * l0_nz, "B")
+        if np.all(s.bf_deg[:, l] == 0):
+            ntask += (L0 + 2) * m0 * m0
+        else:
+            lo, hi = sup[("pwc", l)]
+            add("l0_sample", "hbm", 8.0 * float(np.sum(hi - lo)), "B")
+            add("l0_scan", "hbm", 8.0 * float(np.sum(hi - lo)), "B")
+    if ntask:
+        add("l0_peak", "hbm", 8.0 * ntask, "B")
     # ---- sinc + lattice-summed potential: master written, master read + windows written
     add("sinc", "hbm", 8.0 * (2 * RN + Rtot), "B")
     for l in uniq:
@@ -168,8 +174,8 @@ def stage_work(ctx, s, periodic: bool, L0: int) -> Dict[str, Tuple[str, float, s
         add("fill", "hbm", 8.0 * 2 * Nb * Nb, "B")
     # ---- spectrum
     if periodic:
-        add("scatter_gen", "hbm", 2 * (8.0 * nblocks * mm + 16.0 * K * mm), "B")
-        add("twiddles", "hbm", 16.0 * sum(s.L[l] * s.L[l] for l in wrapped_dirs), "B")
+        # per transformed axis, H and S: read + write K m0^2 complex (single-axis transforms
+        # small enough are fused into the pencil load: no dft_axis stage then)
         add("dft_axis", "hbm", 2 * 2 * 16.0 * K * mm * len(wrapped_dirs), "B")
         add("pencil", "hbm", K * (2 * 16.0 * mm + 8.0 * m0), "B")
     else:
