@@ -751,6 +751,9 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
             f.res[0] = w.massT[l];
             f.res[1] = w.stiffT[l];
             f.slab = f.J <= kResfoldDirectJ ? nullptr : A.get<double>("fem.slab" + std::to_string(l), resfold_slab_doubles(f));
+            f.sup_lo = w.pwl_lo[l];  // b = T v: one point wider on each side
+            f.sup_hi = w.pwl_hi[l];
+            f.bwiden = 1;
             launch_resfold(LF, f, true, true, "fem_fold");
         }
     }
@@ -827,13 +830,23 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
                     f.dlo = 0;
                     f.dhi = f.band;
                     f.dchunk = std::max(1, (f.band + 1 + 3) / 4);
-                    f.W = W;
-                    f.P = w.pot[ndir];
-                    f.Rtot = static_cast<int>(Rtot);
-                    f.prow = d.pot_rows;
+                    if (mm * Rtot <= 8192) {
+                        // small W: every fold CTA forms its residue's V column itself
+                        f.W = W;
+                        f.P = w.pot[ndir];
+                        f.Rtot = static_cast<int>(Rtot);
+                        f.prow = d.pot_rows;
+                    } else {
+                        // large W (read by every CTA otherwise): V once, then the weighted fold
+                        double* V = A.get<double>("nuc.V", mm * d.pot_rows);
+                        launch_vdot(L, static_cast<int>(mm), static_cast<int>(Rtot), d.pot_rows, W, w.pot[ndir], V);
+                        f.V = V;
+                    }
                     f.out[0] = A.get<double>("nuc.fpart", d.n * (d.band + 1) * mm);
                     f.res[0] = w.N;
                     f.slab = f.J <= kResfoldDirectJ ? nullptr : A.get<double>("nuc.slab", resfold_slab_doubles(f));
+                    f.sup_lo = w.pwc_lo[ndir];
+                    f.sup_hi = w.pwc_hi[ndir];
                     if (f.n <= 32) {
                         // few residues: the fill sums them (no reduce launch)
                         launch_resfold(L, f, false, false, "nuc_fold");
@@ -872,6 +885,8 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
                         f.dchunk = std::max(1, (f.band + 1 + 3) / 4);
                         f.out[0] = Qf;  // [t][d][e]
                         f.slab = f.J <= kResfoldDirectJ ? nullptr : A.get<double>("nuc.slab" + std::to_string(s), resfold_slab_doubles(f));
+                        f.sup_lo = w.pwc_lo[s];
+                        f.sup_hi = w.pwc_hi[s];
                         launch_resfold(L, f, false, false, "nuc_fold");
                         launch_fgemm(L, static_cast<int>(m0), static_cast<int>(Rtot), d, w.pot[s], Qf, Tl[s]);
                     }
@@ -1574,8 +1589,14 @@ lt_status lt_create(int device, lt_ctx** out) {
         auto c = std::make_unique<lt_ctx>();
         c->device = device;
         LT_CU(cudaSetDevice(device));
-        LT_CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-        for (auto& a : c->aux) LT_CU(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
+        // priorities: the main stream carries the critical path (potential -> nuclear chain ->
+        // fill -> pencils); side branch 0 (profiles -> FEM folds) has slack and, its folds
+        // filling every SM's shared memory, must not hold SMs the main stream waits for
+        int prio_lo = 0, prio_hi = 0;
+        LT_CU(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+        LT_CU(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi));
+        LT_CU(cudaStreamCreateWithPriority(&c->aux[0], cudaStreamNonBlocking, prio_lo));
+        LT_CU(cudaStreamCreateWithPriority(&c->aux[1], cudaStreamNonBlocking, prio_hi));
         for (auto& e : c->ev) LT_CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         const char* pt = std::getenv("LT_PHASE_TIMING");
         c->phase_timing = pt && pt[0] == '1';

@@ -14,6 +14,8 @@
 // T = tridiag{lo, diag, lo}; each row value (T v)_i equals the reference's `row`
 // bit for bit (absent neighbours add +0.0), so every term u_i * row_i is the
 // reference's term; only the summation order differs.
+#include <cstdlib>
+
 #include "dmma.cuh"
 #include "lt_device.cuh"
 #include "lt_internal.cuh"
@@ -186,14 +188,46 @@ __global__ void __launch_bounds__(256) k_resfold(ResFold f) {
     const int mm = f.m0 * f.m0;
     // j - d must stay in the stored range: [0, J) or, with guards, [-1, J]
     const int glo = f.bguard ? -1 : 0, ghi = f.bguard ? J + 1 : J;
+    // per 8-function tile: the j range of residue t where some function of the tile is
+    // non-zero (a side: t + j n in [lo, hi); b side: t + j' n in [lo - w, hi + w))
+    __shared__ int tja[2][4], tjb[2][4];
+    __shared__ long long slo[32], shi[32];
+    if (f.sup_lo && threadIdx.x < f.m0) {  // all supports in one round of loads
+        slo[threadIdx.x] = static_cast<long long>(f.sup_lo[threadIdx.x]);
+        shi[threadIdx.x] = static_cast<long long>(f.sup_hi[threadIdx.x]);
+    }
+    __syncthreads();
+    if (threadIdx.x < 2 * ntile && threadIdx.x < 8) {
+        const int side = threadIdx.x / ntile, tile = threadIdx.x % ntile;
+        int jl = 1 << 30, jh = -(1 << 30);
+        if (f.sup_lo) {
+            const long long w = side ? f.bwiden : 0;
+            for (int u = 0; u < 8; ++u) {
+                const int mu = tile * 8 + u;
+                if (mu >= f.m0) break;
+                if (slo[mu] >= shi[mu]) continue;
+                const long long lo = slo[mu] - w;
+                const long long hi = shi[mu] + w;
+                auto cdiv = [&](long long x) { return x >= 0 ? (x + f.n - 1) / f.n : -((-x) / f.n); };
+                jl = min(jl, static_cast<int>(cdiv(lo - t)));
+                jh = max(jh, static_cast<int>(cdiv(hi - t)));
+            }
+        } else {
+            jl = -1;
+            jh = J + 1;
+        }
+        (side ? tjb : tja)[0][tile] = jl;
+        (side ? tjb : tja)[1][tile] = jh;
+    }
+    __syncthreads();
     for (int task = warp; task < tasks; task += blockDim.x >> 5) {
         const int d = dlo + task / (ntile * ntile);
         const int mt = (task / ntile) % ntile, nt = task % ntile;
         double c0[NB][2], c1[NB][2];
 #pragma unroll
         for (int q = 0; q < NB; ++q) c0[q][0] = c0[q][1] = c1[q][0] = c1[q][1] = 0.0;
-        const int j0 = max(0, d + glo);
-        const int j1 = min(J, d + ghi);
+        const int j0 = max(max(0, d + glo), max(tja[0][mt], tjb[0][nt] + d));
+        const int j1 = max(j0, min(min(J, d + ghi), min(tja[1][mt], tjb[1][nt] + d)));
         const double* ap = As + (mt * 8 + g) * ldj + j0 + tq;
         const double* bp = Bs + (nt * 8 + g) * ldj + j0 + tq - d + 1;
         const int steps = (j1 - j0 + 3) >> 2;
@@ -249,7 +283,13 @@ __global__ void k_resfold_reduce(ResFold f, int mirror) {
     }
 }
 
-void launch_resfold(const Launch& L, const ResFold& f, bool reduce, bool mirror, const char* name) {
+void launch_resfold(const Launch& L, const ResFold& f_in, bool reduce, bool mirror, const char* name) {
+    ResFold f = f_in;
+    static const bool no_sup = [] {
+        const char* e = std::getenv("LT_FOLD_NO_SUPPORT");
+        return e && e[0] == '1';
+    }();
+    if (no_sup) f.sup_lo = f.sup_hi = nullptr;
     const int m0p = (f.m0 + 7) / 8 * 8;
     const size_t mme = static_cast<size_t>(f.m0) * f.m0;
     const size_t vparts = f.W ? std::max<size_t>(1, 256 / mme) : 0;

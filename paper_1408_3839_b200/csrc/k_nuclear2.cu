@@ -39,13 +39,16 @@ __device__ __forceinline__ void sym_pair(int es, int m0, int& mu, int& nu) {
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_triv_gemm(TrivJobs jobs, int m0, int Rtot, int nsym, int splits,
                                                    double* __restrict__ part) {
-    __shared__ GemmSmem sm;
+    __shared__ double As[kGBM * kGLDA];   // potential rows [64][16 + pad]
+    __shared__ double Gs[32 * 17];        // profile rows of all functions [m0 <= 32][16 + 1]
     const int job = blockIdx.z / splits, split = blockIdx.z % splits;
     const TrivJob& J = jobs.j[job];
     const int r0 = blockIdx.x * kGBM, e0 = blockIdx.y * kGBN;
     // union of the supports (products vanish outside every pair's overlap): one parallel
     // load per function and a warp reduction instead of a serial chain of m0 loads
     __shared__ long long sk[2];
+    __shared__ double tqs[kGBM];    // in-place potential: t_q of each tile row
+    __shared__ long long s0s[kGBM];  // and its window start s0[v]
     if (threadIdx.x < 32) {
         long long lo = J.G, hi = 0;
         for (int m = threadIdx.x; m < m0; m += 32) {
@@ -61,20 +64,7 @@ __global__ void __launch_bounds__(256) k_triv_gemm(TrivJobs jobs, int m0, int Rt
             sk[1] = hi;
         }
     }
-    __syncthreads();
-    const long long klo = sk[0];
-    const long long khi = min(sk[1], static_cast<long long>(J.rows));
-    const long long len = khi > klo ? khi - klo : 0;
-    const long long per = ((len + splits - 1) / splits + kGBK - 1) / kGBK * kGBK;
-    const long long k0 = klo + split * per, k1 = min(khi, k0 + per);
-    __shared__ int smu[64], snu[64];
-    __shared__ double tqs[kGBM];    // in-place potential: t_q of each tile row
-    __shared__ long long s0s[kGBM];  // and its window start s0[v]
-    if (threadIdx.x < 64) {
-        int mu = 0, nu = 0;
-        if (e0 + static_cast<int>(threadIdx.x) < nsym) sym_pair(e0 + threadIdx.x, m0, mu, nu);
-        smu[threadIdx.x] = mu;
-        snu[threadIdx.x] = nu;
+    if (threadIdx.x < kGBM) {
         const int r = r0 + static_cast<int>(threadIdx.x);
         if (!J.pot && r < Rtot) {
             tqs[threadIdx.x] = sinc_node(r % J.RN, J.M);
@@ -82,20 +72,78 @@ __global__ void __launch_bounds__(256) k_triv_gemm(TrivJobs jobs, int m0, int Rt
         }
     }
     __syncthreads();
+    const long long klo = sk[0];
+    const long long khi = min(sk[1], static_cast<long long>(J.rows));
+    const long long len = khi > klo ? khi - klo : 0;
+    const long long per = ((len + splits - 1) / splits + kGBK - 1) / kGBK * kGBK;
+    const long long k0 = klo + split * per, k1 = min(khi, k0 + per);
     const double* P = J.pot;
     const double* g = J.pwc;
     const long long G = J.G, rows = J.rows;
-    // A = the potential panel P[r][i], read or (P null) evaluated in place from the master
-    // cells of its window (the panel the window copy would have written, bit for bit)
-    auto loadA = [&](int m, long long k) -> double {
-        if (r0 + m >= Rtot) return 0.0;
-        return P ? P[(r0 + m) * rows + k] : master_cell(s0s[m] + k, J.mrows, J.h, tqs[m]);
-    };
-    auto loadB = [&](long long k, int n) -> double {
-        return e0 + n < nsym ? g[smu[n] * G + k] * g[snu[n] * G + k] : 0.0;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int wm = warp & 3, wn = warp >> 2, gg = lane >> 2, tq = lane & 3;
+    // this lane's four B columns: symmetric pairs (mu, nu) of the tile (zero beyond nsym)
+    int cmu[4], cnu[4];
+    bool cok[4];
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+        const int es = e0 + wn * 32 + nt * 8 + gg;
+        cok[nt] = es < nsym;
+        int mu = 0, nu = 0;
+        if (cok[nt]) sym_pair(es, m0, mu, nu);
+        cmu[nt] = mu;
+        cnu[nt] = nu;
+    }
+    double ra[4], rg[2];
+    auto fetch = [&](long long kb) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = tid + 256 * u;
+            const int am = e >> 4, ak = e & 15;  // k fastest: contiguous rows of P
+            const long long k = kb + ak;
+            double v = 0.0;
+            if (k < k1 && r0 + am < Rtot)
+                v = P ? P[(r0 + am) * rows + k] : master_cell(s0s[am] + k, J.mrows, J.h, tqs[am]);
+            ra[u] = v;
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int e = tid + 256 * u;
+            const int gm = e >> 4, gk = e & 15;
+            const long long k = kb + gk;
+            rg[u] = (gm < m0 && k < k1) ? g[gm * G + k] : 0.0;
+        }
     };
     double acc[4][4] = {};
-    cta_gemm_64x64(loadA, loadB, k0, k1, acc, sm);
+    if (k0 < k1) {
+        fetch(k0);
+        for (long long kb = k0; kb < k1; kb += kGBK) {
+            __syncthreads();
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = tid + 256 * u;
+                As[(e >> 4) * kGLDA + (e & 15)] = ra[u];
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int e = tid + 256 * u;
+                Gs[(e >> 4) * 17 + (e & 15)] = rg[u];
+            }
+            __syncthreads();
+            if (kb + kGBK < k1) fetch(kb + kGBK);  // next tile's loads overlap the MMAs
+#pragma unroll
+            for (int ks = 0; ks < kGBK; ks += 4) {
+                const double a0 = As[(wm * 16 + gg) * kGLDA + ks + tq];
+                const double a1 = As[(wm * 16 + gg + 8) * kGLDA + ks + tq];
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) {
+                    // B fragment (k = ks + tq, column gg of n-tile nt): g_mu(k) g_nu(k)
+                    const double b0 = cok[nt] ? Gs[cmu[nt] * 17 + ks + tq] * Gs[cnu[nt] * 17 + ks + tq] : 0.0;
+                    dmma_m16n8k4(acc[nt], a0, a1, b0);
+                }
+            }
+        }
+    }
     double* out = part + (static_cast<long long>(job) * splits + split) * Rtot * nsym;
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt)
@@ -109,31 +157,15 @@ __global__ void __launch_bounds__(256) k_triv_gemm(TrivJobs jobs, int m0, int Rt
 
 // W[r][e] = w_r * prod over trivial directions of T_l[r][e] (T_l reduced over splits in
 // fixed order); e over all m0^2 ordered pairs (mirror of the symmetric index)
-// one warp per (r, symmetric pair): split-K partials summed in a fixed lane/tree order
-__global__ void k_triv_reduce_w(const double* __restrict__ part, int njobs, const int* dir_job_unused, WSpec ws,
-                                int m0, int Rtot, int nsym, int splits, const double* __restrict__ potw,
-                                double* __restrict__ W, double* __restrict__ Tout) {
-    const int lane = threadIdx.x & 31;
-    const long long wid = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+__device__ __forceinline__ void triv_finish(const double (&tj)[3], int njobs, const WSpec& ws, int m0, int Rtot, int r,
+                                            int mu, int nu, const double* __restrict__ potw, double* __restrict__ W,
+                                            double* __restrict__ Tout) {
     const int mm = m0 * m0;
-    if (wid >= static_cast<long long>(Rtot) * nsym) return;
-    const int r = static_cast<int>(wid / nsym), es = static_cast<int>(wid % nsym);
-    int mu, nu;
-    sym_pair(es, m0, mu, nu);
-    double tj[3] = {1.0, 1.0, 1.0};
-    for (int j = 0; j < njobs; ++j) {
-        double s = 0.0;
-        for (int sp = lane; sp < splits; sp += 32)
-            s += part[((static_cast<long long>(j) * splits + sp) * Rtot + r) * nsym + es];
-        tj[j] = __shfl_sync(0xffffffffu, warp_sum(s), 0);
-    }
-    if (lane != 0) return;
-    // product in direction order (directions may share a job)
-    double prod = 1.0;
+    double prod = 1.0;  // product in direction order (directions may share a job)
     bool first = true;
     for (int l = 0; l < 3; ++l) {
         if (ws.job_of_dir[l] < 0) continue;
-        const double v = tj[ws.job_of_dir[l]];
+        const double v = ws.job_of_dir[l] == 0 ? tj[0] : (ws.job_of_dir[l] == 1 ? tj[1] : tj[2]);
         prod = first ? v : prod * v;
         first = false;
     }
@@ -142,9 +174,62 @@ __global__ void k_triv_reduce_w(const double* __restrict__ part, int njobs, cons
     W[r * mm + nu + mu * m0] = wv;
     if (Tout)
         for (int j = 0; j < njobs; ++j) {
-            Tout[(static_cast<long long>(j) * Rtot + r) * mm + mu + nu * m0] = tj[j];
-            Tout[(static_cast<long long>(j) * Rtot + r) * mm + nu + mu * m0] = tj[j];
+            const double v = j == 0 ? tj[0] : (j == 1 ? tj[1] : tj[2]);
+            Tout[(static_cast<long long>(j) * Rtot + r) * mm + mu + nu * m0] = v;
+            Tout[(static_cast<long long>(j) * Rtot + r) * mm + nu + mu * m0] = v;
         }
+}
+
+// few outputs, many splits: one warp per (r, symmetric pair), lanes over the splits
+__global__ void k_triv_reduce_w_warp(const double* __restrict__ part, int njobs, WSpec ws, int m0, int Rtot, int nsym,
+                                     int splits, const double* __restrict__ potw, double* __restrict__ W,
+                                     double* __restrict__ Tout) {
+    const int lane = threadIdx.x & 31;
+    const long long wid = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (wid >= static_cast<long long>(Rtot) * nsym) return;
+    const int r = static_cast<int>(wid / nsym), es = static_cast<int>(wid % nsym);
+    int mu, nu;
+    sym_pair(es, m0, mu, nu);
+    double tj[3] = {1.0, 1.0, 1.0};
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        if (j >= njobs) break;
+        double sacc = 0.0;
+        for (int sp = lane; sp < splits; sp += 32)
+            sacc += part[((static_cast<long long>(j) * splits + sp) * Rtot + r) * nsym + es];
+        tj[j] = __shfl_sync(0xffffffffu, warp_sum(sacc), 0);
+    }
+    if (lane == 0) triv_finish(tj, njobs, ws, m0, Rtot, r, mu, nu, potw, W, Tout);
+}
+
+// many outputs: one thread per (r, symmetric pair), consecutive threads over consecutive
+// pairs (each split row read coalesced), four partial sums over the splits
+__global__ void k_triv_reduce_w(const double* __restrict__ part, int njobs, WSpec ws, int m0, int Rtot, int nsym,
+                                int splits, const double* __restrict__ potw, double* __restrict__ W,
+                                double* __restrict__ Tout) {
+    const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (tid >= static_cast<long long>(Rtot) * nsym) return;
+    const int r = static_cast<int>(tid / nsym), es = static_cast<int>(tid % nsym);
+    int mu, nu;
+    sym_pair(es, m0, mu, nu);
+    double tj[3] = {1.0, 1.0, 1.0};
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        if (j >= njobs) break;
+        const double* pj = part + (static_cast<long long>(j) * splits * Rtot + r) * nsym + es;
+        const long long stride = static_cast<long long>(Rtot) * nsym;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int sp = 0;
+        for (; sp + 3 < splits; sp += 4) {
+            s0 += pj[(sp + 0) * stride];
+            s1 += pj[(sp + 1) * stride];
+            s2 += pj[(sp + 2) * stride];
+            s3 += pj[(sp + 3) * stride];
+        }
+        for (; sp < splits; ++sp) s0 += pj[sp * stride];
+        tj[j] = (s0 + s1) + (s2 + s3);
+    }
+    triv_finish(tj, njobs, ws, m0, Rtot, r, mu, nu, potw, W, Tout);
 }
 
 void launch_triv_tables(const Launch& L, const TrivJobs& jobs, int njobs, const WSpec& ws, int m0, int Rtot,
@@ -157,10 +242,14 @@ void launch_triv_tables(const Launch& L, const TrivJobs& jobs, int njobs, const 
         LT_CU(cudaGetLastError());
         L.tick();
     }
-    const long long warps = static_cast<long long>(Rtot) * nsym;
+    const long long outs = static_cast<long long>(Rtot) * nsym;
     Stage st2_(L, "triv_reduce_w");
-    k_triv_reduce_w<<<static_cast<unsigned>((warps + 7) / 8), 256, 0, L.st>>>(part, njobs, nullptr, ws, m0, Rtot,
-                                                                            nsym, splits, potw, W, Tout);
+    if (outs < 8192)
+        k_triv_reduce_w_warp<<<static_cast<unsigned>((outs + 7) / 8), 256, 0, L.st>>>(part, njobs, ws, m0, Rtot, nsym,
+                                                                                      splits, potw, W, Tout);
+    else
+        k_triv_reduce_w<<<static_cast<unsigned>((outs + 127) / 128), 128, 0, L.st>>>(part, njobs, ws, m0, Rtot, nsym,
+                                                                                   splits, potw, W, Tout);
     LT_CU(cudaGetLastError());
     L.tick();
 }
@@ -185,6 +274,33 @@ __global__ void __launch_bounds__(256) k_vgemm(int mm, int Rtot, long long rows,
             acc_coord(nt, i, m, n);
             if (e0 + m < mm && i0 + n < rows) V[(e0 + m) * rows + i0 + n] = acc[nt][i];
         }
+}
+
+// V[e][t] = sum_r W[r][e] P[r][t] for a periodic cell panel (rows = n residues): four
+// lanes per (e, t) split the rank sum (r = lane4, lane4 + 4, ...), combined by shuffles;
+// lanes of a warp cover 8 consecutive e (coalesced W reads, P broadcast)
+__global__ void k_vdot(int mm, int Rtot, long long rows, const double* __restrict__ W, const double* __restrict__ P,
+                       double* __restrict__ V) {
+    const long long gid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int part = static_cast<int>(gid & 3);
+    const long long idx = gid >> 2;
+    const bool ok = idx < static_cast<long long>(mm) * rows;
+    const int e = static_cast<int>(idx % mm);
+    const long long t = idx / mm;
+    double v = 0.0;
+    if (ok)
+        for (int r = part; r < Rtot; r += 4) v = fma(W[r * mm + e], P[r * rows + t], v);
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    if (ok && part == 0) V[static_cast<long long>(e) * rows + t] = v;
+}
+
+void launch_vdot(const Launch& L, int mm, int Rtot, long long rows, const double* W, const double* P, double* V) {
+    const long long tot = 4LL * mm * rows;
+    Stage st_(L, "vgemm");
+    k_vdot<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, L.st>>>(mm, Rtot, rows, W, P, V);
+    LT_CU(cudaGetLastError());
+    L.tick();
 }
 
 void launch_vgemm(const Launch& L, int mm, int Rtot, long long rows, const double* W, const double* P, double* V) {

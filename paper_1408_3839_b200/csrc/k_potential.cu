@@ -86,23 +86,30 @@ __global__ void k_window_sum_uniform(Src src, Index RN, Index nnuc, const Index*
 }
 
 // size <= step (the periodic cell window: every residue class holds one output): no
-// running-sum recurrence, so the K-term sum of each output is split over a warp
-// (lane-strided partial sums, then a fixed shuffle tree) instead of one serial chain
+// running-sum recurrence. CTA = 8 warps over 32 consecutive outputs r (coalesced reads
+// along r); warp w sums the k-slice k = w, w+8, ...; the 8 slice sums are added in warp
+// order (a fixed order, instead of the serial K-term chain)
 template <class Src>
-__global__ void k_window_sum_short(Src src, Index RN, Index nnuc, const Index* __restrict__ s0v, Index K, Index step,
-                                   Index size, double* __restrict__ out) {
-    const int lane = threadIdx.x & 31;
-    const Index w = (static_cast<Index>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    if (w >= nnuc * RN * size) return;
-    const Index r = w % size;
-    const Index q = (w / size) % RN;
-    const Index v = w / (size * RN);
+__global__ void __launch_bounds__(256) k_window_sum_short(Src src, Index RN, Index nnuc, const Index* __restrict__ s0v,
+                                                          Index K, Index step, Index size, double* __restrict__ out) {
+    __shared__ double part[8][33];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const Index rblocks = (size + 31) / 32;
+    const Index col = blockIdx.x / rblocks;  // v*RN + q
+    const Index r = (blockIdx.x % rblocks) * 32 + lane;
+    const Index v = col / RN, q = col % RN;
     const double tq = src.tq(q);
     const Index s0 = s0v[v];
     double acc = 0.0;
-    for (Index k = lane; k < K; k += 32) acc += src(s0 + r + k * step, q, tq);
-    acc = warp_sum(acc);
-    if (lane == 0) out[(v * RN + q) * size + r] = acc;
+    if (r < size)
+        for (Index k = warp; k < K; k += 8) acc += src(s0 + r + k * step, q, tq);
+    part[warp][lane] = acc;
+    __syncthreads();
+    if (warp == 0 && r < size) {
+        double t = part[0][lane];
+        for (int w = 1; w < 8; ++w) t += part[w][lane];
+        out[col * size + r] = t;
+    }
 }
 
 // single shift (non-uniform branch with one window): out = 0 + m[s0 + i]
@@ -121,9 +128,9 @@ static void window_sum(const Launch& L, const Src& src, Index RN, Index nnuc, co
                        Index step, Index size, double* out) {
     Stage st_(L, "window_sum");
     if (nsum >= 32 && size <= step) {
-        const Index warps = nnuc * RN * size;
-        k_window_sum_short<<<static_cast<unsigned>((warps + 7) / 8), 256, 0, L.st>>>(src, RN, nnuc, s0_dev, nsum, step,
-                                                                                     size, out);
+        const Index blocks = nnuc * RN * ((size + 31) / 32);
+        k_window_sum_short<<<static_cast<unsigned>(blocks), 256, 0, L.st>>>(src, RN, nnuc, s0_dev, nsum, step, size,
+                                                                              out);
     } else if (nsum >= 2) {
         const Index nres = std::min(step, size);
         const Index threads = nnuc * RN * nres;

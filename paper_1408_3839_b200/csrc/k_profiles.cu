@@ -33,17 +33,24 @@ __global__ void k_profile_sample(DevSys s, ProfileJobs jobs, double eps) {
         jb.values[mu * jb.grid + i] = v;
         keep = !(fabs(v) < eps);
     }
-    // warp-aggregated support bounds
+    // CTA-aggregated support bounds: warp ballots, then one atomic pair per CTA (thousands
+    // of CTAs hit the same m0 addresses otherwise)
+    __shared__ unsigned long long cta_lo, cta_hi;
+    if (threadIdx.x == 0) {
+        cta_lo = ~0ull;
+        cta_hi = 0ull;
+    }
+    __syncthreads();
     const unsigned mask = __ballot_sync(0xffffffffu, keep);
-    if (mask) {
-        const int lane = threadIdx.x & 31;
-        const Index wbase = i - lane;
-        if (lane == 0) {
-            const Index first = wbase + (__ffs(mask) - 1);
-            const Index last = wbase + (31 - __clz(mask));
-            atomicMin(&jb.lo[mu], static_cast<unsigned long long>(first));
-            atomicMax(&jb.hi[mu], static_cast<unsigned long long>(last + 1));
-        }
+    if (mask && (threadIdx.x & 31) == 0) {
+        const Index wbase = i;  // lane 0's index
+        atomicMin(&cta_lo, static_cast<unsigned long long>(wbase + (__ffs(mask) - 1)));
+        atomicMax(&cta_hi, static_cast<unsigned long long>(wbase + (31 - __clz(mask)) + 1));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && cta_hi > 0) {
+        atomicMin(&jb.lo[mu], cta_lo);
+        atomicMax(&jb.hi[mu], cta_hi);
     }
 }
 

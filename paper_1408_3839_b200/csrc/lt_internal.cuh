@@ -285,6 +285,8 @@ struct KRArgs {
 };
 void launch_triv_tables(const Launch& L, const TrivJobs& jobs, int njobs, const WSpec& ws, int m0, int Rtot,
                         const double* potw, double* part, int splits, double* W, double* Tout);
+// V = W^T P on a periodic cell panel, one thread per output (large W; small ones fuse into the fold)
+void launch_vdot(const Launch& L, int mm, int Rtot, long long rows, const double* W, const double* P, double* V);
 void launch_vgemm(const Launch& L, int mm, int Rtot, long long rows, const double* W, const double* P, double* V);
 void launch_hankel(const Launch& L, int m0, const DirPlan& d, const double* pwc, const unsigned long long* lo,
                    const unsigned long long* hi, const double* V, double* part, double* N, int splits);
@@ -319,6 +321,12 @@ struct ResFold {
     const double* P = nullptr;
     int Rtot = 0;
     long long prow = 0;
+    // supports [lo, hi) in grid index of the a- and b-profiles (b: the a support widened by
+    // bwiden on each side, e.g. 1 for T v); when set, each (tile, d) task sweeps only the j
+    // range where both tiles have non-zero values
+    const unsigned long long* sup_lo = nullptr;
+    const unsigned long long* sup_hi = nullptr;
+    int bwiden = 0;
 };
 // slab row stride: >= J + 5 (two guard columns plus zero padding for the unchecked last
 // k-step), == 4 mod 16 so the 8 rows x 4 columns of an m8n8k4 fragment hit distinct banks
