@@ -642,9 +642,12 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
             }
             const Launch& LL = (nth++ == 1) ? LP : L;
             w.pot[l] = A.get<double>("pot.panel" + std::to_string(l), d.pot_rows * Rtot);
-            if (d.nsum == 1 && p.nnuc == 1) {
+            static const bool fuse_short = !std::getenv("LT_POT_NO_FUSE_SHORT");
+            if ((d.nsum == 1 && p.nnuc == 1) || (fuse_short && d.nsum >= 32 && d.pot_rows <= d.n && p.nnuc <= 2)) {
                 // a single window copy of one nucleus: each master cell is read once, so it
-                // is evaluated in the copy kernel instead of being materialised first
+                // is evaluated in the copy kernel instead of being materialised first. The
+                // periodic cell window (one output per residue class) of <= 2 nuclei reads each
+                // cell at most twice: evaluating in place costs less than a serial master node
                 launch_potential_fused(LL, d.mrows, d.h, p.M, RN, p.nnuc, s0d + l * p.nnuc, d.nsum, d.n,
                                        d.pot_rows, w.pot[l]);
             } else {
@@ -1246,8 +1249,10 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
     const DftPrep& dp = cp.dp;
     // device work after L0 (with L0 in front under speculation): kernels and memsets only
     auto enqueue = [&]() {
-        if (spec) l0w.enqueue(c->L(), 1, static_cast<int>(L0) + 3, true);
-        LT_CU(cudaMemsetAsync(fk, 0xff, sizeof(unsigned long long), c->stream));
+        if (spec)  // k_l0_init also resets the failure key
+            l0w.enqueue(c->L(), 1, static_cast<int>(L0) + 3, true);
+        else
+            LT_CU(cudaMemsetAsync(fk, 0xff, sizeof(unsigned long long), c->stream));
         run_assembly(c, sd, p, NEED_MS | NEED_NUC, 0, out, nullptr, s0d);
         if (periodic) {
             int wrapped = 0, ax = -1;

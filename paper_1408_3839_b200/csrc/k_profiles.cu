@@ -19,88 +19,58 @@ struct ProfileJobs {
     ProfileJob j[kMaxProfileJobs];
 };
 
-__global__ void k_profile_sample(DevSys s, ProfileJobs jobs, double eps) {
-    const ProfileJob& jb = jobs.j[blockIdx.z];
-    const Index mu = blockIdx.y;
-    const Index i = static_cast<Index>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const bool in = i < jb.grid;
-    bool keep = false;
-    if (in) {
-        const Index base = jb.cell_index * jb.per_cell;
+// One CTA per (job, function) over its whole grid: samples, the support [lo, hi) (first /
+// last index with |v| >= eps, the reference's tail trim) from a block reduction, and the
+// trimmed values in the same pass: a sample below eps is written as 0. That equals the
+// zero-extended Supported1D wherever sub-eps samples occur only in the tails — for a
+// Gaussian times (x - c)^deg a non-zero sample below 1e-280 away from the tails would need
+// |x - c| < 1e-280^(1/deg), i.e. a grid point on the centre, where the sample is exactly 0.
+__global__ void __launch_bounds__(512) k_profiles(DevSys s, ProfileJobs jobs, double eps) {
+    const ProfileJob& jb = jobs.j[blockIdx.y];
+    const Index mu = blockIdx.x;
+    const Index base = jb.cell_index * jb.per_cell;
+    long long lo = jb.grid, hi = -1;
+    for (Index i = threadIdx.x; i < jb.grid; i += blockDim.x) {
         const double x =
             __dsub_rn(__dmul_rn(__dadd_rn(static_cast<double>(i - base), jb.align), jb.step), __dmul_rn(0.5, s.b));
         const double v = gto_eval1d(s, mu, jb.dir, x);
-        jb.values[mu * jb.grid + i] = v;
-        keep = !(fabs(v) < eps);
-    }
-    // CTA-aggregated support bounds: warp ballots, then one atomic pair per CTA (thousands
-    // of CTAs hit the same m0 addresses otherwise)
-    __shared__ unsigned long long cta_lo, cta_hi;
-    if (threadIdx.x == 0) {
-        cta_lo = ~0ull;
-        cta_hi = 0ull;
-    }
-    __syncthreads();
-    const unsigned mask = __ballot_sync(0xffffffffu, keep);
-    if (mask && (threadIdx.x & 31) == 0) {
-        const Index wbase = i;  // lane 0's index
-        atomicMin(&cta_lo, static_cast<unsigned long long>(wbase + (__ffs(mask) - 1)));
-        atomicMax(&cta_hi, static_cast<unsigned long long>(wbase + (31 - __clz(mask)) + 1));
-    }
-    __syncthreads();
-    if (threadIdx.x == 0 && cta_hi > 0) {
-        atomicMin(&jb.lo[mu], cta_lo);
-        atomicMax(&jb.hi[mu], cta_hi);
-    }
-}
-
-__global__ void k_profile_trim(ProfileJobs jobs) {
-    const ProfileJob& jb = jobs.j[blockIdx.z];
-    const Index mu = blockIdx.y;
-    const Index i = static_cast<Index>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= jb.grid) return;
-    unsigned long long lo = jb.lo[mu], hi = jb.hi[mu];
-    const bool empty = lo == ~0ull;
-    if (empty) {
-        lo = 0;
-        hi = 0;
-    }
-    if (static_cast<unsigned long long>(i) < lo || static_cast<unsigned long long>(i) >= hi)
-        jb.values[mu * jb.grid + i] = 0.0;
-    if (i == 0 && empty) {  // Supported1D{0, empty}
-        jb.lo[mu] = 0;
-        jb.hi[mu] = 0;
-    }
-}
-
-// support bounds of every job reset in one launch (lo = all ones, hi = 0): a memset per
-// array would put 2 x njobs serial graph nodes in front of the sampling
-__global__ void k_profile_bounds_init(ProfileJobs jobs, int njobs, Index m0) {
-    for (int k = 0; k < njobs; ++k)
-        for (Index mu = threadIdx.x; mu < m0; mu += blockDim.x) {
-            jobs.j[k].lo[mu] = ~0ull;
-            jobs.j[k].hi[mu] = 0ull;
+        const bool keep = !(fabs(v) < eps);
+        jb.values[mu * jb.grid + i] = keep ? v : 0.0;
+        if (keep) {
+            lo = min(lo, static_cast<long long>(i));
+            hi = max(hi, static_cast<long long>(i));
         }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    __shared__ long long slo[16], shi[16];
+    if ((threadIdx.x & 31) == 0) {
+        slo[threadIdx.x >> 5] = lo;
+        shi[threadIdx.x >> 5] = hi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) {
+            lo = min(lo, slo[w]);
+            hi = max(hi, shi[w]);
+        }
+        const bool empty = hi < 0;  // Supported1D{0, empty}
+        jb.lo[mu] = empty ? 0ull : static_cast<unsigned long long>(lo);
+        jb.hi[mu] = empty ? 0ull : static_cast<unsigned long long>(hi + 1);
+    }
 }
 
 void launch_profiles(const Launch& L, const DevSys& s, const ProfileJob* jobs, int njobs, double eps) {
     if (njobs > kMaxProfileJobs) fail(LT_EGENERIC, "launch_profiles: too many jobs");
     ProfileJobs pj{};
-    Index gmax = 1;
-    for (int k = 0; k < njobs; ++k) {
-        pj.j[k] = jobs[k];
-        gmax = std::max(gmax, jobs[k].grid);
-    }
-    dim3 grid(static_cast<unsigned>((gmax + 255) / 256), s.m0, njobs);
+    for (int k = 0; k < njobs; ++k) pj.j[k] = jobs[k];
+    dim3 grid(static_cast<unsigned>(s.m0), static_cast<unsigned>(njobs));
     Stage st_(L, "profiles");
-    k_profile_bounds_init<<<1, 64, 0, L.st>>>(pj, njobs, s.m0);
+    k_profiles<<<grid, 512, 0, L.st>>>(s, pj, eps);
     LT_CU(cudaGetLastError());
-    k_profile_sample<<<grid, 256, 0, L.st>>>(s, pj, eps);
-    LT_CU(cudaGetLastError());
-    // trimming depends on the complete bounds: second pass (stream-ordered)
-    k_profile_trim<<<grid, 256, 0, L.st>>>(pj);
-    LT_CU(cudaGetLastError());
-    L.tick(3);
+    L.tick();
 }
 
 // ---------------------------------------------------------------------------

@@ -150,6 +150,8 @@ __global__ void k_l0_init(int* found, int* state, unsigned* nz, int nnz) {
         state[2] = 1;  // next s
         state[3] = 0;  // done
         state[4] = 0;  // finished-block counter of the fused scan/finalize
+        state[6] = -1;  // ints 6-7: the pencil failure key (~0 = none) of the read-back block
+        state[7] = -1;
     }
 }
 
