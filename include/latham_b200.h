@@ -124,6 +124,30 @@ lt_status lt_solve_box_dense(lt_ctx* ctx, int64_t n, const double* H, const doub
 /* batch of Hermitian-definite pencils (eigensolver.cpp:72-93); complex interleaved col-major */
 lt_status lt_pencil_eig(lt_ctx* ctx, int64_t count, int64_t m0, const double* Hc, const double* Sc, double* eig);
 
+/* ---- eigenvectors (want_vectors = true; eigensolver.cpp:29-32, :88-92) ------------ *
+ * Box: vec = N_b x N_b col-major, S-orthonormal columns X = L^-T Z (DenseSpectrum::eigenvectors).
+ * Periodic / pencils: vec = K blocks of m0 x m0 complex (re,im interleaved, col-major), block j
+ * = KPointSpectrum::eigenvectors[j] (columns u_{j,m}, S_j-orthonormal). Columns are defined up
+ * to sign (box) or a unit phase (periodic), and within degenerate eigenspaces up to rotation. */
+lt_status lt_solve_box_dense_vectors(lt_ctx* ctx, int64_t n, const double* H, const double* S, int64_t cap,
+                                     double* eig, double* vec);
+lt_status lt_pencil_eigvec(lt_ctx* ctx, int64_t count, int64_t m0, const double* Hc, const double* Sc, double* eig,
+                           double* vec);
+lt_status lt_solve_periodic_ops_vectors(lt_ctx* ctx, const lt_operator* H, const lt_operator* S, double* eig,
+                                        double* vec);
+lt_status lt_solve_periodic_vectors(lt_ctx* ctx, const int64_t* dims, int64_t m0, int64_t nH, const int64_t* kH,
+                                    const double* bH, int64_t nS, const int64_t* kS, const double* bS, double* eig,
+                                    double* vec);
+lt_status lt_solve_periodic_factorized_vectors(lt_ctx* ctx, const lt_operator* H, const lt_operator* S,
+                                               double metadata_tol, double* eig, double* vec);
+/* reconstruct_eigenvectors (eigensolver.hpp; eigensolver.cpp:164-175): out = N x N complex
+ * col-major, N = K m0, column (j m0 + m) = bc_full_eigenvector(j, m); N > cap -> LT_ECAP */
+lt_status lt_reconstruct_eigenvectors(lt_ctx* ctx, const int64_t* dims, int64_t m0, const double* vec, int64_t cap,
+                                      double* out);
+/* bc_full_eigenvector (block_circulant.hpp; block_circulant.cpp:267-289): out = N complex */
+lt_status lt_bc_full_eigenvector(lt_ctx* ctx, const int64_t* dims, int64_t m0, const double* vec, int64_t j,
+                                 int64_t m, double* out);
+
 /* ---- separable metadata and the factorized Fourier path -------------------------- *
  * Periodic operators carry their rank metadata (galerkin.cpp:394-423; combine scales level 0
  * and concatenates, eigensolver.cpp:57-64). Layout of a term list: [t][level l][L_l][m0*m0]

@@ -101,6 +101,19 @@ class Oracle:
         self._pencil = getattr(lib, p + "solve_pencil", None)
         if self._pencil is not None:
             self._pencil.argtypes = [_i64, _dp, _dp, _i64, _dp]
+        # eigenvector entries (Oracle-R only: the reference's want_vectors paths)
+        self._box_vec = getattr(lib, p + "solve_box_dense_vec", None)
+        if self._box_vec is not None:
+            self._box_vec.argtypes = [_i64, _dp, _dp, _i64, _dp, _dp]
+        self._gen_vec = getattr(lib, p + "solve_periodic_vec", None)
+        if self._gen_vec is not None:
+            self._gen_vec.argtypes = [_ip, _i64, _i64, _ip, _dp, _i64, _ip, _dp, _i64, _dp, _dp]
+        self._recon = getattr(lib, p + "reconstruct_eigenvectors", None)
+        if self._recon is not None:
+            self._recon.argtypes = [_ip, _i64, _dp, _i64, _dp]
+        self._fullvec = getattr(lib, p + "bc_full_eigenvector", None)
+        if self._fullvec is not None:
+            self._fullvec.argtypes = [_ip, _i64, _dp, _i64, _i64, _dp]
         self._err = f("last_error")
         self._err.restype = ctypes.c_char_p
         self._sinc = getattr(lib, p + "sinc_quadrature", None)
@@ -242,6 +255,59 @@ class Oracle:
         out = np.zeros(n)
         self._check(self._box(n, Hc.ctypes.data_as(_dp), Sc.ctypes.data_as(_dp), cap, _dptr(out)))
         return out
+
+    def solve_box_dense_vectors(self, H: np.ndarray, S: np.ndarray, cap: int = 4096):
+        """solve_box_dense(H, S, want_vectors = true): (eigenvalues, eigenvectors [n, n])."""
+        n = H.shape[0]
+        Hc = np.asfortranarray(H, dtype=np.float64)
+        Sc = np.asfortranarray(S, dtype=np.float64)
+        out = np.zeros(n)
+        vec = np.zeros(max(n * n, 1))
+        self._check(self._box_vec(n, Hc.ctypes.data_as(_dp), Sc.ctypes.data_as(_dp), cap, _dptr(out), _dptr(vec)))
+        return out, vec[:n * n].reshape(n, n).T.copy()
+
+    def solve_periodic_vectors(self, dims, m0, Hgen: dict, Sgen: dict, threads: int = 1):
+        """solve_periodic(gen, gen, want_vectors = true): (eig [K, m0], vec [K, m0, m0])."""
+        def pack(g):
+            keys = sorted(g)
+            k = np.array(keys, dtype=np.int64).reshape(-1, 3)
+            b = np.concatenate([np.asarray(g[key], dtype=np.float64).T.reshape(-1) for key in keys]) if keys else np.zeros(0)
+            return len(keys), k, np.ascontiguousarray(b)
+        nH, kH, bH = pack(Hgen)
+        nS, kS, bS = pack(Sgen)
+        d = np.array(dims, dtype=np.int64)
+        K = int(np.prod(d))
+        out = np.zeros(K * m0)
+        vec = np.zeros(2 * K * m0 * m0)
+        self._check(self._gen_vec(_iptr(d), m0, nH, _iptr(kH), _dptr(bH), nS, _iptr(kS), _dptr(bS), threads,
+                                  _dptr(out), _dptr(vec)))
+        z = vec[0::2] + 1j * vec[1::2]
+        return out.reshape(K, m0), z.reshape(K, m0, m0).transpose(0, 2, 1).copy()
+
+    @staticmethod
+    def _pack_vec(vecs: np.ndarray) -> np.ndarray:
+        a = np.asarray(vecs, dtype=np.complex128).transpose(0, 2, 1).reshape(-1)
+        o = np.empty(2 * a.size)
+        o[0::2], o[1::2] = a.real, a.imag
+        return o
+
+    def reconstruct_eigenvectors(self, dims, vecs: np.ndarray, cap: int = 4096) -> np.ndarray:
+        K, m0, _ = vecs.shape
+        N = K * m0
+        d = np.array(dims, dtype=np.int64)
+        u = self._pack_vec(vecs)
+        out = np.zeros(2 * N * N if N <= cap else 2)
+        self._check(self._recon(_iptr(d), m0, _dptr(u), cap, _dptr(out)))
+        z = out[0::2] + 1j * out[1::2]
+        return z.reshape(N, N).T.copy()
+
+    def bc_full_eigenvector(self, dims, vecs: np.ndarray, j: int, m: int) -> np.ndarray:
+        K, m0, _ = vecs.shape
+        d = np.array(dims, dtype=np.int64)
+        u = self._pack_vec(vecs)
+        out = np.zeros(2 * K * m0)
+        self._check(self._fullvec(_iptr(d), m0, _dptr(u), j, m, _dptr(out)))
+        return out[0::2] + 1j * out[1::2]
 
     def solve_pencil(self, Hj: np.ndarray, Sj: np.ndarray, j: int = 0) -> np.ndarray:
         m0 = Hj.shape[0]

@@ -191,6 +191,76 @@ int ref_solve_box_dense(int64_t n, const double* H, const double* S, int64_t cap
     });
 }
 
+// want_vectors = true (eigensolver.cpp:31-32): vec = n x n col-major
+int ref_solve_box_dense_vec(int64_t n, const double* H, const double* S, int64_t cap, double* eig, double* vec) {
+    return guarded([&] {
+        Eigen::MatrixXd h(n, n), s(n, n);
+        std::memcpy(h.data(), H, sizeof(double) * n * n);
+        std::memcpy(s.data(), S, sizeof(double) * n * n);
+        const DenseSpectrum ds = solve_box_dense(h, s, true, cap);
+        for (int64_t i = 0; i < n; ++i) eig[i] = ds.eigenvalues[i];
+        std::memcpy(vec, ds.eigenvectors.data(), sizeof(double) * n * n);
+    });
+}
+
+static void put_vectors(const KPointSpectrum& spec, double* eig, double* vec) {
+    const int64_t mm = spec.m0 * spec.m0;
+    for (int64_t j = 0; j < spec.k_count(); ++j) {
+        for (int64_t m = 0; m < spec.m0; ++m) eig[j * spec.m0 + m] = spec.eigenvalues[j][m];
+        const auto& v = spec.eigenvectors[j];
+        for (int64_t i = 0; i < mm; ++i) {
+            vec[2 * (j * mm + i)] = v.data()[i].real();
+            vec[2 * (j * mm + i) + 1] = v.data()[i].imag();
+        }
+    }
+}
+
+// solve_periodic(gen, gen, want_vectors = true): vec = K blocks m0 x m0 complex interleaved
+int ref_solve_periodic_vec(const int64_t* dims, int64_t m0, int64_t nH, const int64_t* kH, const double* bH,
+                           int64_t nS, const int64_t* kS, const double* bS, int64_t threads, double* eig,
+                           double* vec) {
+    return guarded([&] {
+        put_vectors(solve_periodic(gen_from(dims, m0, nH, kH, bH), gen_from(dims, m0, nS, kS, bS), true, threads), eig,
+                    vec);
+    });
+}
+
+static KPointSpectrum spec_from(const int64_t* dims, int64_t m0, const double* vec) {
+    KPointSpectrum spec;
+    spec.dims = {dims[0], dims[1], dims[2]};
+    spec.m0 = m0;
+    const int64_t mm = m0 * m0;
+    for (int64_t j = 0; j < spec.k_count(); ++j) {
+        spec.eigenvalues.push_back(Eigen::VectorXd::Zero(m0));
+        Eigen::MatrixXcd v(m0, m0);
+        for (int64_t i = 0; i < mm; ++i) v.data()[i] = {vec[2 * (j * mm + i)], vec[2 * (j * mm + i) + 1]};
+        spec.eigenvectors.push_back(v);
+    }
+    return spec;
+}
+
+// reconstruct_eigenvectors (eigensolver.cpp:164-175): out = N x N complex col-major
+int ref_reconstruct_eigenvectors(const int64_t* dims, int64_t m0, const double* vec, int64_t cap, double* out) {
+    return guarded([&] {
+        const Eigen::MatrixXcd U = reconstruct_eigenvectors(spec_from(dims, m0, vec), cap);
+        for (int64_t i = 0; i < U.size(); ++i) {
+            out[2 * i] = U.data()[i].real();
+            out[2 * i + 1] = U.data()[i].imag();
+        }
+    });
+}
+
+// bc_full_eigenvector (block_circulant.cpp:267-289)
+int ref_bc_full_eigenvector(const int64_t* dims, int64_t m0, const double* vec, int64_t j, int64_t m, double* out) {
+    return guarded([&] {
+        const Eigen::VectorXcd u = bc_full_eigenvector(spec_from(dims, m0, vec), j, m);
+        for (int64_t i = 0; i < u.size(); ++i) {
+            out[2 * i] = u[i].real();
+            out[2 * i + 1] = u[i].imag();
+        }
+    });
+}
+
 void ref_sinc_quadrature(int64_t M, double* nodes, double* weights) {
     const SincQuadrature q = build_sinc_quadrature(M);
     for (int64_t i = 0; i < q.rank(); ++i) {

@@ -10,7 +10,9 @@ this module                               reference
 ``combine(wa, a, wb, b)``                 ``eigensolver.hpp:23-24``
 ``assemble_core(sys, periodic)``          ``tools/commands.cpp:51-59`` (fused on the device)
 ``solve_periodic(H, S)``                  ``eigensolver.hpp:29-33``
-``solve_box_dense(H, S, cap)``            ``eigensolver.hpp:17-18`` (eigenvalues only)
+``solve_box_dense(H, S, cap, want_vectors)`` ``eigensolver.hpp:17-18`` (DenseSpectrum with vectors)
+``reconstruct_eigenvectors(spec, cap)``   ``eigensolver.hpp`` (reconstruct_eigenvectors)
+``bc_full_eigenvector(spec, j, m)``       ``block_circulant.hpp`` (bc_full_eigenvector)
 ``bc_block_diagonalize(dims, m0, gen)``   ``block_circulant.hpp:86``
 ``build_sinc_quadrature(M)``              ``sinc_quadrature.hpp:35``
 ``overlap_constant(sys)``                 ``gto_basis.hpp:74``
@@ -123,6 +125,57 @@ def unpack_terms(flat: np.ndarray, L, m0):
     return out
 
 
+@dataclass
+class DenseSpectrum:
+    """DenseSpectrum (eigensolver.hpp): ascending eigenvalues, S-orthonormal eigenvector
+    columns (None unless requested)."""
+
+    eigenvalues: np.ndarray
+    eigenvectors: Optional[np.ndarray] = None
+
+
+@dataclass
+class KPointSpectrum:
+    """KPointSpectrum (spectrum.hpp): per-k ascending eigenvalues [K, m0] and, when
+    requested, per-k eigenvector blocks [K, m0, m0] (columns u_{j,m})."""
+
+    dims: Tuple[int, int, int]
+    m0: int
+    eigenvalues: np.ndarray
+    eigenvectors: Optional[np.ndarray] = None
+    solver_path: str = "periodic_fft"
+
+    def k_count(self) -> int:
+        return int(self.dims[0] * self.dims[1] * self.dims[2])
+
+    def has_vectors(self) -> bool:
+        return self.eigenvectors is not None
+
+    def k_multi(self, lin: int):
+        d = self.dims
+        return (lin // (d[1] * d[2]), (lin // d[2]) % d[1], lin % d[2])
+
+    def sorted_all(self) -> np.ndarray:
+        return np.sort(self.eigenvalues.reshape(-1))
+
+
+def _cvec_out(n: int) -> np.ndarray:
+    return np.zeros(2 * n)
+
+
+def _cblocks(flat: np.ndarray, K: int, m0: int) -> np.ndarray:
+    """C-ABI complex column-major blocks -> (K, m0, m0) [row, col]."""
+    z = flat[0::2] + 1j * flat[1::2]
+    return z.reshape(K, m0, m0).transpose(0, 2, 1).copy()
+
+
+def _cblocks_in(blocks: np.ndarray) -> np.ndarray:
+    a = np.asarray(blocks, dtype=np.complex128).transpose(0, 2, 1).reshape(-1)
+    o = np.empty(2 * a.size)
+    o[0::2], o[1::2] = a.real, a.imag
+    return o
+
+
 class Context:
     """One GPU: stream, solver handle and cached device buffers (lt_ctx)."""
 
@@ -225,13 +278,19 @@ class Context:
     def upload(self, sys: LatticeSystem) -> "DeviceSystem":
         return DeviceSystem(self, sys)
 
-    def solve_periodic(self, H: Operator, S: Operator) -> np.ndarray:
+    def solve_periodic(self, H: Operator, S: Operator, want_vectors: bool = False):
+        """solve_periodic (eigensolver.hpp:32-33): [K, m0] eigenvalues, or with want_vectors
+        the KPointSpectrum carrying the per-k eigenvector blocks."""
         K = H.L[0] * H.L[1] * H.L[2]
         out = np.zeros(K * H.m0)
-        check(self.lib.lt_solve_periodic_ops(self.h, H.handle, S.handle, _d(out)))
-        return out.reshape(K, H.m0)
+        if not want_vectors:
+            check(self.lib.lt_solve_periodic_ops(self.h, H.handle, S.handle, _d(out)))
+            return out.reshape(K, H.m0)
+        vec = _cvec_out(K * H.m0 * H.m0)
+        check(self.lib.lt_solve_periodic_ops_vectors(self.h, H.handle, S.handle, _d(out), _d(vec)))
+        return KPointSpectrum(tuple(H.L), H.m0, out.reshape(K, H.m0), _cblocks(vec, K, H.m0))
 
-    def solve_periodic_gen(self, dims, m0: int, Hgen: dict, Sgen: dict) -> np.ndarray:
+    def solve_periodic_gen(self, dims, m0: int, Hgen: dict, Sgen: dict, want_vectors: bool = False):
         def pack(g):
             keys = sorted(g)
             k = np.ascontiguousarray(np.array(keys, dtype=np.int64).reshape(-1, 3))
@@ -243,8 +302,13 @@ class Context:
         d = np.array(dims, dtype=np.int64)
         K = int(np.prod(d))
         out = np.zeros(K * m0)
-        check(self.lib.lt_solve_periodic(self.h, _i(d), m0, nH, _i(kH), _d(bH), nS, _i(kS), _d(bS), _d(out)))
-        return out.reshape(K, m0)
+        if not want_vectors:
+            check(self.lib.lt_solve_periodic(self.h, _i(d), m0, nH, _i(kH), _d(bH), nS, _i(kS), _d(bS), _d(out)))
+            return out.reshape(K, m0)
+        vec = _cvec_out(K * m0 * m0)
+        check(self.lib.lt_solve_periodic_vectors(self.h, _i(d), m0, nH, _i(kH), _d(bH), nS, _i(kS), _d(bS), _d(out),
+                                                 _d(vec)))
+        return KPointSpectrum(tuple(int(x) for x in dims), m0, out.reshape(K, m0), _cblocks(vec, K, m0))
 
     def box_circulant_defect(self, sys: LatticeSystem, want_defect: bool = False):
         """box_circulant_defect (galerkin.cpp:445-454): relative Frobenius norm of the box
@@ -263,12 +327,19 @@ class Context:
         check(self.lib.lt_separable_residual(self.h, op.handle, ctypes.byref(r)))
         return r.value
 
-    def solve_periodic_factorized(self, H: Operator, S: Operator, metadata_tol: float = 1e-10) -> np.ndarray:
-        """solve_periodic_factorized (eigensolver.hpp): [K, m0] eigenvalues."""
+    def solve_periodic_factorized(self, H: Operator, S: Operator, metadata_tol: float = 1e-10,
+                                  want_vectors: bool = False):
+        """solve_periodic_factorized (eigensolver.hpp): [K, m0] eigenvalues (KPointSpectrum
+        with the eigenvector blocks when want_vectors)."""
         K = H.L[0] * H.L[1] * H.L[2]
         out = np.zeros(K * H.m0)
-        check(self.lib.lt_solve_periodic_factorized(self.h, H.handle, S.handle, metadata_tol, _d(out)))
-        return out.reshape(K, H.m0)
+        if not want_vectors:
+            check(self.lib.lt_solve_periodic_factorized(self.h, H.handle, S.handle, metadata_tol, _d(out)))
+            return out.reshape(K, H.m0)
+        vec = _cvec_out(K * H.m0 * H.m0)
+        check(self.lib.lt_solve_periodic_factorized_vectors(self.h, H.handle, S.handle, metadata_tol, _d(out),
+                                                            _d(vec)))
+        return KPointSpectrum(tuple(H.L), H.m0, out.reshape(K, H.m0), _cblocks(vec, K, H.m0), "periodic_factorized")
 
     def factorized_block_diagonalize(self, levels: int, dims, m0: int, terms) -> np.ndarray:
         """factorized_block_diagonalize (factorized_diag.hpp): (K, m0, m0) complex blocks."""
@@ -311,13 +382,21 @@ class Context:
         z = out[0::2] + 1j * out[1::2]
         return z.reshape(K, m0, m0).transpose(0, 2, 1).copy()
 
-    def solve_box_dense(self, H: np.ndarray, S: np.ndarray, cap: int = 4096) -> np.ndarray:
+    def solve_box_dense(self, H: np.ndarray, S: np.ndarray, cap: int = 4096, want_vectors: bool = False):
+        """solve_box_dense (eigensolver.hpp:17-18): ascending eigenvalues, or with
+        want_vectors the DenseSpectrum with S-orthonormal eigenvector columns."""
         n = H.shape[0]
         Hc = np.asfortranarray(H, dtype=np.float64)
         Sc = np.asfortranarray(S, dtype=np.float64)
         out = np.zeros(n)
-        check(self.lib.lt_solve_box_dense(self.h, n, Hc.ctypes.data_as(_dp), Sc.ctypes.data_as(_dp), cap, _d(out)))
-        return out
+        if not want_vectors:
+            check(self.lib.lt_solve_box_dense(self.h, n, Hc.ctypes.data_as(_dp), Sc.ctypes.data_as(_dp), cap,
+                                              _d(out)))
+            return out
+        vec = np.zeros(max(n * n, 1))
+        check(self.lib.lt_solve_box_dense_vectors(self.h, n, Hc.ctypes.data_as(_dp), Sc.ctypes.data_as(_dp), cap,
+                                                  _d(out), _d(vec)))
+        return DenseSpectrum(out, vec[:n * n].reshape(n, n).T.copy())
 
     def pencil_eig(self, Hs: np.ndarray, Ss: np.ndarray) -> np.ndarray:
         """Batch of Hermitian-definite pencils (count, m0, m0) complex."""
@@ -331,6 +410,40 @@ class Context:
         out = np.zeros(cnt * m0)
         check(self.lib.lt_pencil_eig(self.h, cnt, m0, _d(h), _d(s), _d(out)))
         return out.reshape(cnt, m0)
+
+    def pencil_eigvec(self, Hs: np.ndarray, Ss: np.ndarray):
+        """Batch of pencils with eigenvectors (solve_pencil with want_vectors,
+        eigensolver.cpp:72-93): (eig [count, m0], vec [count, m0, m0] complex)."""
+        cnt, m0, _ = Hs.shape
+        h, s = _cblocks_in(Hs), _cblocks_in(Ss)
+        out = np.zeros(cnt * m0)
+        vec = _cvec_out(cnt * m0 * m0)
+        check(self.lib.lt_pencil_eigvec(self.h, cnt, m0, _d(h), _d(s), _d(out), _d(vec)))
+        return out.reshape(cnt, m0), _cblocks(vec, cnt, m0)
+
+    def reconstruct_eigenvectors(self, spec: KPointSpectrum, cap: int = 4096) -> np.ndarray:
+        """reconstruct_eigenvectors (eigensolver.cpp:164-175): the (K m0)^2 complex matrix
+        whose column j m0 + m is bc_full_eigenvector(spec, j, m)."""
+        if not spec.has_vectors():
+            raise StructureError("reconstruct_eigenvectors: spectrum carries no eigenvectors")
+        d = np.array(spec.dims, dtype=np.int64)
+        N = spec.k_count() * spec.m0
+        u = _cblocks_in(spec.eigenvectors)
+        out = _cvec_out(N * N) if N <= cap else np.zeros(2)
+        check(self.lib.lt_reconstruct_eigenvectors(self.h, _i(d), spec.m0, _d(u), cap, _d(out)))
+        z = out[0::2] + 1j * out[1::2]
+        return z.reshape(N, N).T.copy()
+
+    def bc_full_eigenvector(self, spec: KPointSpectrum, j: int, m: int) -> np.ndarray:
+        """bc_full_eigenvector (block_circulant.cpp:267-289): full-space vector of (j, m)."""
+        if not spec.has_vectors():
+            raise StructureError("bc_full_eigenvector: no eigenvectors stored")
+        d = np.array(spec.dims, dtype=np.int64)
+        N = spec.k_count() * spec.m0
+        u = _cblocks_in(spec.eigenvectors)
+        out = _cvec_out(N)
+        check(self.lib.lt_bc_full_eigenvector(self.h, _i(d), spec.m0, _d(u), j, m, _d(out)))
+        return out[0::2] + 1j * out[1::2]
 
     # ---- stages --------------------------------------------------------
     def build_sinc_quadrature(self, M: int):
@@ -453,12 +566,20 @@ def combine(wa: float, a: Operator, wb: float, b: Operator) -> Operator:
     return default_context().combine(wa, a, wb, b)
 
 
-def solve_periodic(H: Operator, S: Operator) -> np.ndarray:
-    return default_context().solve_periodic(H, S)
+def solve_periodic(H: Operator, S: Operator, want_vectors: bool = False):
+    return default_context().solve_periodic(H, S, want_vectors)
 
 
-def solve_box_dense(H: np.ndarray, S: np.ndarray, cap: int = 4096) -> np.ndarray:
-    return default_context().solve_box_dense(H, S, cap)
+def reconstruct_eigenvectors(spec: KPointSpectrum, cap: int = 4096) -> np.ndarray:
+    return default_context().reconstruct_eigenvectors(spec, cap)
+
+
+def bc_full_eigenvector(spec: KPointSpectrum, j: int, m: int) -> np.ndarray:
+    return default_context().bc_full_eigenvector(spec, j, m)
+
+
+def solve_box_dense(H: np.ndarray, S: np.ndarray, cap: int = 4096, want_vectors: bool = False):
+    return default_context().solve_box_dense(H, S, cap, want_vectors)
 
 
 def solve_core(sys: LatticeSystem, periodic: bool) -> np.ndarray:

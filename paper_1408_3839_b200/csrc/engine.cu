@@ -1107,9 +1107,17 @@ __global__ void k_real_to_complex(Index n, const double* __restrict__ a, double2
     if (i < n) out[i] = make_double2(a[i], 0.0);
 }
 
+__global__ void k_complex_real(Index n, const double2* __restrict__ a, double* __restrict__ out) {
+    const Index i = static_cast<Index>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = a[i].x;
+}
+
 // Box pencil on device buffers H, S (n x n col-major; both may be overwritten).
-// Eigenvalues -> eig_dev. Returns the failure key through *fail (device) for the warp path.
-static void box_eig_device(lt_ctx* c, Index n, double* H, double* S, double* eig_dev, unsigned long long* fail_dev) {
+// Eigenvalues -> eig_dev; with vec_dev, the S-orthonormal eigenvectors X = L^-T Z (n x n
+// col-major, eigensolver.cpp:31-32). Returns the failure key through *fail (device) for
+// the batched-pencil path.
+static void box_eig_device(lt_ctx* c, Index n, double* H, double* S, double* eig_dev, unsigned long long* fail_dev,
+                           double* vec_dev = nullptr) {
     const Launch L = c->L();
     if (n <= 32) {
         double2* hc = c->arena.get<double2>("box.hc", n * n);
@@ -1121,23 +1129,31 @@ static void box_eig_device(lt_ctx* c, Index n, double* H, double* S, double* eig
             LT_CU(cudaGetLastError());
             L.tick(2);
         }
-        launch_pencil(L, 1, n, hc, sc, eig_dev, fail_dev, false);
+        double2* vc = vec_dev ? c->arena.get<double2>("box.vc", n * n) : nullptr;
+        launch_pencil(L, 1, n, hc, sc, eig_dev, fail_dev, false, PencilDft{}, vc);
+        if (vec_dev) {  // real symmetric input: the Jacobi rotations stay real
+            Stage st_(L, "c2r");
+            k_complex_real<<<static_cast<unsigned>((n * n + 255) / 256), 256, 0, c->stream>>>(n * n, vc, vec_dev);
+            LT_CU(cudaGetLastError());
+            L.tick();
+        }
         return;
     }
     if (!c->solver) {
         if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS) fail(LT_ECUDA, "cusolverDnCreate failed");
     }
     cusolverDnSetStream(c->solver, c->stream);
+    const cusolverEigMode_t mode = vec_dev ? CUSOLVER_EIG_MODE_VECTOR : CUSOLVER_EIG_MODE_NOVECTOR;
     int lwork = 0;
-    if (cusolverDnDsygvd_bufferSize(c->solver, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_NOVECTOR, CUBLAS_FILL_MODE_LOWER,
-                                    static_cast<int>(n), H, static_cast<int>(n), S, static_cast<int>(n), eig_dev,
+    if (cusolverDnDsygvd_bufferSize(c->solver, CUSOLVER_EIG_TYPE_1, mode, CUBLAS_FILL_MODE_LOWER, static_cast<int>(n), H,
+                                    static_cast<int>(n), S, static_cast<int>(n), eig_dev,
                                     &lwork) != CUSOLVER_STATUS_SUCCESS)
         fail(LT_ECUDA, "cusolverDnDsygvd_bufferSize failed");
     double* work = c->arena.get<double>("box.work", static_cast<size_t>(lwork) + 1);
     int* info = c->arena.get<int>("box.info", 1);
     Stage st_(L, "sygvd");
-    if (cusolverDnDsygvd(c->solver, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_NOVECTOR, CUBLAS_FILL_MODE_LOWER,
-                         static_cast<int>(n), H, static_cast<int>(n), S, static_cast<int>(n), eig_dev, work, lwork,
+    if (cusolverDnDsygvd(c->solver, CUSOLVER_EIG_TYPE_1, mode, CUBLAS_FILL_MODE_LOWER, static_cast<int>(n), H,
+                         static_cast<int>(n), S, static_cast<int>(n), eig_dev, work, lwork,
                          info) != CUSOLVER_STATUS_SUCCESS)
         fail(LT_ECUDA, "cusolverDnDsygvd failed");
     // map info > n (leading minor of S not positive) onto the failure key
@@ -1146,6 +1162,8 @@ static void box_eig_device(lt_ctx* c, Index n, double* H, double* S, double* eig
     LT_CU(cudaStreamSynchronize(c->stream));
     if (hinfo > n) fail(LT_EDEFINITE, "solve_box_dense: overlap matrix is not positive definite (near-linear-dependent basis?)");
     if (hinfo != 0) fail(LT_EGENERIC, "solve_box_dense: eigensolver failed");
+    if (vec_dev)  // sygvd leaves the eigenvectors (X^T S X = I) in H
+        LT_CU(cudaMemcpyAsync(vec_dev, H, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, c->stream));
 }
 
 // graph-cache key: everything the captured launches bake in (host-derived parameters of
@@ -1567,20 +1585,29 @@ static double2* sep_fourier(lt_ctx* c, const SepMeta& m, const std::string& tag)
     return b.out;
 }
 
-// eigenvalues of the factorized pencils (solve_blocks with the factorized blocks)
-static void sep_solve(lt_ctx* c, const SepMeta& H, const SepMeta& S, double* eig) {
+// batched pencils on device blocks (solve_blocks, eigensolver.cpp:95-121): eigenvalues and,
+// when vec != null, the per-k eigenvector blocks (complex, column-major) to the host
+static void pencils_to_host(lt_ctx* c, Index K, Index m0, const double2* Hb, const double2* Sb, double* eig,
+                            double* vec, bool periodic_checks = true) {
+    double* e = c->arena.get<double>("solve.eig", K * m0);
+    double2* v = vec ? c->arena.get<double2>("solve.vec", K * m0 * m0) : nullptr;
+    unsigned long long* fk = c->arena.get<unsigned long long>("solve.fail", 1);
+    LT_CU(cudaMemsetAsync(fk, 0xff, sizeof(unsigned long long), c->stream));
+    launch_pencil(c->L(), K, m0, Hb, Sb, e, fk, periodic_checks, PencilDft{}, v);
+    unsigned long long key = ~0ull;
+    LT_CU(cudaMemcpyAsync(&key, fk, sizeof(key), cudaMemcpyDeviceToHost, c->stream));
+    LT_CU(cudaMemcpyAsync(eig, e, sizeof(double) * K * m0, cudaMemcpyDeviceToHost, c->stream));
+    if (vec) LT_CU(cudaMemcpyAsync(vec, v, sizeof(double2) * K * m0 * m0, cudaMemcpyDeviceToHost, c->stream));
+    LT_CU(cudaStreamSynchronize(c->stream));
+    raise_fail_key(key, periodic_checks);
+}
+
+// eigenvalues (and vectors) of the factorized pencils (solve_blocks with the factorized blocks)
+static void sep_solve(lt_ctx* c, const SepMeta& H, const SepMeta& S, double* eig, double* vec = nullptr) {
     const Index K = H.L[0] * H.L[1] * H.L[2];
     double2* Hb = sep_fourier(c, H, "H");
     double2* Sb = sep_fourier(c, S, "S");
-    double* e = c->arena.get<double>("solve.eig", K * H.m0);
-    unsigned long long* fk = c->arena.get<unsigned long long>("solve.fail", 1);
-    LT_CU(cudaMemsetAsync(fk, 0xff, sizeof(unsigned long long), c->stream));
-    launch_pencil(c->L(), K, H.m0, Hb, Sb, e, fk, true);
-    unsigned long long key = ~0ull;
-    LT_CU(cudaMemcpyAsync(&key, fk, sizeof(key), cudaMemcpyDeviceToHost, c->stream));
-    LT_CU(cudaMemcpyAsync(eig, e, sizeof(double) * K * H.m0, cudaMemcpyDeviceToHost, c->stream));
-    LT_CU(cudaStreamSynchronize(c->stream));
-    raise_fail_key(key, true);
+    pencils_to_host(c, K, H.m0, Hb, Sb, eig, vec);
 }
 
 static void sep_check_resid(double resid, double tol) {
@@ -1851,27 +1878,24 @@ lt_status lt_op_blocks(const lt_operator* op, int64_t* kidx, double* blocks) {
     });
 }
 
+static void solve_periodic_ops(lt_ctx* c, const lt_operator* H, const lt_operator* S, double* eig, double* vec) {
+    if (!H->periodic || !S->periodic) fail(LT_ESTRUCT, "solve_periodic: operators must be periodic assemblies");
+    if (H->m0 != S->m0 || H->L[0] != S->L[0] || H->L[1] != S->L[1] || H->L[2] != S->L[2])
+        fail(LT_ESTRUCT, "solve_periodic: H and S layouts differ");
+    LT_CU(cudaSetDevice(c->device));
+    const Index K = H->L[0] * H->L[1] * H->L[2];
+    double2* Hb = block_diag_device(c, H->L, H->m0, H->kidx, H->data, "H");
+    double2* Sb = block_diag_device(c, S->L, S->m0, S->kidx, S->data, "S");
+    pencils_to_host(c, K, H->m0, Hb, Sb, eig, vec);
+}
+
 lt_status lt_solve_periodic_ops(lt_ctx* c, const lt_operator* H, const lt_operator* S, double* eig) {
-    return guarded([&] {
-        if (!H->periodic || !S->periodic) fail(LT_ESTRUCT, "solve_periodic: operators must be periodic assemblies");
-        if (H->m0 != S->m0 || H->L[0] != S->L[0] || H->L[1] != S->L[1] || H->L[2] != S->L[2])
-            fail(LT_ESTRUCT, "solve_periodic: H and S layouts differ");
-        LT_CU(cudaSetDevice(c->device));
-        const Index mm = H->m0 * H->m0;
-        const Index K = H->L[0] * H->L[1] * H->L[2];
-        double2* Hb = block_diag_device(c, H->L, H->m0, H->kidx, H->data, "H");
-        double2* Sb = block_diag_device(c, S->L, S->m0, S->kidx, S->data, "S");
-        double* e = c->arena.get<double>("solve.eig", K * H->m0);
-        unsigned long long* fk = c->arena.get<unsigned long long>("solve.fail", 1);
-        LT_CU(cudaMemsetAsync(fk, 0xff, sizeof(unsigned long long), c->stream));
-        launch_pencil(c->L(), K, H->m0, Hb, Sb, e, fk, true);
-        (void)mm;
-        unsigned long long key = ~0ull;
-        LT_CU(cudaMemcpyAsync(&key, fk, sizeof(key), cudaMemcpyDeviceToHost, c->stream));
-        LT_CU(cudaMemcpyAsync(eig, e, sizeof(double) * K * H->m0, cudaMemcpyDeviceToHost, c->stream));
-        LT_CU(cudaStreamSynchronize(c->stream));
-        raise_fail_key(key, true);
-    });
+    return guarded([&] { solve_periodic_ops(c, H, S, eig, nullptr); });
+}
+
+lt_status lt_solve_periodic_ops_vectors(lt_ctx* c, const lt_operator* H, const lt_operator* S, double* eig,
+                                        double* vec) {
+    return guarded([&] { solve_periodic_ops(c, H, S, eig, vec); });
 }
 
 static void gen_to_device(lt_ctx* c, int64_t nblk, const int64_t* k, const double* b, Index m0,
@@ -1896,29 +1920,31 @@ static void check_gen_dims(const int64_t* dims, int64_t m0) {
     if (m0 < 1) fail(LT_EDIM, "GeneratingBlockTensor: m0 must be >= 1");
 }
 
+static void solve_periodic_gen(lt_ctx* c, const int64_t* dims, int64_t m0, int64_t nH, const int64_t* kH,
+                               const double* bH, int64_t nS, const int64_t* kS, const double* bS, double* eig,
+                               double* vec) {
+    LT_CU(cudaSetDevice(c->device));
+    check_gen_dims(dims, m0);
+    std::vector<std::array<Index, 3>> keysH, keysS;
+    double *dH = nullptr, *dS = nullptr;
+    gen_to_device(c, nH, kH, bH, m0, keysH, &dH, "H");
+    gen_to_device(c, nS, kS, bS, m0, keysS, &dS, "S");
+    const Index d3[3] = {dims[0], dims[1], dims[2]};
+    const Index K = d3[0] * d3[1] * d3[2];
+    double2* Hb = block_diag_device(c, d3, m0, keysH, dH, "H");
+    double2* Sb = block_diag_device(c, d3, m0, keysS, dS, "S");
+    pencils_to_host(c, K, m0, Hb, Sb, eig, vec);
+}
+
 lt_status lt_solve_periodic(lt_ctx* c, const int64_t* dims, int64_t m0, int64_t nH, const int64_t* kH, const double* bH,
                             int64_t nS, const int64_t* kS, const double* bS, double* eig) {
-    return guarded([&] {
-        LT_CU(cudaSetDevice(c->device));
-        check_gen_dims(dims, m0);
-        std::vector<std::array<Index, 3>> keysH, keysS;
-        double *dH = nullptr, *dS = nullptr;
-        gen_to_device(c, nH, kH, bH, m0, keysH, &dH, "H");
-        gen_to_device(c, nS, kS, bS, m0, keysS, &dS, "S");
-        const Index d3[3] = {dims[0], dims[1], dims[2]};
-        const Index K = d3[0] * d3[1] * d3[2];
-        double2* Hb = block_diag_device(c, d3, m0, keysH, dH, "H");
-        double2* Sb = block_diag_device(c, d3, m0, keysS, dS, "S");
-        double* e = c->arena.get<double>("solve.eig", K * m0);
-        unsigned long long* fk = c->arena.get<unsigned long long>("solve.fail", 1);
-        LT_CU(cudaMemsetAsync(fk, 0xff, sizeof(unsigned long long), c->stream));
-        launch_pencil(c->L(), K, m0, Hb, Sb, e, fk, true);
-        unsigned long long key = ~0ull;
-        LT_CU(cudaMemcpyAsync(&key, fk, sizeof(key), cudaMemcpyDeviceToHost, c->stream));
-        LT_CU(cudaMemcpyAsync(eig, e, sizeof(double) * K * m0, cudaMemcpyDeviceToHost, c->stream));
-        LT_CU(cudaStreamSynchronize(c->stream));
-        raise_fail_key(key, true);
-    });
+    return guarded([&] { solve_periodic_gen(c, dims, m0, nH, kH, bH, nS, kS, bS, eig, nullptr); });
+}
+
+lt_status lt_solve_periodic_vectors(lt_ctx* c, const int64_t* dims, int64_t m0, int64_t nH, const int64_t* kH,
+                                    const double* bH, int64_t nS, const int64_t* kS, const double* bS, double* eig,
+                                    double* vec) {
+    return guarded([&] { solve_periodic_gen(c, dims, m0, nH, kH, bH, nS, kS, bS, eig, vec); });
 }
 
 lt_status lt_block_diagonalize(lt_ctx* c, const int64_t* dims, int64_t m0, int64_t nblk, const int64_t* kidx,
@@ -1937,44 +1963,90 @@ lt_status lt_block_diagonalize(lt_ctx* c, const int64_t* dims, int64_t m0, int64
     });
 }
 
+static void solve_box_dense_host(lt_ctx* c, int64_t n, const double* H, const double* S, int64_t cap, double* eig,
+                                 double* vec) {
+    if (n > cap)
+        fail(LT_ECAP, "solve_box_dense: size " + std::to_string(n) + " exceeds dense cap " + std::to_string(cap));
+    LT_CU(cudaSetDevice(c->device));
+    double* dH = c->arena.get<double>("boxapi.H", n * n);
+    double* dS = c->arena.get<double>("boxapi.S", n * n);
+    double* e = c->arena.get<double>("boxapi.eig", n);
+    double* dv = vec ? c->arena.get<double>("boxapi.vec", n * n) : nullptr;
+    unsigned long long* fk = c->arena.get<unsigned long long>("solve.fail", 1);
+    LT_CU(cudaMemsetAsync(fk, 0xff, sizeof(unsigned long long), c->stream));
+    upload(c, dH, H, sizeof(double) * n * n);
+    upload(c, dS, S, sizeof(double) * n * n);
+    box_eig_device(c, n, dH, dS, e, fk, dv);
+    unsigned long long key = ~0ull;
+    LT_CU(cudaMemcpyAsync(&key, fk, sizeof(key), cudaMemcpyDeviceToHost, c->stream));
+    LT_CU(cudaMemcpyAsync(eig, e, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    if (vec) LT_CU(cudaMemcpyAsync(vec, dv, sizeof(double) * n * n, cudaMemcpyDeviceToHost, c->stream));
+    LT_CU(cudaStreamSynchronize(c->stream));
+    raise_fail_key(key, false);
+}
+
 lt_status lt_solve_box_dense(lt_ctx* c, int64_t n, const double* H, const double* S, int64_t cap, double* eig) {
-    return guarded([&] {
-        if (n > cap)
-            fail(LT_ECAP, "solve_box_dense: size " + std::to_string(n) + " exceeds dense cap " + std::to_string(cap));
-        LT_CU(cudaSetDevice(c->device));
-        double* dH = c->arena.get<double>("boxapi.H", n * n);
-        double* dS = c->arena.get<double>("boxapi.S", n * n);
-        double* e = c->arena.get<double>("boxapi.eig", n);
-        unsigned long long* fk = c->arena.get<unsigned long long>("solve.fail", 1);
-        LT_CU(cudaMemsetAsync(fk, 0xff, sizeof(unsigned long long), c->stream));
-        upload(c, dH, H, sizeof(double) * n * n);
-        upload(c, dS, S, sizeof(double) * n * n);
-        box_eig_device(c, n, dH, dS, e, fk);
-        unsigned long long key = ~0ull;
-        LT_CU(cudaMemcpyAsync(&key, fk, sizeof(key), cudaMemcpyDeviceToHost, c->stream));
-        LT_CU(cudaMemcpyAsync(eig, e, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
-        LT_CU(cudaStreamSynchronize(c->stream));
-        raise_fail_key(key, false);
-    });
+    return guarded([&] { solve_box_dense_host(c, n, H, S, cap, eig, nullptr); });
+}
+
+lt_status lt_solve_box_dense_vectors(lt_ctx* c, int64_t n, const double* H, const double* S, int64_t cap, double* eig,
+                                     double* vec) {
+    return guarded([&] { solve_box_dense_host(c, n, H, S, cap, eig, vec); });
+}
+
+static void pencil_eig_host(lt_ctx* c, int64_t count, int64_t m0, const double* Hc, const double* Sc, double* eig,
+                            double* vec) {
+    LT_CU(cudaSetDevice(c->device));
+    const Index mm = m0 * m0;
+    double2* dH = c->arena.get<double2>("pen.H", count * mm);
+    double2* dS = c->arena.get<double2>("pen.S", count * mm);
+    upload(c, dH, Hc, sizeof(double2) * count * mm);
+    upload(c, dS, Sc, sizeof(double2) * count * mm);
+    pencils_to_host(c, count, m0, dH, dS, eig, vec);
 }
 
 lt_status lt_pencil_eig(lt_ctx* c, int64_t count, int64_t m0, const double* Hc, const double* Sc, double* eig) {
+    return guarded([&] { pencil_eig_host(c, count, m0, Hc, Sc, eig, nullptr); });
+}
+
+lt_status lt_pencil_eigvec(lt_ctx* c, int64_t count, int64_t m0, const double* Hc, const double* Sc, double* eig,
+                           double* vec) {
+    return guarded([&] { pencil_eig_host(c, count, m0, Hc, Sc, eig, vec); });
+}
+
+// reconstruct_eigenvectors (eigensolver.cpp:164-175): N x N complex, N = K m0 <= cap
+lt_status lt_reconstruct_eigenvectors(lt_ctx* c, const int64_t* dims, int64_t m0, const double* vec, int64_t cap,
+                                      double* out) {
     return guarded([&] {
+        check_gen_dims(dims, m0);
+        const Index d3[3] = {dims[0], dims[1], dims[2]};
+        const Index K = d3[0] * d3[1] * d3[2], N = K * m0;
+        if (N > cap) fail(LT_ECAP, "reconstruct_eigenvectors: size exceeds cap");
         LT_CU(cudaSetDevice(c->device));
-        const Index mm = m0 * m0;
-        double2* dH = c->arena.get<double2>("pen.H", count * mm);
-        double2* dS = c->arena.get<double2>("pen.S", count * mm);
-        double* e = c->arena.get<double>("pen.eig", count * m0);
-        unsigned long long* fk = c->arena.get<unsigned long long>("solve.fail", 1);
-        LT_CU(cudaMemsetAsync(fk, 0xff, sizeof(unsigned long long), c->stream));
-        upload(c, dH, Hc, sizeof(double2) * count * mm);
-        upload(c, dS, Sc, sizeof(double2) * count * mm);
-        launch_pencil(c->L(), count, m0, dH, dS, e, fk, true);
-        unsigned long long key = ~0ull;
-        LT_CU(cudaMemcpyAsync(&key, fk, sizeof(key), cudaMemcpyDeviceToHost, c->stream));
-        LT_CU(cudaMemcpyAsync(eig, e, sizeof(double) * count * m0, cudaMemcpyDeviceToHost, c->stream));
+        double2* u = c->arena.get<double2>("rec.u", K * m0 * m0);
+        double2* o = c->arena.get<double2>("rec.out", N * N);
+        upload(c, u, vec, sizeof(double2) * K * m0 * m0);
+        launch_reconstruct(c->L(), d3, m0, u, 0, N, o);
+        LT_CU(cudaMemcpyAsync(out, o, sizeof(double2) * N * N, cudaMemcpyDeviceToHost, c->stream));
         LT_CU(cudaStreamSynchronize(c->stream));
-        raise_fail_key(key, true);
+    });
+}
+
+// bc_full_eigenvector (block_circulant.cpp:267-289): column (j, m), N complex
+lt_status lt_bc_full_eigenvector(lt_ctx* c, const int64_t* dims, int64_t m0, const double* vec, int64_t j, int64_t m,
+                                 double* out) {
+    return guarded([&] {
+        check_gen_dims(dims, m0);
+        const Index d3[3] = {dims[0], dims[1], dims[2]};
+        const Index K = d3[0] * d3[1] * d3[2], N = K * m0;
+        if (j < 0 || j >= K || m < 0 || m >= m0) fail(LT_EBOUNDS, "bc_full_eigenvector: (k-point, band) out of range");
+        LT_CU(cudaSetDevice(c->device));
+        double2* u = c->arena.get<double2>("rec.u", K * m0 * m0);
+        double2* o = c->arena.get<double2>("rec.col", N);
+        upload(c, u, vec, sizeof(double2) * K * m0 * m0);
+        launch_reconstruct(c->L(), d3, m0, u, j * m0 + m, 1, o);
+        LT_CU(cudaMemcpyAsync(out, o, sizeof(double2) * N, cudaMemcpyDeviceToHost, c->stream));
+        LT_CU(cudaStreamSynchronize(c->stream));
     });
 }
 
@@ -2191,18 +2263,26 @@ lt_status lt_separable_residual(lt_ctx* c, const lt_operator* op, double* resid)
     });
 }
 
+static void solve_factorized_ops(lt_ctx* c, const lt_operator* H, const lt_operator* S, double metadata_tol,
+                                 double* eig, double* vec) {
+    if (!H->periodic || !S->periodic)
+        fail(LT_ESTRUCT, "solve_periodic_factorized: operators must be periodic assemblies");
+    if (!H->sep || !S->sep || H->sep->terms == 0 || S->sep->terms == 0)
+        fail(LT_ESTRUCT, "solve_periodic_factorized: rank metadata missing");
+    LT_CU(cudaSetDevice(c->device));
+    sep_check_resid(sep_residual(c, *H->sep, H->kidx, H->data, "H"), metadata_tol);
+    sep_check_resid(sep_residual(c, *S->sep, S->kidx, S->data, "S"), metadata_tol);
+    sep_solve(c, *H->sep, *S->sep, eig, vec);
+}
+
 lt_status lt_solve_periodic_factorized(lt_ctx* c, const lt_operator* H, const lt_operator* S, double metadata_tol,
                                        double* eig) {
-    return guarded([&] {
-        if (!H->periodic || !S->periodic)
-            fail(LT_ESTRUCT, "solve_periodic_factorized: operators must be periodic assemblies");
-        if (!H->sep || !S->sep || H->sep->terms == 0 || S->sep->terms == 0)
-            fail(LT_ESTRUCT, "solve_periodic_factorized: rank metadata missing");
-        LT_CU(cudaSetDevice(c->device));
-        sep_check_resid(sep_residual(c, *H->sep, H->kidx, H->data, "H"), metadata_tol);
-        sep_check_resid(sep_residual(c, *S->sep, S->kidx, S->data, "S"), metadata_tol);
-        sep_solve(c, *H->sep, *S->sep, eig);
-    });
+    return guarded([&] { solve_factorized_ops(c, H, S, metadata_tol, eig, nullptr); });
+}
+
+lt_status lt_solve_periodic_factorized_vectors(lt_ctx* c, const lt_operator* H, const lt_operator* S,
+                                               double metadata_tol, double* eig, double* vec) {
+    return guarded([&] { solve_factorized_ops(c, H, S, metadata_tol, eig, vec); });
 }
 
 static void check_levels(int levels, const int64_t* dims, Index nterms) {

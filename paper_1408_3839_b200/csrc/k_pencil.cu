@@ -12,6 +12,13 @@
 // Eigenvalues come out ascending by construction. Results agree with the reference's
 // SelfAdjointEigenSolver to O(eps ||A||).
 //
+// Vector mode (want_vectors, eigensolver.cpp:88-92): steps 4-5 are replaced by a parallel
+// cyclic Jacobi on A (round-robin pair ordering, n/2 disjoint complex rotations per round,
+// the rotation and stopping rule of a one-sided-phase Jacobi: phase a_pq to real, then the
+// real rotation t = sign(tau) / (|tau| + sqrt(1 + tau^2))), which yields eigenvalues and an
+// orthonormal Z together and is robust to degenerate eigenvalues; columns are sorted
+// ascending and back-transformed X = L^-H Z (llt.matrixU().solve(Z)).
+//
 // Layout: a group of G threads per pencil; m0 padded to NM in {8, 16, 32} (the
 // padding is an exactly decoupled block, H_pad = 0, S_pad = I, never touched by
 // steps 4-5 which run on the leading m0 x m0 block); compile-time index maps.
@@ -68,6 +75,11 @@ struct PSmem {
     double red[4][32];
     double scal[4];
     double2 tw[kPencilDftMax];  // fused DFT: twiddles of this k-point
+    // vector mode (parallel Jacobi): rotation of pair i = (jp[i], jq[i]); pair of index x
+    double jc[NM / 2 + 1], js[NM / 2 + 1], jtr[NM / 2 + 1];
+    double2 jph[NM / 2 + 1];
+    int jp[NM / 2 + 1], jq[NM / 2 + 1], jrot[NM / 2 + 1], jpair[NM + 1], perm[NM];
+    int rot[2];
 };
 
 // group reduction of NV values at once (one pair of barriers for all of them)
@@ -137,14 +149,201 @@ __device__ __forceinline__ void sturm_counts(const double* d, const double* e2, 
     }
 }
 
+
+// Vector mode on the reduced matrix A (leading n x n): parallel cyclic Jacobi with the
+// eigenvectors accumulated in C, then ascending order and X = L^-H Z (B holds the unscaled
+// Cholesky factor, L[r][i] = B[r][i] invd[i]). Writes eig[k*n ..] and vec[k*n*n ..]
+// (column-major, complex).
+template <int NM, int G, int EPT>
+__device__ void pencil_vectors(PSmem<NM>& sm, int n, int t, int slot, Index k, double* __restrict__ eig,
+                               double2* __restrict__ vec) {
+    auto& A = sm.A;
+    auto& B = sm.B;
+    auto& C = sm.C;
+    // C = I; the stopping floor 1e-17 ||A||_F
+    double fro[1] = {0.0};
+#pragma unroll
+    for (int u = 0; u < EPT; ++u) {
+        const int e = t + G * u;
+        if (e < NM * NM) {
+            const int r = e % NM, c = e / NM;
+            C[r][c] = make_double2(r == c ? 1.0 : 0.0, 0.0);
+            if (r < n && c < n) fro[0] += cabs2(A[r][c]);
+        }
+    }
+    if (t < 2) sm.rot[t] = 0;
+    greduce<G, 1, false>(fro, sm.red, t, slot);  // also orders C and rot
+    const double floor_abs = 1e-17 * sqrt(fro[0]);
+    const int n2 = n + (n & 1);  // round-robin over an even count (index n: the idle slot)
+    const int npair = n2 / 2;
+    for (int sweep = 0; sweep < 60 && n > 1; ++sweep) {
+        const int cur = sweep & 1;
+        for (int round = 0; round < n2 - 1; ++round) {
+            if (t < npair) {
+                const int a = t, b = n2 - 1 - t;
+                const int ia = a == 0 ? 0 : 1 + (a - 1 + round) % (n2 - 1);
+                const int ib = b == 0 ? 0 : 1 + (b - 1 + round) % (n2 - 1);
+                const int p = min(ia, ib), q = max(ia, ib);
+                double c = 1.0, sn = 0.0, tr = 0.0;
+                int rotated = 0;
+                double2 cph = make_double2(1.0, 0.0);
+                if (q < n) {
+                    const double2 apq = A[p][q];
+                    const double r = cabs_(apq);
+                    const double app = A[p][p].x, aqq = A[q][q].x;
+                    if (r > floor_abs && r > 1.1102230246251565e-16 * sqrt(fabs(app * aqq))) {
+                        const double ir = 1.0 / r;
+                        cph = make_double2(apq.x * ir, -apq.y * ir);  // conj(a_pq / r)
+                        const double tau = (aqq - app) / (2.0 * r);
+                        const double tt = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                        c = 1.0 / sqrt(1.0 + tt * tt);
+                        sn = tt * c;
+                        tr = tt * r;
+                        rotated = 1;
+                        sm.rot[cur] = 1;
+                    }
+                }
+                sm.jp[t] = p;
+                sm.jq[t] = q;
+                sm.jc[t] = c;
+                sm.js[t] = sn;
+                sm.jtr[t] = tr;
+                sm.jrot[t] = rotated;
+                sm.jph[t] = cph;
+                sm.jpair[p] = t;
+                sm.jpair[q] = t;
+            }
+            gsync<G>(slot);
+            // the next sweep's flag: every thread has passed this one's read of it
+            if (round == 0 && t == 0) sm.rot[cur ^ 1] = 0;
+            // J = D R per pair: J[p][p] = c, J[p][q] = s, J[q][p] = -s cph, J[q][q] = c cph;
+            // A' = J^H A J entrywise from the 2 x 2 block of the two pairs, V' = V J
+            double2 na[EPT], nv[EPT];
+#pragma unroll
+            for (int u = 0; u < EPT; ++u) {
+                const int e = t + G * u;
+                if (e < NM * NM) {
+                    const int x = e % NM, y = e / NM;
+                    if (x < n && y < n) {
+                        const int P = sm.jpair[x], Q = sm.jpair[y];
+                        const int xp = sm.jp[P], xq = sm.jq[P], yp = sm.jp[Q], yq = sm.jq[Q];
+                        const double cx = sm.jc[P], sx = sm.js[P], cy = sm.jc[Q], sy = sm.js[Q];
+                        const double2 phx = sm.jph[P], phy = sm.jph[Q];
+                        // column x of J_P: (J[xp][x], J[xq][x]); column y of J_Q
+                        double2 jx0, jx1, jy0, jy1;
+                        if (x == xp) {
+                            jx0 = make_double2(cx, 0.0);
+                            jx1 = cscale(-sx, phx);
+                        } else {
+                            jx0 = make_double2(sx, 0.0);
+                            jx1 = cscale(cx, phx);
+                        }
+                        if (y == yp) {
+                            jy0 = make_double2(cy, 0.0);
+                            jy1 = cscale(-sy, phy);
+                        } else {
+                            jy0 = make_double2(sy, 0.0);
+                            jy1 = cscale(cy, phy);
+                        }
+                        const bool xin = xq < n, yin = yq < n;  // idle-slot partners carry J = 1
+                        if (!xin) {
+                            jx0 = make_double2(1.0, 0.0);
+                            jx1 = make_double2(0.0, 0.0);
+                        }
+                        if (!yin) {
+                            jy0 = make_double2(1.0, 0.0);
+                            jy1 = make_double2(0.0, 0.0);
+                        }
+                        const int rx0 = xin ? xp : x, rx1 = xin ? xq : x, cy0 = yin ? yp : y, cy1 = yin ? yq : y;
+                        // A' = sum conj(J[x'][x]) A[x'][y'] J[y'][y]
+                        const double2 t0 = cadd(cmul(A[rx0][cy0], jy0), cmul(A[rx0][cy1], jy1));
+                        const double2 t1 = cadd(cmul(A[rx1][cy0], jy0), cmul(A[rx1][cy1], jy1));
+                        double2 r = cadd(cmulc(jx0, t0), cmulc(jx1, t1));
+                        if (P == Q && sm.jrot[P]) {  // the rotated diagonal block, exactly
+                            r = (x == y) ? make_double2(A[x][x].x + (x == xp ? -sm.jtr[P] : sm.jtr[P]), 0.0)
+                                         : make_double2(0.0, 0.0);
+                        }
+                        na[u] = r;
+                        nv[u] = cadd(cmul(C[x][cy0], jy0), cmul(C[x][cy1], jy1));
+                    } else if (y < n) {
+                        nv[u] = make_double2(0.0, 0.0);
+                    }
+                }
+            }
+            gsync<G>(slot);
+#pragma unroll
+            for (int u = 0; u < EPT; ++u) {
+                const int e = t + G * u;
+                if (e < NM * NM) {
+                    const int x = e % NM, y = e / NM;
+                    if (x < n && y < n) {
+                        A[x][y] = na[u];
+                        C[x][y] = nv[u];
+                    }
+                }
+            }
+            gsync<G>(slot);
+        }
+        if (sm.rot[cur] == 0) break;
+    }
+    // ascending order (ties by index): rank of each diagonal entry
+    if (t < n) {
+        const double dx = A[t][t].x;
+        int rank = 0;
+        for (int y = 0; y < n; ++y) {
+            const double dy = A[y][y].x;
+            rank += (dy < dx) || (dy == dx && y < t);
+        }
+        sm.perm[rank] = t;
+        sm.d[rank] = dx;
+    }
+    gsync<G>(slot);
+    // Z (sorted columns of C) into A
+#pragma unroll
+    for (int u = 0; u < EPT; ++u) {
+        const int e = t + G * u;
+        if (e < NM * NM) {
+            const int r = e % NM, c = e / NM;
+            if (r < n && c < n) A[r][c] = C[r][sm.perm[c]];
+        }
+    }
+    gsync<G>(slot);
+    // X = L^-H Z: row r final before step r; rows i < r take -= conj(L[r][i]) x_r with
+    // x_r = A[r][.] invd[r]; the row scaling by invd is applied at the end
+    for (int r = n - 1; r >= 1; --r) {
+        const double ir = sm.invd[r];
+#pragma unroll
+        for (int u = 0; u < EPT; ++u) {
+            const int e = t + G * u;
+            if (e < NM * NM) {
+                const int i = e % NM, c = e / NM;
+                if (i < r && c < n)
+                    A[i][c] = csub(A[i][c], cscale(sm.invd[i] * ir, cmulc(B[r][i], A[r][c])));
+            }
+        }
+        gsync<G>(slot);
+    }
+    const Index mmo = static_cast<Index>(n) * n;
+#pragma unroll
+    for (int u = 0; u < EPT; ++u) {
+        const int e = t + G * u;
+        if (e < NM * NM) {
+            const int i = e % NM, c = e / NM;
+            if (i < n && c < n) vec[k * mmo + i + c * n] = cscale(sm.invd[i], A[i][c]);
+        }
+    }
+    for (int i = t; i < n; i += G) eig[k * n + i] = sm.d[i];
+}
+
 }  // namespace
 
 // Threads of a group own matrix entries e = t + G*u (row e % NM, column e / NM); the
 // Householder mat-vec uses TPR = G / NM threads per row.
-template <int NM, int G, int BS>
+template <int NM, int G, int BS, bool VEC>
 __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double2* __restrict__ Hb,
                                                 const double2* __restrict__ Sb, double* __restrict__ eig,
-                                                unsigned long long* fail_key, int periodic_checks, PencilDft dft) {
+                                                unsigned long long* fail_key, int periodic_checks, PencilDft dft,
+                                                double2* __restrict__ vec) {
     constexpr int PPC = BS / G;                 // pencils per CTA
     constexpr int EPT = (NM * NM + G - 1) / G;  // matrix entries per thread
     constexpr int TPR = G / NM;                 // mat-vec threads per row
@@ -323,6 +522,10 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
         gsync<G>(slot);
     }
     PPROF(4);
+    if constexpr (VEC) {
+        pencil_vectors<NM, G, EPT>(sm, n, t, slot, k, eig, vec);
+        return;
+    }
     // 4. Householder tridiagonalisation of the leading n x n block (zhetd2, lower)
     const int row = t / TPR, part = t % TPR;
     for (int kk = 0; kk + 1 < n; ++kk) {
@@ -475,22 +678,22 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
     PPROF(6);
 }
 
-template <int NM, int G, int BS>
+template <int NM, int G, int BS, bool VEC>
 static void run_pencil(const Launch& L, Index count, Index m0, const double2* H, const double2* S, double* eig,
-                       unsigned long long* fail_key, bool checks, const PencilDft& dft) {
+                       unsigned long long* fail_key, bool checks, const PencilDft& dft, double2* vec) {
     static_assert(BS % G == 0 && (G <= 32 || G % 32 == 0), "group layout");
     constexpr int PPC = BS / G;
     const size_t smem = sizeof(PSmem<NM>) * PPC;
     static bool attr = false;
     if (!attr) {
-        LT_CU(cudaFuncSetAttribute(k_pencil<NM, G, BS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        LT_CU(cudaFuncSetAttribute(k_pencil<NM, G, BS, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem)));
         attr = true;
     }
     const Index blocks = (count + PPC - 1) / PPC;
     Stage st_(L, "pencil");
-    k_pencil<NM, G, BS><<<static_cast<unsigned>(blocks), BS, smem, L.st>>>(count, static_cast<int>(m0), H, S, eig,
-                                                                            fail_key, checks ? 1 : 0, dft);
+    k_pencil<NM, G, BS, VEC><<<static_cast<unsigned>(blocks), BS, smem, L.st>>>(
+        count, static_cast<int>(m0), H, S, eig, fail_key, checks ? 1 : 0, dft, vec);
     LT_CU(cudaGetLastError());
     L.tick();
 }
@@ -499,20 +702,27 @@ static void run_pencil(const Launch& L, Index count, Index m0, const double2* H,
 // only pay off for m0 <= 8 batches that cannot fill the GPU (16 multisection points per
 // eigenvalue instead of 4); for larger blocks the extra threads lengthen every barrier of
 // the Cholesky/Householder chains more than they shorten the bisection.
-void launch_pencil(const Launch& L, Index count, Index m0, const double2* H, const double2* S, double* eig,
-                   unsigned long long* fail_key, bool periodic_checks, const PencilDft& dft) {
-    if (count <= 0) return;
-    if (dft.nc > kPencilDftMax) fail(LT_EGENERIC, "pencil_eig: fused DFT supports at most 64 stored offsets");
+template <bool VEC>
+static void dispatch_pencil(const Launch& L, Index count, Index m0, const double2* H, const double2* S, double* eig,
+                            unsigned long long* fail_key, bool periodic_checks, const PencilDft& dft, double2* vec) {
     if (m0 <= 8) {
-        if (count <= 1184) run_pencil<8, 128, 256>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft);
-        else run_pencil<8, 32, 256>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft);
+        if (count <= 1184) run_pencil<8, 128, 256, VEC>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft, vec);
+        else run_pencil<8, 32, 256, VEC>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft, vec);
     } else if (m0 <= 16) {
-        run_pencil<16, 64, 256>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft);
+        run_pencil<16, 64, 256, VEC>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft, vec);
     } else if (m0 <= 32) {
-        run_pencil<32, 256, 256>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft);
+        run_pencil<32, 256, 256, VEC>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft, vec);
     } else {
         fail(LT_EDIM, "pencil_eig: block size m0 > 32 is not supported by the batched solver");
     }
+}
+
+void launch_pencil(const Launch& L, Index count, Index m0, const double2* H, const double2* S, double* eig,
+                   unsigned long long* fail_key, bool periodic_checks, const PencilDft& dft, double2* vec) {
+    if (count <= 0) return;
+    if (dft.nc > kPencilDftMax) fail(LT_EGENERIC, "pencil_eig: fused DFT supports at most 64 stored offsets");
+    if (vec) dispatch_pencil<true>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft, vec);
+    else dispatch_pencil<false>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft, nullptr);
 }
 
 }  // namespace lt

@@ -11,6 +11,8 @@
 #include "lt_device.cuh"
 #include "lt_internal.cuh"
 
+#include <cmath>
+
 namespace lt {
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
@@ -91,6 +93,46 @@ void launch_dft_axis2(const Launch& L, const DftAxisArgs& a, int nops) {
     dim3 grid(static_cast<unsigned>(a.Lax), nops, static_cast<unsigned>(chunks));
     Stage st_(L, "dft_axis");
     k_dft_axis2<<<grid, 256, sizeof(double2) * a.ncomp, L.st>>>(a);
+    LT_CU(cudaGetLastError());
+    L.tick();
+}
+
+// Full-space eigenvectors (block_circulant.cpp:267-289, eigensolver.cpp:164-175):
+// out[(i m0 + r) + col N] = L^-1/2 e^{i phi(i, j)} u_{j,m}[r] for columns col = j m0 + m in
+// [c0, c0 + ncols), phi = sum_l 2 pi (i_l j_l) / L_l accumulated as the reference does.
+// One thread per output entry, rows fastest (coalesced column writes).
+__global__ void k_reconstruct(Index d0, Index d1, Index d2, Index m0, const double2* __restrict__ u, Index c0,
+                              Index ncols, double norm, double2* __restrict__ out) {
+    const Index N = d0 * d1 * d2 * m0;
+    const Index e = static_cast<Index>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= N * ncols) return;
+    const Index row = e % N, col = c0 + e / N;
+    const Index i = row / m0, r = row % m0, j = col / m0, m = col % m0;
+    const Index mi[3] = {i / (d1 * d2), (i / d2) % d1, i % d2};
+    const Index jm[3] = {j / (d1 * d2), (j / d2) % d1, j % d2};
+    const Index dims[3] = {d0, d1, d2};
+    const double two_pi = 6.283185307179586;
+    double phase = 0.0;
+    for (int l = 0; l < 3; ++l)
+        phase += two_pi * static_cast<double>(mi[l] * jm[l]) / static_cast<double>(dims[l]);
+    double sn, cs;
+    sincos(phase, &sn, &cs);
+    const double2 f = make_double2(norm * cs, norm * sn);
+    const double2 v = u[j * m0 * m0 + r + m * m0];
+    out[e] = make_double2(f.x * v.x - f.y * v.y, f.x * v.y + f.y * v.x);
+}
+
+void launch_reconstruct(const Launch& L, const Index* dims, Index m0, const double2* u, Index c0, Index ncols,
+                        double2* out) {
+    const Index N = dims[0] * dims[1] * dims[2] * m0;
+    const Index total = N * ncols;
+    if (total <= 0) return;
+    double norm = 1.0;
+    for (int l = 0; l < 3; ++l) norm *= static_cast<double>(dims[l]);
+    norm = 1.0 / std::sqrt(norm);
+    Stage st_(L, "reconstruct");
+    k_reconstruct<<<static_cast<unsigned>((total + 255) / 256), 256, 0, L.st>>>(dims[0], dims[1], dims[2], m0, u, c0,
+                                                                                 ncols, norm, out);
     LT_CU(cudaGetLastError());
     L.tick();
 }

@@ -439,6 +439,9 @@ struct DftAxisArgs {
     double2* out_buf[2] = {nullptr, nullptr};
 };
 void launch_dft_axis2(const Launch& L, const DftAxisArgs& a, int nops);
+// full-space eigenvector columns [c0, c0 + ncols) from the per-k blocks u (K m0 x m0 complex)
+void launch_reconstruct(const Launch& L, const Index* dims, Index m0, const double2* u, Index c0, Index ncols,
+                        double2* out);
 
 // batched Hermitian-definite pencils (eigensolver.cpp:72-93)
 // fused lattice DFT in the pencil load stage (single wrapped axis): generating blocks
@@ -453,7 +456,8 @@ struct PencilDft {
     const double* GS = nullptr;
 };
 void launch_pencil(const Launch& L, Index count, Index m0, const double2* H, const double2* S, double* eig,
-                   unsigned long long* fail_key, bool periodic_checks, const PencilDft& dft = PencilDft{});
+                   unsigned long long* fail_key, bool periodic_checks, const PencilDft& dft = PencilDft{},
+                   double2* vec = nullptr);  // vec: K m0 x m0 complex eigenvector blocks (vector mode)
 
 // combine (eigensolver.cpp:37-67) on device buffers with index maps
 void launch_axpby_map(const Launch& L, Index nout, Index mm, double wa, const double* a, const int64_t* ia, double wb,

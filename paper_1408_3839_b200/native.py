@@ -95,6 +95,13 @@ def lib():
             "lt_block_diagonalize": ([_vp, _ip, _i64, _i64, _ip, _dp, _dp], ctypes.c_int),
             "lt_solve_box_dense": ([_vp, _i64, _dp, _dp, _i64, _dp], ctypes.c_int),
             "lt_pencil_eig": ([_vp, _i64, _i64, _dp, _dp, _dp], ctypes.c_int),
+            "lt_solve_box_dense_vectors": ([_vp, _i64, _dp, _dp, _i64, _dp, _dp], ctypes.c_int),
+            "lt_pencil_eigvec": ([_vp, _i64, _i64, _dp, _dp, _dp, _dp], ctypes.c_int),
+            "lt_solve_periodic_ops_vectors": ([_vp, _vp, _vp, _dp, _dp], ctypes.c_int),
+            "lt_solve_periodic_vectors": ([_vp, _ip, _i64, _i64, _ip, _dp, _i64, _ip, _dp, _dp, _dp], ctypes.c_int),
+            "lt_solve_periodic_factorized_vectors": ([_vp, _vp, _vp, ctypes.c_double, _dp, _dp], ctypes.c_int),
+            "lt_reconstruct_eigenvectors": ([_vp, _ip, _i64, _dp, _i64, _dp], ctypes.c_int),
+            "lt_bc_full_eigenvector": ([_vp, _ip, _i64, _dp, _i64, _i64, _dp], ctypes.c_int),
             "lt_sinc_quadrature": ([_vp, _i64, _dp, _dp], ctypes.c_int),
             "lt_overlap_constant": ([_vp, _vp, _ip], ctypes.c_int),
             "lt_newton_master": ([_vp, _i64, _d, _i64, _dp], ctypes.c_int),
@@ -124,6 +131,8 @@ EXPORTS = (
     "lt_solve_periodic_factorized_gen", "lt_factorized_block_diagonalize", "lt_box_circulant_defect", "lt_solve_core", "lt_sys_upload",
     "lt_sys_free", "lt_solve_core_dev", "lt_assemble", "lt_assemble_core", "lt_combine", "lt_op_free", "lt_op_info",
     "lt_op_dense", "lt_op_blocks", "lt_solve_periodic_ops", "lt_solve_periodic", "lt_block_diagonalize",
-    "lt_solve_box_dense", "lt_pencil_eig", "lt_sinc_quadrature", "lt_overlap_constant", "lt_newton_master",
+    "lt_solve_box_dense", "lt_pencil_eig", "lt_solve_box_dense_vectors", "lt_pencil_eigvec",
+    "lt_solve_periodic_ops_vectors", "lt_solve_periodic_vectors", "lt_solve_periodic_factorized_vectors",
+    "lt_reconstruct_eigenvectors", "lt_bc_full_eigenvector", "lt_sinc_quadrature", "lt_overlap_constant", "lt_newton_master",
     "lt_potential", "lt_assembled_window_sum", "lt_profiles",
 )
