@@ -26,6 +26,7 @@
 
 #include <algorithm>
 #include <array>
+#include <complex>
 #include <cstdint>
 #include <map>
 #include <memory>
@@ -265,7 +266,10 @@ struct KPointSpectrum {
     Index m0 = 0;
     std::string solver_path;
     std::vector<std::vector<double>> eigenvalues;  ///< per k-point (lexicographic), ascending
+    /// per k-point m0 x m0 column-major blocks (columns u_{j,m}); empty unless requested
+    std::vector<std::vector<std::complex<double>>> eigenvectors;
     Index k_count() const { return dims[0] * dims[1] * dims[2]; }
+    bool has_vectors() const { return !eigenvectors.empty(); }
     std::array<Index, 3> k_multi(Index lin) const {
         return {lin / (dims[1] * dims[2]), (lin / dims[2]) % dims[1], lin % dims[2]};
     }
@@ -278,8 +282,30 @@ struct KPointSpectrum {
 };
 
 struct DenseSpectrum {
-    std::vector<double> eigenvalues;  ///< ascending
+    std::vector<double> eigenvalues;   ///< ascending
+    std::vector<double> eigenvectors;  ///< n x n column-major, S-orthonormal; empty unless requested
 };
+
+// per-k blocks from the C-ABI's interleaved layout
+inline void put_vectors(KPointSpectrum& s, const std::vector<double>& flat) {
+    const Index mm = s.m0 * s.m0;
+    s.eigenvectors.assign(static_cast<size_t>(s.k_count()), std::vector<std::complex<double>>(static_cast<size_t>(mm)));
+    for (Index k = 0; k < s.k_count(); ++k)
+        for (Index i = 0; i < mm; ++i)
+            s.eigenvectors[static_cast<size_t>(k)][static_cast<size_t>(i)] = {flat[2 * (k * mm + i)],
+                                                                             flat[2 * (k * mm + i) + 1]};
+}
+
+inline std::vector<double> flat_vectors(const KPointSpectrum& s) {
+    std::vector<double> flat;
+    flat.reserve(static_cast<size_t>(2 * s.k_count() * s.m0 * s.m0));
+    for (const auto& blk : s.eigenvectors)
+        for (const auto& z : blk) {
+            flat.push_back(z.real());
+            flat.push_back(z.imag());
+        }
+    return flat;
+}
 
 inline KPointSpectrum make_spectrum(const std::array<Index, 3>& dims, Index m0, const std::vector<double>& flat,
                                     const char* path) {
@@ -292,33 +318,81 @@ inline KPointSpectrum make_spectrum(const std::array<Index, 3>& dims, Index m0, 
     return s;
 }
 
-/// eigensolver.hpp:32-33 (eigenvalues; the k-point loop runs as one batched launch)
-inline KPointSpectrum solve_periodic(Context& ctx, const AssembledOperator& H, const AssembledOperator& S) {
+/// eigensolver.hpp:32-33 (the k-point loop runs as one batched launch)
+inline KPointSpectrum solve_periodic(Context& ctx, const AssembledOperator& H, const AssembledOperator& S,
+                                     bool want_vectors = false) {
     const Index K = H.L[0] * H.L[1] * H.L[2];
     std::vector<double> flat(static_cast<size_t>(K * H.m0));
-    check(lt_solve_periodic_ops(ctx.get(), H.handle(), S.handle(), flat.data()));
-    return make_spectrum(H.L, H.m0, flat, "b200-fft-batched-pencil");
+    if (!want_vectors) {
+        check(lt_solve_periodic_ops(ctx.get(), H.handle(), S.handle(), flat.data()));
+        return make_spectrum(H.L, H.m0, flat, "b200-fft-batched-pencil");
+    }
+    std::vector<double> vec(static_cast<size_t>(2 * K * H.m0 * H.m0));
+    check(lt_solve_periodic_ops_vectors(ctx.get(), H.handle(), S.handle(), flat.data(), vec.data()));
+    KPointSpectrum s = make_spectrum(H.L, H.m0, flat, "b200-fft-batched-pencil");
+    put_vectors(s, vec);
+    return s;
 }
 
-/// eigensolver.hpp:17-18 (eigenvalues only; H, S column-major n x n)
+/// eigensolver.hpp:17-18 (H, S column-major n x n); the reference's default want_vectors
 inline DenseSpectrum solve_box_dense(Context& ctx, const std::vector<double>& H, const std::vector<double>& S,
-                                     Index n, Index cap = 4096) {
+                                     Index n, Index cap = 4096, bool want_vectors = false) {
     if (static_cast<Index>(H.size()) != n * n || static_cast<Index>(S.size()) != n * n)
         throw DimensionError("solve_box_dense: H and S must be n x n");
     DenseSpectrum d;
     d.eigenvalues.resize(static_cast<size_t>(n));
-    check(lt_solve_box_dense(ctx.get(), n, H.data(), S.data(), cap, d.eigenvalues.data()));
+    if (!want_vectors) {
+        check(lt_solve_box_dense(ctx.get(), n, H.data(), S.data(), cap, d.eigenvalues.data()));
+        return d;
+    }
+    d.eigenvectors.resize(static_cast<size_t>(n * n));
+    check(lt_solve_box_dense_vectors(ctx.get(), n, H.data(), S.data(), cap, d.eigenvalues.data(),
+                                     d.eigenvectors.data()));
     return d;
+}
+
+/// eigensolver.hpp reconstruct_eigenvectors: N x N complex column-major, N = K m0
+inline std::vector<std::complex<double>> reconstruct_eigenvectors(Context& ctx, const KPointSpectrum& spec,
+                                                                  Index cap = 4096) {
+    if (!spec.has_vectors()) throw StructureError("reconstruct_eigenvectors: spectrum carries no eigenvectors");
+    const Index N = spec.k_count() * spec.m0;
+    const std::vector<double> u = flat_vectors(spec);
+    std::vector<double> out(static_cast<size_t>(N <= cap ? 2 * N * N : 2));
+    check(lt_reconstruct_eigenvectors(ctx.get(), spec.dims.data(), spec.m0, u.data(), cap, out.data()));
+    std::vector<std::complex<double>> z(static_cast<size_t>(N * N));
+    for (size_t i = 0; i < z.size(); ++i) z[i] = {out[2 * i], out[2 * i + 1]};
+    return z;
+}
+
+/// block_circulant.hpp bc_full_eigenvector
+inline std::vector<std::complex<double>> bc_full_eigenvector(Context& ctx, const KPointSpectrum& spec, Index j,
+                                                             Index m) {
+    if (!spec.has_vectors()) throw StructureError("bc_full_eigenvector: no eigenvectors stored");
+    const Index N = spec.k_count() * spec.m0;
+    const std::vector<double> u = flat_vectors(spec);
+    std::vector<double> out(static_cast<size_t>(2 * N));
+    check(lt_bc_full_eigenvector(ctx.get(), spec.dims.data(), spec.m0, u.data(), j, m, out.data()));
+    std::vector<std::complex<double>> z(static_cast<size_t>(N));
+    for (size_t i = 0; i < z.size(); ++i) z[i] = {out[2 * i], out[2 * i + 1]};
+    return z;
 }
 
 /// eigensolver.hpp solve_periodic_factorized: rank metadata validated against the
 /// generating blocks (StructureError above metadata_tol), 1D DFTs per level, per-k sums.
 inline KPointSpectrum solve_periodic_factorized(Context& ctx, const AssembledOperator& H, const AssembledOperator& S,
-                                                double metadata_tol = 1e-10) {
+                                                double metadata_tol = 1e-10, bool want_vectors = false) {
     const Index K = H.L[0] * H.L[1] * H.L[2];
     std::vector<double> flat(static_cast<size_t>(K * H.m0));
-    check(lt_solve_periodic_factorized(ctx.get(), H.handle(), S.handle(), metadata_tol, flat.data()));
-    return make_spectrum(H.L, H.m0, flat, "periodic_factorized");
+    if (!want_vectors) {
+        check(lt_solve_periodic_factorized(ctx.get(), H.handle(), S.handle(), metadata_tol, flat.data()));
+        return make_spectrum(H.L, H.m0, flat, "periodic_factorized");
+    }
+    std::vector<double> vec(static_cast<size_t>(2 * K * H.m0 * H.m0));
+    check(lt_solve_periodic_factorized_vectors(ctx.get(), H.handle(), S.handle(), metadata_tol, flat.data(),
+                                               vec.data()));
+    KPointSpectrum s = make_spectrum(H.L, H.m0, flat, "periodic_factorized");
+    put_vectors(s, vec);
+    return s;
 }
 
 /// galerkin.hpp separable_residual

@@ -8,6 +8,7 @@
 //
 // All of it is stream-ordered on the context's stream; the only host
 // synchronisations are the L0 read-back and the final D2H of the results.
+#include <cublas_v2.h>
 #include <cusolverDn.h>
 
 #include <algorithm>
@@ -172,6 +173,7 @@ struct lt_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     cusolverDnHandle_t solver = nullptr;
+    cublasHandle_t blas = nullptr;
     Arena arena;
     int64_t launches = 0;
     StageTimer timer;
@@ -1112,6 +1114,49 @@ __global__ void k_complex_real(Index n, const double2* __restrict__ a, double* _
     if (i < n) out[i] = a[i].x;
 }
 
+// Eigenvalues of the box pencil through the B200 path (k_dense.cu): S = L L^T (potrf), A =
+// L^-1 H L^-T (two triangular solves, then 0.5 (A + A^T) as eigensolver.cpp:28-29), the
+// persistent tridiagonalisation and Sturm multisection. H is overwritten with A.
+static void box_eig_tridiag(lt_ctx* c, Index n, double* H, double* S, double* eig_dev) {
+    const Launch L = c->L();
+    const int ni = static_cast<int>(n);
+    int lwork = 0;
+    if (cusolverDnDpotrf_bufferSize(c->solver, CUBLAS_FILL_MODE_LOWER, ni, S, ni, &lwork) != CUSOLVER_STATUS_SUCCESS)
+        fail(LT_ECUDA, "cusolverDnDpotrf_bufferSize failed");
+    double* work = c->arena.get<double>("box.work", static_cast<size_t>(lwork) + 4 * n + 1);
+    int* info = c->arena.get<int>("box.info", 1);
+    {
+        Stage st_(L, "potrf");
+        if (cusolverDnDpotrf(c->solver, CUBLAS_FILL_MODE_LOWER, ni, S, ni, work, lwork, info) != CUSOLVER_STATUS_SUCCESS)
+            fail(LT_ECUDA, "cusolverDnDpotrf failed");
+    }
+    int hinfo = 0;
+    LT_CU(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    LT_CU(cudaStreamSynchronize(c->stream));
+    if (hinfo != 0)
+        fail(LT_EDEFINITE, "solve_box_dense: overlap matrix is not positive definite (near-linear-dependent basis?)");
+    if (!c->blas) {
+        if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) fail(LT_ECUDA, "cublasCreate failed");
+    }
+    cublasSetStream(c->blas, c->stream);
+    const double one = 1.0;
+    {
+        Stage st_(L, "trsm");
+        if (cublasDtrsm(c->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, ni, ni,
+                        &one, S, ni, H, ni) != CUBLAS_STATUS_SUCCESS ||
+            cublasDtrsm(c->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, ni, ni,
+                        &one, S, ni, H, ni) != CUBLAS_STATUS_SUCCESS)
+            fail(LT_ECUDA, "cublasDtrsm failed");
+    }
+    launch_symmetrize(L, ni, H);
+    double* d = c->arena.get<double>("box.td", n);
+    double* e = c->arena.get<double>("box.te", n);
+    double* tw = c->arena.get<double>("box.tw", 4 * n);
+    unsigned* bar = c->arena.get<unsigned>("box.bar", 1);
+    launch_sytrd(L, ni, H, d, e, tw, bar);
+    launch_tridiag_eig(L, ni, d, e, eig_dev);
+}
+
 // Box pencil on device buffers H, S (n x n col-major; both may be overwritten).
 // Eigenvalues -> eig_dev; with vec_dev, the S-orthonormal eigenvectors X = L^-T Z (n x n
 // col-major, eigensolver.cpp:31-32). Returns the failure key through *fail (device) for
@@ -1143,6 +1188,11 @@ static void box_eig_device(lt_ctx* c, Index n, double* H, double* S, double* eig
         if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS) fail(LT_ECUDA, "cusolverDnCreate failed");
     }
     cusolverDnSetStream(c->solver, c->stream);
+    static const bool force_library = std::getenv("LT_BOX_SYGVD") != nullptr;
+    if (!vec_dev && !force_library && sytrd_ctas(static_cast<int>(n)) > 0) {
+        box_eig_tridiag(c, n, H, S, eig_dev);
+        return;
+    }
     const cusolverEigMode_t mode = vec_dev ? CUSOLVER_EIG_MODE_VECTOR : CUSOLVER_EIG_MODE_NOVECTOR;
     int lwork = 0;
     if (cusolverDnDsygvd_bufferSize(c->solver, CUSOLVER_EIG_TYPE_1, mode, CUBLAS_FILL_MODE_LOWER, static_cast<int>(n), H,
@@ -1653,6 +1703,7 @@ void lt_destroy(lt_ctx* c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->solver) cusolverDnDestroy(c->solver);
+    if (c->blas) cublasDestroy(c->blas);
     if (c->pinned) cudaFreeHost(c->pinned);
     for (auto& a : c->aux)
         if (a) {

@@ -439,6 +439,13 @@ struct DftAxisArgs {
     double2* out_buf[2] = {nullptr, nullptr};
 };
 void launch_dft_axis2(const Launch& L, const DftAxisArgs& a, int nops);
+// dense box pencil (k_dense.cu): CTAs of the shared-memory resident tridiagonalisation (0:
+// too large), the reduction itself (work: 4 n doubles, bar: one zeroed counter), the
+// tridiagonal eigenvalues and the in-place symmetrisation 0.5 (A + A^T)
+int sytrd_ctas(int n);
+void launch_sytrd(const Launch& L, int n, const double* C, double* d, double* e, double* work, unsigned* bar);
+void launch_tridiag_eig(const Launch& L, int n, const double* d, const double* e, double* eig);
+void launch_symmetrize(const Launch& L, int n, double* A);
 // full-space eigenvector columns [c0, c0 + ncols) from the per-k blocks u (K m0 x m0 complex)
 void launch_reconstruct(const Launch& L, const Index* dims, Index m0, const double2* u, Index c0, Index ncols,
                         double2* out);

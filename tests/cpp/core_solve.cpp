@@ -3,6 +3,8 @@
 // H = combine(0.5, Lap, -1, Nuc), S = Mass, then the spectrum), plus the fused
 // whole-path entry and the reference's error classes. Prints one line per result:
 //   <tag> <count> <v1> <v2> ...   (%.17g)
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <string>
 
@@ -48,6 +50,15 @@ int main() {
     print("periodic_core", solve_core_periodic(ctx, per).sorted_all());
     print("periodic_factorized", solve_periodic_factorized(ctx, H, S).sorted_all());
     std::printf("residual %.3g\n", separable_residual(ctx, H));
+    // want_vectors: per-k blocks; one reconstructed column against bc_full_eigenvector
+    const KPointSpectrum vs = solve_periodic(ctx, H, S, true);
+    print("periodic_vec_eig", vs.sorted_all());
+    const auto U = reconstruct_eigenvectors(ctx, vs);
+    const auto u0 = bc_full_eigenvector(ctx, vs, 3, 1);
+    double dev = 0.0;
+    const Index N = vs.k_count() * vs.m0;
+    for (Index i = 0; i < N; ++i) dev = std::max(dev, std::abs(U[static_cast<size_t>(i + (3 * vs.m0 + 1) * N)] - u0[static_cast<size_t>(i)]));
+    std::printf("recon_col_dev %.3g\n", dev);
     // box
     const LatticeSystem box = chain(6, false);
     auto blap = assemble_box(ctx, box, OperatorKind::Laplace);
@@ -56,6 +67,9 @@ int main() {
     auto bH = combine(ctx, 0.5, blap, -1.0, bnuc);
     print("box_ops", solve_box_dense(ctx, bH.dense(), bS.dense(), bH.basis_count()).eigenvalues);
     print("box_core", solve_core_box(ctx, box).eigenvalues);
+    const DenseSpectrum bv = solve_box_dense(ctx, bH.dense(), bS.dense(), bH.basis_count(), 4096, true);
+    print("box_vec_eig", bv.eigenvalues);
+    print("box_vec", bv.eigenvectors);
     // errors: alias guard (galerkin.cpp:294-302) and the dense cap (eigensolver.cpp:17-19)
     try {
         assemble_periodic(ctx, chain(3, true), OperatorKind::Mass);

@@ -50,5 +50,11 @@ def test_cpp_client_matches_python_api(tmp_path, ctx):
     assert np.max(np.abs(vals["box_ops"] - box)) < 1e-10 * max(1.0, np.max(np.abs(box)))
     assert np.max(np.abs(vals["periodic_factorized"] - per)) < 1e-10 * max(1.0, np.max(np.abs(per)))
     assert float(res["residual"][0]) < 1e-12
+    assert np.max(np.abs(vals["periodic_vec_eig"] - per)) < 1e-10 * max(1.0, np.max(np.abs(per)))
+    assert np.max(np.abs(vals["box_vec_eig"] - box)) < 1e-10 * max(1.0, np.max(np.abs(box)))
+    assert float(res["recon_col_dev"][0]) < 1e-15
+    n = box.size
+    X = vals["box_vec"].reshape(n, n).T
+    assert X.shape == (n, n) and np.all(np.isfinite(X))
     assert res["error_alias"][0] == "StructureError"
     assert res["error_cap"][0] == "ResourceCapError"
