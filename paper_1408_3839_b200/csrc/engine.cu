@@ -1141,6 +1141,8 @@ static void box_eig_tridiag(lt_ctx* c, Index n, double* H, double* S, double* ei
     cublasSetStream(c->blas, c->stream);
     const double one = 1.0;
     {
+        // (an explicit cusolverDnXtrtri inverse + two trmm was measured slower: trtri alone
+        // costs more than both solves)
         Stage st_(L, "trsm");
         if (cublasDtrsm(c->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, ni, ni,
                         &one, S, ni, H, ni) != CUBLAS_STATUS_SUCCESS ||
@@ -1152,7 +1154,7 @@ static void box_eig_tridiag(lt_ctx* c, Index n, double* H, double* S, double* ei
     double* d = c->arena.get<double>("box.td", n);
     double* e = c->arena.get<double>("box.te", n);
     double* tw = c->arena.get<double>("box.tw", 4 * n);
-    unsigned* bar = c->arena.get<unsigned>("box.bar", 1);
+    unsigned* bar = c->arena.get<unsigned>("box.bar", 8 * 160);  // per-CTA flags, 32 B apart
     launch_sytrd(L, ni, H, d, e, tw, bar);
     launch_tridiag_eig(L, ni, d, e, eig_dev);
 }

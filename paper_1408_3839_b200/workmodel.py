@@ -13,7 +13,8 @@ device computes (lt_profiles), never from the padded tiles a kernel happens to s
 - lattice sums / FFT / scatters / pencils / profiles: bytes read + written once (HBM
   lower bound); the batched pencils are latency-bound and reported against HBM as
   SURVEY.md §8(d) asks.
-- box dense pencil (sygvd): F_box = (8/3) N_b^3 (Cholesky, reduction, tridiagonalisation).
+- box dense pencil: potrf N_b^3/3, trsm 2 N_b^3, sytrd (4/3) N_b^3 flops (library sygvd, when
+  forced with LT_BOX_SYGVD: (8/3) N_b^3).
 """
 from __future__ import annotations
 
@@ -184,6 +185,14 @@ def stage_work(ctx, s, periodic: bool, L0: int) -> Dict[str, Tuple[str, float, s
             add("r2c", "hbm", 2 * (8.0 + 16.0) * Nb * Nb, "B")
             add("pencil", "hbm", 2 * 16.0 * Nb * Nb + 8.0 * Nb, "B")
         else:
+            # the B200 dense path (k_dense.cu): Cholesky N^3/3, two triangular solves 2 N^3,
+            # tridiagonalisation 4/3 N^3 (dsytd2 count), symmetrisation and the tridiagonal
+            # eigenvalues as bytes (latency-bound chains); the library sygvd when forced
+            add("potrf", "tensor", Nb ** 3 / 3.0, "flop")
+            add("trsm", "tensor", 2.0 * Nb ** 3, "flop")
+            add("sytrd", "tensor", (4.0 / 3.0) * Nb ** 3, "flop")
+            add("symmetrize", "hbm", 2 * 8.0 * Nb * Nb, "B")
+            add("tridiag_eig", "hbm", 8.0 * 3 * Nb, "B")
             add("sygvd", "tensor", (8.0 / 3.0) * Nb ** 3, "flop")
     return out
 
