@@ -174,6 +174,7 @@ struct lt_ctx {
     cudaStream_t stream = nullptr;
     cusolverDnHandle_t solver = nullptr;
     cublasHandle_t blas = nullptr;
+    unsigned* pencil_done = nullptr;  // self-resetting arrival counter of the in-kernel read-back
     Arena arena;
     int64_t launches = 0;
     StageTimer timer;
@@ -1164,7 +1165,7 @@ static void box_eig_tridiag(lt_ctx* c, Index n, double* H, double* S, double* ei
 // col-major, eigensolver.cpp:31-32). Returns the failure key through *fail (device) for
 // the batched-pencil path.
 static void box_eig_device(lt_ctx* c, Index n, double* H, double* S, double* eig_dev, unsigned long long* fail_dev,
-                           double* vec_dev = nullptr) {
+                           double* vec_dev = nullptr, const PencilReadback& rb = PencilReadback{}) {
     const Launch L = c->L();
     if (n <= 32) {
         double2* hc = c->arena.get<double2>("box.hc", n * n);
@@ -1177,7 +1178,7 @@ static void box_eig_device(lt_ctx* c, Index n, double* H, double* S, double* eig
             L.tick(2);
         }
         double2* vc = vec_dev ? c->arena.get<double2>("box.vc", n * n) : nullptr;
-        launch_pencil(L, 1, n, hc, sc, eig_dev, fail_dev, false, PencilDft{}, vc);
+        launch_pencil(L, 1, n, hc, sc, eig_dev, fail_dev, false, PencilDft{}, vc, rb);
         if (vec_dev) {  // real symmetric input: the Jacobi rotations stay real
             Stage st_(L, "c2r");
             k_complex_real<<<static_cast<unsigned>((n * n + 255) / 256), 256, 0, c->stream>>>(n * n, vc, vec_dev);
@@ -1318,11 +1319,17 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
     const int64_t* s0d = cp.s0d;
     const DftPrep& dp = cp.dp;
     // device work after L0 (with L0 in front under speculation): kernels and memsets only
+    // eigenvalues straight into the pinned staging buffer (host API) and the result block
+    // copied by the pencil kernel's last group: no copy nodes at the end of the graph
+    static const bool no_kr = std::getenv("LT_NO_KERNEL_READBACK") != nullptr;  // A/B switch
+    double* eig_out = (epin && !no_kr) ? static_cast<double*>(epin) : eig_dev;
+    const bool kernel_readback = !no_kr && inline_readback && (small_box || k_begin < k_end);
+    PencilReadback rb;
+    if (kernel_readback) rb = PencilReadback{ret, rpin, c->pencil_done};
     auto enqueue = [&]() {
-        if (spec)  // k_l0_init also resets the failure key
-            l0w.enqueue(c->L(), 1, static_cast<int>(L0) + 3, true);
-        else
-            LT_CU(cudaMemsetAsync(fk, 0xff, sizeof(unsigned long long), c->stream));
+        // k_l0_init resets the failure key: in front of this graph under speculation, else in
+        // the L0 graph that just ran
+        if (spec) l0w.enqueue(c->L(), 1, static_cast<int>(L0) + 3, true);
         run_assembly(c, sd, p, NEED_MS | NEED_NUC, 0, out, nullptr, s0d);
         if (periodic) {
             int wrapped = 0, ax = -1;
@@ -1345,8 +1352,8 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
                 f.GH = out.out0;
                 f.GS = out.out1;
                 if (k_begin < k_end)
-                    launch_pencil(c->L(), k_end - k_begin, p.m0, nullptr, nullptr, eig_dev + k_begin * p.m0, fk, true,
-                                  f);
+                    launch_pencil(c->L(), k_end - k_begin, p.m0, nullptr, nullptr, eig_out + k_begin * p.m0, fk, true,
+                                  f, nullptr, rb);
             } else {
                 const double* blocks[2] = {out.out0, out.out1};
                 double2* bd[2];
@@ -1355,15 +1362,15 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
                 double2* Sb = bd[1];
                 if (k_begin < k_end)
                     launch_pencil(c->L(), k_end - k_begin, p.m0, Hb + k_begin * mm, Sb + k_begin * mm,
-                                  eig_dev + k_begin * p.m0, fk, true);
+                                  eig_out + k_begin * p.m0, fk, true, PencilDft{}, nullptr, rb);
             }
         } else if (small_box) {
-            box_eig_device(c, p.Nb, out.out0, out.out1, eig_dev, fk);
+            box_eig_device(c, p.Nb, out.out0, out.out1, eig_out, fk, nullptr, rb);
         }
-        if (inline_readback) {
+        if (inline_readback && !kernel_readback)  // (an empty k-point shard launches no pencil)
             LT_CU(cudaMemcpyAsync(rpin, ret, 8 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-            if (epin) LT_CU(cudaMemcpyAsync(epin, eig_dev, ebytes, cudaMemcpyDeviceToHost, c->stream));
-        }
+        if (inline_readback && epin && eig_out != epin)
+            LT_CU(cudaMemcpyAsync(epin, eig_dev, ebytes, cudaMemcpyDeviceToHost, c->stream));
     };
     c->phase_mark(2);
     c->host_mark(1);
@@ -1682,6 +1689,8 @@ lt_status lt_create(int device, lt_ctx** out) {
         LT_CU(cudaStreamCreateWithPriority(&c->aux[0], cudaStreamNonBlocking, prio_lo));
         LT_CU(cudaStreamCreateWithPriority(&c->aux[1], cudaStreamNonBlocking, prio_hi));
         for (auto& e : c->ev) LT_CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        LT_CU(cudaMalloc(&c->pencil_done, sizeof(unsigned)));
+        LT_CU(cudaMemset(c->pencil_done, 0, sizeof(unsigned)));
         const char* pt = std::getenv("LT_PHASE_TIMING");
         c->phase_timing = pt && pt[0] == '1';
         const char* ht = std::getenv("LT_HOST_TIMING");
@@ -1706,6 +1715,7 @@ void lt_destroy(lt_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->solver) cusolverDnDestroy(c->solver);
     if (c->blas) cublasDestroy(c->blas);
+    if (c->pencil_done) cudaFree(c->pencil_done);
     if (c->pinned) cudaFreeHost(c->pinned);
     for (auto& a : c->aux)
         if (a) {

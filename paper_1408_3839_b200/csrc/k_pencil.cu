@@ -337,13 +337,25 @@ __device__ void pencil_vectors(PSmem<NM>& sm, int n, int t, int slot, Index k, d
 
 }  // namespace
 
+// called once per finished pencil by its group leader (every exit path)
+__device__ __forceinline__ void group_done(const PencilReadback& rb, Index count) {
+    if (rb.done == nullptr) return;
+    __threadfence();  // this group's failure key update before its arrival
+    if (atomicAdd(rb.done, 1u) == static_cast<unsigned>(count - 1)) {
+        __threadfence();
+        const volatile int* src = rb.ret_dev;
+        for (int i = 0; i < 8; ++i) rb.ret_host[i] = src[i];
+        *rb.done = 0u;  // ready for the next launch or graph replay
+    }
+}
+
 // Threads of a group own matrix entries e = t + G*u (row e % NM, column e / NM); the
 // Householder mat-vec uses TPR = G / NM threads per row.
 template <int NM, int G, int BS, bool VEC>
 __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double2* __restrict__ Hb,
                                                 const double2* __restrict__ Sb, double* __restrict__ eig,
                                                 unsigned long long* fail_key, int periodic_checks, PencilDft dft,
-                                                double2* __restrict__ vec) {
+                                                double2* __restrict__ vec, PencilReadback rb) {
     constexpr int PPC = BS / G;                 // pencils per CTA
     constexpr int EPT = (NM * NM + G - 1) / G;  // matrix entries per thread
     constexpr int TPR = G / NM;                 // mat-vec threads per row
@@ -459,7 +471,10 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
         }
     }
     if (code != 0) {
-        if (t == 0) atomicMin(fail_key, static_cast<unsigned long long>(k) * 4ull + static_cast<unsigned long long>(code));
+        if (t == 0) {
+            atomicMin(fail_key, static_cast<unsigned long long>(k) * 4ull + static_cast<unsigned long long>(code));
+            group_done(rb, count);
+        }
         return;
     }
     for (int i = t; i < n; i += G) sm.invd[i] = 1.0 / sqrt(B[i][i].x);
@@ -524,6 +539,7 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
     PPROF(4);
     if constexpr (VEC) {
         pencil_vectors<NM, G, EPT>(sm, n, t, slot, k, eig, vec);
+        if (t == 0) group_done(rb, count);
         return;
     }
     // 4. Householder tridiagonalisation of the leading n x n block (zhetd2, lower)
@@ -676,11 +692,13 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
         if (active && sub == 0) eig[k * m0 + mi] = 0.5 * (a + b);
     }
     PPROF(6);
+    if (t == 0) group_done(rb, count);
 }
 
 template <int NM, int G, int BS, bool VEC>
 static void run_pencil(const Launch& L, Index count, Index m0, const double2* H, const double2* S, double* eig,
-                       unsigned long long* fail_key, bool checks, const PencilDft& dft, double2* vec) {
+                       unsigned long long* fail_key, bool checks, const PencilDft& dft, double2* vec,
+                       const PencilReadback& rb) {
     static_assert(BS % G == 0 && (G <= 32 || G % 32 == 0), "group layout");
     constexpr int PPC = BS / G;
     const size_t smem = sizeof(PSmem<NM>) * PPC;
@@ -693,7 +711,7 @@ static void run_pencil(const Launch& L, Index count, Index m0, const double2* H,
     const Index blocks = (count + PPC - 1) / PPC;
     Stage st_(L, "pencil");
     k_pencil<NM, G, BS, VEC><<<static_cast<unsigned>(blocks), BS, smem, L.st>>>(
-        count, static_cast<int>(m0), H, S, eig, fail_key, checks ? 1 : 0, dft, vec);
+        count, static_cast<int>(m0), H, S, eig, fail_key, checks ? 1 : 0, dft, vec, rb);
     LT_CU(cudaGetLastError());
     L.tick();
 }
@@ -704,25 +722,27 @@ static void run_pencil(const Launch& L, Index count, Index m0, const double2* H,
 // the Cholesky/Householder chains more than they shorten the bisection.
 template <bool VEC>
 static void dispatch_pencil(const Launch& L, Index count, Index m0, const double2* H, const double2* S, double* eig,
-                            unsigned long long* fail_key, bool periodic_checks, const PencilDft& dft, double2* vec) {
+                            unsigned long long* fail_key, bool periodic_checks, const PencilDft& dft, double2* vec,
+                            const PencilReadback& rb) {
     if (m0 <= 8) {
-        if (count <= 1184) run_pencil<8, 128, 256, VEC>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft, vec);
-        else run_pencil<8, 32, 256, VEC>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft, vec);
+        if (count <= 1184) run_pencil<8, 128, 256, VEC>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft, vec, rb);
+        else run_pencil<8, 32, 256, VEC>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft, vec, rb);
     } else if (m0 <= 16) {
-        run_pencil<16, 64, 256, VEC>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft, vec);
+        run_pencil<16, 64, 256, VEC>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft, vec, rb);
     } else if (m0 <= 32) {
-        run_pencil<32, 256, 256, VEC>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft, vec);
+        run_pencil<32, 256, 256, VEC>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft, vec, rb);
     } else {
         fail(LT_EDIM, "pencil_eig: block size m0 > 32 is not supported by the batched solver");
     }
 }
 
 void launch_pencil(const Launch& L, Index count, Index m0, const double2* H, const double2* S, double* eig,
-                   unsigned long long* fail_key, bool periodic_checks, const PencilDft& dft, double2* vec) {
+                   unsigned long long* fail_key, bool periodic_checks, const PencilDft& dft, double2* vec,
+                   const PencilReadback& rb) {
     if (count <= 0) return;
     if (dft.nc > kPencilDftMax) fail(LT_EGENERIC, "pencil_eig: fused DFT supports at most 64 stored offsets");
-    if (vec) dispatch_pencil<true>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft, vec);
-    else dispatch_pencil<false>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft, nullptr);
+    if (vec) dispatch_pencil<true>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft, vec, rb);
+    else dispatch_pencil<false>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft, nullptr, rb);
 }
 
 }  // namespace lt

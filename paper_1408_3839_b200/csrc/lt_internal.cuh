@@ -462,9 +462,18 @@ struct PencilDft {
     const double* GH = nullptr;
     const double* GS = nullptr;
 };
+// In-kernel read-back: the last pencil group to finish copies the 8-int result block
+// (L0 state, failure key) to pinned host memory, replacing a device-to-host copy node at
+// the end of the graph; `done` is a zeroed counter the kernel resets itself.
+struct PencilReadback {
+    const int* ret_dev = nullptr;
+    int* ret_host = nullptr;
+    unsigned* done = nullptr;
+};
 void launch_pencil(const Launch& L, Index count, Index m0, const double2* H, const double2* S, double* eig,
                    unsigned long long* fail_key, bool periodic_checks, const PencilDft& dft = PencilDft{},
-                   double2* vec = nullptr);  // vec: K m0 x m0 complex eigenvector blocks (vector mode)
+                   double2* vec = nullptr,  // vec: K m0 x m0 complex eigenvector blocks (vector mode)
+                   const PencilReadback& rb = PencilReadback{});
 
 // combine (eigensolver.cpp:37-67) on device buffers with index maps
 void launch_axpby_map(const Launch& L, Index nout, Index mm, double wa, const double* a, const int64_t* ia, double wb,
