@@ -6,8 +6,10 @@
 //
 //   latham_b200 {kernel|solve|bench|energy} --config FILE --out DIR
 //
-// All numerics run on the GPU through include/latham_b200.hpp. Eigenvectors are not part
-// of the B200 path: `solve.eigenvectors = true` is refused as a configuration error.
+// All numerics run on the GPU through include/latham_b200.hpp. `solve.eigenvectors = true`
+// writes eigenvectors_box.csv / eigenvectors_periodic.csv like commands.cpp:183-205 (box:
+// S-orthonormal columns of the dense pencil; periodic: reconstruct_eigenvectors under
+// caps.dense).
 #include <algorithm>
 #include <array>
 #include <chrono>
@@ -230,7 +232,6 @@ Experiment read_experiment(const std::string& path) {
     if ((x.cap_dense != kDenseCap || x.cap_materialize != kMaterializeCap) &&
         (x.cap_dense > kDenseCap || x.cap_materialize > kMaterializeCap) && !x.cap_ack)
         throw ConfigError("config: raising caps.dense or caps.materialize requires caps.acknowledge = true");
-    if (x.eigenvectors) throw ConfigError("config: solve.eigenvectors is not supported by the B200 path");
 
     auto put = [&](const char* k, const std::string& v) { x.resolved.emplace_back(k, v); };
     put("cell.b", shortest(x.b));
@@ -383,15 +384,42 @@ void run_solve(Context& ctx, const Experiment& x, const fs::path& out) {
         if (sys.basis_count() > x.cap_dense)
             throw ResourceCapError("solve_box_dense: size " + std::to_string(sys.basis_count()) +
                                    " exceeds dense cap " + std::to_string(x.cap_dense));
-        box_sorted = solve_core_box(ctx, sys).eigenvalues;
+        DenseSpectrum ds;
+        if (x.eigenvectors) {  // commands.cpp:176-178 with want_vectors
+            SystemView v(sys);
+            lt_operator *hp = nullptr, *sp = nullptr;
+            check(lt_assemble_core(ctx.get(), v.get(), 0, &hp, &sp));
+            AssembledOperator Hb(hp, OperatorKind::Laplace), Sb(sp, OperatorKind::Mass);
+            ds = solve_box_dense(ctx, Hb.dense(), Sb.dense(), sys.basis_count(), x.cap_dense, true);
+        } else {
+            ds = solve_core_box(ctx, sys);
+        }
+        box_sorted = ds.eigenvalues;
         Sheet f(out, "spectrum_box.csv", "solve", x);
         f << "k1,k2,k3,band,eigenvalue\n";
         for (size_t i = 0; i < box_sorted.size(); ++i) f << "-1,-1,-1," << i << "," << Sheet::num(box_sorted[i]) << "\n";
         f.land();
         bands_sheet(out, "bands_box.csv", x, chunk_bands(box_sorted, sys.m0(), sys.lattice_count()));
+        if (x.eigenvectors) {  // commands.cpp:183-190
+            const Index nb = sys.basis_count();
+            Sheet ev(out, "eigenvectors_box.csv", "solve", x);
+            ev << "index,component,value\n";
+            for (Index c = 0; c < nb; ++c)
+                for (Index r = 0; r < nb; ++r)
+                    ev << c << "," << r << "," << Sheet::num(ds.eigenvectors[static_cast<size_t>(c * nb + r)]) << "\n";
+            ev.land();
+        }
     }
     if (per) {
-        spec = solve_core_periodic(ctx, sys);
+        if (x.eigenvectors) {  // commands.cpp:192-194 with want_vectors
+            SystemView v(sys);
+            lt_operator *hp = nullptr, *sp = nullptr;
+            check(lt_assemble_core(ctx.get(), v.get(), 1, &hp, &sp));
+            AssembledOperator H(hp, OperatorKind::Laplace), S(sp, OperatorKind::Mass);
+            spec = solve_periodic(ctx, H, S, true);
+        } else {
+            spec = solve_core_periodic(ctx, sys);
+        }
         Sheet f(out, "spectrum_periodic.csv", "solve", x);
         f << "k1,k2,k3,band,eigenvalue\n";
         for (Index j = 0; j < spec.k_count(); ++j) {
@@ -402,6 +430,18 @@ void run_solve(Context& ctx, const Experiment& x, const fs::path& out) {
         }
         f.land();
         bands_sheet(out, "bands_periodic.csv", x, spectral_bands(spec));
+        if (x.eigenvectors) {  // commands.cpp:197-205
+            const Index N = spec.k_count() * spec.m0;
+            const std::vector<std::complex<double>> U = reconstruct_eigenvectors(ctx, spec, x.cap_dense);
+            Sheet ev(out, "eigenvectors_periodic.csv", "solve", x);
+            ev << "index,component,re,im\n";
+            for (Index c = 0; c < N; ++c)
+                for (Index r = 0; r < N; ++r) {
+                    const auto z = U[static_cast<size_t>(c * N + r)];
+                    ev << c << "," << r << "," << Sheet::num(z.real()) << "," << Sheet::num(z.imag()) << "\n";
+                }
+            ev.land();
+        }
     }
     if (box && per) {
         const DefectReport d = box_circulant_defect(ctx, sys);

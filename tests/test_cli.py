@@ -50,7 +50,6 @@ def test_config_errors_exit_two(tmp_path):
     assert run(tmp_path, "solve", "cell.b = 8\nnucleus = 7 0 0 1\nbasis = 0 0 0 0.3\n") == 2  # outside the cell
     assert run(tmp_path, "kernel", CHAIN + "lattice.L = 1 1 1\n") == 2  # duplicate key
     assert run(tmp_path, "solve", CHAIN + "caps.dense = 9000\n") == 2  # raised cap without acknowledgement
-    assert run(tmp_path, "solve", CHAIN + "solve.eigenvectors = true\n") == 2  # not on the B200 path
 
 
 def test_usage_errors(tmp_path):
@@ -103,6 +102,41 @@ def test_solve_both_files_defect_and_byte_identical_reruns(tmp_path, oracle):
     refb = oracle.solve_box_dense(Hb.dense, Sb.dense)
     gotb = np.array([float(r.split(",")[4]) for r in data_lines(tmp_path / "a" / "spectrum_box.csv")[1:]])
     assert np.max(np.abs(gotb - refb)) <= 1e-9 * max(1.0, np.max(np.abs(refb)))
+
+
+@pytest.mark.gpu
+def test_solve_eigenvectors_files(tmp_path, oracle):
+    """solve.eigenvectors = true (commands.cpp:183-205): eigenvectors_box.csv holds the
+    S-orthonormal pencil eigenvectors, eigenvectors_periodic.csv the reconstructed
+    lattice eigenvectors; both satisfy the generalised eigenproblem of the dense matrices."""
+    assert run(tmp_path, "solve", CHAIN + "solve.eigenvectors = true\n", out="v") == 0
+    assert run(tmp_path, "solve", CHAIN + "solve.eigenvectors = true\n", out="w") == 0
+    for f in ("eigenvectors_box.csv", "eigenvectors_periodic.csv", "spectrum_box.csv"):
+        assert (tmp_path / "v" / f).read_bytes() == (tmp_path / "w" / f).read_bytes(), f
+    s = LatticeSystem(b=8.0, L=(4, 1, 1), n=(8,) * 3, nbar=(8,) * 3, quad_M=10, nuc_pos=[(0, 0, 0)],
+                      nuc_charge=[1.0], bf_center=[(0, 0, 0)], bf_alpha=[0.3])
+    Hb, Sb = oracle.assemble_core(s, False)
+    rows = data_lines(tmp_path / "v" / "eigenvectors_box.csv")
+    assert rows[0] == "index,component,value" and len(rows) == 1 + 16
+    X = np.zeros((4, 4))
+    for r in rows[1:]:
+        c, i, v = r.split(",")
+        X[int(i), int(c)] = float(v)
+    lam = np.array([float(r.split(",")[4]) for r in data_lines(tmp_path / "v" / "spectrum_box.csv")[1:]])
+    assert np.max(np.abs(X.T @ Sb.dense @ X - np.eye(4))) < 1e-9
+    assert np.max(np.abs(Hb.dense @ X - Sb.dense @ X * lam)) < 1e-9 * max(1.0, np.max(np.abs(Hb.dense)))
+    rows = data_lines(tmp_path / "v" / "eigenvectors_periodic.csv")
+    assert rows[0] == "index,component,re,im" and len(rows) == 1 + 16
+    U = np.zeros((4, 4), dtype=complex)
+    for r in rows[1:]:
+        c, i, re, im = r.split(",")
+        U[int(i), int(c)] = float(re) + 1j * float(im)
+    H, S = oracle.assemble_core(s, True)
+    ev = oracle.solve_periodic_ops(H, S).reshape(-1)
+    from test_gpu_vectors import bc_to_dense
+    Hd, Sd = bc_to_dense(H.gen_dict(), (4, 1, 1), 1), bc_to_dense(S.gen_dict(), (4, 1, 1), 1)
+    assert np.max(np.abs(U.conj().T @ Sd @ U - np.eye(4))) < 1e-9
+    assert np.max(np.abs(Hd @ U - (Sd @ U) * ev)) < 1e-9 * max(1.0, np.max(np.abs(Hd)))
 
 
 @pytest.mark.gpu
