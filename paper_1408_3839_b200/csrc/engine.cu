@@ -599,6 +599,39 @@ static int64_t* upload_s0(lt_ctx* c, const Plan& p) {
 // nucT layout) instead of the fused reassociations; AS_NO_FILL stops after the tables.
 enum AsmFlags : unsigned { AS_GENERAL_NUC = 1u, AS_NO_FILL = 2u };
 
+// Cells [j0, j0 + J) of direction l's extended grid that hold every sampled support (pwl:
+// nbar grid, align 0; pwc: n grid, align 0.5; functions sit in cell `margin`, galerkin.cpp:
+// 127-149). A sample |x - c|^deg exp(-alpha (x - c)^2) survives the 1e-280 trim (k_profiles)
+// only if alpha r^2 <= 644.8 + deg ln r, so r <= sqrt((650 + deg ln(max(1, extent))) / alpha)
+// bounds it; one spare cell each side. The residue folds cover only this window: for long
+// periodic chains the extended grid is (L + 2 margin) cells, almost all of them empty.
+static void support_window(const HostSys& s, const Plan& p, int l, bool pwl, long long& j0, long long& J) {
+    const DirPlan& d = p.d[l];
+    const Index per = pwl ? d.nbar : d.n;
+    const double step = pwl ? d.hbar : d.h;
+    const long long cells = (pwl ? d.Gbar : d.G) / per;
+    const double align = pwl ? 0.0 : 0.5;
+    const double extent = step * static_cast<double>(cells * per) + s.b;
+    const double base = static_cast<double>(p.margin * per);
+    long long lo = cells, hi = -1;
+    auto fdiv = [&](long long x) { return x >= 0 ? x / per : -((-x + per - 1) / per); };
+    for (Index mu = 0; mu < s.m0(); ++mu) {
+        const double r = std::sqrt((650.0 + s.deg[3 * mu + l] * std::log(std::max(1.0, extent))) / s.alpha[mu]);
+        const double ic = (s.center[3 * mu + l] + 0.5 * s.b) / step + base - align;
+        const double ilo = std::floor(ic - r / step) - 2.0, ihi = std::ceil(ic + r / step) + 2.0;
+        lo = std::min(lo, ilo < -1e15 ? -1 : fdiv(static_cast<long long>(ilo)));
+        hi = std::max(hi, ihi > 1e15 ? cells : fdiv(static_cast<long long>(ihi)));
+    }
+    lo = std::max(0LL, lo - 1);
+    hi = std::min(cells - 1, hi + 1);
+    if (hi < lo) {  // no function reaches this grid: an empty one-cell window
+        lo = 0;
+        hi = 0;
+    }
+    j0 = lo;
+    J = hi - lo + 1;
+}
+
 static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need, int mode, AsmOut out,
                          Work* wout = nullptr, const int64_t* s0_dev = nullptr, unsigned flags = 0) {
     // Three concurrent branches (parallel branches of the captured graph):
@@ -739,8 +772,8 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
             ResFold f;
             f.m0 = static_cast<int>(m0);
             f.n = d.nbar;
-            f.J = d.Gbar / d.nbar;
             f.G = d.Gbar;
+            support_window(sd->hs, p, l, true, f.jw0, f.J);
             f.a = w.pwl[l];
             f.b[0] = wm[l];
             f.b[1] = wsf[l];
@@ -828,8 +861,8 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
                     ResFold f;
                     f.m0 = static_cast<int>(m0);
                     f.n = d.n;
-                    f.J = d.G / d.n;
                     f.G = d.G;
+                    support_window(sd->hs, p, ndir, false, f.jw0, f.J);
                     f.a = f.b[0] = w.pwc[ndir];
                     f.nb = 1;
                     f.band = static_cast<int>(d.band);
@@ -881,8 +914,8 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
                         ResFold f;
                         f.m0 = static_cast<int>(m0);
                         f.n = d.n;
-                        f.J = d.G / d.n;
                         f.G = d.G;
+                        support_window(sd->hs, p, s, false, f.jw0, f.J);
                         f.a = f.b[0] = w.pwc[s];
                         f.nb = 1;
                         f.band = static_cast<int>(d.band);
@@ -1140,16 +1173,70 @@ static void box_eig_tridiag(lt_ctx* c, Index n, double* H, double* S, double* ei
         if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) fail(LT_ECUDA, "cublasCreate failed");
     }
     cublasSetStream(c->blas, c->stream);
-    const double one = 1.0;
-    {
-        // (an explicit cusolverDnXtrtri inverse + two trmm was measured slower: trtri alone
-        // costs more than both solves)
+    const double one = 1.0, zero = 0.0, mone = -1.0;
+    static const bool use_trsm = std::getenv("LT_BOX_TRSM") != nullptr;  // A/B: two library solves
+    if (use_trsm) {
         Stage st_(L, "trsm");
         if (cublasDtrsm(c->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, ni, ni,
                         &one, S, ni, H, ni) != CUBLAS_STATUS_SUCCESS ||
             cublasDtrsm(c->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, ni, ni,
                         &one, S, ni, H, ni) != CUBLAS_STATUS_SUCCESS)
             fail(LT_ECUDA, "cublasDtrsm failed");
+    } else {
+        // L^-1 explicitly by recursive doubling (the library trsm / trtri are latency-bound
+        // column sweeps at this size): the 64 x 64 diagonal blocks in one launch, then per
+        // level s = 64, 128, ... the off-diagonal block of every pair of s-blocks,
+        //   X21 = -L22^-1 (L21 L11^-1),
+        // as two strided-batched DMMA GEMMs (pairs sit at a constant stride 2s (n + 1)); then
+        // A = L^-1 H L^-T as two GEMMs.
+        double* Li = c->arena.get<double>("box.Li", n * n);
+        double* W = c->arena.get<double>("box.W", n * n);
+        LT_CU(cudaMemsetAsync(Li, 0, sizeof(double) * n * n, c->stream));
+        launch_trtri_leaf(L, ni, S, Li);
+        {
+            Stage st_(L, "trtri_merge");
+            for (int sz = 64; sz < ni; sz *= 2) {
+                const int full = ni / (2 * sz);  // pairs with both blocks of size sz
+                const long long stride = 2LL * sz * (ni + 1);
+                bool ok = true;
+                if (full > 0) {
+                    ok = ok && cublasDgemmStridedBatched(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, sz, sz, sz, &one, S + sz, ni,
+                                                         stride, Li, ni, stride, &zero, W + sz, ni, stride,
+                                                         full) == CUBLAS_STATUS_SUCCESS;
+                    ok = ok && cublasDgemmStridedBatched(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, sz, sz, sz, &mone,
+                                                         Li + sz + static_cast<size_t>(sz) * ni, ni, stride, W + sz, ni,
+                                                         stride, &zero, Li + sz, ni, stride,
+                                                         full) == CUBLAS_STATUS_SUCCESS;
+                }
+                const int r0 = full * 2 * sz;        // a trailing pair: block of sz, then m2 < sz
+                const int m2 = ni - r0 - sz;
+                if (m2 > 0) {
+                    const size_t o11 = static_cast<size_t>(r0) * ni + r0, o21 = o11 + sz;
+                    const size_t o22 = o11 + static_cast<size_t>(sz) * ni + sz;
+                    ok = ok && cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, m2, sz, sz, &one, S + o21, ni, Li + o11, ni,
+                                           &zero, W + o21, ni) == CUBLAS_STATUS_SUCCESS;
+                    ok = ok && cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, m2, sz, m2, &mone, Li + o22, ni, W + o21,
+                                           ni, &zero, Li + o21, ni) == CUBLAS_STATUS_SUCCESS;
+                }
+                if (!ok) fail(LT_ECUDA, "cublasDgemm (triangular inverse) failed");
+            }
+        }
+        {
+            Stage st_(L, "reduce_gemm");
+            static const bool use_trmm = std::getenv("LT_BOX_GEMM") == nullptr;  // A/B: dense GEMMs
+            bool ok;
+            if (use_trmm)
+                ok = cublasDtrmm(c->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, ni,
+                                 ni, &one, Li, ni, H, ni, W, ni) == CUBLAS_STATUS_SUCCESS &&
+                     cublasDtrmm(c->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT,
+                                 ni, ni, &one, Li, ni, W, ni, H, ni) == CUBLAS_STATUS_SUCCESS;
+            else
+                ok = cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, ni, ni, ni, &one, Li, ni, H, ni, &zero, W, ni) ==
+                         CUBLAS_STATUS_SUCCESS &&
+                     cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_T, ni, ni, ni, &one, W, ni, Li, ni, &zero, H, ni) ==
+                         CUBLAS_STATUS_SUCCESS;
+            if (!ok) fail(LT_ECUDA, "cublasDgemm (L^-1 H L^-T) failed");
+        }
     }
     launch_symmetrize(L, ni, H);
     double* d = c->arena.get<double>("box.td", n);

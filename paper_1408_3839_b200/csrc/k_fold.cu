@@ -82,9 +82,9 @@ __global__ void k_resfold_prep(ResFold f) {
         double v = 0.0;
         if (mu < f.m0 && t < f.n) {
             if (src == 0) {
-                if (c < J) v = f.a[mu * f.G + t + c * f.n];
+                if (c < J) v = f.a[mu * f.G + t + (c + f.jw0) * f.n];
             } else {
-                const long long gi = t + (c - 1) * f.n;  // j' = c - 1
+                const long long gi = t + (c - 1 + f.jw0) * f.n;  // j' = c - 1
                 if (c < J + 2) {
                     if (f.bguard) {
                         if (gi >= -1 && gi <= f.G) v = bsrc[mu * gb + gi + 1];
@@ -135,10 +135,10 @@ __global__ void __launch_bounds__(256) k_resfold(ResFold f) {
             double v = 0.0;
             if (mu < f.m0) {
                 if (src == 0) {
-                    if (c < J) v = f.a[mu * f.G + t + c * f.n];
+                    if (c < J) v = f.a[mu * f.G + t + (c + f.jw0) * f.n];
                 } else if (c < J + 2) {
                     const double* bsrc = src == 2 ? f.b[1] : f.b[0];
-                    const long long gi = t + (c - 1) * f.n;
+                    const long long gi = t + (c - 1 + f.jw0) * f.n;
                     if (f.bguard) {
                         if (gi >= -1 && gi <= f.G) v = bsrc[mu * gb + gi + 1];
                     } else if (gi >= 0 && gi < f.G) {
@@ -209,8 +209,8 @@ __global__ void __launch_bounds__(256) k_resfold(ResFold f) {
                 const long long lo = slo[mu] - w;
                 const long long hi = shi[mu] + w;
                 auto cdiv = [&](long long x) { return x >= 0 ? (x + f.n - 1) / f.n : -((-x) / f.n); };
-                jl = min(jl, static_cast<int>(cdiv(lo - t)));
-                jh = max(jh, static_cast<int>(cdiv(hi - t)));
+                jl = min(jl, static_cast<int>(cdiv(lo - t) - f.jw0));
+                jh = max(jh, static_cast<int>(cdiv(hi - t) - f.jw0));
             }
         } else {
             jl = -1;

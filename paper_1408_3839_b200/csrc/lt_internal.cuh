@@ -327,6 +327,10 @@ struct ResFold {
     const unsigned long long* sup_lo = nullptr;
     const unsigned long long* sup_hi = nullptr;
     int bwiden = 0;
+    // window: the fold covers grid cells [jw0, jw0 + J) (J counts window cells); every
+    // profile is zero outside it (support_window in engine.cu), so long periodic chains do
+    // not stage the empty cells of the extended grid
+    long long jw0 = 0;
 };
 // slab row stride: >= J + 5 (two guard columns plus zero padding for the unchecked last
 // k-step), == 4 mod 16 so the 8 rows x 4 columns of an m8n8k4 fragment hit distinct banks
@@ -446,6 +450,7 @@ int sytrd_ctas(int n);
 void launch_sytrd(const Launch& L, int n, const double* C, double* d, double* e, double* work, unsigned* bar);
 void launch_tridiag_eig(const Launch& L, int n, const double* d, const double* e, double* eig);
 void launch_symmetrize(const Launch& L, int n, double* A);
+void launch_trtri_leaf(const Launch& L, int n, const double* Lm, double* Li);
 // full-space eigenvector columns [c0, c0 + ncols) from the per-k blocks u (K m0 x m0 complex)
 void launch_reconstruct(const Launch& L, const Index* dims, Index m0, const double2* u, Index c0, Index ncols,
                         double2* out);

@@ -177,3 +177,28 @@ def test_config_against_oracle(ctx, oracle, cfg):
     oev = oracle.solve_periodic_ops(oH, oS) if periodic else oracle.solve_box_dense(oH.dense, oS.dense)
     tol = eig_tolerance(oracle, periodic, oH, oS, oev)
     assert np.all(np.abs(ev - oev) <= tol), np.max(np.abs(ev - oev) / tol)
+
+
+def criterion7_chain(L):
+    """gaussian_chain(L, {0.3, 0.5, 0.9, 1.5}, 8, 8, 8) of acceptance_main.cpp:92-103, :360-407."""
+    from paper_1408_3839_b200.system import LatticeSystem
+    return LatticeSystem(b=8.0, L=(L, 1, 1), n=(8, 8, 8), nbar=(8, 8, 8), quad_M=8, nuc_pos=[(0.0, 0.0, 0.0)],
+                         nuc_charge=[1.0], bf_center=[(0.0, 0.0, 0.0)] * 4, bf_alpha=[0.3, 0.5, 0.9, 1.5])
+
+
+@pytest.mark.parametrize("L", [2048, 8192])
+def test_long_periodic_chain(ctx, oracle, L):
+    """Long periodic chains (the Table-1 FFT sweep): the residue folds cover only the cells
+    holding the supports, not the (L + 2 margin)-cell extended grid."""
+    sys = criterion7_chain(L)
+    H, S = ctx.assemble_core(sys, True)
+    oH, oS = oracle.assemble_core(sys, True)
+    for g, o in ((H, oH), (S, oS)):
+        gk, gb = g.blocks()
+        assert np.array_equal(gk, o.kidx)
+        ok, worst = entries_close(gb, o.blocks)
+        assert ok, worst
+    ev = ctx.solve_core(sys, True)
+    oev = oracle.solve_periodic_ops(oH, oS)
+    assert ev.shape == (L, 4)
+    assert np.max(np.abs(ev - oev)) < 1e-9
