@@ -98,6 +98,22 @@ void lt_sys_free(lt_sysdev* s);
 lt_status lt_solve_core_dev(lt_ctx* ctx, const lt_sysdev* sys, int periodic, double* eig_dev, int64_t k_begin,
                             int64_t k_end, int64_t* info);
 
+/* ---- multi-GPU: assembly sharded by rank terms ---------------------- *
+ * The nuclear operator is a rank-R_tot sum (galerkin.cpp:275-283: sum_r w_r prod_l T_l);
+ * a shard assembles the terms r in [r_begin, r_end) (r_end < 0: all) and, with_kinetic != 0,
+ * 0.5 Laplace, so the shards' H sum to H = 0.5 Laplace - Nuclear (one all-reduce); S = Mass
+ * is complete on every shard. Buffers are device pointers of lt_core_layout's size:
+ * periodic -> [nblocks][m0*m0] generating blocks in std::map order of kidx, box -> N_b x N_b
+ * column-major. lt_spectrum_dev then solves the k-points [k_begin, k_end) of the reduced
+ * pencil (eigenvalues at eig_dev + k_begin*m0; box: all N_b).
+ * info (8 int64): L0, nblocks (0 for box), N_b, K, m0, R_tot, doubles per operator,
+ * eigenvalues per k-point; kidx (optional, periodic): [nblocks][3]. */
+lt_status lt_core_layout(lt_ctx* ctx, const lt_sysdev* sys, int periodic, int64_t* info, int64_t* kidx);
+lt_status lt_assemble_core_dev(lt_ctx* ctx, const lt_sysdev* sys, int periodic, int64_t r_begin, int64_t r_end,
+                               int with_kinetic, double* H_dev, double* S_dev);
+lt_status lt_spectrum_dev(lt_ctx* ctx, const lt_sysdev* sys, int periodic, const double* H_dev, const double* S_dev,
+                          double* eig_dev, int64_t k_begin, int64_t k_end);
+
 /* ---- assembly (galerkin.hpp:70, :74; eigensolver.hpp:23-24) ------------------ */
 lt_status lt_assemble(lt_ctx* ctx, const lt_system* sys, int periodic, lt_kind kind, lt_operator** out);
 /* fused Laplace+Nuclear+Mass assembly: H = 0.5 Laplace - Nuclear, S = Mass */

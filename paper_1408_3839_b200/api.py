@@ -531,6 +531,29 @@ class DeviceSystem:
                                              k_end, _i(inf)))
         return inf
 
+    # ---- multi-GPU assembly shards (lt_core_layout / lt_assemble_core_dev / lt_spectrum_dev)
+    def layout(self, periodic: bool):
+        """(info, kidx): info = L0, nblocks, N_b, K, m0, R_tot, doubles per operator,
+        eigenvalues per k-point; kidx [nblocks, 3] (periodic) or None."""
+        info = np.zeros(8, dtype=np.int64)
+        check(self.ctx.lib.lt_core_layout(self.ctx.h, self.h, int(periodic), _i(info), None))
+        kidx = None
+        if periodic:
+            kidx = np.zeros((int(info[1]), 3), dtype=np.int64)
+            check(self.ctx.lib.lt_core_layout(self.ctx.h, self.h, 1, _i(info), _i(kidx)))
+        return info, kidx
+
+    def assemble_shard(self, periodic: bool, r_begin: int, r_end: int, with_kinetic: bool, H_ptr: int, S_ptr: int):
+        """H shard = [0.5 Laplace] - sum_{r in [r_begin, r_end)} w_r prod_l T_l, S = Mass, into
+        device buffers of layout()[0][6] doubles."""
+        check(self.ctx.lib.lt_assemble_core_dev(self.ctx.h, self.h, int(periodic), int(r_begin), int(r_end),
+                                                int(bool(with_kinetic)), ctypes.c_void_p(H_ptr),
+                                                ctypes.c_void_p(S_ptr)))
+
+    def spectrum(self, periodic: bool, H_ptr: int, S_ptr: int, eig_ptr: int, k_begin: int = 0, k_end: int = -1):
+        check(self.ctx.lib.lt_spectrum_dev(self.ctx.h, self.h, int(periodic), ctypes.c_void_p(H_ptr),
+                                           ctypes.c_void_p(S_ptr), ctypes.c_void_p(eig_ptr), int(k_begin), int(k_end)))
+
     def __del__(self):
         if getattr(self, "h", None):
             try:

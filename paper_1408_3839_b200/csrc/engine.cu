@@ -181,6 +181,7 @@ struct lt_ctx {
     // CUDA graphs of the L0 sequence and of the post-L0 launch sequence
     bool graphs = true;
     GraphCache l0graph, coregraph, fullgraph;  // fullgraph: L0 + post-L0 under speculation
+    GraphCache asmgraph, specgraph;            // multi-GPU phases: assembly shard, spectrum
     int* pinned = nullptr;  // small pinned read-back buffer
     // side streams for independent branches of the assembly (captured into the same graph
     // as parallel branches) and the fork/join events between them
@@ -544,6 +545,23 @@ struct AsmOut {
 
 enum Need : int { NEED_MS = 1, NEED_NUC = 2 };
 
+// one assembly shard of the multi-GPU path: the nuclear rank terms
+// [r0, r1) (weights outside are 0) and the Laplace part with weight kin (0.5 on the
+// leading shard, 0 elsewhere); the shards' H sum to the full H, S is complete on each
+struct CoreShard {
+    Index r0 = 0, r1 = -1;
+    double kin = 0.5;
+};
+
+// solve_core_dev phases: 0 assembly + spectrum (one graph), 1 assembly only into caller
+// buffers (H, S), 2 spectrum only from caller buffers
+struct CoreOpts {
+    int phase = 0;
+    CoreShard shard;
+    double* H = nullptr;
+    double* S = nullptr;
+};
+
 
 struct Work {
     double *t = nullptr, *w = nullptr, *potw = nullptr;
@@ -633,7 +651,8 @@ static void support_window(const HostSys& s, const Plan& p, int l, bool pwl, lon
 }
 
 static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need, int mode, AsmOut out,
-                         Work* wout = nullptr, const int64_t* s0_dev = nullptr, unsigned flags = 0) {
+                         Work* wout = nullptr, const int64_t* s0_dev = nullptr, unsigned flags = 0,
+                         const CoreShard& shard = CoreShard{}) {
     // Three concurrent branches (parallel branches of the captured graph):
     //   main   : sinc -> potential of the 1st, 3rd distinct direction -> nuclear -> fill
     //   aux[1] : potential of the 2nd distinct direction (joins main before the nuclear part)
@@ -663,7 +682,7 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
     w.potw = A.get<double>("sinc.potw", Rtot);
     // nodes and weights Z_v w_q on the side branch: the master kernels evaluate their nodes
     // in place, the weights are first needed after the join before the nuclear part
-    launch_sinc(LP, p.M, sd->ds, w.t, w.w, w.potw);
+    launch_sinc(LP, p.M, sd->ds, w.t, w.w, w.potw, shard.r0, shard.r1);
     if (nuc) {
         int nth = 0;
         for (int l = 0; l < 3; ++l) {
@@ -981,6 +1000,7 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
     fa.s2_dir = ndir;
     fa.nuc_mode = nuc_mode;
     fa.mode = mode;
+    fa.kin = shard.kin;
     fa.periodic = p.periodic;
     fa.out0 = out.out0;
     fa.out1 = out.out1;
@@ -1341,7 +1361,10 @@ static std::vector<int64_t> graph_key(const HostSys& h, const Plan& p, bool peri
 
 // full path on device; eigenvalues -> eig_dev (device)
 static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double* eig_dev, Index k_begin,
-                           Index k_end, int64_t* info, double* eig_host = nullptr, bool allow_spec = true) {
+                           Index k_end, int64_t* info, double* eig_host = nullptr, bool allow_spec = true,
+                           const CoreOpts& opt = CoreOpts{}) {
+    const int phase = opt.phase;
+    if (phase != 0) allow_spec = false;
     c->host_mark(0);
     validate(sd->hs);
     c->phase_mark(0);
@@ -1390,14 +1413,15 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
     // failure key (ints 6-7), fetched with one copy at the end of the graph
     int* ret = c->arena.get<int>("l0.state", 8);
     auto* fk = reinterpret_cast<unsigned long long*>(ret + 6);
-    if (periodic) {
-        out.out0 = c->arena.get<double>("core.H", p.nblocks * mm);
-        out.out1 = c->arena.get<double>("core.S", p.nblocks * mm);
-        out.kidx = c->arena.get<int64_t>("core.kidx", p.nblocks * 3);
+    const Index ocount = periodic ? p.nblocks * mm : p.Nb * p.Nb;
+    if (phase == 1 || (phase == 2 && periodic)) {  // caller buffers (the DFT only reads them)
+        out.out0 = opt.H;
+        out.out1 = opt.S;
     } else {
-        out.out0 = c->arena.get<double>("core.H", p.Nb * p.Nb);
-        out.out1 = c->arena.get<double>("core.S", p.Nb * p.Nb);
+        out.out0 = c->arena.get<double>("core.H", ocount);
+        out.out1 = c->arena.get<double>("core.S", ocount);
     }
+    if (periodic) out.kidx = c->arena.get<int64_t>("core.kidx", p.nblocks * 3);
     const bool small_box = !periodic && p.Nb <= 32;
     const bool inline_readback = periodic || small_box;  // no host step after the graph
     const size_t ebytes = sizeof(double) * (periodic ? p.K * p.m0 : p.Nb);
@@ -1410,14 +1434,22 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
     // copied by the pencil kernel's last group: no copy nodes at the end of the graph
     static const bool no_kr = std::getenv("LT_NO_KERNEL_READBACK") != nullptr;  // A/B switch
     double* eig_out = (epin && !no_kr) ? static_cast<double*>(epin) : eig_dev;
-    const bool kernel_readback = !no_kr && inline_readback && (small_box || k_begin < k_end);
+    const bool kernel_readback = phase != 1 && !no_kr && inline_readback && (small_box || k_begin < k_end);
     PencilReadback rb;
     if (kernel_readback) rb = PencilReadback{ret, rpin, c->pencil_done};
     auto enqueue = [&]() {
         // k_l0_init resets the failure key: in front of this graph under speculation, else in
         // the L0 graph that just ran
         if (spec) l0w.enqueue(c->L(), 1, static_cast<int>(L0) + 3, true);
-        run_assembly(c, sd, p, NEED_MS | NEED_NUC, 0, out, nullptr, s0d);
+        if (phase != 2) run_assembly(c, sd, p, NEED_MS | NEED_NUC, 0, out, nullptr, s0d, 0, opt.shard);
+        if (phase == 2 && !periodic) {  // the box pencil factorises in place: work on copies
+            LT_CU(cudaMemcpyAsync(out.out0, opt.H, sizeof(double) * ocount, cudaMemcpyDeviceToDevice, c->stream));
+            LT_CU(cudaMemcpyAsync(out.out1, opt.S, sizeof(double) * ocount, cudaMemcpyDeviceToDevice, c->stream));
+        }
+        if (phase == 1) {
+            LT_CU(cudaMemcpyAsync(rpin, ret, 8 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+            return;
+        }
         if (periodic) {
             int wrapped = 0, ax = -1;
             for (int l = 0; l < 3; ++l)
@@ -1462,16 +1494,24 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
     c->phase_mark(2);
     c->host_mark(1);
     run_cached(
-        c, spec ? c->fullgraph : c->coregraph,
+        c, spec ? c->fullgraph : (phase == 1 ? c->asmgraph : (phase == 2 ? c->specgraph : c->coregraph)),
         [&]() {
             auto k = graph_key(sd->hs, p, periodic, k_begin, k_end, eig_dev, sd->mem, c->arena.generation());
             k.push_back(spec ? 1 : 0);
             k.push_back(reinterpret_cast<int64_t>(epin));
             k.push_back(reinterpret_cast<int64_t>(rpin));
+            k.push_back(phase);
+            k.push_back(opt.shard.r0);
+            k.push_back(opt.shard.r1);
+            int64_t kb;
+            std::memcpy(&kb, &opt.shard.kin, sizeof(kb));
+            k.push_back(kb);
+            k.push_back(reinterpret_cast<int64_t>(opt.H));
+            k.push_back(reinterpret_cast<int64_t>(opt.S));
             return k;
         },
         enqueue);
-    if (!inline_readback) {
+    if (!inline_readback && phase != 1) {
         box_eig_device(c, p.Nb, out.out0, out.out1, eig_dev, fk);
         LT_CU(cudaMemcpyAsync(rpin, ret, 8 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
         if (epin) LT_CU(cudaMemcpyAsync(epin, eig_dev, ebytes, cudaMemcpyDeviceToHost, c->stream));
@@ -1882,6 +1922,63 @@ lt_status lt_solve_core_dev(lt_ctx* c, const lt_sysdev* s, int periodic, double*
         LT_CU(cudaSetDevice(c->device));
         StageScope ss(c, 1 << 20);
         solve_core_dev(c, s, periodic != 0, eig_dev, k_begin, k_end, info);
+    });
+}
+
+lt_status lt_core_layout(lt_ctx* c, const lt_sysdev* s, int periodic, int64_t* info, int64_t* kidx) {
+    return guarded([&] {
+        LT_CU(cudaSetDevice(c->device));
+        validate(s->hs);
+        const Index L0 = compute_L0(c, s);
+        Plan p;
+        plan_after_L0(s->hs, periodic != 0, L0, p, true);
+        if (!periodic && p.Nb > 4096)
+            fail(LT_ECAP, "solve_box_dense: size " + std::to_string(p.Nb) + " exceeds dense cap 4096");
+        const Index mm = p.m0 * p.m0;
+        info[0] = p.L0;
+        info[1] = periodic ? p.nblocks : 0;
+        info[2] = p.Nb;
+        info[3] = p.K;
+        info[4] = p.m0;
+        info[5] = p.Rtot;
+        info[6] = periodic ? p.nblocks * mm : p.Nb * p.Nb;
+        info[7] = periodic ? p.m0 : p.Nb;  // eigenvalues per k-point
+        if (kidx && periodic) {
+            const auto k = periodic_kidx(p);
+            for (size_t b = 0; b < k.size(); ++b)
+                for (int l = 0; l < 3; ++l) kidx[3 * b + l] = k[b][static_cast<size_t>(l)];
+        }
+    });
+}
+
+lt_status lt_assemble_core_dev(lt_ctx* c, const lt_sysdev* s, int periodic, int64_t r_begin, int64_t r_end,
+                               int with_kinetic, double* H_dev, double* S_dev) {
+    return guarded([&] {
+        LT_CU(cudaSetDevice(c->device));
+        if (!H_dev || !S_dev) fail(LT_EDIM, "assemble_core_dev: H and S device buffers are required");
+        StageScope ss(c, 1 << 20);
+        CoreOpts o;
+        o.phase = 1;
+        o.shard.r0 = std::max<int64_t>(0, r_begin);
+        o.shard.r1 = r_end;
+        o.shard.kin = with_kinetic ? 0.5 : 0.0;
+        o.H = H_dev;
+        o.S = S_dev;
+        solve_core_dev(c, s, periodic != 0, nullptr, 0, 0, nullptr, nullptr, false, o);
+    });
+}
+
+lt_status lt_spectrum_dev(lt_ctx* c, const lt_sysdev* s, int periodic, const double* H_dev, const double* S_dev,
+                          double* eig_dev, int64_t k_begin, int64_t k_end) {
+    return guarded([&] {
+        LT_CU(cudaSetDevice(c->device));
+        if (!H_dev || !S_dev || !eig_dev) fail(LT_EDIM, "spectrum_dev: H, S and eigenvalue buffers are required");
+        StageScope ss(c, 1 << 20);
+        CoreOpts o;
+        o.phase = 2;
+        o.H = const_cast<double*>(H_dev);  // read only (box: copied before the in-place factorisation)
+        o.S = const_cast<double*>(S_dev);
+        solve_core_dev(c, s, periodic != 0, eig_dev, k_begin, k_end, nullptr, nullptr, false, o);
     });
 }
 

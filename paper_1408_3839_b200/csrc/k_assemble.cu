@@ -24,6 +24,7 @@ struct FillDev {
     const double* Npart;
     Index Nres, Nnd;
     int s2_dir, mode, periodic, nuc_mode;
+    double kin;
     double* out0;
     double* out1;
     int64_t* kidx;
@@ -98,7 +99,7 @@ __global__ void k_fill(FillDev f) {
         }
         double v0 = 0.0, v1 = 0.0;
         switch (f.mode) {
-            case 0: v0 = __dadd_rn(__dmul_rn(0.5, lap), __dmul_rn(-1.0, nuc)); v1 = mass; break;
+            case 0: v0 = __dadd_rn(__dmul_rn(f.kin, lap), __dmul_rn(-1.0, nuc)); v1 = mass; break;
             case 1: v0 = lap; break;
             case 2: v0 = mass; break;
             default: v0 = nuc; break;
@@ -140,6 +141,7 @@ void launch_fill(const Launch& L, const FillArgs& a, Index Nb, Index nblocks) {
     f.s2_dir = a.s2_dir;
     f.nuc_mode = a.nuc_mode;
     f.mode = a.mode;
+    f.kin = a.kin;
     f.periodic = a.periodic ? 1 : 0;
     f.out0 = a.out0;
     f.out1 = a.out1;

@@ -16,7 +16,10 @@
 
 namespace lt {
 
-__global__ void k_sinc(int M, int nnuc, const double* __restrict__ Z, double* t, double* w, double* potw) {
+// potw[r] = Z_v w_q for rank terms r = v R + q in [r0, r1), 0 outside (a rank-term shard of
+// the multi-GPU assembly: the shards' nuclear parts sum to the full one)
+__global__ void k_sinc(int M, int nnuc, const double* __restrict__ Z, double* t, double* w, double* potw, long long r0,
+                       long long r1) {
     const int R = 2 * M + 1;
     double step = log(static_cast<double>(M)) / static_cast<double>(M);
     if (M == 1) step = 0.5;
@@ -28,13 +31,16 @@ __global__ void k_sinc(int M, int nnuc, const double* __restrict__ Z, double* t,
         const double wi = __dmul_rn(c, __dadd_rn(ti, exp(-eu)));
         t[i] = ti;
         w[i] = wi;
-        for (int v = 0; v < nnuc; ++v) potw[v * R + i] = __dmul_rn(wi, Z[v]);
+        for (int v = 0; v < nnuc; ++v) {
+            const long long r = static_cast<long long>(v) * R + i;
+            potw[r] = (r >= r0 && r < r1) ? __dmul_rn(wi, Z[v]) : 0.0;
+        }
     }
 }
 
-void launch_sinc(const Launch& L, Index M, const DevSys& s, double* t, double* w, double* potw) {
+void launch_sinc(const Launch& L, Index M, const DevSys& s, double* t, double* w, double* potw, Index r0, Index r1) {
     Stage st_(L, "sinc");
-    k_sinc<<<1, 128, 0, L.st>>>(static_cast<int>(M), s.nnuc, s.Z, t, w, potw);
+    k_sinc<<<1, 128, 0, L.st>>>(static_cast<int>(M), s.nnuc, s.Z, t, w, potw, r0, r1 < 0 ? (1LL << 62) : r1);
     LT_CU(cudaGetLastError());
     L.tick();
 }

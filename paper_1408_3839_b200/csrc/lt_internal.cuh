@@ -195,7 +195,9 @@ struct Stage {
 };
 
 // sinc quadrature (sinc_quadrature.cpp:9-29) and the nuclear weights Z_v w_q
-void launch_sinc(const Launch& L, Index M, const DevSys& s, double* t, double* w, double* potw);
+// rank terms outside [r0, r1) get weight 0 (r1 < 0: all)
+void launch_sinc(const Launch& L, Index M, const DevSys& s, double* t, double* w, double* potw, Index r0 = 0,
+                 Index r1 = -1);
 
 // overlap constant (gto_basis.cpp:87-126)
 struct OverlapBufs {
@@ -359,6 +361,7 @@ struct FillArgs {
     int s2_dir = -1;
     int nuc_mode = 0;          // 0 tables, 1 N along s2_dir, 2 N by dlin
     int mode = 0;
+    double kin = 0.5;          // mode 0: H = kin Laplace - Nuclear (0 on the non-leading assembly shards)
     bool periodic = false;
     double* out0 = nullptr;    // H (or single operator)
     double* out1 = nullptr;    // S
