@@ -212,6 +212,9 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--stages", action="store_true", help="print per-kernel stage times to stderr")
+    ap.add_argument("--split", default="kpoints", choices=["kpoints", "rankterms"],
+                    help="N > 1: k-point shards with a replicated assembly (default), or the assembly sharded "
+                         "by nuclear rank terms with one all-reduce of H, then k-point shards (SURVEY 8(e))")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -224,7 +227,7 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_1408_3839_b200.api import Context
-    from paper_1408_3839_b200.dist import solve_core_distributed
+    from paper_1408_3839_b200.dist import solve_core_distributed, solve_core_sharded
 
     if world > 1:
         torch.cuda.set_device(local)
@@ -242,7 +245,16 @@ def main():
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
     info = np.zeros(8, dtype=np.int64)
 
+    dsys.solve(periodic, eig.data_ptr(), 0, -1, info)  # fills info (L0, bands, R_tot, ...) for the report
+    shard_bufs = None
+    if world > 1 and args.split == "rankterms":
+        li, _ = dsys.layout(periodic)
+        shard_bufs = (torch.empty(int(li[6]), dtype=torch.float64, device=dev),
+                      torch.empty(int(li[6]), dtype=torch.float64, device=dev), eig)
+
     def step():
+        if shard_bufs is not None:
+            return solve_core_sharded(ctx, sysobj, periodic, dsys=dsys, buffers=shard_bufs)
         return solve_core_distributed(ctx, sysobj, periodic, dsys=dsys, eig_dev=eig, info=info)
 
     for _ in range(args.warmup):
@@ -298,7 +310,7 @@ def main():
         if world == 1:
             ctx.solve_core(sysobj, periodic)
         else:
-            solve_core_distributed(ctx, sysobj, periodic)
+            (solve_core_sharded if shard_bufs is not None else solve_core_distributed)(ctx, sysobj, periodic)
     torch.cuda.synchronize()
     e2e_ms = []
     for i in range(args.steps):
@@ -310,7 +322,8 @@ def main():
         if world == 1:
             ev_host = ctx.solve_core(sysobj, periodic)
         else:
-            ev_host = solve_core_distributed(ctx, sysobj, periodic).cpu().numpy()
+            ev_host = (solve_core_sharded if shard_bufs is not None else solve_core_distributed)(
+                ctx, sysobj, periodic).cpu().numpy()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
     e2e_t = torch.tensor([float(np.mean(e2e_ms))], dtype=torch.float64, device=dev)
     if world > 1:
@@ -375,8 +388,8 @@ def main():
             "config": {"workload": args.workload, "desc": WORKLOAD_DESC[args.workload], "L": list(sysobj.L),
                        "n_per_cell": list(sysobj.n), "m0": sysobj.m0, "R_N": sysobj.rank_N, "L0": L0,
                        "band": [int(x) for x in info[1:4]], "R_tot": int(info[4]), "N_b": int(info[5]),
-                       "k_points": int(info[6]), "parallelism": f"k-point shards x{world}" if periodic else
-                       f"replicas x{world}", "l2": "flushed between timed iterations (256 MB write)",
+                       "k_points": int(info[6]), "parallelism": (f"rank-term assembly shards + all-reduce, " if shard_bufs is not None else "")
+                       + (f"k-point shards x{world}" if periodic else f"replicas x{world}"), "l2": "flushed between timed iterations (256 MB write)",
                        "exponent_draw": sysobj.notes["exponent_draw"]},
             "galerkin_entries_per_s": float(entries) / (ms_per_step * 1e-3) if ms_per_step else None,
             "roofline": roof,
