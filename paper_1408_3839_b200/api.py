@@ -71,7 +71,7 @@ class Operator:
     def dense(self) -> np.ndarray:
         out = np.zeros(self.Nb * self.Nb)
         check(native.lib().lt_op_dense(self.handle, _d(out)))
-        return out.reshape(self.Nb, self.Nb).T.copy()
+        return out.reshape(self.Nb, self.Nb).T  # column-major data: a Fortran-ordered view, no copy
 
     def blocks(self):
         """(kidx (n,3), blocks (n, m0, m0) [row, col]) in std::map order."""

@@ -46,7 +46,7 @@ static void run(int count, int m0, int reps) {
     cudaMemcpy(dS, S.data(), S.size() * sizeof(double2), cudaMemcpyHostToDevice);
     constexpr int PPC = BS / G;
     const size_t smem = sizeof(lt::PSmem<NM>) * PPC;
-    cudaFuncSetAttribute(lt::k_pencil<NM, G, BS>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(lt::k_pencil<NM, G, BS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     const int blocks = (count + PPC - 1) / PPC;
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
@@ -55,7 +55,8 @@ static void run(int count, int m0, int reps) {
     for (int r = 0; r < reps; ++r) {
         cudaMemset(fk, 0xff, sizeof(unsigned long long));
         cudaEventRecord(e0);
-        lt::k_pencil<NM, G, BS><<<blocks, BS, smem>>>(count, m0, dH, dS, de, fk, 1, lt::PencilDft{});
+        lt::k_pencil<NM, G, BS, false><<<blocks, BS, smem>>>(count, m0, dH, dS, de, fk, 1, lt::PencilDft{}, nullptr,
+                                                             lt::PencilReadback{});
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms;
@@ -86,5 +87,8 @@ int main() {
     run<32, 256, 256>(1, 32, 5);
     run<8, 128, 256>(1184, 8, 5);
     run<8, 32, 256>(4096, 8, 5);
+    run<32, 256, 256>(1, 32, 5);
+    run<32, 512, 512>(1, 32, 5);
+    run<32, 1024, 1024>(1, 32, 5);
     return 0;
 }

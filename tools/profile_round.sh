@@ -20,4 +20,8 @@ timeout 900 ncu --set full --import-source on -k regex:"k_pencil|k_l0_scan|k_l0_
 timeout 900 ncu --set full --import-source on -k regex:"k_pencil|k_resfold|k_triv_gemm|k_window|k_l0_scan" \
     -s 30 -c 8 -o gpurun_out/prof/${R}_c4_full python bench.py --workload c4 --steps 3 --warmup 3 \
     --no-cpu-baseline > gpurun_out/prof/${R}_c4_full.log 2>&1
+timeout 900 ncu --set full --import-source on -k regex:"k_sytrd|k_tridiag_eig3|k_trtri_leaf|k_hankel" \
+    -s 8 -c 4 -o gpurun_out/prof/${R}_c3_full python bench.py --workload c3 --steps 3 --warmup 3 \
+    --no-cpu-baseline > gpurun_out/prof/${R}_c3_full.log 2>&1
+timeout 600 python tools/table1.py > gpurun_out/prof/${R}_table1.json 2> gpurun_out/prof/${R}_table1.err
 ls -la gpurun_out/prof

@@ -34,7 +34,9 @@ STAGE = {
     "k_resfold_prep": "fold_prep", "k_resfold_reduce": "resfold_reduce", "k_fem_apply": "fem_apply",
     "k_profile_sample": "profiles", "k_profile_trim": "profiles", "k_sinc": "sinc", "k_hankel": "hankel_gemm",
     "k_split_reduce": "split_reduce", "k_fgemm": "fold_gemm", "k_kr_combine": "kr_combine",
-    "k_vgemm": "vgemm", "k_real_to_complex": "r2c",
+    "k_vgemm": "vgemm", "k_real_to_complex": "r2c", "k_sytrd_reg": "sytrd", "k_sytrd": "sytrd",
+    "k_tridiag_eig3": "tridiag_eig", "k_symmetrize": "symmetrize", "k_trtri_leaf": "trtri_leaf",
+    "k_l0_peak": "l0_peak", "k_profiles": "profiles", "k_window_sum_short": "window_sum",
 }
 
 FULL_METRICS = [
@@ -150,16 +152,17 @@ def main():
     for cfg in ("c1", "c2", "c3", "c4", "c5"):
         launches(cfg, R)
     traffic = {}
-    for cfg in ("c2", "c4"):
+    for cfg in ("c2", "c3", "c4"):
         full(cfg, R, traffic)
     # per stage: mean DRAM bytes per launch
     agg = {cfg: {st: {"dram_bytes_per_launch": sum(x["dram_bytes"] for x in v) / len(v), "launches": len(v),
                       "kernels": sorted({x["kernel"] for x in v})} for st, v in d.items()}
            for cfg, d in traffic.items()}
     open(os.path.join(DST, f"{R}_traffic.json"), "w").write(json.dumps(agg, indent=1) + "\n")
-    b = os.path.join(SRC, f"{R}_bench.json")
-    if os.path.exists(b):
-        shutil.copy(b, os.path.join(DST, f"{R}_bench.json"))
+    for name in ("bench.json", "table1.json"):
+        b = os.path.join(SRC, f"{R}_{name}")
+        if os.path.exists(b) and os.path.getsize(b) > 0:
+            shutil.copy(b, os.path.join(DST, f"{R}_{name}"))
 
 
 if __name__ == "__main__":
