@@ -12,7 +12,7 @@
 
 #include "../paper_1408_3839_b200/csrc/k_pencil.cu"
 
-template <int NM, int G, int BS>
+template <int NM, int G, int BS, bool VEC = false>
 static void run(int count, int m0, int reps) {
     std::mt19937_64 rng(count * 131 + m0);
     std::normal_distribution<double> nd;
@@ -42,11 +42,13 @@ static void run(int count, int m0, int reps) {
     cudaMalloc(&dS, S.size() * sizeof(double2));
     cudaMalloc(&de, static_cast<size_t>(count) * m0 * sizeof(double));
     cudaMalloc(&fk, sizeof(unsigned long long));
+    double2* dv = nullptr;
+    if (VEC) cudaMalloc(&dv, static_cast<size_t>(count) * m0 * m0 * sizeof(double2));
     cudaMemcpy(dH, H.data(), H.size() * sizeof(double2), cudaMemcpyHostToDevice);
     cudaMemcpy(dS, S.data(), S.size() * sizeof(double2), cudaMemcpyHostToDevice);
     constexpr int PPC = BS / G;
     const size_t smem = sizeof(lt::PSmem<NM>) * PPC;
-    cudaFuncSetAttribute(lt::k_pencil<NM, G, BS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(lt::k_pencil<NM, G, BS, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     const int blocks = (count + PPC - 1) / PPC;
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
@@ -55,7 +57,7 @@ static void run(int count, int m0, int reps) {
     for (int r = 0; r < reps; ++r) {
         cudaMemset(fk, 0xff, sizeof(unsigned long long));
         cudaEventRecord(e0);
-        lt::k_pencil<NM, G, BS, false><<<blocks, BS, smem>>>(count, m0, dH, dS, de, fk, 1, lt::PencilDft{}, nullptr,
+        lt::k_pencil<NM, G, BS, VEC><<<blocks, BS, smem>>>(count, m0, dH, dS, de, fk, 1, lt::PencilDft{}, dv,
                                                              lt::PencilReadback{});
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
@@ -69,9 +71,9 @@ static void run(int count, int m0, int reps) {
     const int nk = count < 8192 ? count : 8192;
     for (int k = 0; k < nk; ++k)
         for (int i = 0; i < 6; ++i) ph[i] += static_cast<double>(prof[k * 8 + i + 1] - prof[k * 8 + i]) / nk;
-    std::printf("count %5d m0 %2d NM %2d G %4d BS %4d: kernel %8.1f us | cycles load %7.0f herm %7.0f chol %7.0f "
+    std::printf("%s count %5d m0 %2d NM %2d G %4d BS %4d: kernel %8.1f us | cycles load %7.0f herm %7.0f chol %7.0f "
                 "reduce %7.0f hh %7.0f bisect %7.0f | err %s\n",
-                count, m0, NM, G, BS, best * 1e3, ph[0], ph[1], ph[2], ph[3], ph[4], ph[5],
+                VEC ? "vec" : "val", count, m0, NM, G, BS, best * 1e3, ph[0], ph[1], ph[2], ph[3], ph[4], ph[5],
                 cudaGetErrorString(cudaGetLastError()));
     cudaFree(dH);
     cudaFree(dS);
@@ -87,8 +89,10 @@ int main() {
     run<32, 256, 256>(1, 32, 5);
     run<8, 128, 256>(1184, 8, 5);
     run<8, 32, 256>(4096, 8, 5);
-    run<32, 256, 256>(1, 32, 5);
-    run<32, 512, 512>(1, 32, 5);
-    run<32, 1024, 1024>(1, 32, 5);
+    run<8, 128, 256, true>(32, 8, 5);
+    run<8, 32, 256, true>(32, 8, 5);
+    run<16, 64, 256, true>(512, 16, 5);
+    run<32, 256, 256, true>(1, 32, 5);
+    run<8, 32, 256, true>(4096, 8, 5);
     return 0;
 }
