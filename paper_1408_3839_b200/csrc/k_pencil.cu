@@ -7,8 +7,9 @@
 //   3. A = L^-1 H L^-H through the explicit triangular inverse, A symmetrised;
 //   4. complex Householder tridiagonalisation (zhetd2 scheme, real sub-diagonal);
 //   5. all eigenvalues of the real tridiagonal by parallel multisection: P threads
-//      per eigenvalue evaluate Sturm counts (LDL^T pivots with LAPACK's pivmin guard)
-//      at P interior points per iteration, shrinking the bracket (P+1)-fold.
+//      per eigenvalue evaluate Sturm counts (the three-term recurrence of sturm3 on T
+//      scaled by a power of two: one FMA per step, no reciprocal on the chain) at Q
+//      points each per iteration, shrinking the bracket (P Q + 1)-fold.
 // Eigenvalues come out ascending by construction. Results agree with the reference's
 // SelfAdjointEigenSolver to O(eps ||A||).
 //
@@ -123,32 +124,6 @@ __device__ __forceinline__ double safe_rcp(double q) {
     const double a = fabs(q);
     return (a >= 1e-300 && a <= 1e300) ? fast_rcp(q) : 1.0 / q;
 }
-
-// Sturm counts (eigenvalues of the symmetric tridiagonal (d, e^2) strictly below x) at Q
-// shifts at once: Q independent LDL^T pivot chains interleaved for ILP. LAPACK's pivmin
-// guard; the counts are backward stable, so bisection converges to within O(eps ||T||)
-// of the exact eigenvalues.
-template <int Q>
-__device__ __forceinline__ void sturm_counts(const double* d, const double* e2, int n, const double (&x)[Q],
-                                             double pivmin, int (&cnt)[Q]) {
-    double q[Q];
-#pragma unroll
-    for (int j = 0; j < Q; ++j) {
-        q[j] = d[0] - x[j];
-        if (fabs(q[j]) < pivmin) q[j] = -pivmin;
-        cnt[j] = q[j] < 0.0;
-    }
-    for (int i = 1; i < n; ++i) {
-        const double di = d[i], ei = e2[i - 1];
-#pragma unroll
-        for (int j = 0; j < Q; ++j) {
-            q[j] = (di - x[j]) - ei * fast_rcp(q[j]);
-            if (fabs(q[j]) < pivmin) q[j] = -pivmin;
-            cnt[j] += q[j] < 0.0;
-        }
-    }
-}
-
 
 // Vector mode on the reduced matrix A (leading n x n): parallel cyclic Jacobi with the
 // eigenvectors accumulated in C, then ascending order and X = L^-H Z (B holds the unscaled
@@ -607,6 +582,18 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
     }
     if (t == 0) {
         sm.d[n - 1] = A[n - 1][n - 1].x;
+        // exact power-of-two scale (max |d|, |e| in [0.5, 1)) for the three-term Sturm counts;
+        // the multisection runs on the scaled T and the eigenvalues are unscaled exactly
+        double mx = 0.0;
+        for (int i = 0; i < n; ++i) mx = fmax(mx, fmax(fabs(sm.d[i]), i + 1 < n ? fabs(sm.e[i]) : 0.0));
+        int ex = mx > 0.0 ? static_cast<int>((__double_as_longlong(mx) >> 52) & 0x7ff) - 1022 : 0;
+        ex = max(-1000, min(1000, ex));
+        const double sc = __longlong_as_double(static_cast<long long>(1023 - ex) << 52);
+        sm.scal[2] = __longlong_as_double(static_cast<long long>(1023 + ex) << 52);  // 1 / sc
+        for (int i = 0; i < n; ++i) {
+            sm.d[i] *= sc;
+            if (i + 1 < n) sm.e[i] *= sc;
+        }
         double emax = 0.0;
         for (int i = 0; i + 1 < n; ++i) {
             sm.e2[i] = sm.e[i] * sm.e[i];
@@ -622,7 +609,7 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
         const double wid = fmax(hi - lo, fmax(fabs(lo), fabs(hi))) * 4.4e-16 * n + 1e-300;
         sm.scal[0] = lo - wid;
         sm.scal[1] = hi + wid;
-        sm.scal[2] = 2.2250738585072014e-308 * fmax(1.0, emax);
+        (void)emax;
         // absolute tolerance ulp * ||T|| (LAPACK dstebz's default ABSTOL): eigenvalues near
         // zero stop at the normwise-backward-stable accuracy instead of chasing relative ulps
         sm.scal[3] = 2.2e-16 * fmax(fabs(lo), fabs(hi));
@@ -634,7 +621,7 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
     constexpr int Q = 4;
     int P = 1;
     while (P * 2 <= 32 && P * 2 * n <= G) P *= 2;
-    const double pivmin = sm.scal[2];
+    const double unscale = sm.scal[2];
     const double atol = sm.scal[3];
     const int per_round = G / P;  // eigenvalues handled concurrently
     const double inv_pts = 1.0 / static_cast<double>(P * Q + 1);
@@ -652,7 +639,7 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
 #pragma unroll
             for (int j = 0; j < Q; ++j) x[j] = a + (b - a) * (static_cast<double>(sub * Q + j + 1) * inv_pts);
             if (active) {
-                sturm_counts<Q>(sm.d, sm.e2, n, x, pivmin, cnt);
+                sturm3<Q>(sm.d, sm.e2, n, x, cnt);
             } else {
 #pragma unroll
                 for (int j = 0; j < Q; ++j) cnt[j] = 0;
@@ -689,7 +676,7 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
             b = nb;
             if (__all_sync(0xffffffffu, done || !active)) break;
         }
-        if (active && sub == 0) eig[k * m0 + mi] = 0.5 * (a + b);
+        if (active && sub == 0) eig[k * m0 + mi] = 0.5 * (a + b) * unscale;
     }
     PPROF(6);
     if (t == 0) group_done(rb, count);

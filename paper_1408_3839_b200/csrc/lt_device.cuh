@@ -55,4 +55,57 @@ __device__ __forceinline__ double warp_max(double v) {
     return v;
 }
 
+// Sturm counts by the three-term (continuant) recurrence p_i = (d_i - x) p_{i-1} - e_{i-1}^2
+// p_{i-2} (Wilkinson's bisection form): the count of eigenvalues below x is the number of
+// negative ratios q_i = p_i / p_{i-1}, the LDL^T pivots, without a division on the
+// dependent chain (one FMA per step instead of a reciprocal). T is pre-scaled by a power of
+// two to max |entry| < 1; a ratio with |q_i| < 2^-100 is replaced by -2^-100 (the pivmin rule
+// of the ratio form, a perturbation of d_i far below eps ||T||), and (p_i, p_{i-1}) are
+// rescaled by an exact power of two every 4 steps, which keeps them normal (|q| <= 4).
+template <int Q>
+__device__ __forceinline__ void sturm3(const double* sd, const double* se2, int n, const double (&x)[Q],
+                                       int (&cnt)[Q]) {
+    constexpr double kDelta = 7.888609052210118e-31;  // 2^-100
+    double prev[Q], cur[Q];
+#pragma unroll
+    for (int j = 0; j < Q; ++j) {
+        prev[j] = 1.0;
+        cur[j] = sd[0] - x[j];
+        if (fabs(cur[j]) < kDelta) cur[j] = -kDelta;
+        cnt[j] = cur[j] < 0.0;
+    }
+    auto step = [&](double di, double ei) {
+#pragma unroll
+        for (int j = 0; j < Q; ++j) {
+            double nx = fma(di - x[j], cur[j], -ei * prev[j]);
+            const double thr = kDelta * fabs(cur[j]);
+            if (fabs(nx) < thr) nx = cur[j] < 0.0 ? thr : -thr;  // q = -2^-100
+            cnt[j] += (nx < 0.0) != (cur[j] < 0.0);
+            prev[j] = cur[j];
+            cur[j] = nx;
+        }
+    };
+    int i = 1;
+    // blocks of 4 steps: the 8 shared-memory loads are issued ahead of the dependent chain
+    for (; i + 3 < n; i += 4) {
+        const double d0 = sd[i], d1 = sd[i + 1], d2 = sd[i + 2], d3 = sd[i + 3];
+        const double e0 = se2[i - 1], e1 = se2[i], e2 = se2[i + 1], e3 = se2[i + 2];
+        step(d0, e0);
+        step(d1, e1);
+        step(d2, e2);
+        step(d3, e3);
+#pragma unroll
+        for (int j = 0; j < Q; ++j) {
+            const double a = fabs(cur[j]);
+            if (a > 0x1p+400 || a < 0x1p-400) {
+                const int ex = static_cast<int>((__double_as_longlong(a) >> 52) & 0x7ff) - 1023;
+                const double sc = __longlong_as_double(static_cast<long long>(1023 - ex) << 52);
+                cur[j] *= sc;
+                prev[j] *= sc;
+            }
+        }
+    }
+    for (; i < n; ++i) step(sd[i], se2[i - 1]);
+}
+
 }  // namespace lt
