@@ -1097,6 +1097,29 @@ static void launch_dft(lt_ctx* c, const DftPrep& P, int nops, const double* cons
         buf[op][0] = c->arena.get<double2>("dft.a" + P.tag + std::to_string(op), P.maxsz * mm);
         buf[op][1] = c->arena.get<double2>("dft.b" + P.tag + std::to_string(op), P.maxsz * mm);
     }
+    {
+        // two or more wrapped axes: one fused launch when an entry's cube fits shared memory
+        DftFusedArgs f;
+        f.mm = mm;
+        f.maxsz = P.maxsz;
+        f.slot2blk = P.slot2blk;
+        for (int l = 0; l < 3; ++l) {
+            f.dims[l] = P.dims[l];
+            f.ext[l] = P.ext[l];
+            f.ncomp[l] = P.ncomp[l];
+            f.comp[l] = P.comp[l];
+            if (P.dims[l] > 1) f.axes[f.nax++] = l;
+        }
+        static const bool no_fused = std::getenv("LT_DFT_AXES") != nullptr;  // A/B: per-axis launches
+        if (!no_fused && f.nax >= 2 && dft_fused_smem(f) <= 200 * 1024) {
+            for (int op = 0; op < nops; ++op) {
+                f.gen[op] = blocks[op];
+                f.out[op] = out[op] = buf[op][1];
+            }
+            launch_dft_fused(L, f, nops);
+            return;
+        }
+    }
     DftAxisArgs a;
     a.mm = mm;
     for (int l = 0; l < 3; ++l) a.in[l] = P.ext[l];

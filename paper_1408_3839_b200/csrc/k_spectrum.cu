@@ -97,6 +97,155 @@ void launch_dft_axis2(const Launch& L, const DftAxisArgs& a, int nops) {
     L.tick();
 }
 
+// ---------------------------------------------------------------------------
+// Multi-axis lattice DFT in one launch: CTA per (block entry e, operator). The entry's
+// compressed generating cube (at most (2b+1)^3 stored offsets) is gathered once into shared
+// memory and every wrapped axis is transformed there in turn (same twiddles and the same
+// ascending-c accumulation per output as k_dft_axis2); only the last axis writes to global
+// memory. The per-axis kernel re-reads its input once per output frequency (L-fold L2
+// traffic) and runs one launch per axis; this reads the cube once.
+// ---------------------------------------------------------------------------
+// One pass along axis AX (n: input extents, updated to the output extents). A thread takes
+// (line, chunk of JT outputs): its nc inputs are read once, the twiddles are read as
+// broadcasts (chunks vary slowest across threads), and the JT accumulators stay in
+// registers. Compile-time AX and scalar extents keep every index in registers (a
+// dynamically indexed extent array would live in local memory).
+template <int AX>
+__device__ __forceinline__ void dft_pass(unsigned& n0, unsigned& n1, unsigned& n2, unsigned L, unsigned nc,
+                                         const double2* __restrict__ t, const double2* in, double2* outs,
+                                         double2* __restrict__ outg, Index mm, Index e) {
+    constexpr unsigned JT = 8;
+    const unsigned o0 = AX == 0 ? L : n0, o1 = AX == 1 ? L : n1, o2 = AX == 2 ? L : n2;
+    const unsigned uext = AX == 0 ? n1 : n0, wext = AX == 2 ? n1 : n2;
+    const unsigned nlines = uext * wext;
+    const unsigned sin_ = AX == 0 ? n1 * n2 : (AX == 1 ? n2 : 1u);
+    const unsigned sout = AX == 0 ? o1 * o2 : (AX == 1 ? o2 : 1u);
+    const unsigned nch = (L + JT - 1) / JT;
+    for (unsigned task = threadIdx.x; task < nlines * nch; task += blockDim.x) {
+        const unsigned line = task % nlines, ch = task / nlines;
+        const unsigned u = line / wext, w = line % wext;
+        unsigned bin, bout;
+        if (AX == 0) {
+            bin = u * n2 + w;
+            bout = u * o2 + w;
+        } else if (AX == 1) {
+            bin = u * n1 * n2 + w;
+            bout = u * o1 * o2 + w;
+        } else {
+            bin = (u * n1 + w) * n2;
+            bout = (u * o1 + w) * o2;
+        }
+        const unsigned j0 = ch * JT;
+        double2 acc[JT];
+#pragma unroll
+        for (unsigned jj = 0; jj < JT; ++jj) acc[jj] = make_double2(0.0, 0.0);
+        for (unsigned c = 0; c < nc; ++c) {
+            const double2 x = in[bin + c * sin_];
+#pragma unroll
+            for (unsigned jj = 0; jj < JT; ++jj)
+                if (j0 + jj < L) acc[jj] = cadd(acc[jj], cmul(t[(j0 + jj) * nc + c], x));
+        }
+#pragma unroll
+        for (unsigned jj = 0; jj < JT; ++jj) {
+            if (j0 + jj >= L) break;
+            const unsigned q = bout + (j0 + jj) * sout;
+            if (outg) outg[static_cast<Index>(q) * mm + e] = acc[jj];
+            else outs[q] = acc[jj];
+        }
+    }
+    n0 = o0;
+    n1 = o1;
+    n2 = o2;
+}
+
+__global__ void __launch_bounds__(512) k_dft_fused(DftFusedArgs a) {
+    extern __shared__ double2 fsm[];
+    const Index e = blockIdx.x;
+    const int op = blockIdx.y;
+    const Index mm = a.mm;
+    // twiddles of the wrapped axes in pass order, then two cube buffers
+    unsigned twoff = 0;
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        const Index L = a.dims[ax], nc = a.ncomp[ax];
+        if (L == 1) continue;
+        for (Index q = threadIdx.x; q < L * nc; q += blockDim.x) {
+            const Index j = q / nc, c = q % nc;
+            const Index m = (j * a.comp[ax][c]) % L;
+            double sn, cs;
+            sincospi(-2.0 * static_cast<double>(m) / static_cast<double>(L), &sn, &cs);
+            fsm[twoff + q] = make_double2(cs, sn);
+        }
+        twoff += static_cast<unsigned>(L * nc);
+    }
+    double2* buf0 = fsm + twoff;
+    double2* buf1 = buf0 + a.maxsz;
+    const double* gen = a.gen[op];
+    const unsigned ncube = static_cast<unsigned>(a.ext[0] * a.ext[1] * a.ext[2]);
+    {
+        // gather the entry's stored values: block indices first, then the values, four
+        // independent loads in flight per thread
+        constexpr unsigned U = 4;
+        for (unsigned q0 = threadIdx.x; q0 < ncube; q0 += U * blockDim.x) {
+            int bi[U];
+#pragma unroll
+            for (unsigned u = 0; u < U; ++u) {
+                const unsigned q = q0 + u * blockDim.x;
+                bi[u] = q < ncube ? a.slot2blk[q] : -1;
+            }
+            double v[U];
+#pragma unroll
+            for (unsigned u = 0; u < U; ++u) v[u] = bi[u] >= 0 ? gen[static_cast<Index>(bi[u]) * mm + e] : 0.0;
+#pragma unroll
+            for (unsigned u = 0; u < U; ++u) {
+                const unsigned q = q0 + u * blockDim.x;
+                if (q < ncube) buf0[q] = make_double2(v[u], 0.0);
+            }
+        }
+    }
+    __syncthreads();
+    unsigned n0 = static_cast<unsigned>(a.ext[0]), n1 = static_cast<unsigned>(a.ext[1]),
+             n2 = static_cast<unsigned>(a.ext[2]);
+    const double2* t = fsm;
+    double2* cur = buf0;
+    double2* nxt = buf1;
+    int done = 0;
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        const unsigned L = static_cast<unsigned>(a.dims[ax]), nc = static_cast<unsigned>(a.ncomp[ax]);
+        if (L == 1) continue;
+        ++done;
+        double2* og = done == a.nax ? a.out[op] : nullptr;
+        if (ax == 0) dft_pass<0>(n0, n1, n2, L, nc, t, cur, nxt, og, mm, e);
+        else if (ax == 1) dft_pass<1>(n0, n1, n2, L, nc, t, cur, nxt, og, mm, e);
+        else dft_pass<2>(n0, n1, n2, L, nc, t, cur, nxt, og, mm, e);
+        t += L * nc;
+        double2* tmp = cur;
+        cur = nxt;
+        nxt = tmp;
+        __syncthreads();
+    }
+}
+
+size_t dft_fused_smem(const DftFusedArgs& a) {
+    size_t tw = 0;
+    for (int i = 0; i < a.nax; ++i) tw += static_cast<size_t>(a.dims[a.axes[i]] * a.ncomp[a.axes[i]]);
+    return sizeof(double2) * (tw + 2 * static_cast<size_t>(a.maxsz));
+}
+
+void launch_dft_fused(const Launch& L, const DftFusedArgs& a, int nops) {
+    const size_t smem = dft_fused_smem(a);
+    static size_t attr = 0;
+    if (smem > attr) {
+        LT_CU(cudaFuncSetAttribute(k_dft_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        attr = smem;
+    }
+    Stage st_(L, "dft_fused");
+    k_dft_fused<<<dim3(static_cast<unsigned>(a.mm), nops), 512, smem, L.st>>>(a);
+    LT_CU(cudaGetLastError());
+    L.tick();
+}
+
 // Full-space eigenvectors (block_circulant.cpp:267-289, eigensolver.cpp:164-175):
 // out[(i m0 + r) + col N] = L^-1/2 e^{i phi(i, j)} u_{j,m}[r] for columns col = j m0 + m in
 // [c0, c0 + ncols), phi = sum_l 2 pi (i_l j_l) / L_l accumulated as the reference does.

@@ -446,6 +446,19 @@ struct DftAxisArgs {
     double2* out_buf[2] = {nullptr, nullptr};
 };
 void launch_dft_axis2(const Launch& L, const DftAxisArgs& a, int nops);
+// all wrapped axes in one launch (k_spectrum.cu): CTA per (entry, operator), the entry's
+// cube in shared memory (two buffers of maxsz complex + twiddles; dft_fused_smem bytes)
+struct DftFusedArgs {
+    Index dims[3]{1, 1, 1}, ext[3]{1, 1, 1}, ncomp[3]{1, 1, 1};
+    Index mm = 0, maxsz = 0;
+    int nax = 0, axes[3]{0, 0, 0};
+    const int64_t* comp[3]{nullptr, nullptr, nullptr};
+    const int* slot2blk = nullptr;
+    const double* gen[2] = {nullptr, nullptr};
+    double2* out[2] = {nullptr, nullptr};
+};
+size_t dft_fused_smem(const DftFusedArgs& a);
+void launch_dft_fused(const Launch& L, const DftFusedArgs& a, int nops);
 // dense box pencil (k_dense.cu): CTAs of the shared-memory resident tridiagonalisation (0:
 // too large), the reduction itself (work: 4 n doubles, bar: one zeroed counter), the
 // tridiagonal eigenvalues and the in-place symmetrisation 0.5 (A + A^T)

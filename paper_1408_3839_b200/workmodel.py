@@ -178,6 +178,9 @@ def stage_work(ctx, s, periodic: bool, L0: int) -> Dict[str, Tuple[str, float, s
         # per transformed axis, H and S: read + write K m0^2 complex (single-axis transforms
         # small enough are fused into the pencil load: no dft_axis stage then)
         add("dft_axis", "hbm", 2 * 2 * 16.0 * K * mm * len(wrapped_dirs), "B")
+        # >= 2 wrapped axes: one fused launch reads the stored generating blocks once and
+        # writes the K Fourier blocks once, H and S
+        add("dft_fused", "hbm", 2 * (8.0 * nblocks * mm + 16.0 * K * mm), "B")
         add("pencil", "hbm", K * (2 * 16.0 * mm + 8.0 * m0), "B")
     else:
         Nb = s.basis_count

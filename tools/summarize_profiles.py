@@ -29,7 +29,7 @@ DST = os.path.join(ROOT, "profiles")
 # kernel -> bench stage (engine Stage names)
 STAGE = {
     "k_pencil": "pencil", "k_l0_scan": "l0_scan", "k_l0_sample": "l0_sample", "k_l0_init": "l0_init",
-    "k_triv_gemm": "triv_gemm", "k_triv_reduce_w": "triv_reduce_w", "k_dft_axis2": "dft_axis", "k_fill": "fill",
+    "k_triv_gemm": "triv_gemm", "k_triv_reduce_w": "triv_reduce_w", "k_dft_axis2": "dft_axis", "k_dft_fused": "dft_fused", "k_fill": "fill",
     "k_master": "master", "k_window_sum_uniform": "window_sum", "k_window_copy": "window_sum",
     "k_resfold_prep": "fold_prep", "k_resfold_reduce": "resfold_reduce", "k_fem_apply": "fem_apply",
     "k_profile_sample": "profiles", "k_profile_trim": "profiles", "k_sinc": "sinc", "k_hankel": "hankel_gemm",
