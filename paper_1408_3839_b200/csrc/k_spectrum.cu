@@ -158,25 +158,102 @@ __device__ __forceinline__ void dft_pass(unsigned& n0, unsigned& n1, unsigned& n
     n2 = o2;
 }
 
+// Power-of-two axes (L = 2^LOG <= 16): each line is zero-filled to L points from its
+// compressed inputs (cmap: position -> compressed index or -1) and transformed in registers
+// by a radix-2 decimation-in-frequency FFT (L/2 log2 L butterflies instead of L nc
+// multiply-adds); the output of slot j is X[bitrev(j)]. tw: w^m = e^{-2 pi i m / L}, m < L/2.
+template <int AX, int LOG>
+__device__ __forceinline__ void fft_pass(unsigned& n0, unsigned& n1, unsigned& n2, const int* __restrict__ cmap,
+                                         const double2* __restrict__ tw, const double2* in, double2* outs,
+                                         double2* __restrict__ outg, Index mm, Index e) {
+    constexpr unsigned L = 1u << LOG;
+    const unsigned o0 = AX == 0 ? L : n0, o1 = AX == 1 ? L : n1, o2 = AX == 2 ? L : n2;
+    const unsigned uext = AX == 0 ? n1 : n0, wext = AX == 2 ? n1 : n2;
+    const unsigned nlines = uext * wext;
+    const unsigned sin_ = AX == 0 ? n1 * n2 : (AX == 1 ? n2 : 1u);
+    const unsigned sout = AX == 0 ? o1 * o2 : (AX == 1 ? o2 : 1u);
+    double2 w[L / 2];
+#pragma unroll
+    for (unsigned m = 0; m < L / 2; ++m) w[m] = tw[m];
+    for (unsigned line = threadIdx.x; line < nlines; line += blockDim.x) {
+        const unsigned u = line / wext, v = line % wext;
+        unsigned bin, bout;
+        if (AX == 0) {
+            bin = u * n2 + v;
+            bout = u * o2 + v;
+        } else if (AX == 1) {
+            bin = u * n1 * n2 + v;
+            bout = u * o1 * o2 + v;
+        } else {
+            bin = (u * n1 + v) * n2;
+            bout = (u * o1 + v) * o2;
+        }
+        double2 x[L];
+#pragma unroll
+        for (unsigned p = 0; p < L; ++p) {
+            const int c = cmap[p];
+            x[p] = c >= 0 ? in[bin + static_cast<unsigned>(c) * sin_] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (unsigned span = L / 2; span >= 1; span >>= 1) {
+#pragma unroll
+            for (unsigned b = 0; b < L; b += 2 * span)
+#pragma unroll
+                for (unsigned i = 0; i < span; ++i) {
+                    const double2 a = x[b + i], c = x[b + i + span];
+                    x[b + i] = cadd(a, c);
+                    x[b + i + span] = cmul(csub(a, c), w[i * (L / (2 * span))]);
+                }
+        }
+#pragma unroll
+        for (unsigned j = 0; j < L; ++j) {
+            unsigned r = 0;
+#pragma unroll
+            for (int bit = 0; bit < LOG; ++bit) r |= ((j >> bit) & 1u) << (LOG - 1 - bit);
+            const unsigned q = bout + j * sout;
+            if (outg) outg[static_cast<Index>(q) * mm + e] = x[r];
+            else outs[q] = x[r];
+        }
+    }
+    n0 = o0;
+    n1 = o1;
+    n2 = o2;
+}
+
 __global__ void __launch_bounds__(512) k_dft_fused(DftFusedArgs a) {
     extern __shared__ double2 fsm[];
     const Index e = blockIdx.x;
     const int op = blockIdx.y;
     const Index mm = a.mm;
-    // twiddles of the wrapped axes in pass order, then two cube buffers
+    // per wrapped axis in pass order: DFT twiddles (L x nc), or for power-of-two L <= 16 the
+    // FFT twiddles (L/2) and the position -> compressed-index map (L ints, 8-byte slots);
+    // then two cube buffers
     unsigned twoff = 0;
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
         const Index L = a.dims[ax], nc = a.ncomp[ax];
         if (L == 1) continue;
-        for (Index q = threadIdx.x; q < L * nc; q += blockDim.x) {
-            const Index j = q / nc, c = q % nc;
-            const Index m = (j * a.comp[ax][c]) % L;
-            double sn, cs;
-            sincospi(-2.0 * static_cast<double>(m) / static_cast<double>(L), &sn, &cs);
-            fsm[twoff + q] = make_double2(cs, sn);
+        if (dft_fft_log(L) > 0) {
+            for (Index q = threadIdx.x; q < L / 2; q += blockDim.x) {
+                double sn, cs;
+                sincospi(-2.0 * static_cast<double>(q) / static_cast<double>(L), &sn, &cs);
+                fsm[twoff + q] = make_double2(cs, sn);
+            }
+            int* cm = reinterpret_cast<int*>(fsm + twoff + L / 2);
+            for (Index q = threadIdx.x; q < L; q += blockDim.x) cm[q] = -1;
+            __syncthreads();
+            for (Index c = threadIdx.x; c < nc; c += blockDim.x) cm[a.comp[ax][c]] = static_cast<int>(c);
+            twoff += static_cast<unsigned>(L / 2 + L);
+        } else {
+            for (Index q = threadIdx.x; q < L * nc; q += blockDim.x) {
+                const Index j = q / nc, c = q % nc;
+                const Index m = (j * a.comp[ax][c]) % L;
+                double sn, cs;
+                sincospi(-2.0 * static_cast<double>(m) / static_cast<double>(L), &sn, &cs);
+                fsm[twoff + q] = make_double2(cs, sn);
+            }
+            twoff += static_cast<unsigned>(L * nc);
         }
-        twoff += static_cast<unsigned>(L * nc);
     }
     double2* buf0 = fsm + twoff;
     double2* buf1 = buf0 + a.maxsz;
@@ -216,10 +293,29 @@ __global__ void __launch_bounds__(512) k_dft_fused(DftFusedArgs a) {
         if (L == 1) continue;
         ++done;
         double2* og = done == a.nax ? a.out[op] : nullptr;
-        if (ax == 0) dft_pass<0>(n0, n1, n2, L, nc, t, cur, nxt, og, mm, e);
-        else if (ax == 1) dft_pass<1>(n0, n1, n2, L, nc, t, cur, nxt, og, mm, e);
-        else dft_pass<2>(n0, n1, n2, L, nc, t, cur, nxt, og, mm, e);
-        t += L * nc;
+        const int lg = dft_fft_log(L);
+        if (lg > 0) {
+            const int* cm = reinterpret_cast<const int*>(t + L / 2);
+#define LT_FFT_CASE(LG)                                                                            \
+    case LG:                                                                                       \
+        if (ax == 0) fft_pass<0, LG>(n0, n1, n2, cm, t, cur, nxt, og, mm, e);                      \
+        else if (ax == 1) fft_pass<1, LG>(n0, n1, n2, cm, t, cur, nxt, og, mm, e);                 \
+        else fft_pass<2, LG>(n0, n1, n2, cm, t, cur, nxt, og, mm, e);                              \
+        break;
+            switch (lg) {
+                LT_FFT_CASE(1)
+                LT_FFT_CASE(2)
+                LT_FFT_CASE(3)
+                LT_FFT_CASE(4)
+            }
+#undef LT_FFT_CASE
+            t += L / 2 + L;
+        } else {
+            if (ax == 0) dft_pass<0>(n0, n1, n2, L, nc, t, cur, nxt, og, mm, e);
+            else if (ax == 1) dft_pass<1>(n0, n1, n2, L, nc, t, cur, nxt, og, mm, e);
+            else dft_pass<2>(n0, n1, n2, L, nc, t, cur, nxt, og, mm, e);
+            t += L * nc;
+        }
         double2* tmp = cur;
         cur = nxt;
         nxt = tmp;
@@ -229,7 +325,10 @@ __global__ void __launch_bounds__(512) k_dft_fused(DftFusedArgs a) {
 
 size_t dft_fused_smem(const DftFusedArgs& a) {
     size_t tw = 0;
-    for (int i = 0; i < a.nax; ++i) tw += static_cast<size_t>(a.dims[a.axes[i]] * a.ncomp[a.axes[i]]);
+    for (int i = 0; i < a.nax; ++i) {
+        const Index L = a.dims[a.axes[i]];
+        tw += static_cast<size_t>(dft_fft_log(L) > 0 ? L / 2 + L : L * a.ncomp[a.axes[i]]);
+    }
     return sizeof(double2) * (tw + 2 * static_cast<size_t>(a.maxsz));
 }
 

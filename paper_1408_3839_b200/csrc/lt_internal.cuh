@@ -457,6 +457,18 @@ struct DftFusedArgs {
     const double* gen[2] = {nullptr, nullptr};
     double2* out[2] = {nullptr, nullptr};
 };
+// log2 L for the register FFT of power-of-two axes 2 <= L <= 16 (0: DFT pass); LT_DFT_NO_FFT
+// at compile time forces the DFT pass
+__host__ __device__ inline int dft_fft_log(Index L) {
+#ifdef LT_DFT_NO_FFT
+    (void)L;
+    return 0;
+#else
+    for (int lg = 1; lg <= 4; ++lg)
+        if (L == (Index(1) << lg)) return lg;
+    return 0;
+#endif
+}
 size_t dft_fused_smem(const DftFusedArgs& a);
 void launch_dft_fused(const Launch& L, const DftFusedArgs& a, int nops);
 // dense box pencil (k_dense.cu): CTAs of the shared-memory resident tridiagonalisation (0:
