@@ -674,7 +674,12 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
             const bool done = !(nb - na > 2.2e-16 * fmax(fabs(na), fabs(nb)) + atol) || (na == a && nb == b);
             a = na;
             b = nb;
-            if (__all_sync(0xffffffffu, done || !active)) break;
+            if (__all_sync(0xffffffffu, done || !active)) {
+#ifdef LT_PENCIL_PROFILE
+                if (t == 0 && k < 8192) lt_pencil_prof[k][7] = it + 1;  // multisection rounds
+#endif
+                break;
+            }
         }
         if (active && sub == 0) eig[k * m0 + mi] = 0.5 * (a + b) * unscale;
     }

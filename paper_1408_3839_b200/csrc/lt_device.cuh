@@ -74,13 +74,20 @@ __device__ __forceinline__ void sturm3(const double* sd, const double* se2, int 
         if (fabs(cur[j]) < kDelta) cur[j] = -kDelta;
         cnt[j] = cur[j] < 0.0;
     }
+    // The guard and the sign count run on the integer pipe (the FP64 pipe, shared by every
+    // warp of the SM, then carries only the DADD, DMUL and DFMA of the recurrence): |nx| below
+    // 2^-100 |cur| is detected from the exponent fields and nx replaced by the power of two
+    // 2^(e(cur) - 100) (within a factor 2 of 2^-100 |cur|) of the sign opposite to cur.
+    // The rescaling keeps e(cur) in [623, 1423], so the replacement stays normal.
     auto step = [&](double di, double ei) {
 #pragma unroll
         for (int j = 0; j < Q; ++j) {
             double nx = fma(di - x[j], cur[j], -ei * prev[j]);
-            const double thr = kDelta * fabs(cur[j]);
-            if (fabs(nx) < thr) nx = cur[j] < 0.0 ? thr : -thr;  // q = -2^-100
-            cnt[j] += (nx < 0.0) != (cur[j] < 0.0);
+            const int hn = __double2hiint(nx), hc = __double2hiint(cur[j]);
+            const int ec = (hc >> 20) & 0x7ff;
+            if (((hn >> 20) & 0x7ff) < ec - 100)
+                nx = __hiloint2double(static_cast<int>((~hc & 0x80000000u) | static_cast<unsigned>((ec - 100) << 20)), 0);
+            cnt[j] += static_cast<int>(static_cast<unsigned>(__double2hiint(nx) ^ hc) >> 31);
             prev[j] = cur[j];
             cur[j] = nx;
         }
@@ -96,9 +103,8 @@ __device__ __forceinline__ void sturm3(const double* sd, const double* se2, int 
         step(d3, e3);
 #pragma unroll
         for (int j = 0; j < Q; ++j) {
-            const double a = fabs(cur[j]);
-            if (a > 0x1p+400 || a < 0x1p-400) {
-                const int ex = static_cast<int>((__double_as_longlong(a) >> 52) & 0x7ff) - 1023;
+            const int ex = ((__double2hiint(cur[j]) >> 20) & 0x7ff) - 1023;
+            if (ex > 400 || ex < -400) {  // rare: exact power-of-two rescale of (cur, prev)
                 const double sc = __longlong_as_double(static_cast<long long>(1023 - ex) << 52);
                 cur[j] *= sc;
                 prev[j] *= sc;

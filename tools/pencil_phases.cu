@@ -67,13 +67,14 @@ static void run(int count, int m0, int reps) {
     }
     std::vector<long long> prof(8192 * 8);
     cudaMemcpyFromSymbol(prof.data(), lt_pencil_prof, prof.size() * sizeof(long long));
-    double ph[6] = {0, 0, 0, 0, 0, 0};
+    double ph[6] = {0, 0, 0, 0, 0, 0}, rounds = 0;
     const int nk = count < 8192 ? count : 8192;
     for (int k = 0; k < nk; ++k)
         for (int i = 0; i < 6; ++i) ph[i] += static_cast<double>(prof[k * 8 + i + 1] - prof[k * 8 + i]) / nk;
+    for (int k = 0; k < nk; ++k) rounds += static_cast<double>(prof[k * 8 + 7]) / nk;
     std::printf("%s count %5d m0 %2d NM %2d G %4d BS %4d: kernel %8.1f us | cycles load %7.0f herm %7.0f chol %7.0f "
-                "reduce %7.0f hh %7.0f bisect %7.0f | err %s\n",
-                VEC ? "vec" : "val", count, m0, NM, G, BS, best * 1e3, ph[0], ph[1], ph[2], ph[3], ph[4], ph[5],
+                "reduce %7.0f hh %7.0f bisect %7.0f rounds %4.1f | err %s\n",
+                VEC ? "vec" : "val", count, m0, NM, G, BS, best * 1e3, ph[0], ph[1], ph[2], ph[3], ph[4], ph[5], rounds,
                 cudaGetErrorString(cudaGetLastError()));
     cudaFree(dH);
     cudaFree(dS);
