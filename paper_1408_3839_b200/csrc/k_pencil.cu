@@ -717,8 +717,10 @@ static void dispatch_pencil(const Launch& L, Index count, Index m0, const double
                             unsigned long long* fail_key, bool periodic_checks, const PencilDft& dft, double2* vec,
                             const PencilReadback& rb) {
     if (m0 <= 8) {
-        if (count <= 1184) run_pencil<8, 128, 256, VEC>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft, vec, rb);
-        else run_pencil<8, 32, 256, VEC>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft, vec, rb);
+        // one pencil per 64-thread CTA while the batch is small (more SMs, fewer warps per
+        // SM sharing the FP64 pipe), warp-per-pencil in 128-thread CTAs for large batches
+        if (count <= 1184) run_pencil<8, 64, 64, VEC>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft, vec, rb);
+        else run_pencil<8, 32, 128, VEC>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft, vec, rb);
     } else if (m0 <= 16) {
         run_pencil<16, 64, 256, VEC>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft, vec, rb);
     } else if (m0 <= 32) {

@@ -85,6 +85,17 @@ static void run(int count, int m0, int reps) {
 int main() {
     run<8, 32, 256>(32, 8, 5);
     run<8, 128, 256>(32, 8, 5);
+    run<8, 128, 128>(32, 8, 5);
+    run<8, 64, 64>(32, 8, 5);
+    run<8, 64, 128>(32, 8, 5);
+    run<8, 256, 256>(32, 8, 5);
+    run<16, 64, 64>(512, 16, 5);
+    run<16, 128, 128>(512, 16, 5);
+    run<8, 32, 64>(4096, 8, 5);
+    run<8, 32, 128>(4096, 8, 5);
+    run<8, 64, 128>(4096, 8, 5);
+    run<32, 256, 256>(1, 32, 5);
+    run<32, 128, 128>(1, 32, 5);
     run<16, 64, 256>(512, 16, 5);
     run<16, 256, 256>(512, 16, 5);
     run<32, 256, 256>(1, 32, 5);
