@@ -126,27 +126,41 @@ __global__ void __launch_bounds__(256) k_resfold(ResFold f) {
         double2* dstp = reinterpret_cast<double2*>(sh);
         for (int idx = threadIdx.x; idx < tot / 2; idx += blockDim.x) dstp[idx] = srcp[idx];
     } else {
-        // short residue classes: gather the strided rows directly (same values as the slab)
+        // short residue classes: gather the strided rows directly (same values as the slab);
+        // U addresses per thread first, then U loads in flight, then the stores
         const long long gb = f.bguard ? f.G + 2 : f.G;
-        for (long long idx = threadIdx.x; idx < tot; idx += blockDim.x) {
-            const int src = static_cast<int>(idx / (static_cast<long long>(m0p) * ldj));
-            const int mu = static_cast<int>((idx / ldj) % m0p);
-            const long long c = idx % ldj;
-            double v = 0.0;
-            if (mu < f.m0) {
+        constexpr int U = 8;
+        const int itot = static_cast<int>(tot), plane = m0p * ldj;
+        for (int i0 = threadIdx.x; i0 < itot; i0 += U * blockDim.x) {
+            const double* ptr[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int idx = i0 + u * static_cast<int>(blockDim.x);
+                ptr[u] = nullptr;
+                if (idx >= itot) continue;
+                const int src = idx / plane, rem = idx % plane;
+                const int mu = rem / ldj, c = rem % ldj;
+                if (mu >= f.m0) continue;
                 if (src == 0) {
-                    if (c < J) v = f.a[mu * f.G + t + (c + f.jw0) * f.n];
+                    if (c < J) ptr[u] = f.a + mu * f.G + t + (c + f.jw0) * f.n;
                 } else if (c < J + 2) {
                     const double* bsrc = src == 2 ? f.b[1] : f.b[0];
                     const long long gi = t + (c - 1 + f.jw0) * f.n;
                     if (f.bguard) {
-                        if (gi >= -1 && gi <= f.G) v = bsrc[mu * gb + gi + 1];
+                        if (gi >= -1 && gi <= f.G) ptr[u] = bsrc + mu * gb + gi + 1;
                     } else if (gi >= 0 && gi < f.G) {
-                        v = bsrc[mu * gb + gi];
+                        ptr[u] = bsrc + mu * gb + gi;
                     }
                 }
             }
-            sh[idx] = v;
+            double v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) v[u] = ptr[u] ? __ldg(ptr[u]) : 0.0;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int idx = i0 + u * static_cast<int>(blockDim.x);
+                if (idx < itot) sh[idx] = v[u];
+            }
         }
     }
     if (f.W) {
@@ -161,6 +175,23 @@ __global__ void __launch_bounds__(256) k_resfold(ResFold f) {
             const int r0 = (f.Rtot * part) / parts, r1 = (f.Rtot * (part + 1)) / parts;
             double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
             int r = r0;
+            // eight (W, P) pairs in flight per round trip, four accumulators
+            for (; r + 7 < r1; r += 8) {
+                double w[8], pv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    w[u] = f.W[(r + u) * mme + e];
+                    pv[u] = f.P[(r + u) * f.prow + t];
+                }
+                v0 = fma(w[0], pv[0], v0);
+                v1 = fma(w[1], pv[1], v1);
+                v2 = fma(w[2], pv[2], v2);
+                v3 = fma(w[3], pv[3], v3);
+                v0 = fma(w[4], pv[4], v0);
+                v1 = fma(w[5], pv[5], v1);
+                v2 = fma(w[6], pv[6], v2);
+                v3 = fma(w[7], pv[7], v3);
+            }
             for (; r + 3 < r1; r += 4) {
                 v0 = fma(f.W[(r + 0) * mme + e], f.P[(r + 0) * f.prow + t], v0);
                 v1 = fma(f.W[(r + 1) * mme + e], f.P[(r + 1) * f.prow + t], v1);

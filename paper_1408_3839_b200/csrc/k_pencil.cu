@@ -76,6 +76,7 @@ struct PSmem {
     double red[4][32];
     double scal[4];
     double2 tw[kPencilDftMax];  // fused DFT: twiddles of this k-point
+    int blk[kPencilDftMax];     // fused DFT: stored block of each compressed offset (-1: none)
     // vector mode (parallel Jacobi): rotation of pair i = (jp[i], jq[i]); pair of index x
     double jc[NM / 2 + 1], js[NM / 2 + 1], jtr[NM / 2 + 1];
     double2 jph[NM / 2 + 1];
@@ -357,6 +358,7 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
             double sn, co;
             sincospi(-2.0 * static_cast<double>(mres) / static_cast<double>(dft.L), &sn, &co);
             sm.tw[c] = make_double2(co, sn);
+            sm.blk[c] = static_cast<int>(dft.blk[c]);
         }
         gsync<G>(slot);
     }
@@ -367,11 +369,29 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
             const int r = e % NM, c = e / NM;
             if (r < m0 && c < m0) {
                 if (dft.nc > 0) {
+                    // block indices from shared memory and eight (H, S) loads in flight per
+                    // batch; the sums stay in ascending q
                     double2 ah = make_double2(0.0, 0.0), as = make_double2(0.0, 0.0);
-                    for (int q = 0; q < dft.nc; ++q) {
-                        const Index b = dft.blk[q];
-                        const double vh = b >= 0 ? dft.GH[b * mm + r + c * m0] : 0.0;
-                        const double vs = b >= 0 ? dft.GS[b * mm + r + c * m0] : 0.0;
+                    const Index off = r + c * m0;
+                    int q = 0;
+                    for (; q + 7 < dft.nc; q += 8) {
+                        double vh[8], vs[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const int b = sm.blk[q + u];
+                            vh[u] = b >= 0 ? dft.GH[static_cast<Index>(b) * mm + off] : 0.0;
+                            vs[u] = b >= 0 ? dft.GS[static_cast<Index>(b) * mm + off] : 0.0;
+                        }
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            ah = cadd(ah, cmul(sm.tw[q + u], make_double2(vh[u], 0.0)));
+                            as = cadd(as, cmul(sm.tw[q + u], make_double2(vs[u], 0.0)));
+                        }
+                    }
+                    for (; q < dft.nc; ++q) {
+                        const int b = sm.blk[q];
+                        const double vh = b >= 0 ? dft.GH[static_cast<Index>(b) * mm + off] : 0.0;
+                        const double vs = b >= 0 ? dft.GS[static_cast<Index>(b) * mm + off] : 0.0;
                         ah = cadd(ah, cmul(sm.tw[q], make_double2(vh, 0.0)));
                         as = cadd(as, cmul(sm.tw[q], make_double2(vs, 0.0)));
                     }
