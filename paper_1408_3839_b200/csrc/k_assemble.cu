@@ -80,7 +80,17 @@ __global__ void k_fill(FillDev f) {
                 const Index ad = d[l] < 0 ? -d[l] : d[l];
                 const Index ee = d[l] < 0 ? (e / f.m0) + (e % f.m0) * f.m0 : e;
                 double acc = 0.0;
-                for (Index t = 0; t < f.Nres; ++t) acc += f.Npart[(t * f.Nnd + ad) * mm + ee];
+                const double* src = f.Npart + ad * mm + ee;
+                const Index step = f.Nnd * mm;
+                Index t = 0;
+                for (; t + 7 < f.Nres; t += 8) {  // eight loads in flight, summed in t order
+                    double v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) v[u] = src[(t + u) * step];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) acc += v[u];
+                }
+                for (; t < f.Nres; ++t) acc += src[t * step];
                 nuc = acc;
             } else if (f.nuc_mode == 1) {
                 const int l = f.s2_dir;
