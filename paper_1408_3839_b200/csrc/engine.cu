@@ -1308,7 +1308,7 @@ static void box_eig_device(lt_ctx* c, Index n, double* H, double* S, double* eig
             L.tick(2);
         }
         double2* vc = vec_dev ? c->arena.get<double2>("box.vc", n * n) : nullptr;
-        launch_pencil(L, 1, n, hc, sc, eig_dev, fail_dev, false, PencilDft{}, vc, rb);
+        launch_pencil(L, 1, n, hc, sc, eig_dev, fail_dev, false, PencilDft{}, vc, rb, true);
         if (vec_dev) {  // real symmetric input: the Jacobi rotations stay real
             Stage st_(L, "c2r");
             k_complex_real<<<static_cast<unsigned>((n * n + 255) / 256), 256, 0, c->stream>>>(n * n, vc, vec_dev);

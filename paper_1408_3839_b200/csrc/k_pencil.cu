@@ -52,6 +52,32 @@ __device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -
 __device__ __forceinline__ double2 cscale(double s, double2 a) { return make_double2(s * a.x, s * a.y); }
 __device__ __forceinline__ double cabs2(double2 a) { return a.x * a.x + a.y * a.y; }
 __device__ __forceinline__ double cabs_(double2 a) { return sqrt(a.x * a.x + a.y * a.y); }
+// real-arithmetic variants (RE: a real symmetric pencil carried in the complex layout with
+// zero imaginary parts, the box path): the same formulas without the imaginary terms
+template <bool RE> __device__ __forceinline__ double2 cmul_(double2 a, double2 b) {
+    if constexpr (RE) return make_double2(a.x * b.x, 0.0); else return cmul(a, b);
+}
+template <bool RE> __device__ __forceinline__ double2 cmulc_(double2 a, double2 b) {
+    if constexpr (RE) return make_double2(a.x * b.x, 0.0); else return cmulc(a, b);
+}
+template <bool RE> __device__ __forceinline__ double2 cadd_(double2 a, double2 b) {
+    if constexpr (RE) return make_double2(a.x + b.x, 0.0); else return cadd(a, b);
+}
+template <bool RE> __device__ __forceinline__ double2 csub_(double2 a, double2 b) {
+    if constexpr (RE) return make_double2(a.x - b.x, 0.0); else return csub(a, b);
+}
+template <bool RE> __device__ __forceinline__ double2 cconj_(double2 a) {
+    if constexpr (RE) return make_double2(a.x, 0.0); else return cconj(a);
+}
+template <bool RE> __device__ __forceinline__ double2 cscale_(double sc, double2 a) {
+    if constexpr (RE) return make_double2(sc * a.x, 0.0); else return cscale(sc, a);
+}
+template <bool RE> __device__ __forceinline__ double cabs2_(double2 a) {
+    if constexpr (RE) return a.x * a.x; else return cabs2(a);
+}
+template <bool RE> __device__ __forceinline__ double cabsr_(double2 a) {
+    if constexpr (RE) return fabs(a.x); else return cabs_(a);
+}
 
 template <int G>
 __device__ __forceinline__ void gsync(int slot) {
@@ -327,7 +353,7 @@ __device__ __forceinline__ void group_done(const PencilReadback& rb, Index count
 
 // Threads of a group own matrix entries e = t + G*u (row e % NM, column e / NM); the
 // Householder mat-vec uses TPR = G / NM threads per row.
-template <int NM, int G, int BS, bool VEC>
+template <int NM, int G, int BS, bool VEC, bool RE = false>
 __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double2* __restrict__ Hb,
                                                 const double2* __restrict__ Sb, double* __restrict__ eig,
                                                 unsigned long long* fail_key, int periodic_checks, PencilDft dft,
@@ -384,16 +410,16 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
                         }
 #pragma unroll
                         for (int u = 0; u < 8; ++u) {
-                            ah = cadd(ah, cmul(sm.tw[q + u], make_double2(vh[u], 0.0)));
-                            as = cadd(as, cmul(sm.tw[q + u], make_double2(vs[u], 0.0)));
+                            ah = cadd_<RE>(ah, cmul_<RE>(sm.tw[q + u], make_double2(vh[u], 0.0)));
+                            as = cadd_<RE>(as, cmul_<RE>(sm.tw[q + u], make_double2(vs[u], 0.0)));
                         }
                     }
                     for (; q < dft.nc; ++q) {
                         const int b = sm.blk[q];
                         const double vh = b >= 0 ? dft.GH[static_cast<Index>(b) * mm + off] : 0.0;
                         const double vs = b >= 0 ? dft.GS[static_cast<Index>(b) * mm + off] : 0.0;
-                        ah = cadd(ah, cmul(sm.tw[q], make_double2(vh, 0.0)));
-                        as = cadd(as, cmul(sm.tw[q], make_double2(vs, 0.0)));
+                        ah = cadd_<RE>(ah, cmul_<RE>(sm.tw[q], make_double2(vh, 0.0)));
+                        as = cadd_<RE>(as, cmul_<RE>(sm.tw[q], make_double2(vs, 0.0)));
                     }
                     A[r][c] = ah;
                     B[r][c] = as;
@@ -419,12 +445,12 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
             if (e < NM * NM) {
                 const int r = e % NM, c = e / NM;
                 const double2 a = A[r][c], at = A[c][r], b = B[r][c], bt = B[c][r];
-                red4[0] = fmax(red4[0], cabs_(a));
-                red4[1] = fmax(red4[1], cabs_(b));
-                red4[2] = fmax(red4[2], cabs_(csub(a, cconj(at))));
-                red4[3] = fmax(red4[3], cabs_(csub(b, cconj(bt))));
-                va[u] = cscale(0.5, cadd(a, cconj(at)));
-                vb[u] = cscale(0.5, cadd(b, cconj(bt)));
+                red4[0] = fmax(red4[0], cabsr_<RE>(a));
+                red4[1] = fmax(red4[1], cabsr_<RE>(b));
+                red4[2] = fmax(red4[2], cabsr_<RE>(csub_<RE>(a, cconj_<RE>(at))));
+                red4[3] = fmax(red4[3], cabsr_<RE>(csub_<RE>(b, cconj_<RE>(bt))));
+                va[u] = cscale_<RE>(0.5, cadd_<RE>(a, cconj_<RE>(at)));
+                vb[u] = cscale_<RE>(0.5, cadd_<RE>(b, cconj_<RE>(bt)));
             }
         }
         greduce<G, 4, true>(red4, sm.red, t, slot);  // its barriers also order the reads above
@@ -458,7 +484,7 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
                 if (e < NM * NM) {
                     const int r = e % NM, c = e / NM;
                     if (c > kk && r >= c && r < n)
-                        B[r][c] = csub(B[r][c], cscale(ixk, cmul(B[r][kk], cconj(B[c][kk]))));
+                        B[r][c] = csub_<RE>(B[r][c], cscale_<RE>(ixk, cmul_<RE>(B[r][kk], cconj_<RE>(B[c][kk]))));
                 }
             }
             if (t == 0) sm.ix[kk] = ixk;
@@ -484,7 +510,7 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
             const int e = t + G * u;
             if (e < NM * NM) {
                 const int r = e % NM, c = e / NM;
-                if (r > i && r < n && c < n) A[r][c] = csub(A[r][c], cscale(ixi, cmul(B[r][i], A[i][c])));
+                if (r > i && r < n && c < n) A[r][c] = csub_<RE>(A[r][c], cscale_<RE>(ixi, cmul_<RE>(B[r][i], A[i][c])));
             }
         }
         gsync<G>(slot);
@@ -495,7 +521,7 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
         const int e = t + G * u;
         if (e < NM * NM) {
             const int r = e % NM, c = e / NM;
-            C[r][c] = (r < n && c < n) ? cscale(sm.invd[c], cconj(A[c][r])) : make_double2(0.0, 0.0);
+            C[r][c] = (r < n && c < n) ? cscale_<RE>(sm.invd[c], cconj_<RE>(A[c][r])) : make_double2(0.0, 0.0);
         }
     }
     gsync<G>(slot);
@@ -506,7 +532,7 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
             const int e = t + G * u;
             if (e < NM * NM) {
                 const int r = e % NM, c = e / NM;
-                if (r > i && r < n && c < n) C[r][c] = csub(C[r][c], cscale(ixi, cmul(B[r][i], C[i][c])));
+                if (r > i && r < n && c < n) C[r][c] = csub_<RE>(C[r][c], cscale_<RE>(ixi, cmul_<RE>(B[r][i], C[i][c])));
             }
         }
         gsync<G>(slot);
@@ -520,7 +546,7 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
             if (e < NM * NM) {
                 const int r = e % NM, c = e / NM;
                 y[u] = (r < n && c < n)
-                           ? cscale(0.5, cadd(cscale(sm.invd[r], C[r][c]), cconj(cscale(sm.invd[c], C[c][r]))))
+                           ? cscale_<RE>(0.5, cadd_<RE>(cscale_<RE>(sm.invd[r], C[r][c]), cconj_<RE>(cscale_<RE>(sm.invd[c], C[c][r]))))
                            : make_double2(0.0, 0.0);
             }
         }
@@ -543,7 +569,7 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
         const int m = n - kk - 1;  // reflector length (rows kk+1 .. n-1)
         // zlarfg on x = A[kk+1 .. n-1][kk]
         double xr[1] = {0.0};
-        for (int i = kk + 2 + t; i < n; i += G) xr[0] += cabs2(A[i][kk]);
+        for (int i = kk + 2 + t; i < n; i += G) xr[0] += cabs2_<RE>(A[i][kk]);
         greduce<G, 1, false>(xr, sm.red, t, slot);
         const double xn2 = xr[0];
         const double2 x0 = A[kk + 1][kk];
@@ -564,22 +590,22 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
             scal = make_double2(den.x * id, -den.y * id);
         }
         // v (index 0 <-> row kk+1)
-        for (int i = t; i < m; i += G) sm.v[i] = i == 0 ? make_double2(1.0, 0.0) : cmul(A[kk + 1 + i][kk], scal);
+        for (int i = t; i < m; i += G) sm.v[i] = i == 0 ? make_double2(1.0, 0.0) : cmul_<RE>(A[kk + 1 + i][kk], scal);
         gsync<G>(slot);
         if (tau.x != 0.0 || tau.y != 0.0) {
             // y = A22 v (TPR threads per row), then w = tau y - 1/2 |tau|^2 (v^H y) v
             double2 yi = make_double2(0.0, 0.0);
             if (row < m)
-                for (int j = part; j < m; j += TPR) yi = cadd(yi, cmul(A[kk + 1 + row][kk + 1 + j], sm.v[j]));
+                for (int j = part; j < m; j += TPR) yi = cadd_<RE>(yi, cmul_<RE>(A[kk + 1 + row][kk + 1 + j], sm.v[j]));
 #pragma unroll
             for (int o = TPR / 2; o > 0; o >>= 1) {
                 yi.x += __shfl_xor_sync(0xffffffffu, yi.x, o);
                 yi.y += __shfl_xor_sync(0xffffffffu, yi.y, o);
             }
-            double vr[1] = {(row < m && part == 0) ? cmulc(sm.v[row], yi).x : 0.0};  // Re(v^H y)
+            double vr[1] = {(row < m && part == 0) ? cmulc_<RE>(sm.v[row], yi).x : 0.0};  // Re(v^H y)
             greduce<G, 1, false>(vr, sm.red, t, slot);
             const double half = 0.5 * (tau.x * tau.x + tau.y * tau.y) * vr[0];
-            if (row < m && part == 0) sm.w[row] = csub(cmul(tau, yi), cscale(half, sm.v[row]));
+            if (row < m && part == 0) sm.w[row] = csub_<RE>(cmul_<RE>(tau, yi), cscale_<RE>(half, sm.v[row]));
             gsync<G>(slot);
             // A22 -= w v^H + v w^H
 #pragma unroll
@@ -588,8 +614,8 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
                 if (e < NM * NM) {
                     const int r = e % NM - kk - 1, c = e / NM - kk - 1;
                     if (r >= 0 && c >= 0 && r < m && c < m) {
-                        const double2 upd = cadd(cmul(sm.w[r], cconj(sm.v[c])), cmul(sm.v[r], cconj(sm.w[c])));
-                        A[r + kk + 1][c + kk + 1] = csub(A[r + kk + 1][c + kk + 1], upd);
+                        const double2 upd = cadd_<RE>(cmul_<RE>(sm.w[r], cconj_<RE>(sm.v[c])), cmul_<RE>(sm.v[r], cconj_<RE>(sm.w[c])));
+                        A[r + kk + 1][c + kk + 1] = csub_<RE>(A[r + kk + 1][c + kk + 1], upd);
                     }
                 }
             }
@@ -707,7 +733,7 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
     if (t == 0) group_done(rb, count);
 }
 
-template <int NM, int G, int BS, bool VEC>
+template <int NM, int G, int BS, bool VEC, bool RE = false>
 static void run_pencil(const Launch& L, Index count, Index m0, const double2* H, const double2* S, double* eig,
                        unsigned long long* fail_key, bool checks, const PencilDft& dft, double2* vec,
                        const PencilReadback& rb) {
@@ -716,13 +742,13 @@ static void run_pencil(const Launch& L, Index count, Index m0, const double2* H,
     const size_t smem = sizeof(PSmem<NM>) * PPC;
     static bool attr = false;
     if (!attr) {
-        LT_CU(cudaFuncSetAttribute(k_pencil<NM, G, BS, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        LT_CU(cudaFuncSetAttribute(k_pencil<NM, G, BS, VEC, RE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem)));
         attr = true;
     }
     const Index blocks = (count + PPC - 1) / PPC;
     Stage st_(L, "pencil");
-    k_pencil<NM, G, BS, VEC><<<static_cast<unsigned>(blocks), BS, smem, L.st>>>(
+    k_pencil<NM, G, BS, VEC, RE><<<static_cast<unsigned>(blocks), BS, smem, L.st>>>(
         count, static_cast<int>(m0), H, S, eig, fail_key, checks ? 1 : 0, dft, vec, rb);
     LT_CU(cudaGetLastError());
     L.tick();
@@ -752,8 +778,16 @@ static void dispatch_pencil(const Launch& L, Index count, Index m0, const double
 
 void launch_pencil(const Launch& L, Index count, Index m0, const double2* H, const double2* S, double* eig,
                    unsigned long long* fail_key, bool periodic_checks, const PencilDft& dft, double2* vec,
-                   const PencilReadback& rb) {
+                   const PencilReadback& rb, bool real) {
     if (count <= 0) return;
+    if (real && !vec && dft.nc == 0) {
+        // real symmetric pencils (box, N_b <= 32): real arithmetic in the complex layout
+        if (m0 <= 8) run_pencil<8, 64, 64, false, true>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft, nullptr, rb);
+        else if (m0 <= 16) run_pencil<16, 64, 256, false, true>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft, nullptr, rb);
+        else if (m0 <= 32) run_pencil<32, 256, 256, false, true>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft, nullptr, rb);
+        else fail(LT_EDIM, "pencil_eig: block size m0 > 32 is not supported by the batched solver");
+        return;
+    }
     if (dft.nc > kPencilDftMax) fail(LT_EGENERIC, "pencil_eig: fused DFT supports at most 64 stored offsets");
     if (vec) dispatch_pencil<true>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft, vec, rb);
     else dispatch_pencil<false>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft, nullptr, rb);

@@ -506,7 +506,7 @@ struct PencilReadback {
 void launch_pencil(const Launch& L, Index count, Index m0, const double2* H, const double2* S, double* eig,
                    unsigned long long* fail_key, bool periodic_checks, const PencilDft& dft = PencilDft{},
                    double2* vec = nullptr,  // vec: K m0 x m0 complex eigenvector blocks (vector mode)
-                   const PencilReadback& rb = PencilReadback{});
+                   const PencilReadback& rb = PencilReadback{}, bool real = false);
 
 // combine (eigensolver.cpp:37-67) on device buffers with index maps
 void launch_axpby_map(const Launch& L, Index nout, Index mm, double wa, const double* a, const int64_t* ia, double wb,

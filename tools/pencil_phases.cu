@@ -12,7 +12,7 @@
 
 #include "../paper_1408_3839_b200/csrc/k_pencil.cu"
 
-template <int NM, int G, int BS, bool VEC = false>
+template <int NM, int G, int BS, bool VEC = false, bool RE = false>
 static void run(int count, int m0, int reps) {
     std::mt19937_64 rng(count * 131 + m0);
     std::normal_distribution<double> nd;
@@ -20,8 +20,8 @@ static void run(int count, int m0, int reps) {
     std::vector<double2> H(static_cast<size_t>(count) * mm), S(H.size());
     for (int k = 0; k < count; ++k) {
         std::vector<double2> A(mm), B(mm);
-        for (auto& z : A) z = make_double2(nd(rng), nd(rng));
-        for (auto& z : B) z = make_double2(nd(rng), nd(rng));
+        for (auto& z : A) z = make_double2(nd(rng), RE ? 0.0 : nd(rng));
+        for (auto& z : B) z = make_double2(nd(rng), RE ? 0.0 : nd(rng));
         for (int r = 0; r < m0; ++r)
             for (int c = 0; c < m0; ++c) {
                 const double2 a = A[r + c * m0], at = A[c + r * m0];
@@ -48,7 +48,7 @@ static void run(int count, int m0, int reps) {
     cudaMemcpy(dS, S.data(), S.size() * sizeof(double2), cudaMemcpyHostToDevice);
     constexpr int PPC = BS / G;
     const size_t smem = sizeof(lt::PSmem<NM>) * PPC;
-    cudaFuncSetAttribute(lt::k_pencil<NM, G, BS, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(lt::k_pencil<NM, G, BS, VEC, RE>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     const int blocks = (count + PPC - 1) / PPC;
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
@@ -57,7 +57,7 @@ static void run(int count, int m0, int reps) {
     for (int r = 0; r < reps; ++r) {
         cudaMemset(fk, 0xff, sizeof(unsigned long long));
         cudaEventRecord(e0);
-        lt::k_pencil<NM, G, BS, VEC><<<blocks, BS, smem>>>(count, m0, dH, dS, de, fk, 1, lt::PencilDft{}, dv,
+        lt::k_pencil<NM, G, BS, VEC, RE><<<blocks, BS, smem>>>(count, m0, dH, dS, de, fk, 1, lt::PencilDft{}, dv,
                                                              lt::PencilReadback{});
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
@@ -74,7 +74,7 @@ static void run(int count, int m0, int reps) {
     for (int k = 0; k < nk; ++k) rounds += static_cast<double>(prof[k * 8 + 7]) / nk;
     std::printf("%s count %5d m0 %2d NM %2d G %4d BS %4d: kernel %8.1f us | cycles load %7.0f herm %7.0f chol %7.0f "
                 "reduce %7.0f hh %7.0f bisect %7.0f rounds %4.1f | err %s\n",
-                VEC ? "vec" : "val", count, m0, NM, G, BS, best * 1e3, ph[0], ph[1], ph[2], ph[3], ph[4], ph[5], rounds,
+                VEC ? "vec" : (RE ? "real" : "val"), count, m0, NM, G, BS, best * 1e3, ph[0], ph[1], ph[2], ph[3], ph[4], ph[5], rounds,
                 cudaGetErrorString(cudaGetLastError()));
     cudaFree(dH);
     cudaFree(dS);
@@ -83,6 +83,10 @@ static void run(int count, int m0, int reps) {
 }
 
 int main() {
+    run<32, 256, 256, false, false>(1, 32, 5);
+    run<32, 256, 256, false, true>(1, 32, 5);
+    run<8, 64, 64, false, true>(1, 8, 5);
+    run<8, 64, 64, false, false>(1, 8, 5);
     run<8, 32, 256>(32, 8, 5);
     run<8, 128, 256>(32, 8, 5);
     run<8, 128, 128>(32, 8, 5);
