@@ -596,9 +596,9 @@ static void direction_sources(const HostSys& h, int src[3]) {
 // split-K factor: aim for ~4 CTAs per SM while keeping >= 32 contraction steps (two
 // 16-deep tiles) per CTA: these GEMMs are load-latency bound, so more CTAs with fewer
 // dependent tile loads each finish sooner; the fixed-order split reduction absorbs it
-static int splits_for(long long tiles, long long len) {
+static int splits_for(long long tiles, long long len, int waves = 4) {
     int s = 1;
-    while (tiles * s < 4 * 148 && len / (s * 2) >= 32 && s < 512) s *= 2;
+    while (tiles * s < waves * 148 && len / (s * 2) >= 32 && s < 512) s *= 2;
     return s;
 }
 
@@ -856,7 +856,11 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
             long long maxG = 1;
             for (int j = 0; j < njobs; ++j) maxG = std::max(maxG, tj.j[j].G);
             const int tiles = static_cast<int>(((Rtot + 63) / 64) * ((nsym + 63) / 64));
-            const int splits = njobs ? splits_for(tiles * njobs, maxG) : 1;
+            // one wave of split-K CTAs: more splits shorten each CTA's K range below what
+            // amortises its prologue and multiply the partials the reduction reads (c4:
+            // 43 + 12 us at four waves, 37 + 5 us at one)
+            static const int triv_waves = std::getenv("LT_TRIV_WAVES") ? std::atoi(std::getenv("LT_TRIV_WAVES")) : 1;
+            const int splits = njobs ? splits_for(tiles * njobs, maxG, triv_waves) : 1;
             double* part = A.get<double>("nuc.tpart", std::max<size_t>(1, static_cast<size_t>(njobs) * splits * Rtot * nsym));
             double* W = A.get<double>("nuc.W", Rtot * mm);
             launch_triv_tables(L, tj, njobs, ws, static_cast<int>(m0), static_cast<int>(Rtot), w.potw, part, splits, W,

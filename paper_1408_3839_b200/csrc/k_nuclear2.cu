@@ -39,8 +39,13 @@ __device__ __forceinline__ void sym_pair(int es, int m0, int& mu, int& nu) {
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_triv_gemm(TrivJobs jobs, int m0, int Rtot, int nsym, int splits,
                                                    double* __restrict__ part) {
-    __shared__ double As[kGBM * kGLDA];   // potential rows [64][16 + pad]
-    __shared__ double Gs[32 * 17];        // profile rows of all functions [m0 <= 32][16 + 1]
+    // 32-deep stages: potential rows As[64][32 + 4], profile rows Gs[m0 <= 32][32 + 1] and
+    // the product tile Bs[32][64 + 8] (b(k, n) = g_mu(k) g_nu(k), formed once per stage by
+    // the CTA instead of per fragment by every m-warp)
+    constexpr int TK = 32, TLA = TK + 4, TLG = TK + 1, TLB = kGBN + 8;
+    __shared__ double As[kGBM * TLA];
+    __shared__ double Gs[32 * TLG];
+    __shared__ double Bs[TK * TLB];
     const int job = blockIdx.z / splits, split = blockIdx.z % splits;
     const TrivJob& J = jobs.j[job];
     const int r0 = blockIdx.x * kGBM, e0 = blockIdx.y * kGBN;
@@ -75,31 +80,24 @@ __global__ void __launch_bounds__(256) k_triv_gemm(TrivJobs jobs, int m0, int Rt
     const long long klo = sk[0];
     const long long khi = min(sk[1], static_cast<long long>(J.rows));
     const long long len = khi > klo ? khi - klo : 0;
-    const long long per = ((len + splits - 1) / splits + kGBK - 1) / kGBK * kGBK;
+    const long long per = ((len + splits - 1) / splits + TK - 1) / TK * TK;
     const long long k0 = klo + split * per, k1 = min(khi, k0 + per);
     const double* P = J.pot;
     const double* g = J.pwc;
     const long long G = J.G, rows = J.rows;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int wm = warp & 3, wn = warp >> 2, gg = lane >> 2, tq = lane & 3;
-    // this lane's four B columns: symmetric pairs (mu, nu) of the tile (zero beyond nsym)
-    int cmu[4], cnu[4];
-    bool cok[4];
-#pragma unroll
-    for (int nt = 0; nt < 4; ++nt) {
-        const int es = e0 + wn * 32 + nt * 8 + gg;
-        cok[nt] = es < nsym;
-        int mu = 0, nu = 0;
-        if (cok[nt]) sym_pair(es, m0, mu, nu);
-        cmu[nt] = mu;
-        cnu[nt] = nu;
-    }
-    double ra[4], rg[2];
+    // product-tile column of this thread (fixed): pair (pmu, pnu) of column bn, rows bk0 + 4u
+    const int bn = tid & 63, bk0 = tid >> 6;
+    const bool bok = e0 + bn < nsym;
+    int pmu = 0, pnu = 0;
+    if (bok) sym_pair(e0 + bn, m0, pmu, pnu);
+    double ra[8], rg[4];
     auto fetch = [&](long long kb) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 8; ++u) {
             const int e = tid + 256 * u;
-            const int am = e >> 4, ak = e & 15;  // k fastest: contiguous rows of P
+            const int am = e >> 5, ak = e & 31;  // k fastest: contiguous rows of P
             const long long k = kb + ak;
             double v = 0.0;
             if (k < k1 && r0 + am < Rtot)
@@ -107,9 +105,9 @@ __global__ void __launch_bounds__(256) k_triv_gemm(TrivJobs jobs, int m0, int Rt
             ra[u] = v;
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < 4; ++u) {
             const int e = tid + 256 * u;
-            const int gm = e >> 4, gk = e & 15;
+            const int gm = e >> 5, gk = e & 31;
             const long long k = kb + gk;
             rg[u] = (gm < m0 && k < k1) ? g[gm * G + k] : 0.0;
         }
@@ -117,30 +115,33 @@ __global__ void __launch_bounds__(256) k_triv_gemm(TrivJobs jobs, int m0, int Rt
     double acc[4][4] = {};
     if (k0 < k1) {
         fetch(k0);
-        for (long long kb = k0; kb < k1; kb += kGBK) {
+        for (long long kb = k0; kb < k1; kb += TK) {
             __syncthreads();
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = tid + 256 * u;
+                As[(e >> 5) * TLA + (e & 31)] = ra[u];
+            }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int e = tid + 256 * u;
-                As[(e >> 4) * kGLDA + (e & 15)] = ra[u];
-            }
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const int e = tid + 256 * u;
-                Gs[(e >> 4) * 17 + (e & 15)] = rg[u];
+                Gs[(e >> 5) * TLG + (e & 31)] = rg[u];
             }
             __syncthreads();
-            if (kb + kGBK < k1) fetch(kb + kGBK);  // next tile's loads overlap the MMAs
+            if (kb + TK < k1) fetch(kb + TK);  // next stage's loads overlap the products and MMAs
 #pragma unroll
-            for (int ks = 0; ks < kGBK; ks += 4) {
-                const double a0 = As[(wm * 16 + gg) * kGLDA + ks + tq];
-                const double a1 = As[(wm * 16 + gg + 8) * kGLDA + ks + tq];
+            for (int u = 0; u < 8; ++u) {
+                const int k = bk0 + 4 * u;
+                Bs[k * TLB + bn] = bok ? Gs[pmu * TLG + k] * Gs[pnu * TLG + k] : 0.0;
+            }
+            __syncthreads();
 #pragma unroll
-                for (int nt = 0; nt < 4; ++nt) {
-                    // B fragment (k = ks + tq, column gg of n-tile nt): g_mu(k) g_nu(k)
-                    const double b0 = cok[nt] ? Gs[cmu[nt] * 17 + ks + tq] * Gs[cnu[nt] * 17 + ks + tq] : 0.0;
-                    dmma_m16n8k4(acc[nt], a0, a1, b0);
-                }
+            for (int ks = 0; ks < TK; ks += 4) {
+                const double a0 = As[(wm * 16 + gg) * TLA + ks + tq];
+                const double a1 = As[(wm * 16 + gg + 8) * TLA + ks + tq];
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt)
+                    dmma_m16n8k4(acc[nt], a0, a1, Bs[(ks + tq) * TLB + wn * 32 + nt * 8 + gg]);
             }
         }
     }
