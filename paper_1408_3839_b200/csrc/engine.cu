@@ -856,15 +856,22 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
             long long maxG = 1;
             for (int j = 0; j < njobs; ++j) maxG = std::max(maxG, tj.j[j].G);
             const int tiles = static_cast<int>(((Rtot + 63) / 64) * ((nsym + 63) / 64));
-            // one wave of split-K CTAs: more splits shorten each CTA's K range below what
-            // amortises its prologue and multiply the partials the reduction reads (c4:
-            // 43 + 12 us at four waves, 37 + 5 us at one)
-            static const int triv_waves = std::getenv("LT_TRIV_WAVES") ? std::atoi(std::getenv("LT_TRIV_WAVES")) : 1;
-            const int splits = njobs ? splits_for(tiles * njobs, maxG, triv_waves) : 1;
+            // split-K: one wave of CTAs on the cp.async pipeline when each CTA still gets >= 8
+            // stages (long grids, c4: 43 + 12 us at four waves, 35 + 5 us at one), else four
+            // waves of short register-prefetched CTAs (a short K is latency-bound: c2)
+            static const int triv_waves = std::getenv("LT_TRIV_WAVES") ? std::atoi(std::getenv("LT_TRIV_WAVES")) : 0;
+            int splits = 1;
+            bool triv_async = false;
+            if (njobs) {
+                const int s1 = splits_for(tiles * njobs, maxG, 1);
+                triv_async = maxG / s1 >= 8 * 32;
+                const int w = triv_waves > 0 ? triv_waves : (triv_async ? 1 : 4);
+                splits = splits_for(tiles * njobs, maxG, w);
+            }
             double* part = A.get<double>("nuc.tpart", std::max<size_t>(1, static_cast<size_t>(njobs) * splits * Rtot * nsym));
             double* W = A.get<double>("nuc.W", Rtot * mm);
             launch_triv_tables(L, tj, njobs, ws, static_cast<int>(m0), static_cast<int>(Rtot), w.potw, part, splits, W,
-                               nullptr);
+                               nullptr, triv_async);
             if (nuc_mode == 1) {
                 ndir = wrapped[0];
                 const DirPlan& d = p.d[ndir];

@@ -34,18 +34,35 @@ __device__ __forceinline__ void sym_pair(int es, int m0, int& mu, int& nu) {
     nu = m + (es - base);
 }
 
+constexpr int kTrivTK = 32, kTrivStages = 3;
+
+// cp.async of one double into shared memory; src-size 0 (ok = false) writes a zero
+__device__ __forceinline__ void cp_async8_zfill(double* dst, const double* src, bool ok) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(ok ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // trivial-direction tables: split-K DMMA GEMM over the symmetric pairs
 // ---------------------------------------------------------------------------
+// ASYNC: kTrivStages-deep cp.async pipeline (long K per CTA); else one stage with the next
+// stage prefetched in registers (short K, many CTAs per SM)
+template <bool ASYNC>
 __global__ void __launch_bounds__(256) k_triv_gemm(TrivJobs jobs, int m0, int Rtot, int nsym, int splits,
                                                    double* __restrict__ part) {
-    // 32-deep stages: potential rows As[64][32 + 4], profile rows Gs[m0 <= 32][32 + 1] and
-    // the product tile Bs[32][64 + 8] (b(k, n) = g_mu(k) g_nu(k), formed once per stage by
-    // the CTA instead of per fragment by every m-warp)
-    constexpr int TK = 32, TLA = TK + 4, TLG = TK + 1, TLB = kGBN + 8;
-    __shared__ double As[kGBM * TLA];
-    __shared__ double Gs[32 * TLG];
-    __shared__ double Bs[TK * TLB];
+    // 32-deep stages, kTrivStages of them in flight through cp.async: potential rows
+    // As[st][64][32 + 4], profile rows Gs[st][m0 <= 32][32 + 1]; the product tile
+    // Bs[32][64 + 8] (b(k, n) = g_mu(k) g_nu(k)) is formed once per stage by the CTA
+    constexpr int TK = kTrivTK, TLA = TK + 4, TLG = TK + 1, TLB = kGBN + 8, NST = ASYNC ? kTrivStages : 1;
+    extern __shared__ double tsm_dyn[];
+    double* As = tsm_dyn;                      // [NST][kGBM * TLA]
+    double* Gs = As + NST * kGBM * TLA;        // [NST][32 * TLG]
+    double* Bs = Gs + NST * 32 * TLG;          // [TK * TLB]
     const int job = blockIdx.z / splits, split = blockIdx.z % splits;
     const TrivJob& J = jobs.j[job];
     const int r0 = blockIdx.x * kGBM, e0 = blockIdx.y * kGBN;
@@ -92,6 +109,61 @@ __global__ void __launch_bounds__(256) k_triv_gemm(TrivJobs jobs, int m0, int Rt
     const bool bok = e0 + bn < nsym;
     int pmu = 0, pnu = 0;
     if (bok) sym_pair(e0 + bn, m0, pmu, pnu);
+    double acc[4][4] = {};
+    if constexpr (ASYNC) {
+    // stage kb into buffer st: 8-byte cp.async copies, zero-filled outside the tile
+    auto issue = [&](long long kb, int st) {
+        double* as = As + st * kGBM * TLA;
+        double* gs = Gs + st * 32 * TLG;
+        if (kb < k1) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = tid + 256 * u;
+                const int am = e >> 5, ak = e & 31;  // k fastest: contiguous rows of P
+                const long long k = kb + ak;
+                const bool ok = k < k1 && r0 + am < Rtot;
+                cp_async8_zfill(as + am * TLA + ak, ok ? P + (r0 + am) * rows + k : P, ok);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = tid + 256 * u;
+                const int gm = e >> 5, gk = e & 31;
+                const long long k = kb + gk;
+                const bool ok = gm < m0 && k < k1;
+                cp_async8_zfill(gs + gm * TLG + gk, ok ? g + gm * G + k : g, ok);
+            }
+        }
+        cp_async_commit();
+    };
+    if (k0 < k1) {
+#pragma unroll
+        for (int st = 0; st < NST - 1; ++st) issue(k0 + st * TK, st);
+        int it = 0;
+        for (long long kb = k0; kb < k1; kb += TK, ++it) {
+            const int st = it % NST;
+            cp_async_wait<NST - 2>();  // this thread's copies of stage `it` have landed
+            __syncthreads();           // everyone's copies; every warp is past the MMAs of it - 1
+            issue(kb + (NST - 1) * TK, (it + NST - 1) % NST);
+            const double* as = As + st * kGBM * TLA;
+            const double* gs = Gs + st * 32 * TLG;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int k = bk0 + 4 * u;
+                Bs[k * TLB + bn] = bok ? gs[pmu * TLG + k] * gs[pnu * TLG + k] : 0.0;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int ks = 0; ks < TK; ks += 4) {
+                const double a0 = as[(wm * 16 + gg) * TLA + ks + tq];
+                const double a1 = as[(wm * 16 + gg + 8) * TLA + ks + tq];
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt)
+                    dmma_m16n8k4(acc[nt], a0, a1, Bs[(ks + tq) * TLB + wn * 32 + nt * 8 + gg]);
+            }
+        }
+        cp_async_wait<0>();
+    }
+    } else {
     double ra[8], rg[4];
     auto fetch = [&](long long kb) {
 #pragma unroll
@@ -112,7 +184,6 @@ __global__ void __launch_bounds__(256) k_triv_gemm(TrivJobs jobs, int m0, int Rt
             rg[u] = (gm < m0 && k < k1) ? g[gm * G + k] : 0.0;
         }
     };
-    double acc[4][4] = {};
     if (k0 < k1) {
         fetch(k0);
         for (long long kb = k0; kb < k1; kb += TK) {
@@ -144,6 +215,7 @@ __global__ void __launch_bounds__(256) k_triv_gemm(TrivJobs jobs, int m0, int Rt
                     dmma_m16n8k4(acc[nt], a0, a1, Bs[(ks + tq) * TLB + wn * 32 + nt * 8 + gg]);
             }
         }
+    }
     }
     double* out = part + (static_cast<long long>(job) * splits + split) * Rtot * nsym;
 #pragma unroll
@@ -234,12 +306,23 @@ __global__ void k_triv_reduce_w(const double* __restrict__ part, int njobs, WSpe
 }
 
 void launch_triv_tables(const Launch& L, const TrivJobs& jobs, int njobs, const WSpec& ws, int m0, int Rtot,
-                        const double* potw, double* part, int splits, double* W, double* Tout) {
+                        const double* potw, double* part, int splits, double* W, double* Tout, bool async) {
     const int nsym = m0 * (m0 + 1) / 2;
     if (njobs > 0) {
         dim3 grid((Rtot + kGBM - 1) / kGBM, (nsym + kGBN - 1) / kGBN, njobs * splits);
+        auto smem_of = [](int nst) {
+            return static_cast<int>(sizeof(double)) *
+                   (nst * (kGBM * (kTrivTK + 4) + 32 * (kTrivTK + 1)) + kTrivTK * (kGBN + 8));
+        };
+        static bool attr = false;
+        if (!attr) {
+            LT_CU(cudaFuncSetAttribute(k_triv_gemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       smem_of(kTrivStages)));
+            attr = true;
+        }
         Stage st_(L, "triv_gemm");
-        k_triv_gemm<<<grid, 256, 0, L.st>>>(jobs, m0, Rtot, nsym, splits, part);
+        if (async) k_triv_gemm<true><<<grid, 256, smem_of(kTrivStages), L.st>>>(jobs, m0, Rtot, nsym, splits, part);
+        else k_triv_gemm<false><<<grid, 256, smem_of(1), L.st>>>(jobs, m0, Rtot, nsym, splits, part);
         LT_CU(cudaGetLastError());
         L.tick();
     }

@@ -286,7 +286,7 @@ struct KRArgs {
     double* N = nullptr;
 };
 void launch_triv_tables(const Launch& L, const TrivJobs& jobs, int njobs, const WSpec& ws, int m0, int Rtot,
-                        const double* potw, double* part, int splits, double* W, double* Tout);
+                        const double* potw, double* part, int splits, double* W, double* Tout, bool async = false);
 // V = W^T P on a periodic cell panel, one thread per output (large W; small ones fuse into the fold)
 void launch_vdot(const Launch& L, int mm, int Rtot, long long rows, const double* W, const double* P, double* V);
 void launch_vgemm(const Launch& L, int mm, int Rtot, long long rows, const double* W, const double* P, double* V);
