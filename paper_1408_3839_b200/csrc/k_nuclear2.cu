@@ -372,8 +372,21 @@ __global__ void k_vdot(int mm, int Rtot, long long rows, const double* __restric
     const int e = static_cast<int>(idx % mm);
     const long long t = idx / mm;
     double v = 0.0;
-    if (ok)
-        for (int r = part; r < Rtot; r += 4) v = fma(W[r * mm + e], P[r * rows + t], v);
+    if (ok) {
+        // eight (W, P) pairs in flight per round trip; the sum stays in r order
+        int r = part;
+        for (; r + 28 < Rtot; r += 32) {
+            double w[8], p[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                w[u] = W[(r + 4 * u) * mm + e];
+                p[u] = P[(r + 4 * u) * rows + t];
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v = fma(w[u], p[u], v);
+        }
+        for (; r < Rtot; r += 4) v = fma(W[r * mm + e], P[r * rows + t], v);
+    }
     v += __shfl_xor_sync(0xffffffffu, v, 1);
     v += __shfl_xor_sync(0xffffffffu, v, 2);
     if (ok && part == 0) V[static_cast<long long>(e) * rows + t] = v;
