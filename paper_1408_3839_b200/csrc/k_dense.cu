@@ -603,7 +603,7 @@ __global__ void __launch_bounds__(BS) k_tridiag_eig3(int n, const double* __rest
 #pragma unroll
         for (int j = 0; j < Q; ++j) x[j] = a + (bnd - a) * (static_cast<double>(sub * Q + j + 1) * inv_pts);
         if (active) {
-            sturm3<Q>(sd, se2, n, x, cnt);
+            sturm3<Q, false>(sd, se2, n, x, cnt);
         } else {
 #pragma unroll
             for (int j = 0; j < Q; ++j) cnt[j] = 0;
@@ -757,7 +757,9 @@ void launch_tridiag_eig(const Launch& L, int n, const double* d, const double* e
         // 16 lanes x 2 shifts per eigenvalue (33-fold bracket shrink per round) in 64-thread
         // CTAs: measured best on B200 for n = 1024 (the chain is issue-bound; more shifts per
         // round cost more than the rounds they save)
-        run_eig3<2, 16, 64>(L, n, d, e, eig, smem);
+        static const int q_env = std::getenv("LT_EIG3_Q") ? std::atoi(std::getenv("LT_EIG3_Q")) : 2;
+        if (q_env == 1) run_eig3<1, 32, 64>(L, n, d, e, eig, smem);
+        else run_eig3<2, 16, 64>(L, n, d, e, eig, smem);
     }
     LT_CU(cudaGetLastError());
     L.tick();

@@ -62,7 +62,7 @@ __device__ __forceinline__ double warp_max(double v) {
 // two to max |entry| < 1; a ratio with |q_i| < 2^-100 is replaced by -2^-100 (the pivmin rule
 // of the ratio form, a perturbation of d_i far below eps ||T||), and (p_i, p_{i-1}) are
 // rescaled by an exact power of two every 4 steps, which keeps them normal (|q| <= 4).
-template <int Q>
+template <int Q, bool INTGUARD = true>
 __device__ __forceinline__ void sturm3(const double* sd, const double* se2, int n, const double (&x)[Q],
                                        int (&cnt)[Q]) {
     constexpr double kDelta = 7.888609052210118e-31;  // 2^-100
@@ -74,8 +74,9 @@ __device__ __forceinline__ void sturm3(const double* sd, const double* se2, int 
         if (fabs(cur[j]) < kDelta) cur[j] = -kDelta;
         cnt[j] = cur[j] < 0.0;
     }
-    // The guard and the sign count run on the integer pipe (the FP64 pipe, shared by every
-    // warp of the SM, then carries only the DADD, DMUL and DFMA of the recurrence): |nx| below
+    // INTGUARD: the guard and the sign count run on the integer pipe (the FP64 pipe then
+    // carries only the DADD, DMUL and DFMA of the recurrence; measured faster for the batched
+    // pencils, slower for the long dense chains, which keep the FP64 form): |nx| below
     // 2^-100 |cur| is detected from the exponent fields and nx replaced by the power of two
     // 2^(e(cur) - 100) (within a factor 2 of 2^-100 |cur|) of the sign opposite to cur.
     // The rescaling keeps e(cur) in [623, 1423], so the replacement stays normal.
@@ -83,6 +84,14 @@ __device__ __forceinline__ void sturm3(const double* sd, const double* se2, int 
 #pragma unroll
         for (int j = 0; j < Q; ++j) {
             double nx = fma(di - x[j], cur[j], -ei * prev[j]);
+            if constexpr (!INTGUARD) {  // the same rule on the FP64 pipe (exact 2^-100 |cur|)
+                const double thr = kDelta * fabs(cur[j]);
+                if (fabs(nx) < thr) nx = cur[j] < 0.0 ? thr : -thr;
+                cnt[j] += (nx < 0.0) != (cur[j] < 0.0);
+                prev[j] = cur[j];
+                cur[j] = nx;
+                continue;
+            }
             const int hn = __double2hiint(nx), hc = __double2hiint(cur[j]);
             const int ec = (hc >> 20) & 0x7ff;
             if (((hn >> 20) & 0x7ff) < ec - 100)

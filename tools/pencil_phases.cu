@@ -83,6 +83,10 @@ static void run(int count, int m0, int reps) {
 }
 
 int main() {
+    run<16, 64, 256>(512, 16, 5);
+    run<16, 64, 128>(512, 16, 5);
+    run<16, 32, 128>(512, 16, 5);
+    run<16, 32, 64>(512, 16, 5);
     run<32, 256, 256, false, false>(1, 32, 5);
     run<32, 256, 256, false, true>(1, 32, 5);
     run<8, 64, 64, false, true>(1, 8, 5);
