@@ -185,7 +185,7 @@ struct lt_ctx {
     int* pinned = nullptr;  // small pinned read-back buffer
     // side streams for independent branches of the assembly (captured into the same graph
     // as parallel branches) and the fork/join events between them
-    cudaStream_t aux[2]{nullptr, nullptr};
+    cudaStream_t aux[3]{nullptr, nullptr, nullptr};  // 0, 1: assembly branches; 2: L0 check under speculation
     cudaEvent_t ev[8]{};  // fork/join points of run_assembly (indices 0-5)
     // pinned staging for the small per-call host<->device copies (system, window starts,
     // DFT index maps, eigenvalue read-back): async copies instead of pageable round trips.
@@ -1474,8 +1474,20 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
     auto enqueue = [&]() {
         // k_l0_init resets the failure key: in front of this graph under speculation, else in
         // the L0 graph that just ran
-        if (spec) l0w.enqueue(c->L(), 1, static_cast<int>(L0) + 3, true);
+        // under speculation the L0 check runs as its own branch beside the assembly (its
+        // result is only read back at the end); it joins before the spectrum, whose
+        // failure key it resets and whose read-back carries its state
+        const bool par_l0 = spec && !c->timer.on;
+        if (spec) {
+            if (par_l0) {
+                c->join(6, c->stream, c->aux[2]);
+                l0w.enqueue(c->LA(2), 1, static_cast<int>(L0) + 3, true);
+            } else {
+                l0w.enqueue(c->L(), 1, static_cast<int>(L0) + 3, true);
+            }
+        }
         if (phase != 2) run_assembly(c, sd, p, NEED_MS | NEED_NUC, 0, out, nullptr, s0d, 0, opt.shard);
+        if (par_l0) c->join(7, c->aux[2], c->stream);
         if (phase == 2 && !periodic) {  // the box pencil factorises in place: work on copies
             LT_CU(cudaMemcpyAsync(out.out0, opt.H, sizeof(double) * ocount, cudaMemcpyDeviceToDevice, c->stream));
             LT_CU(cudaMemcpyAsync(out.out1, opt.S, sizeof(double) * ocount, cudaMemcpyDeviceToDevice, c->stream));
@@ -1849,6 +1861,7 @@ lt_status lt_create(int device, lt_ctx** out) {
         LT_CU(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi));
         LT_CU(cudaStreamCreateWithPriority(&c->aux[0], cudaStreamNonBlocking, prio_lo));
         LT_CU(cudaStreamCreateWithPriority(&c->aux[1], cudaStreamNonBlocking, prio_hi));
+        LT_CU(cudaStreamCreateWithPriority(&c->aux[2], cudaStreamNonBlocking, prio_lo));
         for (auto& e : c->ev) LT_CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         LT_CU(cudaMalloc(&c->pencil_done, sizeof(unsigned)));
         LT_CU(cudaMemset(c->pencil_done, 0, sizeof(unsigned)));
