@@ -664,7 +664,10 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
     PPROF(5);
     // 5. parallel multisection: P threads (contiguous lanes) x Q shifts per thread and
     //    eigenvalue; the bracket shrinks (P Q + 1)-fold per round.
-    constexpr int Q = 4;
+#ifndef LT_PENCIL_Q
+#define LT_PENCIL_Q 2  // shifts per thread: measured best (Q = 1, 4, 8 slower on the FP64 pipe)
+#endif
+    constexpr int Q = LT_PENCIL_Q;
     int P = 1;
     while (P * 2 <= 32 && P * 2 * n <= G) P *= 2;
     const double unscale = sm.scal[2];
