@@ -1308,6 +1308,11 @@ static void box_eig_tridiag(lt_ctx* c, Index n, double* H, double* S, double* ei
 static void box_eig_device(lt_ctx* c, Index n, double* H, double* S, double* eig_dev, unsigned long long* fail_dev,
                            double* vec_dev = nullptr, const PencilReadback& rb = PencilReadback{}) {
     const Launch L = c->L();
+    if (n <= 32 && !vec_dev) {  // real pencil straight from H, S (no conversion launches)
+        launch_pencil(L, 1, n, nullptr, nullptr, eig_dev, fail_dev, false, pencil_identity_source(H, S), nullptr, rb,
+                      true);
+        return;
+    }
     if (n <= 32) {
         double2* hc = c->arena.get<double2>("box.hc", n * n);
         double2* sc = c->arena.get<double2>("box.sc", n * n);

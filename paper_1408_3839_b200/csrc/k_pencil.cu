@@ -779,11 +779,31 @@ static void dispatch_pencil(const Launch& L, Index count, Index m0, const double
     }
 }
 
+// a one-offset "lattice DFT" (offset 0, block 0, twiddle 1): lets a real dense pencil be
+// read straight from its double arrays through the fused-DFT load path (no conversion launch)
+__device__ const int64_t kPencilZeroComp[1] = {0};
+__device__ const int kPencilZeroBlk[1] = {0};
+PencilDft pencil_identity_source(const double* H, const double* S) {
+    PencilDft f;
+    void* pc = nullptr;
+    void* pb = nullptr;
+    LT_CU(cudaGetSymbolAddress(&pc, kPencilZeroComp));
+    LT_CU(cudaGetSymbolAddress(&pb, kPencilZeroBlk));
+    f.nc = 1;
+    f.L = 1;
+    f.k0 = 0;
+    f.comp = static_cast<const int64_t*>(pc);
+    f.blk = static_cast<const int*>(pb);
+    f.GH = H;
+    f.GS = S;
+    return f;
+}
+
 void launch_pencil(const Launch& L, Index count, Index m0, const double2* H, const double2* S, double* eig,
                    unsigned long long* fail_key, bool periodic_checks, const PencilDft& dft, double2* vec,
                    const PencilReadback& rb, bool real) {
     if (count <= 0) return;
-    if (real && !vec && dft.nc == 0) {
+    if (real && !vec) {
         // real symmetric pencils (box, N_b <= 32): real arithmetic in the complex layout
         if (m0 <= 8) run_pencil<8, 64, 64, false, true>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft, nullptr, rb);
         else if (m0 <= 16) run_pencil<16, 64, 256, false, true>(L, count, m0, H, S, eig, fail_key, periodic_checks, dft, nullptr, rb);

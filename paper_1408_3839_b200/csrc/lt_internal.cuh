@@ -495,6 +495,8 @@ struct PencilDft {
     const double* GH = nullptr;
     const double* GS = nullptr;
 };
+// real dense pencil read directly from column-major double arrays through the fused-DFT load
+PencilDft pencil_identity_source(const double* H, const double* S);
 // In-kernel read-back: the last pencil group to finish copies the 8-int result block
 // (L0 state, failure key) to pinned host memory, replacing a device-to-host copy node at
 // the end of the graph; `done` is a zeroed counter the kernel resets itself.

@@ -83,9 +83,19 @@ static void run(int count, int m0, int reps) {
 }
 
 int main() {
+    run<8, 32, 32>(32, 8, 5);
     run<8, 64, 64>(32, 8, 5);
-    run<16, 64, 256>(512, 16, 5);
+    run<8, 128, 128>(32, 8, 5);
+    run<8, 32, 64>(4096, 8, 5);
     run<8, 32, 128>(4096, 8, 5);
+    run<8, 32, 256>(4096, 8, 5);
+    run<8, 64, 128>(4096, 8, 5);
+    run<16, 64, 256>(512, 16, 5);
+    run<16, 64, 128>(512, 16, 5);
+    run<16, 128, 128>(512, 16, 5);
+    run<16, 32, 128>(512, 16, 5);
     run<32, 256, 256, false, true>(1, 32, 5);
+    run<32, 512, 512, false, true>(1, 32, 5);
+    run<32, 128, 128, false, true>(1, 32, 5);
     return 0;
 }
