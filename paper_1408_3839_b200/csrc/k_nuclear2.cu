@@ -488,7 +488,7 @@ void launch_hankel(const Launch& L, int m0, const DirPlan& d, const double* pwc,
 }
 
 // ---------------------------------------------------------------------------
-// several wrapped directions: T[d][r][e] = sum_t P[r][t] Qf[d][e][t] (d >= 0), DMMA GEMM
+// several wrapped directions: T[d][e][r] = sum_t P[r][t] Qf[d][e][t] (d >= 0), DMMA GEMM
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_fgemm(int mm, int Rtot, long long n, int ncols, const double* __restrict__ P,
                                                const double* __restrict__ Qf, double* __restrict__ T) {
@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(256) k_fgemm(int mm, int Rtot, long long n, in
             if (r0 + m < Rtot && c0 + nn < ncols) {
                 const int col = c0 + nn;
                 const int dd = col / mm, e = col % mm;
-                T[(static_cast<long long>(dd) * Rtot + r0 + m) * mm + e] = acc[nt][i];
+                T[(static_cast<long long>(dd) * mm + e) * Rtot + r0 + m] = acc[nt][i];  // [d][e][r]
             }
         }
 }
@@ -524,8 +524,9 @@ void launch_fgemm(const Launch& L, int m0, int Rtot, const DirPlan& d, const dou
     L.tick();
 }
 
-// Khatri-Rao combine: N[d0,d1,d2][e] = sum_r W[r][e] prod_{l wrapped} T_l[d_l][r][e]
-// (T_l stored for d >= 0; T_l[-d][r][(mu,nu)] = T_l[d][r][(nu,mu)]). CTA per (e, d0).
+// Khatri-Rao combine: N[d0,d1,d2][e] = sum_r W[r][e] prod_{l wrapped} T_l[d_l][e][r]
+// (T_l stored for d >= 0 with r contiguous, so a CTA's table gathers are coalesced;
+// T_l[-d][(mu,nu)][r] = T_l[d][(nu,mu)][r]). CTA per (e, d0).
 __global__ void k_kr_combine(KRArgs a) {
     extern __shared__ double sh[];
     const int e = blockIdx.x;
@@ -541,11 +542,28 @@ __global__ void k_kr_combine(KRArgs a) {
         const int d = di - a.band[l];
         const int ad = d < 0 ? -d : d;
         const int ee = d < 0 ? eT : e;
-        return a.T[l][(static_cast<long long>(ad) * a.Rtot + r) * mm + ee];
+        return a.T[l][(static_cast<long long>(ad) * mm + ee) * a.Rtot + r];  // [d][e][r]: r contiguous
     };
     for (int r = threadIdx.x; r < a.Rtot; r += blockDim.x) w0[r] = a.W[r * mm + e] * tab(0, i0, r);
-    for (int q = threadIdx.x; q < a.width[1] * a.Rtot; q += blockDim.x) t1[q] = tab(1, q / a.Rtot, q % a.Rtot);
-    for (int q = threadIdx.x; q < a.width[2] * a.Rtot; q += blockDim.x) t2[q] = tab(2, q / a.Rtot, q % a.Rtot);
+    // the two table slabs, eight loads in flight per thread
+    auto gather = [&](int l, double* dst) {
+        const int tot = a.width[l] * a.Rtot;
+        for (int q0 = threadIdx.x; q0 < tot; q0 += 8 * blockDim.x) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int q = q0 + u * static_cast<int>(blockDim.x);
+                v[u] = q < tot ? tab(l, q / a.Rtot, q % a.Rtot) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int q = q0 + u * static_cast<int>(blockDim.x);
+                if (q < tot) dst[q] = v[u];
+            }
+        }
+    };
+    gather(1, t1);
+    gather(2, t2);
     __syncthreads();
     const int nout = a.width[1] * a.width[2];
     for (int o = threadIdx.x; o < nout; o += blockDim.x) {
