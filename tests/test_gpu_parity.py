@@ -23,6 +23,9 @@ SMALL = {
     "box2d": (two_nuclei_system((3, 2, 1), n=(8, 8, 8), alphas=(1.5, 3.0)), False),
     "per3d": (two_nuclei_system((5, 6, 5), n=(6, 6, 6), alphas=(3.0, 5.0), M=6), True),
     "per2d_y": (two_nuclei_system((1, 9, 1), n=(6, 8, 6), alphas=(1.0, 2.0), M=6), True),
+    # fused multi-axis DFT: register FFT (L = 8, 16) beside the line DFT (L = 5, 6)
+    "per3d_fft_dft": (two_nuclei_system((8, 5, 8), n=(6, 6, 6), alphas=(3.0, 5.0), M=6), True),
+    "per2d_fft_dft": (two_nuclei_system((16, 6, 1), n=(6, 6, 6), alphas=(3.0, 5.0), M=6), True),
     "box_z": (two_nuclei_system((1, 1, 5), n=(6, 6, 10), alphas=(1.0, 2.0), M=6), False),
     "pdeg_box": (two_nuclei_system((4, 1, 1), alphas=(1.0, 2.0), deg=[[1, 0, 0], [0, 1, 1]]), False),
     "pdeg_per": (two_nuclei_system((9, 1, 1), alphas=(1.0, 2.0), deg=[[2, 0, 0], [1, 1, 0]]), True),
