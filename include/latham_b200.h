@@ -70,10 +70,23 @@ void lt_destroy(lt_ctx* ctx);
 const char* lt_last_error(void);
 /* stream the context launches on (cudaStream_t as void*); 0 until created */
 void* lt_stream(lt_ctx* ctx);
+/* stream ordering for callers that own device buffers on their own stream (cudaStream_t as
+   void*): lt_stream_wait — work the context enqueues after this call waits for everything
+   enqueued on `stream` so far; lt_stream_join — `stream` waits for everything the context
+   enqueued so far. Device-pointer entry points (lt_*_dev) write caller buffers on the
+   context stream, so a caller brackets them with wait / join. */
+lt_status lt_stream_wait(lt_ctx* ctx, void* stream);
+lt_status lt_stream_join(lt_ctx* ctx, void* stream);
 /* number of kernels this context launched so far (for the bench's gpu_launches) */
 int64_t lt_launch_count(lt_ctx* ctx);
 /* per-kernel CUDA-event timing on the context stream (off by default; resets totals) */
 lt_status lt_set_stage_timing(lt_ctx* ctx, int on);
+/* diagnostics (off by default): phase events between graph launches (accumulated into the
+   stage totals as phase_l0/phase_gap/phase_post) and host-side timestamps (printed to stderr
+   by lt_destroy) */
+#define LT_DIAG_PHASE_TIMING 1
+#define LT_DIAG_HOST_TIMING 2
+lt_status lt_set_diagnostics(lt_ctx* ctx, int flags);
 int64_t lt_stage_count(lt_ctx* ctx);
 lt_status lt_stage_get(lt_ctx* ctx, int64_t idx, char* name, int64_t cap, double* ms, int64_t* launches);
 /* per-launch timeline of the last timed solve: stream 0 main, 1-2 side branches; ms from solve start */

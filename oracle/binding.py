@@ -16,6 +16,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "_build", "liblatham_oracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libref_latham.so")
+NATIVE_SO = os.path.join(HERE, "_native", "liblatham_oracle.so")
 
 _P = ctypes.POINTER
 _d = ctypes.c_double
@@ -392,3 +393,13 @@ def reference() -> Optional[Oracle]:
     if "r" not in _cache:
         _cache["r"] = Oracle(REF_SO, "ref_") if os.path.exists(REF_SO) else None
     return _cache["r"]
+
+
+def native_oracle() -> Optional[Oracle]:
+    """Oracle-X built on THIS host with -O3 -march=native (the reference's build flags,
+    BASELINE.md), for the CPU baseline; None if the compiler is unavailable."""
+    if "n" not in _cache:
+        import subprocess
+        r = subprocess.run(["make", "-s", "-C", HERE, "native"], capture_output=True, text=True)
+        _cache["n"] = Oracle(NATIVE_SO, "or_") if r.returncode == 0 and os.path.exists(NATIVE_SO) else None
+    return _cache["n"]

@@ -28,6 +28,7 @@ CPU computation and no fallback.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 from dataclasses import dataclass
 from typing import Dict, Optional, Tuple
@@ -198,6 +199,12 @@ class Context:
             pass
 
     @property
+    def torch_device(self):
+        """torch.device of this context's GPU (where DeviceSystem buffers live)."""
+        import torch
+        return torch.device("cuda", self.device)
+
+    @property
     def stream(self) -> int:
         return int(self.lib.lt_stream(self.h) or 0)
 
@@ -207,6 +214,10 @@ class Context:
 
     def set_stage_timing(self, on: bool):
         check(self.lib.lt_set_stage_timing(self.h, int(on)))
+
+    def set_diagnostics(self, phase_timing: bool = False, host_timing: bool = False):
+        """Phase events between graph launches / host-side timestamps (diagnostic tools only)."""
+        check(self.lib.lt_set_diagnostics(self.h, (1 if phase_timing else 0) | (2 if host_timing else 0)))
 
     def stage_timeline(self):
         """[(name, stream, t0_ms, t1_ms)] of the last solve run with stage timing on."""
@@ -524,11 +535,25 @@ class DeviceSystem:
         check(ctx.lib.lt_sys_upload(ctx.h, ctypes.byref(c), ctypes.byref(h)))
         self.h = h
 
+    @contextlib.contextmanager
+    def _ordered(self, stream):
+        """Order the engine's work on caller device buffers after the caller's stream (torch's
+        current stream by default) and the caller's later work after the engine's."""
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream(self.ctx.device).cuda_stream
+        check(self.ctx.lib.lt_stream_wait(self.ctx.h, ctypes.c_void_p(stream)))
+        try:
+            yield
+        finally:
+            check(self.ctx.lib.lt_stream_join(self.ctx.h, ctypes.c_void_p(stream)))
+
     def solve(self, periodic: bool, eig_dev_ptr: int, k_begin: int = 0, k_end: int = -1,
-              info: Optional[np.ndarray] = None):
+              info: Optional[np.ndarray] = None, stream: Optional[int] = None):
         inf = np.zeros(8, dtype=np.int64) if info is None else info
-        check(self.ctx.lib.lt_solve_core_dev(self.ctx.h, self.h, int(periodic), ctypes.c_void_p(eig_dev_ptr), k_begin,
-                                             k_end, _i(inf)))
+        with self._ordered(stream):
+            check(self.ctx.lib.lt_solve_core_dev(self.ctx.h, self.h, int(periodic), ctypes.c_void_p(eig_dev_ptr),
+                                                 k_begin, k_end, _i(inf)))
         return inf
 
     # ---- multi-GPU assembly shards (lt_core_layout / lt_assemble_core_dev / lt_spectrum_dev)
@@ -543,16 +568,21 @@ class DeviceSystem:
             check(self.ctx.lib.lt_core_layout(self.ctx.h, self.h, 1, _i(info), _i(kidx)))
         return info, kidx
 
-    def assemble_shard(self, periodic: bool, r_begin: int, r_end: int, with_kinetic: bool, H_ptr: int, S_ptr: int):
+    def assemble_shard(self, periodic: bool, r_begin: int, r_end: int, with_kinetic: bool, H_ptr: int, S_ptr: int,
+                       stream: Optional[int] = None):
         """H shard = [0.5 Laplace] - sum_{r in [r_begin, r_end)} w_r prod_l T_l, S = Mass, into
         device buffers of layout()[0][6] doubles."""
-        check(self.ctx.lib.lt_assemble_core_dev(self.ctx.h, self.h, int(periodic), int(r_begin), int(r_end),
-                                                int(bool(with_kinetic)), ctypes.c_void_p(H_ptr),
-                                                ctypes.c_void_p(S_ptr)))
+        with self._ordered(stream):
+            check(self.ctx.lib.lt_assemble_core_dev(self.ctx.h, self.h, int(periodic), int(r_begin), int(r_end),
+                                                    int(bool(with_kinetic)), ctypes.c_void_p(H_ptr),
+                                                    ctypes.c_void_p(S_ptr)))
 
-    def spectrum(self, periodic: bool, H_ptr: int, S_ptr: int, eig_ptr: int, k_begin: int = 0, k_end: int = -1):
-        check(self.ctx.lib.lt_spectrum_dev(self.ctx.h, self.h, int(periodic), ctypes.c_void_p(H_ptr),
-                                           ctypes.c_void_p(S_ptr), ctypes.c_void_p(eig_ptr), int(k_begin), int(k_end)))
+    def spectrum(self, periodic: bool, H_ptr: int, S_ptr: int, eig_ptr: int, k_begin: int = 0, k_end: int = -1,
+                 stream: Optional[int] = None):
+        with self._ordered(stream):
+            check(self.ctx.lib.lt_spectrum_dev(self.ctx.h, self.h, int(periodic), ctypes.c_void_p(H_ptr),
+                                               ctypes.c_void_p(S_ptr), ctypes.c_void_p(eig_ptr), int(k_begin),
+                                               int(k_end)))
 
     def __del__(self):
         if getattr(self, "h", None):

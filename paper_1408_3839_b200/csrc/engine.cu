@@ -186,7 +186,7 @@ struct lt_ctx {
     // side streams for independent branches of the assembly (captured into the same graph
     // as parallel branches) and the fork/join events between them
     cudaStream_t aux[3]{nullptr, nullptr, nullptr};  // 0, 1: assembly branches; 2: L0 check under speculation
-    cudaEvent_t ev[8]{};  // fork/join points of run_assembly (indices 0-5)
+    cudaEvent_t ev[9]{};  // fork/join points of run_assembly (0-5), the L0 branch (6-7), external streams (8)
     // pinned staging for the small per-call host<->device copies (system, window starts,
     // DFT index maps, eigenvalue read-back): async copies instead of pageable round trips.
     // Valid between stage_begin() (stream idle) and the end of the API call.
@@ -217,7 +217,7 @@ struct lt_ctx {
     // speculation on L0: the last (system, L0) pair the device computed
     std::vector<int64_t> spec_key;
     Index spec_L0 = -1;
-    // optional host-side timestamps (env LT_HOST_TIMING=1): enter / launched / synced / exit
+    // optional host-side timestamps (lt_set_diagnostics LT_DIAG_HOST_TIMING): enter / launched / synced / exit
     bool host_timing = false;
     double host_acc[4] = {0, 0, 0, 0};
     double graph_launch_us = 0.0, key_us = 0.0;
@@ -233,7 +233,7 @@ struct lt_ctx {
             host_acc[i] += std::chrono::duration<double, std::micro>(host_t[i + 1] - host_t[i]).count();
         ++host_n;
     }
-    // optional phase markers (env LT_PHASE_TIMING=1): events between the graph launches,
+    // optional phase markers (lt_set_diagnostics LT_DIAG_PHASE_TIMING): events between the graph launches,
     // accumulated into the stage totals as phase_l0 / phase_gap / phase_post
     bool phase_timing = false;
     cudaEvent_t pev[4]{};
@@ -697,8 +697,7 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
             }
             const Launch& LL = (nth++ == 1) ? LP : L;
             w.pot[l] = A.get<double>("pot.panel" + std::to_string(l), d.pot_rows * Rtot);
-            static const bool fuse_short = !std::getenv("LT_POT_NO_FUSE_SHORT");
-            if ((d.nsum == 1 && p.nnuc == 1) || (fuse_short && d.nsum >= 32 && d.pot_rows <= d.n && p.nnuc <= 2)) {
+            if ((d.nsum == 1 && p.nnuc == 1) || (d.nsum >= 32 && d.pot_rows <= d.n && p.nnuc <= 2)) {
                 // a single window copy of one nucleus: each master cell is read once, so it
                 // is evaluated in the copy kernel instead of being materialised first. The
                 // periodic cell window (one output per residue class) of <= 2 nuclei reads each
@@ -859,13 +858,12 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
             // split-K: one wave of CTAs on the cp.async pipeline when each CTA still gets >= 8
             // stages (long grids, c4: 43 + 12 us at four waves, 35 + 5 us at one), else four
             // waves of short register-prefetched CTAs (a short K is latency-bound: c2)
-            static const int triv_waves = std::getenv("LT_TRIV_WAVES") ? std::atoi(std::getenv("LT_TRIV_WAVES")) : 0;
             int splits = 1;
             bool triv_async = false;
             if (njobs) {
                 const int s1 = splits_for(tiles * njobs, maxG, 1);
                 triv_async = maxG / s1 >= 8 * 32;
-                const int w = triv_waves > 0 ? triv_waves : (triv_async ? 1 : 4);
+                const int w = triv_async ? 1 : 4;
                 splits = splits_for(tiles * njobs, maxG, w);
             }
             double* part = A.get<double>("nuc.tpart", std::max<size_t>(1, static_cast<size_t>(njobs) * splits * Rtot * nsym));
@@ -1121,8 +1119,7 @@ static void launch_dft(lt_ctx* c, const DftPrep& P, int nops, const double* cons
             f.comp[l] = P.comp[l];
             if (P.dims[l] > 1) f.axes[f.nax++] = l;
         }
-        static const bool no_fused = std::getenv("LT_DFT_AXES") != nullptr;  // A/B: per-axis launches
-        if (!no_fused && f.nax >= 2 && dft_fused_smem(f) <= 200 * 1024) {
+        if (f.nax >= 2 && dft_fused_smem(f) <= 200 * 1024) {
             for (int op = 0; op < nops; ++op) {
                 f.gen[op] = blocks[op];
                 f.out[op] = out[op] = buf[op][1];
@@ -1181,9 +1178,11 @@ static double2* block_diag_device(lt_ctx* c, const Index dims[3], Index m0,
     return out;
 }
 
-static void raise_fail_key(unsigned long long key, bool periodic) {
+// key = 4 k + code with k local to the launched pencil range; k0 = the range's first global
+// k-point, so the message names the global lexicographic index like eigensolver.cpp:79-86
+static void raise_fail_key(unsigned long long key, bool periodic, Index k0 = 0) {
     if (key == ~0ull) return;
-    const Index k = static_cast<Index>(key / 4);
+    const Index k = k0 + static_cast<Index>(key / 4);
     const int code = static_cast<int>(key % 4);
     if (!periodic)
         fail(LT_EDEFINITE, "solve_box_dense: overlap matrix is not positive definite (near-linear-dependent basis?)");
@@ -1471,9 +1470,8 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
     // device work after L0 (with L0 in front under speculation): kernels and memsets only
     // eigenvalues straight into the pinned staging buffer (host API) and the result block
     // copied by the pencil kernel's last group: no copy nodes at the end of the graph
-    static const bool no_kr = std::getenv("LT_NO_KERNEL_READBACK") != nullptr;  // A/B switch
-    double* eig_out = (epin && !no_kr) ? static_cast<double*>(epin) : eig_dev;
-    const bool kernel_readback = phase != 1 && !no_kr && inline_readback && (small_box || k_begin < k_end);
+    double* eig_out = epin ? static_cast<double*>(epin) : eig_dev;
+    const bool kernel_readback = phase != 1 && inline_readback && (small_box || k_begin < k_end);
     PencilReadback rb;
     if (kernel_readback) rb = PencilReadback{ret, rpin, c->pencil_done};
     auto enqueue = [&]() {
@@ -1598,11 +1596,11 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
         info[4] = p.Rtot;
         info[5] = p.Nb;
         info[6] = p.K;
-        info[7] = fkey == ~0ull ? -1 : static_cast<int64_t>(fkey);
+        info[7] = fkey == ~0ull ? -1 : static_cast<int64_t>(fkey + (periodic ? 4ull * static_cast<unsigned long long>(k_begin) : 0ull));
     }
     c->host_mark(4);
     c->host_collect();
-    raise_fail_key(fkey, periodic);
+    raise_fail_key(fkey, periodic, periodic ? k_begin : 0);
 }
 
 static lt_operator* new_op(const Plan& p, int which, Index coefficient_rank) {
@@ -1870,12 +1868,7 @@ lt_status lt_create(int device, lt_ctx** out) {
         for (auto& e : c->ev) LT_CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         LT_CU(cudaMalloc(&c->pencil_done, sizeof(unsigned)));
         LT_CU(cudaMemset(c->pencil_done, 0, sizeof(unsigned)));
-        const char* pt = std::getenv("LT_PHASE_TIMING");
-        c->phase_timing = pt && pt[0] == '1';
-        const char* ht = std::getenv("LT_HOST_TIMING");
-        c->host_timing = ht && ht[0] == '1';
-        if (c->phase_timing)
-            for (auto& e : c->pev) LT_CU(cudaEventCreate(&e));
+        for (auto& e : c->pev) LT_CU(cudaEventCreate(&e));
         *out = c.release();
     });
 }
@@ -1910,7 +1903,29 @@ void lt_destroy(lt_ctx* c) {
 }
 
 void* lt_stream(lt_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+lt_status lt_stream_wait(lt_ctx* c, void* stream) {
+    return guarded([&] {
+        LT_CU(cudaSetDevice(c->device));
+        c->join(8, static_cast<cudaStream_t>(stream), c->stream);
+    });
+}
+
+lt_status lt_stream_join(lt_ctx* c, void* stream) {
+    return guarded([&] {
+        LT_CU(cudaSetDevice(c->device));
+        c->join(8, c->stream, static_cast<cudaStream_t>(stream));
+    });
+}
 int64_t lt_launch_count(lt_ctx* c) { return c ? c->launches : 0; }
+
+lt_status lt_set_diagnostics(lt_ctx* c, int flags) {
+    return guarded([&] {
+        LT_CU(cudaStreamSynchronize(c->stream));
+        c->phase_timing = (flags & LT_DIAG_PHASE_TIMING) != 0;
+        c->host_timing = (flags & LT_DIAG_HOST_TIMING) != 0;
+    });
+}
 
 lt_status lt_set_stage_timing(lt_ctx* c, int on) {
     return guarded([&] {

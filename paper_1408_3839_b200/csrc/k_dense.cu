@@ -14,8 +14,7 @@
 //                  update + next-dot pass reads no matrix data from shared memory.
 //   k_tridiag_eig3 eigenvalues of the tridiagonal (d, e): G lanes x Q shifts per eigenvalue of
 //                  three-term Sturm counts (no division on the chain), the bracket shrinks
-//                  G Q + 1-fold per round; ascending by construction. k_tridiag_eig: the
-//                  LDL^T-ratio form (LAPACK's pivmin guard), kept for A/B.
+//                  G Q + 1-fold per round; ascending by construction.
 //   k_symmetrize   A = 0.5 (A + A^T) in place (tiles through shared memory).
 #include "lt_device.cuh"
 #include "lt_internal.cuh"
@@ -438,104 +437,6 @@ __global__ void __launch_bounds__(NT) k_sytrd_reg(int n, int P, const double* __
 #undef SYPROF
 }
 
-// one warp per eigenvalue index; multisection with Q shifts per lane
-template <int Q>
-__global__ void __launch_bounds__(256) k_tridiag_eig(int n, const double* __restrict__ d, const double* __restrict__ e,
-                                                     double* __restrict__ eig) {
-    extern __shared__ __align__(16) double ts[];
-    double* sd = ts;
-    double* se2 = ts + n;
-    __shared__ double red[8][3];
-    double lo = 1e300, hi = -1e300, emax = 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const double di = d[i];
-        const double ei = i + 1 < n ? e[i] : 0.0;
-        sd[i] = di;
-        se2[i] = ei * ei;
-        const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + fabs(ei);
-        lo = fmin(lo, di - r);
-        hi = fmax(hi, di + r);
-        emax = fmax(emax, ei * ei);
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-        emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, o));
-    }
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (lane == 0) {
-        red[warp][0] = lo;
-        red[warp][1] = hi;
-        red[warp][2] = emax;
-    }
-    __syncthreads();
-    lo = red[0][0];
-    hi = red[0][1];
-    emax = red[0][2];
-    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) {
-        lo = fmin(lo, red[w][0]);
-        hi = fmax(hi, red[w][1]);
-        emax = fmax(emax, red[w][2]);
-    }
-    const double wid = fmax(hi - lo, fmax(fabs(lo), fabs(hi))) * 4.4e-16 * n + 1e-300;
-    lo -= wid;
-    hi += wid;
-    const double pivmin = 2.2250738585072014e-308 * fmax(1.0, emax);
-    const double atol = 2.2e-16 * fmax(fabs(lo), fabs(hi));
-    const int mi = blockIdx.x * (blockDim.x >> 5) + warp;
-    if (mi >= n) return;
-    double a = lo, bnd = hi;
-    const double inv_pts = 1.0 / static_cast<double>(32 * Q + 1);
-    for (int it = 0; it < 80; ++it) {
-        double x[Q], q[Q];
-        int cnt[Q];
-#pragma unroll
-        for (int j = 0; j < Q; ++j) {
-            x[j] = a + (bnd - a) * (static_cast<double>(lane * Q + j + 1) * inv_pts);
-            q[j] = sd[0] - x[j];
-            if (fabs(q[j]) < pivmin) q[j] = -pivmin;
-            cnt[j] = q[j] < 0.0;
-        }
-        for (int i = 1; i < n; ++i) {
-            const double di = sd[i], ei = se2[i - 1];
-#pragma unroll
-            for (int j = 0; j < Q; ++j) {
-                q[j] = (di - x[j]) - ei * fast_rcp(q[j]);
-                if (fabs(q[j]) < pivmin) q[j] = -pivmin;
-                cnt[j] += q[j] < 0.0;
-            }
-        }
-        // first shift (lane-major order) whose count exceeds mi
-        int fq = Q;
-#pragma unroll
-        for (int j = Q - 1; j >= 0; --j)
-            if (cnt[j] > mi) fq = j;
-        const double prev_last = __shfl_up_sync(0xffffffffu, x[Q - 1], 1);
-        double clo = lane > 0 ? prev_last : a, chi = x[0];
-#pragma unroll
-        for (int j = 1; j < Q; ++j)
-            if (fq == j) {
-                clo = x[j - 1];
-                chi = x[j];
-            }
-        const unsigned bal = __ballot_sync(0xffffffffu, fq < Q);
-        double na, nb;
-        if (bal) {
-            const int src = __ffs(bal) - 1;
-            na = __shfl_sync(0xffffffffu, clo, src);
-            nb = __shfl_sync(0xffffffffu, chi, src);
-        } else {
-            na = __shfl_sync(0xffffffffu, x[Q - 1], 31);
-            nb = bnd;
-        }
-        const bool done = !(nb - na > 2.2e-16 * fmax(fabs(na), fabs(nb)) + atol) || (na == a && nb == bnd);
-        a = na;
-        bnd = nb;
-        if (done) break;
-    }
-    if (lane == 0) eig[mi] = 0.5 * (a + bnd);
-}
-
 // G lanes per eigenvalue, Q shifts per lane; T scaled by 2^-s (max |d|, |e| < 1) internally
 template <int Q, int G, int BS>
 __global__ void __launch_bounds__(BS) k_tridiag_eig3(int n, const double* __restrict__ d, const double* __restrict__ e,
@@ -674,7 +575,6 @@ int sytrd_ctas(int n) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int P = std::min(n, sms);
-    if (const char* ev = std::getenv("LT_SYTRD_CTAS")) P = std::max(1, std::min(P, std::atoi(ev)));  // experiments
     const int cols = (n + P - 1) / P;
     return sytrd_smem(n, cols) <= 227 * 1024 - 1024 ? P : 0;
 }
@@ -703,13 +603,9 @@ void launch_sytrd(const Launch& L, int n, const double* C, double* d, double* e,
     constexpr int NT = 256;
     const int P = sytrd_ctas(n);
     if (P == 0) fail(LT_EGENERIC, "sytrd: matrix too large for the shared-memory resident reduction");
-    static const bool profile = std::getenv("LT_SYTRD_PROFILE") != nullptr;
-    static const bool smem_only = std::getenv("LT_SYTRD_SMEM") != nullptr;
-    static long long* prof = nullptr;
-    if (profile && !prof) LT_CU(cudaMalloc(&prof, 8 * sizeof(long long)));
-    long long* pp = profile ? prof : nullptr;
+    long long* pp = nullptr;  // per-phase cycle counters (tools/ probes only)
     // own columns in registers when they fit (n <= 256 R, ceil(n / P) <= CM), else in shared memory
-    const bool reg = !smem_only && (try_sytrd_reg<256, 2, 4>(L, n, P, C, d, e, work, bar, pp) ||
+    const bool reg = (try_sytrd_reg<256, 2, 4>(L, n, P, C, d, e, work, bar, pp) ||
                                     try_sytrd_reg<256, 4, 8>(L, n, P, C, d, e, work, bar, pp));
     if (!reg) {
         const int cols = (n + P - 1) / P;
@@ -725,14 +621,6 @@ void launch_sytrd(const Launch& L, int n, const double* C, double* d, double* e,
                                           L.st));
         L.tick();
     }
-    if (profile) {
-        long long h[6];
-        LT_CU(cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, L.st));
-        LT_CU(cudaStreamSynchronize(L.st));
-        std::fprintf(stderr, "sytrd%s n=%d P=%d cycles/step: - %.0f barrier/gather %.0f vp %.0f wc %.0f refl %.0f fused %.0f\n",
-                     reg ? "_reg" : "", n, P, h[0] / double(n), h[1] / double(n), h[2] / double(n), h[3] / double(n),
-                     h[4] / double(n), h[5] / double(n));
-    }
 }
 
 template <int Q, int G, int BS>
@@ -745,22 +633,11 @@ static void run_eig3(const Launch& L, int n, const double* d, const double* e, d
 
 void launch_tridiag_eig(const Launch& L, int n, const double* d, const double* e, double* eig) {
     const size_t smem = sizeof(double) * 2 * static_cast<size_t>(n);
-    // LT_TRIDIAG_RATIO: the LDL^T-ratio Sturm counts (one reciprocal per step) instead of
-    // the three-term recurrence, for A/B measurements
-    static const bool ratio = std::getenv("LT_TRIDIAG_RATIO") != nullptr;
     Stage st_(L, "tridiag_eig");
-    if (ratio) {
-        LT_CU(cudaFuncSetAttribute(k_tridiag_eig<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
-        k_tridiag_eig<4><<<static_cast<unsigned>((n + 7) / 8), 256, smem, L.st>>>(n, d, e, eig);
-    } else {
-        // 16 lanes x 2 shifts per eigenvalue (33-fold bracket shrink per round) in 64-thread
-        // CTAs: measured best on B200 for n = 1024 (the chain is issue-bound; more shifts per
-        // round cost more than the rounds they save)
-        static const int q_env = std::getenv("LT_EIG3_Q") ? std::atoi(std::getenv("LT_EIG3_Q")) : 2;
-        if (q_env == 1) run_eig3<1, 32, 64>(L, n, d, e, eig, smem);
-        else run_eig3<2, 16, 64>(L, n, d, e, eig, smem);
-    }
+    // 16 lanes x 2 shifts per eigenvalue (33-fold bracket shrink per round) in 64-thread
+    // CTAs: measured best on B200 for n = 1024 (the chain is issue-bound; more shifts per
+    // round cost more than the rounds they save; the LDL^T-ratio counts were slower)
+    run_eig3<2, 16, 64>(L, n, d, e, eig, smem);
     LT_CU(cudaGetLastError());
     L.tick();
 }

@@ -316,11 +316,6 @@ __global__ void k_resfold_reduce(ResFold f, int mirror) {
 
 void launch_resfold(const Launch& L, const ResFold& f_in, bool reduce, bool mirror, const char* name) {
     ResFold f = f_in;
-    static const bool no_sup = [] {
-        const char* e = std::getenv("LT_FOLD_NO_SUPPORT");
-        return e && e[0] == '1';
-    }();
-    if (no_sup) f.sup_lo = f.sup_hi = nullptr;
     const int m0p = (f.m0 + 7) / 8 * 8;
     const size_t mme = static_cast<size_t>(f.m0) * f.m0;
     const size_t vparts = f.W ? std::max<size_t>(1, 256 / mme) : 0;

@@ -784,16 +784,23 @@ static void dispatch_pencil(const Launch& L, Index count, Index m0, const double
 __device__ const int64_t kPencilZeroComp[1] = {0};
 __device__ const int kPencilZeroBlk[1] = {0};
 PencilDft pencil_identity_source(const double* H, const double* S) {
+    // symbol addresses resolved once per device (the first call runs eagerly, before any
+    // capture of this path), not inside stream capture
+    static void* pc[64] = {};
+    static void* pb[64] = {};
+    int dev = 0;
+    LT_CU(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) fail(LT_EGENERIC, "pencil_identity_source: device index out of range");
+    if (!pc[dev]) {
+        LT_CU(cudaGetSymbolAddress(&pb[dev], kPencilZeroBlk));
+        LT_CU(cudaGetSymbolAddress(&pc[dev], kPencilZeroComp));
+    }
     PencilDft f;
-    void* pc = nullptr;
-    void* pb = nullptr;
-    LT_CU(cudaGetSymbolAddress(&pc, kPencilZeroComp));
-    LT_CU(cudaGetSymbolAddress(&pb, kPencilZeroBlk));
     f.nc = 1;
     f.L = 1;
     f.k0 = 0;
-    f.comp = static_cast<const int64_t*>(pc);
-    f.blk = static_cast<const int*>(pb);
+    f.comp = static_cast<const int64_t*>(pc[dev]);
+    f.blk = static_cast<const int*>(pb[dev]);
     f.GH = H;
     f.GS = S;
     return f;

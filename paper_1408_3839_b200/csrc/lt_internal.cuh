@@ -251,12 +251,6 @@ void launch_nuc_direct(const Launch& L, Index m0, Index Rtot, const DirPlan& d, 
 void launch_nuc_fold(const Launch& L, Index m0, Index Rtot, const DirPlan& d, const double* pwc,
                      const unsigned long long* lo, const unsigned long long* hi, const double* pot, double* Qf,
                      double* T);
-// box chain (S2): W = w_r prod_trivial T, V = W^T P, N[k][d][e] = sum_j Q_d(j) V(j + k n)
-void launch_box_w(const Launch& L, Index m0, Index Rtot, const double* potw, const double* Ta, const double* Tb,
-                  double* W);
-void launch_box_v(const Launch& L, Index m0, Index Rtot, Index G, const double* W, const double* pot, double* V);
-void launch_box_corr(const Launch& L, Index m0, const DirPlan& d, const double* pwc, const unsigned long long* lo,
-                     const unsigned long long* hi, const double* V, double* Npart, double* N, int nsplit);
 
 // ---- DMMA nuclear contraction (k_nuclear2.cu) ----
 struct TrivJob {

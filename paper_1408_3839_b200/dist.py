@@ -9,8 +9,11 @@ contiguous k-range, and one all-gather of eigenvalues (k-lexicographic, identica
 the single-GPU order) completes the spectrum. Box systems do not shard (the dense
 pencil is one factorisation): every rank computes the same spectrum (replicas).
 
-The partitioning helpers are pure Python so the N > 1 logic is testable on CPU with
-the gloo backend (tests/test_dist_cpu.py).
+The functions take any context whose `upload(sys)` returns an object with the
+DeviceSystem methods (solve / layout / assemble_shard / spectrum, writing through buffer
+pointers) and whose `torch_device` names where the buffers live, so the N > 1 paths run
+unchanged on CPU tensors with the gloo backend (tests/test_dist_cpu.py, with an
+oracle-backed stand-in for the engine).
 """
 from __future__ import annotations
 
@@ -58,7 +61,7 @@ def solve_core_distributed(ctx, sys, periodic: bool, group=None, dsys=None, eig_
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
-    dev = torch.device("cuda", ctx.device)
+    dev = ctx.torch_device
     if dsys is None:
         dsys = ctx.upload(sys)
     K = sys.lattice_count if periodic else 1
@@ -84,7 +87,10 @@ def _gather_k(eig_dev, K: int, m0: int, b: int, e: int, world: int, group=None):
     send = torch.zeros(slot * m0, dtype=torch.float64, device=eig_dev.device)
     send[: (e - b) * m0] = eig_dev[b * m0: e * m0]
     recv = torch.empty(world * slot * m0, dtype=torch.float64, device=eig_dev.device)
-    dist.all_gather_into_tensor(recv, send, group=group)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(recv, send, group=group)
+    else:  # gloo (CPU tests): list form into views of the same buffer
+        dist.all_gather(list(recv.view(world, slot * m0).unbind(0)), send, group=group)
     parts = [recv[r * slot * m0: (r * slot + (ee - bb)) * m0] for r, (bb, ee) in enumerate(shard_ranges(K, world))]
     return torch.cat(parts).view(K, m0)
 
@@ -112,7 +118,7 @@ def solve_core_sharded(ctx, sys, periodic: bool, group=None, dsys=None, buffers=
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
-    dev = torch.device("cuda", ctx.device)
+    dev = ctx.torch_device
     if dsys is None:
         dsys = ctx.upload(sys)
     info, _ = dsys.layout(periodic)
@@ -124,8 +130,7 @@ def solve_core_sharded(ctx, sys, periodic: bool, group=None, dsys=None, buffers=
     r0, r1 = rank_term_range(Rtot, rank, world)
     dsys.assemble_shard(periodic, r0, r1, shard_kinetic(rank), H.data_ptr(), S.data_ptr())
     if world > 1:
-        dist.all_reduce(H, op=dist.ReduceOp.SUM, group=group)
-        torch.cuda.current_stream(dev).synchronize()
+        dist.all_reduce(H, op=dist.ReduceOp.SUM, group=group)  # ordered on the caller's stream
     if not periodic:
         dsys.spectrum(False, H.data_ptr(), S.data_ptr(), eig.data_ptr())
         return eig

@@ -64,8 +64,11 @@ def lib():
             "lt_destroy": ([_vp], None),
             "lt_last_error": ([], ctypes.c_char_p),
             "lt_stream": ([_vp], _vp),
+            "lt_stream_wait": ([_vp, _vp], ctypes.c_int),
+            "lt_stream_join": ([_vp, _vp], ctypes.c_int),
             "lt_launch_count": ([_vp], _i64),
             "lt_set_stage_timing": ([_vp, ctypes.c_int], ctypes.c_int),
+            "lt_set_diagnostics": ([_vp, ctypes.c_int], ctypes.c_int),
             "lt_stage_count": ([_vp], _i64),
             "lt_stage_get": ([_vp, _i64, ctypes.c_char_p, _i64, _dp, _ip], ctypes.c_int),
             "lt_op_separable_count": ([_vp], _i64),
@@ -128,7 +131,7 @@ def check(rc: int):
 
 # symbols declared in include/latham_b200.h (checked by tests/test_abi.py)
 EXPORTS = (
-    "lt_create", "lt_destroy", "lt_last_error", "lt_stream", "lt_launch_count", "lt_set_stage_timing",
+    "lt_create", "lt_destroy", "lt_last_error", "lt_stream", "lt_stream_wait", "lt_stream_join", "lt_launch_count", "lt_set_stage_timing", "lt_set_diagnostics",
     "lt_stage_count", "lt_stage_get", "lt_stage_timeline_count", "lt_stage_timeline_get",
     "lt_op_separable_count", "lt_op_separable", "lt_separable_residual", "lt_solve_periodic_factorized",
     "lt_solve_periodic_factorized_gen", "lt_factorized_block_diagonalize", "lt_box_circulant_defect", "lt_solve_core", "lt_sys_upload",

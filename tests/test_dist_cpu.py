@@ -34,6 +34,8 @@ def _free_port():
 
 
 def _worker(rank, world, port, q):
+    """dist.solve_core_distributed itself (k-point shards + _gather_k's all-gather) on CPU
+    tensors, with the oracle-backed stand-in for the engine (tests/oracle_engine.py)."""
     import sys
     import torch
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -43,25 +45,19 @@ def _worker(rank, world, port, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from conftest import two_nuclei_system
-    from oracle.binding import oracle
-    o = oracle()
-    s = two_nuclei_system((13, 1, 1))
-    H, S = o.assemble_core(s, True)
-    K = s.lattice_count
-    Hb = o.block_diagonalize(s.L, s.m0, H.gen_dict())
-    Sb = o.block_diagonalize(s.L, s.m0, S.gen_dict())
-    b, e = shard_range(K, rank, world)
-    mine = np.zeros((K, s.m0))
-    for j in range(b, e):
-        mine[j] = o.solve_pencil(Hb[j], Sb[j], j)
-    slot = padded_shard(K, world)
-    send = torch.from_numpy(pack_shard(mine, b, e, slot))
-    recv = [torch.zeros_like(send) for _ in range(world)]
-    dist.all_gather(recv, send)
-    full = unpack_gathered(torch.stack(recv).numpy(), K, world)
+    from oracle_engine import OracleContext
+    from paper_1408_3839_b200.dist import solve_core_distributed
+    octx = OracleContext()
+    out = []
+    for s, periodic in ((two_nuclei_system((13, 1, 1)), True), (two_nuclei_system((5, 6, 5), n=(6, 6, 6), alphas=(3.0, 5.0), M=6), True),
+                        (two_nuclei_system((6, 1, 1)), False)):
+        full = solve_core_distributed(octx, s, periodic)
+        assert isinstance(full, torch.Tensor) and full.device.type == "cpu"
+        H, S = octx.o.assemble_core(s, periodic)
+        ref = octx.o.solve_periodic_ops(H, S) if periodic else octx.o.solve_box_dense(H.dense, S.dense)
+        out.append((full.numpy().copy(), ref))
     if rank == 0:
-        ref = np.stack([o.solve_pencil(Hb[j], Sb[j], j) for j in range(K)])
-        q.put((full, ref))
+        q.put(out)
     dist.barrier()
     dist.destroy_process_group()
 
@@ -74,11 +70,12 @@ def test_two_rank_gloo_kpoint_shards_match_single_rank():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    full, ref = q.get(timeout=240)
+    out = q.get(timeout=240)
     for p in procs:
         p.join(timeout=60)
     assert all(p.exitcode == 0 for p in procs)
-    assert np.array_equal(full, ref)
+    for full, ref in out:  # k-lexicographic order and values identical to one rank
+        assert np.array_equal(full.reshape(ref.shape), ref)
 
 
 def test_rank_term_ranges_partition():
@@ -92,10 +89,11 @@ def test_rank_term_ranges_partition():
 
 
 def _rank_term_worker(rank, world, port, q):
-    """SURVEY §8(e) assembly sharding on CPU: each gloo rank forms its partial H from the
-    nuclear rank terms rank_term_range(R_tot) (the oracle's separable metadata: one term per
-    rank term r, weight folded into level 0, galerkin.cpp:394-423) plus 0.5 Laplace on rank 0;
-    one all-reduce completes H; then the k-point shards and the all-gather."""
+    """dist.solve_core_sharded itself on CPU tensors: each gloo rank assembles
+    the nuclear rank terms rank_term_range(R_tot) (+ 0.5 Laplace on rank 0) into its partial H
+    through the engine interface (oracle stand-in: the separable metadata, one term per rank
+    term, galerkin.cpp:394-423), dist.py's all-reduce completes H, each rank solves its
+    k-range and _gather_k's all-gather returns the k-lexicographic spectrum."""
     import sys
     import torch
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -105,44 +103,25 @@ def _rank_term_worker(rank, world, port, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from conftest import two_nuclei_system
-    from oracle.binding import oracle
-    from paper_1408_3839_b200.dist import rank_term_range, shard_kinetic
-    o = oracle()
+    from oracle_engine import OracleContext
+    from paper_1408_3839_b200.dist import solve_core_sharded
+    octx = OracleContext()
     s = two_nuclei_system((13, 1, 1))
-    lap = o.assemble(s, True, "laplace").gen_dict()
-    nuc_op = o.assemble(s, True, "nuclear")
-    terms = o.separable_terms(nuc_op)
-    keys = sorted(nuc_op.gen_dict())
-    Rtot = len(terms)
-    r0, r1 = rank_term_range(Rtot, rank, world)
-    part = np.zeros((len(keys), s.m0, s.m0))
-    for i, k in enumerate(keys):
-        acc = np.zeros((s.m0, s.m0))
-        for t in range(r0, r1):
-            acc += terms[t][0][k[0]] * terms[t][1][k[1]] * terms[t][2][k[2]]
-        part[i] = (0.5 * lap[k] if shard_kinetic(rank) else 0.0) - acc
-    Ht = torch.from_numpy(part)
-    dist.all_reduce(Ht)
-    Hsum = {k: Ht[i].numpy() for i, k in enumerate(keys)}
-    Href, Sref = o.assemble_core(s, True)
-    hd = Href.gen_dict()
-    worst = max(float(np.max(np.abs(Hsum[k] - hd[k]))) for k in keys)
-    scale = max(float(np.max(np.abs(v))) for v in hd.values())
-    K = s.lattice_count
-    Hb = o.block_diagonalize(s.L, s.m0, Hsum)
-    Sb = o.block_diagonalize(s.L, s.m0, Sref.gen_dict())
-    b, e = shard_range(K, rank, world)
-    mine = np.zeros((K, s.m0))
-    for j in range(b, e):
-        mine[j] = o.solve_pencil(Hb[j], Sb[j], j)
-    slot = padded_shard(K, world)
-    send = torch.from_numpy(pack_shard(mine, b, e, slot))
-    recv = [torch.zeros_like(send) for _ in range(world)]
-    dist.all_gather(recv, send)
-    full = unpack_gathered(torch.stack(recv).numpy(), K, world)
+    dsys = octx.upload(s)
+    info, kidx = dsys.layout(True)
+    n = int(info[6])
+    H = torch.zeros(n, dtype=torch.float64)
+    S = torch.zeros(n, dtype=torch.float64)
+    eig = torch.zeros(s.lattice_count * s.m0, dtype=torch.float64)
+    full = solve_core_sharded(octx, s, True, dsys=dsys, buffers=(H, S, eig))
+    Href, Sref = octx.o.assemble_core(s, True)
+    m0 = s.m0
+    Hsum = H.numpy().reshape(-1, m0, m0).transpose(0, 2, 1)  # column-major blocks -> [row, col]
+    worst = float(np.max(np.abs(Hsum - Href.blocks)))
+    scale = float(np.max(np.abs(Href.blocks)))
     if rank == 0:
-        ref = o.solve_periodic_ops(Href, Sref)
-        q.put((worst / scale, float(np.max(np.abs(full - ref))), Rtot))
+        ref = octx.o.solve_periodic_ops(Href, Sref)
+        q.put((worst / scale, float(np.max(np.abs(full.numpy() - ref))), int(info[5])))
     dist.barrier()
     dist.destroy_process_group()
 

@@ -1,10 +1,9 @@
-"""Host-side time split of the device-resident solve (LT_HOST_TIMING=1) and the Python-level
+"""Host-side time split of the device-resident solve (Context.set_diagnostics(host_timing=True)) and the Python-level
 per-call wall time, to separate host overhead from device time."""
 import os
 import sys
 import time
 
-os.environ["LT_HOST_TIMING"] = "1"
 sys.path.insert(0, ".")
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
@@ -14,6 +13,7 @@ from paper_1408_3839_b200.system import make_config  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 ctx = Context(0)
+ctx.set_diagnostics(host_timing=True)
 s = make_config(cfg)
 per = s.notes["periodic"]
 d = ctx.upload(s)

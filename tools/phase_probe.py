@@ -1,9 +1,8 @@
-"""Phase breakdown of the device path under graph replay (LT_PHASE_TIMING=1):
+"""Phase breakdown of the device path under graph replay (Context.set_diagnostics(phase_timing=True)):
 phase_l0 (L0 graph), phase_gap (host sync + planning + uploads), phase_post (post-L0 graph)."""
 import os
 import sys
 
-os.environ["LT_PHASE_TIMING"] = "1"
 sys.path.insert(0, ".")
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
@@ -13,6 +12,7 @@ from paper_1408_3839_b200.system import make_config  # noqa: E402
 
 for cfg in sys.argv[1:] or ["c2"]:
     ctx = Context(0)
+    ctx.set_diagnostics(phase_timing=True)
     s = make_config(cfg)
     per = s.notes["periodic"]
     d = ctx.upload(s)
