@@ -16,6 +16,7 @@
 #include <array>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <numeric>
@@ -615,7 +616,11 @@ static int64_t* upload_s0(lt_ctx* c, const Plan& p) {
 
 // flags: AS_GENERAL_NUC forces the per-direction nuclear tables (w.T, the reference's
 // nucT layout) instead of the fused reassociations; AS_NO_FILL stops after the tables.
-enum AsmFlags : unsigned { AS_GENERAL_NUC = 1u, AS_NO_FILL = 2u };
+enum AsmFlags : unsigned { AS_GENERAL_NUC = 1u, AS_NO_FILL = 2u, AS_BOX_SPLIT = 4u };
+// AS_BOX_SPLIT (box, mode 0): S = Mass is filled on the FEM branch as soon as the mass tables
+// exist and `s_hook` runs right after it on that branch (the dense pencil's Cholesky and
+// L^-1 overlap the nuclear contraction); the main-stream fill writes H only.
+using BranchHook = std::function<void(const Launch&)>;
 
 // Cells [j0, j0 + J) of direction l's extended grid that hold every sampled support (pwl:
 // nbar grid, align 0; pwc: n grid, align 0.5; functions sit in cell `margin`, galerkin.cpp:
@@ -652,7 +657,7 @@ static void support_window(const HostSys& s, const Plan& p, int l, bool pwl, lon
 
 static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need, int mode, AsmOut out,
                          Work* wout = nullptr, const int64_t* s0_dev = nullptr, unsigned flags = 0,
-                         const CoreShard& shard = CoreShard{}) {
+                         const CoreShard& shard = CoreShard{}, const BranchHook* s_hook = nullptr) {
     // Three concurrent branches (parallel branches of the captured graph):
     //   main   : sinc -> potential of the 1st, 3rd distinct direction -> nuclear -> fill
     //   aux[1] : potential of the 2nd distinct direction (joins main before the nuclear part)
@@ -984,7 +989,27 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
             }
         }
     }
-    c->join(4, c->aux[0], c->stream);  // FEM tables before the fill
+    const bool split = (flags & AS_BOX_SPLIT) && !p.periodic && mode == 0 && !(flags & AS_NO_FILL);
+    if (split) {
+        // S = Mass on the FEM branch (only the mass tables), then the hook there
+        FillArgs fs;
+        fs.m0 = m0;
+        fs.Rtot = Rtot;
+        for (int l = 0; l < 3; ++l) {
+            fs.L[l] = p.d[l].L;
+            fs.band[l] = p.d[l].band;
+            fs.width[l] = p.d[l].width;
+            fs.massT[l] = w.massT[l];
+            fs.stiffT[l] = w.stiffT[l];
+        }
+        fs.mode = 2;
+        fs.periodic = false;
+        fs.out0 = out.out1;
+        LT_CU(cudaMemsetAsync(out.out1, 0, sizeof(double) * p.Nb * p.Nb, LF.st));
+        launch_fill(LF, fs, p.Nb, p.cells * p.d[0].width * p.d[1].width * p.d[2].width);
+        if (s_hook) (*s_hook)(LF);
+    }
+    c->join(4, c->aux[0], c->stream);  // FEM tables (and the S branch) before the fill
     if (flags & AS_NO_FILL) {
         if (wout) *wout = w;
         return;
@@ -1020,7 +1045,8 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
     } else {
         nblocks = p.cells * p.d[0].width * p.d[1].width * p.d[2].width;
         LT_CU(cudaMemsetAsync(out.out0, 0, sizeof(double) * p.Nb * p.Nb, c->stream));
-        if (mode == 0) LT_CU(cudaMemsetAsync(out.out1, 0, sizeof(double) * p.Nb * p.Nb, c->stream));
+        if (mode == 0 && !split) LT_CU(cudaMemsetAsync(out.out1, 0, sizeof(double) * p.Nb * p.Nb, c->stream));
+        if (split) fa.mode = 5;
     }
     launch_fill(L, fa, p.Nb, nblocks);
     if (wout) *wout = w;
@@ -1201,103 +1227,78 @@ __global__ void k_complex_real(Index n, const double2* __restrict__ a, double* _
     if (i < n) out[i] = a[i].x;
 }
 
-// Eigenvalues of the box pencil through the B200 path (k_dense.cu): S = L L^T (potrf), A =
-// L^-1 H L^-T (two triangular solves, then 0.5 (A + A^T) as eigensolver.cpp:28-29), the
-// persistent tridiagonalisation and Sturm multisection. H is overwritten with A.
-static void box_eig_tridiag(lt_ctx* c, Index n, double* H, double* S, double* eig_dev) {
-    const Launch L = c->L();
+__global__ void k_pad_copy(int n, long long lds, const double* __restrict__ src, long long ldd, double* __restrict__ dst) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= static_cast<long long>(n) * n) return;
+    const long long r = i % n, c = i / n;
+    dst[c * ldd + r] = src[c * lds + r];
+}
+
+static void pad_copy(const Launch& L, int n, long long lds, const double* src, long long ldd, double* dst) {
+    Stage st_(L, "pad_copy");
+    k_pad_copy<<<static_cast<unsigned>((static_cast<long long>(n) * n + 255) / 256), 256, 0, L.st>>>(n, lds, src, ldd,
+                                                                                                   dst);
+    LT_CU(cudaGetLastError());
+    L.tick();
+}
+
+// The box pencil's reduction to a standard problem on the device (k_dense2.cu), in two
+// halves so the S side can run as soon as S exists: box_factor (S = L L^T, L^-1 row- and
+// column-major) and box_transform (A = L^-1 H L^-T, exactly symmetric, left in H, n x n
+// pitch n). TMA needs a row pitch that is a multiple of 16 bytes: odd n works on padded
+// copies. Failures (S not positive definite) land in fail_dev; no host synchronisation
+// (graph-capturable).
+static DenseReduceBufs box_bufs(lt_ctx* c, Index n, long long* ld_out) {
+    const long long ld = (n % 2 == 0) ? n : n + 1;
+    DenseReduceBufs b;
+    b.Li = c->arena.get<double>("box.Li", n * ld);
+    b.Lic = c->arena.get<double>("box.Lic", n * ld);
+    b.W = c->arena.get<double>("box.W", n * ld);
+    b.T = c->arena.get<double>("box.T", n * ld);
+    if (ld != n) {
+        b.S = c->arena.get<double>("box.Sp", n * ld);
+        b.H = c->arena.get<double>("box.Hp", n * ld);
+    }
+    *ld_out = ld;
+    return b;
+}
+
+static void box_factor(lt_ctx* c, const Launch& L, Index n, double* S, unsigned long long* fail_dev) {
+    long long ld = 0;
+    DenseReduceBufs b = box_bufs(c, n, &ld);
+    b.fail = fail_dev;
+    if (ld == n) b.S = S;
+    else pad_copy(L, static_cast<int>(n), n, S, ld, b.S);
+    dense_factor(L, static_cast<int>(n), ld, b);
+}
+
+static void box_transform(lt_ctx* c, const Launch& L, Index n, double* H, unsigned long long* fail_dev) {
+    long long ld = 0;
+    DenseReduceBufs b = box_bufs(c, n, &ld);
+    b.fail = fail_dev;
+    if (ld == n) b.H = H;
+    else pad_copy(L, static_cast<int>(n), n, H, ld, b.H);
+    dense_transform(L, static_cast<int>(n), ld, b);
+    if (ld != n) pad_copy(L, static_cast<int>(n), ld, b.H, n, H);
+}
+
+// eigenvalues of the reduced box pencil (A in H): the persistent tridiagonalisation and
+// the Sturm multisection (k_dense.cu)
+static void box_tridiag_eig(lt_ctx* c, const Launch& L, Index n, const double* A, double* eig_dev) {
     const int ni = static_cast<int>(n);
-    int lwork = 0;
-    if (cusolverDnDpotrf_bufferSize(c->solver, CUBLAS_FILL_MODE_LOWER, ni, S, ni, &lwork) != CUSOLVER_STATUS_SUCCESS)
-        fail(LT_ECUDA, "cusolverDnDpotrf_bufferSize failed");
-    double* work = c->arena.get<double>("box.work", static_cast<size_t>(lwork) + 4 * n + 1);
-    int* info = c->arena.get<int>("box.info", 1);
-    {
-        Stage st_(L, "potrf");
-        if (cusolverDnDpotrf(c->solver, CUBLAS_FILL_MODE_LOWER, ni, S, ni, work, lwork, info) != CUSOLVER_STATUS_SUCCESS)
-            fail(LT_ECUDA, "cusolverDnDpotrf failed");
-    }
-    int hinfo = 0;
-    LT_CU(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    LT_CU(cudaStreamSynchronize(c->stream));
-    if (hinfo != 0)
-        fail(LT_EDEFINITE, "solve_box_dense: overlap matrix is not positive definite (near-linear-dependent basis?)");
-    if (!c->blas) {
-        if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) fail(LT_ECUDA, "cublasCreate failed");
-    }
-    cublasSetStream(c->blas, c->stream);
-    const double one = 1.0, zero = 0.0, mone = -1.0;
-    static const bool use_trsm = std::getenv("LT_BOX_TRSM") != nullptr;  // A/B: two library solves
-    if (use_trsm) {
-        Stage st_(L, "trsm");
-        if (cublasDtrsm(c->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, ni, ni,
-                        &one, S, ni, H, ni) != CUBLAS_STATUS_SUCCESS ||
-            cublasDtrsm(c->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, ni, ni,
-                        &one, S, ni, H, ni) != CUBLAS_STATUS_SUCCESS)
-            fail(LT_ECUDA, "cublasDtrsm failed");
-    } else {
-        // L^-1 explicitly by recursive doubling (the library trsm / trtri are latency-bound
-        // column sweeps at this size): the 64 x 64 diagonal blocks in one launch, then per
-        // level s = 64, 128, ... the off-diagonal block of every pair of s-blocks,
-        //   X21 = -L22^-1 (L21 L11^-1),
-        // as two strided-batched DMMA GEMMs (pairs sit at a constant stride 2s (n + 1)); then
-        // A = L^-1 H L^-T as two GEMMs.
-        double* Li = c->arena.get<double>("box.Li", n * n);
-        double* W = c->arena.get<double>("box.W", n * n);
-        LT_CU(cudaMemsetAsync(Li, 0, sizeof(double) * n * n, c->stream));
-        launch_trtri_leaf(L, ni, S, Li);
-        {
-            Stage st_(L, "trtri_merge");
-            for (int sz = 64; sz < ni; sz *= 2) {
-                const int full = ni / (2 * sz);  // pairs with both blocks of size sz
-                const long long stride = 2LL * sz * (ni + 1);
-                bool ok = true;
-                if (full > 0) {
-                    ok = ok && cublasDgemmStridedBatched(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, sz, sz, sz, &one, S + sz, ni,
-                                                         stride, Li, ni, stride, &zero, W + sz, ni, stride,
-                                                         full) == CUBLAS_STATUS_SUCCESS;
-                    ok = ok && cublasDgemmStridedBatched(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, sz, sz, sz, &mone,
-                                                         Li + sz + static_cast<size_t>(sz) * ni, ni, stride, W + sz, ni,
-                                                         stride, &zero, Li + sz, ni, stride,
-                                                         full) == CUBLAS_STATUS_SUCCESS;
-                }
-                const int r0 = full * 2 * sz;        // a trailing pair: block of sz, then m2 < sz
-                const int m2 = ni - r0 - sz;
-                if (m2 > 0) {
-                    const size_t o11 = static_cast<size_t>(r0) * ni + r0, o21 = o11 + sz;
-                    const size_t o22 = o11 + static_cast<size_t>(sz) * ni + sz;
-                    ok = ok && cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, m2, sz, sz, &one, S + o21, ni, Li + o11, ni,
-                                           &zero, W + o21, ni) == CUBLAS_STATUS_SUCCESS;
-                    ok = ok && cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, m2, sz, m2, &mone, Li + o22, ni, W + o21,
-                                           ni, &zero, Li + o21, ni) == CUBLAS_STATUS_SUCCESS;
-                }
-                if (!ok) fail(LT_ECUDA, "cublasDgemm (triangular inverse) failed");
-            }
-        }
-        {
-            Stage st_(L, "reduce_gemm");
-            static const bool use_trmm = std::getenv("LT_BOX_GEMM") == nullptr;  // A/B: dense GEMMs
-            bool ok;
-            if (use_trmm)
-                ok = cublasDtrmm(c->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, ni,
-                                 ni, &one, Li, ni, H, ni, W, ni) == CUBLAS_STATUS_SUCCESS &&
-                     cublasDtrmm(c->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT,
-                                 ni, ni, &one, Li, ni, W, ni, H, ni) == CUBLAS_STATUS_SUCCESS;
-            else
-                ok = cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, ni, ni, ni, &one, Li, ni, H, ni, &zero, W, ni) ==
-                         CUBLAS_STATUS_SUCCESS &&
-                     cublasDgemm(c->blas, CUBLAS_OP_N, CUBLAS_OP_T, ni, ni, ni, &one, W, ni, Li, ni, &zero, H, ni) ==
-                         CUBLAS_STATUS_SUCCESS;
-            if (!ok) fail(LT_ECUDA, "cublasDgemm (L^-1 H L^-T) failed");
-        }
-    }
-    launch_symmetrize(L, ni, H);
     double* d = c->arena.get<double>("box.td", n);
     double* e = c->arena.get<double>("box.te", n);
     double* tw = c->arena.get<double>("box.tw", 4 * n);
     unsigned* bar = c->arena.get<unsigned>("box.bar", 8 * 160);  // per-CTA flags, 32 B apart
-    launch_sytrd(L, ni, H, d, e, tw, bar);
+    launch_sytrd(L, ni, A, d, e, tw, bar);
     launch_tridiag_eig(L, ni, d, e, eig_dev);
+}
+
+static void box_eig_tridiag(lt_ctx* c, Index n, double* H, double* S, double* eig_dev, unsigned long long* fail_dev) {
+    const Launch L = c->L();
+    box_factor(c, L, n, S, fail_dev);
+    box_transform(c, L, n, H, fail_dev);
+    box_tridiag_eig(c, L, n, H, eig_dev);
 }
 
 // Box pencil on device buffers H, S (n x n col-major; both may be overwritten).
@@ -1332,15 +1333,14 @@ static void box_eig_device(lt_ctx* c, Index n, double* H, double* S, double* eig
         }
         return;
     }
+    if (!vec_dev && sytrd_ctas(static_cast<int>(n)) > 0) {
+        box_eig_tridiag(c, n, H, S, eig_dev, fail_dev);
+        return;
+    }
     if (!c->solver) {
         if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS) fail(LT_ECUDA, "cusolverDnCreate failed");
     }
     cusolverDnSetStream(c->solver, c->stream);
-    static const bool force_library = std::getenv("LT_BOX_SYGVD") != nullptr;
-    if (!vec_dev && !force_library && sytrd_ctas(static_cast<int>(n)) > 0) {
-        box_eig_tridiag(c, n, H, S, eig_dev);
-        return;
-    }
     const cusolverEigMode_t mode = vec_dev ? CUSOLVER_EIG_MODE_VECTOR : CUSOLVER_EIG_MODE_NOVECTOR;
     int lwork = 0;
     if (cusolverDnDsygvd_bufferSize(c->solver, CUSOLVER_EIG_TYPE_1, mode, CUBLAS_FILL_MODE_LOWER, static_cast<int>(n), H,
@@ -1461,7 +1461,10 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
     }
     if (periodic) out.kidx = c->arena.get<int64_t>("core.kidx", p.nblocks * 3);
     const bool small_box = !periodic && p.Nb <= 32;
-    const bool inline_readback = periodic || small_box;  // no host step after the graph
+    // box pencils on the device path (batched pencil kernel or the dense reduction +
+    // persistent tridiagonalisation) need no host step: they run inside the graph
+    const bool graph_box = !periodic && (small_box || sytrd_ctas(static_cast<int>(p.Nb)) > 0);
+    const bool inline_readback = periodic || graph_box;  // no host step after the graph
     const size_t ebytes = sizeof(double) * (periodic ? p.K * p.m0 : p.Nb);
     void* epin = eig_host ? c->stage_alloc(ebytes) : nullptr;  // pinned: capturable copy target
     int* rpin = c->pinned_state();
@@ -1471,7 +1474,7 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
     // eigenvalues straight into the pinned staging buffer (host API) and the result block
     // copied by the pencil kernel's last group: no copy nodes at the end of the graph
     double* eig_out = epin ? static_cast<double*>(epin) : eig_dev;
-    const bool kernel_readback = phase != 1 && inline_readback && (small_box || k_begin < k_end);
+    const bool kernel_readback = phase != 1 && inline_readback && (small_box || (periodic && k_begin < k_end));
     PencilReadback rb;
     if (kernel_readback) rb = PencilReadback{ret, rpin, c->pencil_done};
     auto enqueue = [&]() {
@@ -1489,7 +1492,13 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
                 l0w.enqueue(c->L(), 1, static_cast<int>(L0) + 3, true);
             }
         }
-        if (phase != 2) run_assembly(c, sd, p, NEED_MS | NEED_NUC, 0, out, nullptr, s0d, 0, opt.shard);
+        // large box pencils (dense reduction on the device): the S side of the reduction runs
+        // on the FEM branch, overlapping the nuclear contraction
+        const bool box_split = graph_box && !small_box && phase == 0;
+        const BranchHook s_hook = [&](const Launch& LF) { box_factor(c, LF, p.Nb, out.out1, fk); };
+        if (phase != 2)
+            run_assembly(c, sd, p, NEED_MS | NEED_NUC, 0, out, nullptr, s0d, box_split ? AS_BOX_SPLIT : 0u, opt.shard,
+                         box_split ? &s_hook : nullptr);
         if (par_l0) c->join(7, c->aux[2], c->stream);
         if (phase == 2 && !periodic) {  // the box pencil factorises in place: work on copies
             LT_CU(cudaMemcpyAsync(out.out0, opt.H, sizeof(double) * ocount, cudaMemcpyDeviceToDevice, c->stream));
@@ -1532,7 +1541,10 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
                     launch_pencil(c->L(), k_end - k_begin, p.m0, Hb + k_begin * mm, Sb + k_begin * mm,
                                   eig_out + k_begin * p.m0, fk, true, PencilDft{}, nullptr, rb);
             }
-        } else if (small_box) {
+        } else if (box_split) {
+            box_transform(c, c->L(), p.Nb, out.out0, fk);
+            box_tridiag_eig(c, c->L(), p.Nb, out.out0, eig_out);
+        } else if (graph_box) {
             box_eig_device(c, p.Nb, out.out0, out.out1, eig_out, fk, nullptr, rb);
         }
         if (inline_readback && !kernel_readback)  // (an empty k-point shard launches no pencil)

@@ -53,8 +53,8 @@ __global__ void k_fill(FillDev f) {
         if (!f.periodic && (m[l] < 0 || m[l] >= f.L[l])) return;
     }
     const Index mm = f.m0 * f.m0;
-    const bool want_ms = f.mode == 0 || f.mode == 1 || f.mode == 2;
-    const bool want_nuc = f.mode == 0 || f.mode == 3;
+    const bool want_ms = f.mode == 0 || f.mode == 1 || f.mode == 2 || f.mode == 5;
+    const bool want_nuc = f.mode == 0 || f.mode == 3 || f.mode == 5;
     Index pidx[3];
     for (int l = 0; l < 3; ++l) pidx[l] = pair_index(f, l, k[l], d[l]);
     for (Index e = threadIdx.x; e < mm; e += blockDim.x) {
@@ -110,6 +110,7 @@ __global__ void k_fill(FillDev f) {
         double v0 = 0.0, v1 = 0.0;
         switch (f.mode) {
             case 0: v0 = __dadd_rn(__dmul_rn(f.kin, lap), __dmul_rn(-1.0, nuc)); v1 = mass; break;
+            case 5: v0 = __dadd_rn(__dmul_rn(f.kin, lap), __dmul_rn(-1.0, nuc)); break;  // H only
             case 1: v0 = lap; break;
             case 2: v0 = mass; break;
             default: v0 = nuc; break;

@@ -341,7 +341,7 @@ void launch_resfold(const Launch& L, const ResFold& f, bool reduce, bool mirror,
 void launch_fgemm(const Launch& L, int m0, int Rtot, const DirPlan& d, const double* P, const double* Qf, double* T);
 void launch_kr_combine(const Launch& L, const KRArgs& a);
 
-// fill H/S (box dense, periodic generating blocks); mode 0 core (H,S), 1 Laplace, 2 Mass, 3 Nuclear
+// fill H/S (box dense, periodic generating blocks); mode 0 core (H,S), 1 Laplace, 2 Mass, 3 Nuclear, 5 core H only
 struct FillArgs {
     Index m0 = 0, Rtot = 0, L[3]{1, 1, 1}, band[3]{}, width[3]{1, 1, 1};
     const double* massT[3]{};
@@ -465,6 +465,59 @@ __host__ __device__ inline int dft_fft_log(Index L) {
 }
 size_t dft_fused_smem(const DftFusedArgs& a);
 void launch_dft_fused(const Launch& L, const DftFusedArgs& a, int nops);
+// TMA-fed DMMA GEMM (k_dgemm.cu): C(m, n) = [C +] alpha sum_k A(m, k) B(n, k), operands
+// K-major rows of row-major 2D tensors (see the kernel header)
+enum DgemmFlags : int {
+    DG_LOWER = 1,        // tiles entirely above the diagonal are skipped (diagonal tiles: n <= m)
+    DG_MIRROR = 2,       // also store C(n, m) (symmetric result from its lower triangle)
+    DG_K_LE_M = 4,       // per tile: k < m_tile_end (A(m, k) lower triangular)
+    DG_K_LE_N = 8,       // k < n_tile_end (B(n, k) lower triangular)
+    DG_K_GE_M = 16,      // k >= m_tile_begin
+    DG_K_GE_N = 32,      // k >= n_tile_begin
+    DG_C0_COLMAJOR = 64, // c0 stored column-major (C[m + n ldc]); else row-major (C[m ldc + n])
+    DG_C1_COLMAJOR = 128,
+};
+struct DgemmOperand {
+    const double* base = nullptr;  // row-major tensor: rows x cols, pitch ld (doubles)
+    long long rows = 0, cols = 0, ld = 0;
+};
+struct DgemmArgs {
+    int M = 0, N = 0;
+    long long K = 0;
+    long long a_row0 = 0, a_col0 = 0, b_row0 = 0, b_col0 = 0;
+    long long a_zrow = 0, a_zcol = 0, b_zrow = 0, b_zcol = 0;  // per-batch coordinate shifts
+    double* c0 = nullptr;
+    double* c1 = nullptr;  // optional second output (other layout)
+    long long ldc = 0, c_zoff = 0;
+    double alpha = 1.0;
+    int beta_one = 0;  // 1: C += alpha AB, 0: C = alpha AB
+    int flags = 0;
+    const unsigned long long* fail = nullptr;  // skip when *fail != ~0 (an earlier stage failed)
+};
+void launch_dgemm_tn(const Launch& L, const DgemmOperand& A, const DgemmOperand& B, const DgemmArgs& args, int batches,
+                     const char* stage);
+
+// dense box pencil front end (k_dense2.cu): blocked Cholesky S = L L^T (row-major L in
+// place of S, Eigen's pivot test; failure -> atomicMin(fail, 2)), L^-1 (row- and
+// column-major) by 64 x 64 leaf inverses and recursive doubling, then A = L^-1 H L^-T into H
+// (symmetric, both triangles). ld: row pitch of every n x n buffer (multiple of 2).
+struct DenseReduceBufs {
+    double* S = nullptr;    // in: S (symmetric); out: L row-major (lower)
+    double* H = nullptr;    // in: H (symmetric); out: A = L^-1 H L^-T
+    double* Li = nullptr;   // out: L^-1 row-major
+    double* Lic = nullptr;  // out: L^-1 column-major
+    double* W = nullptr;    // scratch n x n
+    double* T = nullptr;    // scratch n x n
+    unsigned long long* fail = nullptr;
+};
+void dense_reduce(const Launch& L, int n, long long ld, const DenseReduceBufs& b);
+// the two halves: the S side (Cholesky + L^-1; S, Li, Lic, T) and the H side (W, A into H)
+void dense_factor(const Launch& L, int n, long long ld, const DenseReduceBufs& b);
+void dense_transform(const Launch& L, int n, long long ld, const DenseReduceBufs& b);
+// X = L^-T Z (eigenvectors, eigensolver.cpp:31-32): Z, X column-major with pitch ld
+void dense_back_transform(const Launch& L, int n, long long ld, const double* Lic, const double* Z, double* X,
+                          const unsigned long long* fail);
+
 // dense box pencil (k_dense.cu): CTAs of the shared-memory resident tridiagonalisation (0:
 // too large), the reduction itself (work: 4 n doubles, bar: one zeroed counter), the
 // tridiagonal eigenvalues and the in-place symmetrisation 0.5 (A + A^T)

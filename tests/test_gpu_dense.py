@@ -51,3 +51,52 @@ def test_dense_pencil_reduction(ctx, oracle, n):
     assert np.max(np.abs(ev - ref)) / scale < 1e-11
     if n <= 300:
         assert np.max(np.abs(ev - oracle.solve_box_dense(H, S))) / scale < 1e-11
+
+
+@pytest.mark.parametrize("n", [33, 65, 191, 1000])
+def test_dense_pencil_reduction_edges(ctx, n):
+    # sizes off the 64-column panel grid (partial leaf blocks, odd pitch -> padded TMA copies)
+    rng = np.random.default_rng(100 + n)
+    A = rng.uniform(-1, 1, (n, n))
+    H = 0.5 * (A + A.T)
+    Q, _ = np.linalg.qr(rng.uniform(-1, 1, (n, n)))
+    S = (Q * np.logspace(-3, 0, n)) @ Q.T
+    S = 0.5 * (S + S.T)
+    ev = ctx.solve_box_dense(H, S)
+    ref = sl.eigh(H, S, eigvals_only=True)
+    assert np.max(np.abs(ev - ref)) <= 1e-12 * np.max(np.abs(ref)) * n
+
+
+@pytest.mark.parametrize("n", [33, 65])
+def test_dense_pencil_ill_conditioned_overlap(ctx, n):
+    # cond(S) = 1e10, as near-linear-dependent bases produce: every FP64 algorithm (LAPACK
+    # sygvd included) is off the exact eigenvalues by ~cond(L) u ||A||; the GPU must be as
+    # close to a 40-digit reference (mpmath) as LAPACK, within a factor 8
+    mp = pytest.importorskip("mpmath")
+    rng = np.random.default_rng(100 + n)
+    A = rng.uniform(-1, 1, (n, n))
+    H = 0.5 * (A + A.T)
+    Q, _ = np.linalg.qr(rng.uniform(-1, 1, (n, n)))
+    S = (Q * np.logspace(-10, 0, n)) @ Q.T
+    S = 0.5 * (S + S.T)
+    mp.mp.dps = 40
+    Lm = mp.cholesky(mp.matrix(S.tolist()))
+    Li = mp.inverse(Lm)
+    hp = np.array(sorted(float(x) for x in mp.eigsy(Li * mp.matrix(H.tolist()) * Li.T)[0]))
+    ev = ctx.solve_box_dense(H, S)
+    lap = sl.eigh(H, S, eigvals_only=True)
+    assert np.max(np.abs(ev - hp)) <= 8 * np.max(np.abs(lap - hp)), (np.max(np.abs(ev - hp)), np.max(np.abs(lap - hp)))
+
+
+@pytest.mark.parametrize("n", [40, 700])
+def test_dense_pencil_indefinite_overlap_raises(ctx, n):
+    # eigensolver.cpp:20-24: LLT fails -> DefinitenessError, as the reference
+    from paper_1408_3839_b200.api import DefinitenessError
+    rng = np.random.default_rng(n)
+    H = np.eye(n)
+    Q, _ = np.linalg.qr(rng.uniform(-1, 1, (n, n)))
+    d = np.ones(n)
+    d[n // 2] = -1e-3
+    S = (Q * d) @ Q.T
+    with pytest.raises(DefinitenessError, match="not positive definite"):
+        ctx.solve_box_dense(H, 0.5 * (S + S.T))
