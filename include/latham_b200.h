@@ -111,6 +111,28 @@ void lt_sys_free(lt_sysdev* s);
 lt_status lt_solve_core_dev(lt_ctx* ctx, const lt_sysdev* sys, int periodic, double* eig_dev, int64_t k_begin,
                             int64_t k_end, int64_t* info);
 
+/* ---- several GPUs of one process (parallel.hpp:15-32) ------------------ *
+ * lt_mctx: one lt_ctx per listed device and an in-process NCCL communicator over them
+ * (ncclCommInitAll; NCCL is loaded at creation). lt_solve_core_multi = lt_solve_core on
+ * all devices:
+ *   LT_SPLIT_KPOINTS   every device assembles H, S and solves its contiguous k-range
+ *                      (eigensolver.cpp:95-120); one ncclAllGather of the eigenvalues;
+ *   LT_SPLIT_RANKTERMS device q assembles the nuclear rank terms of its range
+ *                      (galerkin.cpp:275-283) into a partial H (device 0 adds 0.5 Laplace),
+ *                      one ncclAllReduce (sum) completes H; then the k-range solves and the
+ *                      all-gather. Box systems: device 0 solves the dense pencil.
+ * Eigenvalues land on the host in the single-device order (identical values for the
+ * k-point split). lt_multi_ctx(m, i) exposes device i's context for the other entries. */
+typedef struct lt_mctx lt_mctx;
+#define LT_SPLIT_KPOINTS 0
+#define LT_SPLIT_RANKTERMS 1
+lt_status lt_create_multi(const int* devices, int ndev, lt_mctx** out);
+void lt_destroy_multi(lt_mctx* m);
+int lt_multi_ndev(const lt_mctx* m);
+lt_ctx* lt_multi_ctx(lt_mctx* m, int i);
+lt_status lt_solve_core_multi(lt_mctx* m, const lt_system* sys, int periodic, int split, double* eig_host,
+                              int64_t* info);
+
 /* ---- multi-GPU: assembly sharded by rank terms ---------------------- *
  * The nuclear operator is a rank-R_tot sum (galerkin.cpp:275-283: sum_r w_r prod_l T_l);
  * a shard assembles the terms r in [r_begin, r_end) (r_end < 0: all) and, with_kinetic != 0,

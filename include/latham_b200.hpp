@@ -181,6 +181,23 @@ private:
     lt_ctx* h_ = nullptr;
 };
 
+/// Several GPUs of one process (lt_mctx): one Context per device + an in-process NCCL
+/// communicator; the device-parallel analogue of parallel_for (parallel.hpp:15-32).
+class MultiContext {
+public:
+    explicit MultiContext(const std::vector<int>& devices) {
+        check(lt_create_multi(devices.data(), static_cast<int>(devices.size()), &h_));
+    }
+    ~MultiContext() { lt_destroy_multi(h_); }
+    MultiContext(const MultiContext&) = delete;
+    MultiContext& operator=(const MultiContext&) = delete;
+    lt_mctx* get() const { return h_; }
+    int devices() const { return lt_multi_ndev(h_); }
+
+private:
+    lt_mctx* h_ = nullptr;
+};
+
 // ---- assembled operators (galerkin.hpp:43-54) ---------------------------------------
 class AssembledOperator {
 public:
@@ -454,6 +471,16 @@ inline KPointSpectrum solve_core_periodic(Context& ctx, const LatticeSystem& sys
     std::vector<double> flat(static_cast<size_t>(sys.basis_count()));
     check(lt_solve_core(ctx.get(), v.get(), 1, flat.data(), info));
     return make_spectrum(sys.L, sys.m0(), flat, "b200-core");
+}
+
+/// The whole path across the devices of `mctx` (split: LT_SPLIT_KPOINTS or LT_SPLIT_RANKTERMS);
+/// the same KPointSpectrum as solve_core_periodic on one device.
+inline KPointSpectrum solve_core_periodic(MultiContext& mctx, const LatticeSystem& sys, int split = LT_SPLIT_KPOINTS,
+                                          int64_t* info = nullptr) {
+    SystemView v(sys);
+    std::vector<double> flat(static_cast<size_t>(sys.basis_count()));
+    check(lt_solve_core_multi(mctx.get(), v.get(), 1, split, flat.data(), info));
+    return make_spectrum(sys.L, sys.m0(), flat, "b200-core-multi");
 }
 
 /// tools/commands.cpp:51-59 + solve_box_dense, fused on the device.

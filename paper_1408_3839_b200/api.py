@@ -524,6 +524,44 @@ class Context:
         return out
 
 
+class MultiContext:
+    """Several GPUs of this process (lt_mctx): one context per device and an in-process NCCL
+    communicator; solve_core shards the path across them."""
+
+    SPLITS = {"kpoints": 0, "rankterms": 1}
+
+    def __init__(self, devices):
+        self.lib = native.lib()
+        devs = (ctypes.c_int * len(devices))(*devices)
+        h = ctypes.c_void_p()
+        check(self.lib.lt_create_multi(devs, len(devices), ctypes.byref(h)))
+        self.h = h
+        self.devices = list(devices)
+
+    def close(self):
+        if self.h:
+            self.lib.lt_destroy_multi(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def ndev(self) -> int:
+        return int(self.lib.lt_multi_ndev(self.h))
+
+    def solve_core(self, sys: LatticeSystem, periodic: bool, split: str = "kpoints",
+                   info: Optional[np.ndarray] = None) -> np.ndarray:
+        c = sys.to_c()
+        out = np.zeros(sys.basis_count)
+        inf = np.zeros(8, dtype=np.int64) if info is None else info
+        check(self.lib.lt_solve_core_multi(self.h, ctypes.byref(c), int(periodic), self.SPLITS[split], _d(out), _i(inf)))
+        return out.reshape(sys.lattice_count, sys.m0) if periodic else out
+
+
 class DeviceSystem:
     """A LatticeSystem resident on the device (lt_sysdev) for the bench's device-timed leg."""
 

@@ -1662,6 +1662,9 @@ extern "C" {
 
 const char* lt_last_error(void) { return lt::g_err.c_str(); }
 
+// (not in the public header) the multi-device layer (multi.cpp) reports through lt_last_error
+void lt_internal_set_error(const char* msg) { lt::g_err = msg ? msg : ""; }
+
 
 // ---------------------------------------------------------------------------
 // separable metadata and the factorized Fourier path (k_sep.cu)

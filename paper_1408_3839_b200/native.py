@@ -114,6 +114,11 @@ def lib():
             "lt_potential": ([_vp, _vp, ctypes.c_int, _i64, _ip, _ip, _dp, _dp, _i64], ctypes.c_int),
             "lt_assembled_window_sum": ([_vp, _i64, _i64, _dp, _i64, _ip, _i64, _dp], ctypes.c_int),
             "lt_profiles": ([_vp, _vp, _i64, _ip, _ip, _ip, _dp, _i64], ctypes.c_int),
+            "lt_create_multi": ([_P(ctypes.c_int), ctypes.c_int, _P(_vp)], ctypes.c_int),
+            "lt_destroy_multi": ([_vp], None),
+            "lt_multi_ndev": ([_vp], ctypes.c_int),
+            "lt_multi_ctx": ([_vp, ctypes.c_int], _vp),
+            "lt_solve_core_multi": ([_vp, _vp, ctypes.c_int, ctypes.c_int, _dp, _ip], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -131,6 +136,7 @@ def check(rc: int):
 
 # symbols declared in include/latham_b200.h (checked by tests/test_abi.py)
 EXPORTS = (
+    "lt_create_multi", "lt_destroy_multi", "lt_multi_ndev", "lt_multi_ctx", "lt_solve_core_multi",
     "lt_create", "lt_destroy", "lt_last_error", "lt_stream", "lt_stream_wait", "lt_stream_join", "lt_launch_count", "lt_set_stage_timing", "lt_set_diagnostics",
     "lt_stage_count", "lt_stage_get", "lt_stage_timeline_count", "lt_stage_timeline_get",
     "lt_op_separable_count", "lt_op_separable", "lt_separable_residual", "lt_solve_periodic_factorized",

@@ -48,6 +48,12 @@ int main() {
     auto H = combine(ctx, 0.5, lap, -1.0, nuc);
     print("periodic_ops", solve_periodic(ctx, H, S).sorted_all());
     print("periodic_core", solve_core_periodic(ctx, per).sorted_all());
+    {
+        // the multi-device entry over the devices of this box (one on the test box)
+        MultiContext mctx({0});
+        print("periodic_multi_k", solve_core_periodic(mctx, per, LT_SPLIT_KPOINTS).sorted_all());
+        print("periodic_multi_r", solve_core_periodic(mctx, per, LT_SPLIT_RANKTERMS).sorted_all());
+    }
     print("periodic_factorized", solve_periodic_factorized(ctx, H, S).sorted_all());
     std::printf("residual %.3g\n", separable_residual(ctx, H));
     // want_vectors: per-k blocks; one reconstructed column against bc_full_eigenvector

@@ -39,12 +39,17 @@ def chain(Lx, two):
 @pytest.mark.gpu
 def test_cpp_client_matches_python_api(tmp_path, ctx):
     out = subprocess.run([build(tmp_path)], check=True, capture_output=True, text=True).stdout.splitlines()
-    res = {ln.split()[0]: ln.split()[1:] for ln in out}
+    # (NCCL may print its version banner on communicator creation: keep the client's lines)
+    res = {ln.split()[0]: ln.split()[1:] for ln in out if ln.split() and not ln.startswith("NCCL")}
     vals = {k: np.array([float(x) for x in v[1:]]) for k, v in res.items() if not k.startswith(("error", "resid"))}
     per = np.sort(ctx.solve_core(chain(16, True), True).reshape(-1))
     box = ctx.solve_core(chain(6, False), False)
     assert np.array_equal(vals["periodic_core"], per)
     assert np.array_equal(vals["box_core"], box)
+    # lt_solve_core_multi (NCCL communicator over the listed devices): k-point split bitwise,
+    # rank-term split (partial H summed by the all-reduce) to rounding
+    assert np.array_equal(vals["periodic_multi_k"], per)
+    assert np.max(np.abs(vals["periodic_multi_r"] - per)) < 1e-10 * max(1.0, np.max(np.abs(per)))
     # the separate-operator route (assemble x3, combine, solve) agrees to rounding
     assert np.max(np.abs(vals["periodic_ops"] - per)) < 1e-10 * max(1.0, np.max(np.abs(per)))
     assert np.max(np.abs(vals["box_ops"] - box)) < 1e-10 * max(1.0, np.max(np.abs(box)))

@@ -112,3 +112,23 @@ def test_shard_errors(ctx):
     ds = ctx.upload(sys)
     with pytest.raises(DimensionError):
         ds.assemble_shard(True, 0, -1, True, 0, 0)
+
+
+@pytest.mark.parametrize("name", ["c2", "c5", "c1", "c3"])
+def test_gpu_multi_context_matches_single(ctx, name):
+    # lt_create_multi / lt_solve_core_multi over the devices of this box (NCCL communicator
+    # from ncclCommInitAll): the k-point split is bitwise the single-device spectrum, the
+    # rank-term split (partial H per device + ncclAllReduce) within the shard-sum bound
+    from golden_util import load
+
+    from paper_1408_3839_b200.api import MultiContext
+    s, periodic, d = load(name)
+    ref = ctx.solve_core(s, periodic)
+    m = MultiContext([0])
+    assert m.ndev == 1
+    ev_k = m.solve_core(s, periodic, "kpoints")
+    assert np.array_equal(ev_k, ref)
+    ev_r = m.solve_core(s, periodic, "rankterms")
+    tol = np.maximum(1e-9, 2.0 * np.asarray(d["eig_floor"]))
+    assert np.all(np.abs(ev_r.reshape(tol.shape) - ref.reshape(tol.shape)) <= tol)
+    m.close()
