@@ -667,7 +667,12 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
     // stage-timing mode runs the branches back to back on the main stream, so each stage's
     // events bracket that kernel alone (concurrent branches would share SMs)
     const bool serial = c->timer.on;
-    const Launch LF = serial ? L : c->LA(0), LP = serial ? L : c->LA(1);
+    // the FEM branch normally runs on the low-priority side stream; when it feeds the box
+    // pencil's Cholesky (AS_BOX_SPLIT: the S side is then the critical path) it takes the
+    // high-priority one and the second potential the low-priority one
+    const bool fem_hi = (flags & AS_BOX_SPLIT) && !p.periodic;
+    const int fi = fem_hi ? 1 : 0, pi = fem_hi ? 0 : 1;
+    const Launch LF = serial ? L : c->LA(fi), LP = serial ? L : c->LA(pi);
     const Index m0 = p.m0, mm = m0 * m0, RN = p.RN, Rtot = p.Rtot;
     Arena& A = c->arena;
     int src[3];
@@ -676,8 +681,8 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
     const int64_t* s0d = nullptr;
     const bool nuc = need & NEED_NUC, ms = need & NEED_MS;
     if (nuc) s0d = s0_dev ? s0_dev : upload_s0(c, p);
-    c->join(0, c->stream, c->aux[0]);
-    c->join(1, c->stream, c->aux[1]);
+    c->join(0, c->stream, c->aux[fi]);
+    c->join(1, c->stream, c->aux[pi]);
     // Trivial-direction panels could be evaluated inside k_triv_gemm (TrivJob.pot = null):
     // measured slower (erf pairs in the GEMM loader, repeated per N tile), so every panel is
     // materialised by the master-free window kernels.
@@ -719,7 +724,7 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
             }
         }
     }
-    c->join(2, c->aux[1], c->stream);
+    c->join(2, c->aux[pi], c->stream);
     // profiles (galerkin.cpp:127-149), distinct directions only
     ProfileJob jobs[6];
     int nj = 0;
@@ -763,7 +768,7 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
             w.pwl_hi[l] = w.pwl_hi[src[l]];
         }
     launch_profiles(LF, sd->ds, jobs, nj, 1e-280);
-    c->join(3, c->aux[0], c->stream);  // nuclear part needs the profiles
+    c->join(3, c->aux[fi], c->stream);  // nuclear part needs the profiles
     if (ms) {
         // FEM-applied profiles (T v) for every distinct direction, then the tables as
         // residue-class correlations <u_mu, (T v_nu)(. - d nbar)> on DMMA
@@ -1009,7 +1014,7 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
         launch_fill(LF, fs, p.Nb, p.cells * p.d[0].width * p.d[1].width * p.d[2].width);
         if (s_hook) (*s_hook)(LF);
     }
-    c->join(4, c->aux[0], c->stream);  // FEM tables (and the S branch) before the fill
+    c->join(4, c->aux[fi], c->stream);  // FEM tables (and the S branch) before the fill
     if (flags & AS_NO_FILL) {
         if (wout) *wout = w;
         return;
