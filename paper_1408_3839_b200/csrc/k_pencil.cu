@@ -688,7 +688,7 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
 #pragma unroll
             for (int j = 0; j < Q; ++j) x[j] = a + (b - a) * (static_cast<double>(sub * Q + j + 1) * inv_pts);
             if (active) {
-                sturm3<Q>(sm.d, sm.e2, n, x, cnt);
+                sturm3<Q, 2>(sm.d, sm.e2, n, x, cnt);
             } else {
 #pragma unroll
                 for (int j = 0; j < Q; ++j) cnt[j] = 0;

@@ -62,17 +62,59 @@ __device__ __forceinline__ double warp_max(double v) {
 // two to max |entry| < 1; a ratio with |q_i| < 2^-100 is replaced by -2^-100 (the pivmin rule
 // of the ratio form, a perturbation of d_i far below eps ||T||), and (p_i, p_{i-1}) are
 // rescaled by an exact power of two every 4 steps, which keeps them normal (|q| <= 4).
-template <int Q, bool INTGUARD = true>
+// GUARD 1: integer-pipe guard (below); 0: the same rule on the FP64 pipe; 2: no per-step
+// guard, for the short chains of the batched pencils (n <= 32): with T scaled to max |entry|
+// < 1 and x inside the Gershgorin bracket, |p_i| <= 3^i cannot overflow, an exact p_i = 0
+// counts as non-negative (the next term -e^2 p_{i-2} restores the sign-change count), and the
+// every-4-steps power-of-two rescale keeps the chain normal.
+template <int Q, int GUARD = 1>
 __device__ __forceinline__ void sturm3(const double* sd, const double* se2, int n, const double (&x)[Q],
                                        int (&cnt)[Q]) {
+    constexpr bool INTGUARD = GUARD == 1;
+    if constexpr (GUARD == 2) {
+        // short chains: plain registers, no lambda (keeps x / cnt out of local memory)
+        double xv[Q], pv[Q], cv[Q];
+        int cn[Q];
+#pragma unroll
+        for (int j = 0; j < Q; ++j) {
+            xv[j] = x[j];
+            pv[j] = 1.0;
+            cv[j] = sd[0] - xv[j];
+            cn[j] = static_cast<int>(static_cast<unsigned>(__double2hiint(cv[j])) >> 31);
+        }
+        for (int i = 1; i < n; ++i) {
+            const double di = sd[i], ei = se2[i - 1];
+#pragma unroll
+            for (int j = 0; j < Q; ++j) {
+                const double nx = fma(di - xv[j], cv[j], -ei * pv[j]);
+                cn[j] += static_cast<int>(static_cast<unsigned>(__double2hiint(nx) ^ __double2hiint(cv[j])) >> 31);
+                pv[j] = cv[j];
+                cv[j] = nx;
+            }
+            if ((i & 3) == 0) {
+#pragma unroll
+                for (int j = 0; j < Q; ++j) {
+                    const int ex = ((__double2hiint(cv[j]) >> 20) & 0x7ff) - 1023;
+                    if (ex > 400 || ex < -400) {  // rare: exact power-of-two rescale of (cur, prev)
+                        const double scl = __longlong_as_double(static_cast<long long>(1023 - ex) << 52);
+                        cv[j] *= scl;
+                        pv[j] *= scl;
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < Q; ++j) cnt[j] = cn[j];
+        return;
+    }
     constexpr double kDelta = 7.888609052210118e-31;  // 2^-100
     double prev[Q], cur[Q];
 #pragma unroll
     for (int j = 0; j < Q; ++j) {
         prev[j] = 1.0;
         cur[j] = sd[0] - x[j];
-        if (fabs(cur[j]) < kDelta) cur[j] = -kDelta;
-        cnt[j] = cur[j] < 0.0;
+        if (GUARD != 2 && fabs(cur[j]) < kDelta) cur[j] = -kDelta;
+        cnt[j] = static_cast<int>(static_cast<unsigned>(__double2hiint(cur[j])) >> 31);
     }
     // INTGUARD: the guard and the sign count run on the integer pipe (the FP64 pipe then
     // carries only the DADD, DMUL and DFMA of the recurrence; measured faster for the batched
@@ -84,6 +126,12 @@ __device__ __forceinline__ void sturm3(const double* sd, const double* se2, int 
 #pragma unroll
         for (int j = 0; j < Q; ++j) {
             double nx = fma(di - x[j], cur[j], -ei * prev[j]);
+            if constexpr (GUARD == 2) {
+                cnt[j] += static_cast<int>(static_cast<unsigned>(__double2hiint(nx) ^ __double2hiint(cur[j])) >> 31);
+                prev[j] = cur[j];
+                cur[j] = nx;
+                continue;
+            }
             if constexpr (!INTGUARD) {  // the same rule on the FP64 pipe (exact 2^-100 |cur|)
                 const double thr = kDelta * fabs(cur[j]);
                 if (fabs(nx) < thr) nx = cur[j] < 0.0 ? thr : -thr;

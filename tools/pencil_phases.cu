@@ -6,6 +6,8 @@
 //        -o tools/pencil_phases
 // Phases: 0 load, 1 Hermitian check, 2 Cholesky, 3 reduction L^-1 H L^-H,
 //         4 Householder tridiagonalisation, 5 multisection.
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <random>
 #include <vector>
