@@ -15,7 +15,6 @@
 //   k_tridiag_eig3 eigenvalues of the tridiagonal (d, e): G lanes x Q shifts per eigenvalue of
 //                  three-term Sturm counts (no division on the chain), the bracket shrinks
 //                  G Q + 1-fold per round; ascending by construction.
-//   k_symmetrize   A = 0.5 (A + A^T) in place (tiles through shared memory).
 #include "lt_device.cuh"
 #include "lt_internal.cuh"
 
@@ -543,28 +542,6 @@ __global__ void __launch_bounds__(BS) k_tridiag_eig3(int n, const double* __rest
 }
 
 // A = 0.5 (A + A^T) in place: CTA per tile pair (bi >= bj), 32 x 32 tiles
-__global__ void k_symmetrize(int n, double* A) {
-    __shared__ double t1[32][33], t2[32][33];
-    const int bi = blockIdx.x, bj = blockIdx.y;
-    if (bi < bj) return;
-    const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
-    for (int r = ty; r < 32; r += 8) {
-        const int i1 = bi * 32 + tx, j1 = bj * 32 + r;  // tile (bi, bj), column j1
-        const int i2 = bj * 32 + tx, j2 = bi * 32 + r;  // tile (bj, bi)
-        t1[r][tx] = (i1 < n && j1 < n) ? A[static_cast<size_t>(j1) * n + i1] : 0.0;
-        t2[r][tx] = (i2 < n && j2 < n) ? A[static_cast<size_t>(j2) * n + i2] : 0.0;
-    }
-    __syncthreads();
-    for (int r = ty; r < 32; r += 8) {
-        const int i1 = bi * 32 + tx, j1 = bj * 32 + r;
-        const int i2 = bj * 32 + tx, j2 = bi * 32 + r;
-        // (i1, j1) pairs with (j1, i1) = tile (bj, bi) entry [row j1 - bj*32][col i1 - bi*32]
-        const double s1 = 0.5 * (t1[r][tx] + t2[tx][r]);
-        const double s2 = 0.5 * (t2[r][tx] + t1[tx][r]);
-        if (i1 < n && j1 < n) A[static_cast<size_t>(j1) * n + i1] = s1;
-        if (i2 < n && j2 < n) A[static_cast<size_t>(j2) * n + i2] = s2;
-    }
-}
 
 static size_t sytrd_smem(int n, int cols) {
     return sizeof(double) * (static_cast<size_t>(cols) * n + 4 * static_cast<size_t>(n) + cols);
@@ -638,67 +615,6 @@ void launch_tridiag_eig(const Launch& L, int n, const double* d, const double* e
     // CTAs: measured best on B200 for n = 1024 (the chain is issue-bound; more shifts per
     // round cost more than the rounds they save; the LDL^T-ratio counts were slower)
     run_eig3<2, 16, 64>(L, n, d, e, eig, smem);
-    LT_CU(cudaGetLastError());
-    L.tick();
-}
-
-// Inverses of the lower-triangular diagonal blocks (size <= 64) of L (n x n col-major) into
-// the same blocks of Li: one CTA per block, four lanes per column j (lane q sums the k = q
-// mod 4 terms, a two-step shuffle combines them) with a row loop uniform across the CTA (L
-// rows are broadcast reads; X(k, j) = 0 for k < j). A column lives in one warp, so a row
-// needs only a warp barrier.
-__global__ void __launch_bounds__(256) k_trtri_leaf(int n, const double* __restrict__ Lm, double* __restrict__ Li) {
-    extern __shared__ double tsm[];  // sL[64][65], sX[64][65], rd[64]
-    double(*sL)[65] = reinterpret_cast<double(*)[65]>(tsm);
-    double(*sX)[65] = reinterpret_cast<double(*)[65]>(tsm + 64 * 65);
-    double* rd = tsm + 2 * 64 * 65;
-    const int b0 = blockIdx.x * 64, m = min(64, n - b0);
-    for (int idx = threadIdx.x; idx < 64 * 64; idx += blockDim.x) {
-        const int r = idx % 64, c = idx / 64;
-        sL[r][c] = (r < m && c < m && r >= c) ? Lm[static_cast<size_t>(b0 + c) * n + b0 + r] : 0.0;
-        sX[r][c] = 0.0;
-    }
-    if (threadIdx.x < 64) rd[threadIdx.x] = threadIdx.x < m ? 1.0 / Lm[static_cast<size_t>(b0 + threadIdx.x) * n + b0 + threadIdx.x] : 0.0;
-    __syncthreads();
-    const int j = threadIdx.x >> 2, q = threadIdx.x & 3;
-    for (int i = 0; i < m; ++i) {
-        double s0 = 0.0, s1 = 0.0;
-        int k = q;
-        for (; k + 4 < i; k += 8) {
-            s0 = fma(sL[i][k], sX[k][j], s0);
-            s1 = fma(sL[i][k + 4], sX[k + 4][j], s1);
-        }
-        if (k < i) s0 = fma(sL[i][k], sX[k][j], s0);
-        double t = s0 + s1;
-        t += __shfl_xor_sync(0xffffffffu, t, 1);
-        t += __shfl_xor_sync(0xffffffffu, t, 2);
-        if (q == 0 && i >= j) sX[i][j] = ((i == j ? 1.0 : 0.0) - t) * rd[i];
-        __syncwarp();
-    }
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
-        const int r = idx % m, c = idx / m;
-        Li[static_cast<size_t>(b0 + c) * n + b0 + r] = sX[r][c];
-    }
-}
-
-void launch_trtri_leaf(const Launch& L, int n, const double* Lm, double* Li) {
-    const int smem = static_cast<int>(sizeof(double) * (2 * 64 * 65 + 64));
-    static bool attr = false;
-    if (!attr) {
-        LT_CU(cudaFuncSetAttribute(k_trtri_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr = true;
-    }
-    Stage st_(L, "trtri_leaf");
-    k_trtri_leaf<<<static_cast<unsigned>((n + 63) / 64), 256, smem, L.st>>>(n, Lm, Li);
-    LT_CU(cudaGetLastError());
-    L.tick();
-}
-
-void launch_symmetrize(const Launch& L, int n, double* A) {
-    const unsigned t = static_cast<unsigned>((n + 31) / 32);
-    Stage st_(L, "symmetrize");
-    k_symmetrize<<<dim3(t, t), dim3(32, 8), 0, L.st>>>(n, A);
     LT_CU(cudaGetLastError());
     L.tick();
 }

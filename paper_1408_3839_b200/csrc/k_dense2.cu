@@ -22,15 +22,6 @@ namespace lt {
 
 constexpr int kLeaf = 64;
 
-__device__ __forceinline__ double leaf_rcp(double q) {  // 1/q within an ulp: MUFU seed + 2 Newton steps
-    double r;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
-    double t = fma(-q, r, 1.0);
-    r = fma(r, t, r);
-    t = fma(-q, r, 1.0);
-    return fma(r, t, r);
-}
-
 __device__ __forceinline__ double leaf_rsqrt(double x) {  // 1/sqrt(x) within an ulp
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));

@@ -20,7 +20,6 @@
 #include "dmma.cuh"
 #include "lt_device.cuh"
 #include "lt_internal.cuh"
-#include "tma.cuh"
 
 namespace lt {
 
@@ -229,123 +228,6 @@ __global__ void __launch_bounds__(256) k_triv_gemm(TrivJobs jobs, int m0, int Rt
         }
 }
 
-// TMA-fed variant of the long-K trivial-direction GEMM: per 32-deep stage one thread issues
-// cp.async.bulk.tensor loads of the potential tile P[r0 .. r0+64][k .. k+32] and of the
-// profile tile g[0 .. m0][k .. k+32] (two SWIZZLE_128B boxes of 16 columns each) into a
-// kTrivTmaStages ring signalled by mbarriers (complete_tx); the CTA forms the pair-product tile
-// b(k, n) = g_mu(k) g_nu(k) from the landed profile stage and runs m16n8k4 DMMA with the
-// potential stage as the A operand. Out-of-range rows read as zero (TMA bounds); columns past
-// the split's K range are zeroed in the product tile.
-constexpr int kTrivTmaStages = 4;
-struct TrivTmaMaps {
-    CUtensorMap P[3];
-    CUtensorMap g[3];
-};
-
-__global__ void __launch_bounds__(256) k_triv_gemm_tma(const __grid_constant__ TrivTmaMaps maps, TrivJobs jobs, int m0,
-                                                       int Rtot, int nsym, int splits, double* __restrict__ part) {
-    constexpr int TK = kTrivTK, NST = kTrivTmaStages, TLB = kGBN + 8;
-    constexpr int ABOX = kGBM * 16, GBOX = 32 * 16;           // doubles per box (A: 64 rows, g: 32 rows)
-    constexpr int STAGE = 2 * ABOX + 2 * GBOX;                 // A (2 boxes) + g (2 boxes)
-    extern __shared__ __align__(1024) unsigned char tt_raw[];
-    double* st0 = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(tt_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-    double* Bs = st0 + NST * STAGE;                            // [TK][TLB]
-    __shared__ __align__(8) uint64_t full[NST];
-    __shared__ long long sk[2];
-    const int job = blockIdx.z / splits, split = blockIdx.z % splits;
-    const TrivJob& J = jobs.j[job];
-    const CUtensorMap* mP = job == 0 ? &maps.P[0] : (job == 1 ? &maps.P[1] : &maps.P[2]);
-    const CUtensorMap* mg = job == 0 ? &maps.g[0] : (job == 1 ? &maps.g[1] : &maps.g[2]);
-    const int r0 = blockIdx.x * kGBM, e0 = blockIdx.y * kGBN;
-    const int tid = threadIdx.x;
-    if (tid < 32) {
-        long long lo = J.G, hi = 0;
-        for (int m = tid; m < m0; m += 32) {
-            lo = min(lo, static_cast<long long>(J.lo[m]));
-            hi = max(hi, static_cast<long long>(J.hi[m]));
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-        }
-        if (tid == 0) {
-            sk[0] = lo;
-            sk[1] = hi;
-            for (int q = 0; q < NST; ++q) mbar_init(&full[q], 1);
-            mbar_fence_init();
-        }
-    }
-    __syncthreads();
-    const long long klo = sk[0];
-    const long long khi = min(sk[1], static_cast<long long>(J.rows));
-    const long long len = khi > klo ? khi - klo : 0;
-    const long long per = ((len + splits - 1) / splits + TK - 1) / TK * TK;
-    const long long k0 = klo + split * per, k1 = min(khi, k0 + per);
-    const int nk = k1 > k0 ? static_cast<int>((k1 - k0 + TK - 1) / TK) : 0;
-    // a box always lands whole (out-of-bounds rows / columns zero-filled): full byte count
-    constexpr unsigned bytes = static_cast<unsigned>(sizeof(double)) * STAGE;
-    auto issue = [&](int it) {
-        double* sa = st0 + (it % NST) * STAGE;
-        double* sg = sa + 2 * ABOX;
-        uint64_t* bar = &full[it % NST];
-        const int kc = static_cast<int>(k0 + static_cast<long long>(it) * TK);
-        mbar_arrive_expect_tx(bar, bytes);
-        tma_load_2d(sa, mP, bar, kc, r0);
-        tma_load_2d(sa + ABOX, mP, bar, kc + 16, r0);
-        tma_load_2d(sg, mg, bar, kc, 0);
-        tma_load_2d(sg + GBOX, mg, bar, kc + 16, 0);
-    };
-    if (tid == 0) {
-        tma_prefetch_desc(mP);
-        tma_prefetch_desc(mg);
-        for (int it = 0; it < NST && it < nk; ++it) issue(it);
-    }
-    const int warp = tid >> 5, lane = tid & 31;
-    const int wm = warp & 3, wn = warp >> 2, gg = lane >> 2, tq = lane & 3;
-    const int bn = tid & 63, bk0 = tid >> 6;
-    const bool bok = e0 + bn < nsym;
-    int pmu = 0, pnu = 0;
-    if (bok) sym_pair(e0 + bn, m0, pmu, pnu);
-    double acc[4][4] = {};
-    for (int it = 0; it < nk; ++it) {
-        const int s = it % NST;
-        mbar_wait(&full[s], (it / NST) & 1);
-        const double* sa = st0 + s * STAGE;
-        const double* sg = sa + 2 * ABOX;
-        const long long kb = k0 + static_cast<long long>(it) * TK;
-        // product tile (k columns past the split's range are zero)
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int k = bk0 + 4 * u;
-            const double* gb = sg + (k >> 4) * GBOX;
-            const int kk = k & 15;
-            Bs[k * TLB + bn] = (bok && kb + k < k1) ? gb[swz128(pmu, kk)] * gb[swz128(pnu, kk)] : 0.0;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int ks = 0; ks < TK; ks += 4) {
-            const double* ab = sa + (ks >> 4) * ABOX;
-            const int kk = (ks & 15) + tq;
-            const double a0 = ab[swz128(wm * 16 + gg, kk)];
-            const double a1 = ab[swz128(wm * 16 + gg + 8, kk)];
-#pragma unroll
-            for (int nt = 0; nt < 4; ++nt)
-                dmma_m16n8k4(acc[nt], a0, a1, Bs[(ks + tq) * TLB + wn * 32 + nt * 8 + gg]);
-        }
-        __syncthreads();  // stage s and the product tile are free again
-        if (tid == 0 && it + NST < nk) issue(it + NST);
-    }
-    double* out = part + (static_cast<long long>(job) * splits + split) * Rtot * nsym;
-#pragma unroll
-    for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            int m, n;
-            acc_coord(nt, i, m, n);
-            if (r0 + m < Rtot && e0 + n < nsym) out[(r0 + m) * nsym + e0 + n] = acc[nt][i];
-        }
-}
-
 // W[r][e] = w_r * prod over trivial directions of T_l[r][e] (T_l reduced over splits in
 // fixed order); e over all m0^2 ordered pairs (mirror of the symmetric index)
 __device__ __forceinline__ void triv_finish(const double (&tj)[3], int njobs, const WSpec& ws, int m0, int Rtot, int r,
@@ -438,28 +320,8 @@ void launch_triv_tables(const Launch& L, const TrivJobs& jobs, int njobs, const 
                                        smem_of(kTrivStages)));
             attr = true;
         }
-        // TMA path: long K per CTA, materialised panels with 16-byte row pitches, m0 <= 32
-        bool tma = async && m0 <= 32;
-        for (int j = 0; j < njobs && tma; ++j)
-            tma = jobs.j[j].pot && (jobs.j[j].rows * 8) % 16 == 0 && (jobs.j[j].G * 8) % 16 == 0 &&
-                  (reinterpret_cast<uintptr_t>(jobs.j[j].pot) & 15) == 0 && (reinterpret_cast<uintptr_t>(jobs.j[j].pwc) & 15) == 0;
         Stage st_(L, "triv_gemm");
-        if (tma) {
-            TrivTmaMaps maps;
-            for (int j = 0; j < 3; ++j) {
-                const TrivJob& J = jobs.j[j < njobs ? j : 0];
-                maps.P[j] = tma_map_2d(J.pot, Rtot, J.rows, J.rows, kGBM);
-                maps.g[j] = tma_map_2d(J.pwc, m0, J.G, J.G, 32);
-            }
-            const int smem = static_cast<int>(sizeof(double)) *
-                                 (kTrivTmaStages * (2 * kGBM * 16 + 2 * 32 * 16) + kTrivTK * (kGBN + 8)) + 1024;
-            static bool attr_t = false;
-            if (!attr_t) {
-                LT_CU(cudaFuncSetAttribute(k_triv_gemm_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-                attr_t = true;
-            }
-            k_triv_gemm_tma<<<grid, 256, smem, L.st>>>(maps, jobs, m0, Rtot, nsym, splits, part);
-        } else if (async) {
+        if (async) {
             k_triv_gemm<true><<<grid, 256, smem_of(kTrivStages), L.st>>>(jobs, m0, Rtot, nsym, splits, part);
         } else {
             k_triv_gemm<false><<<grid, 256, smem_of(1), L.st>>>(jobs, m0, Rtot, nsym, splits, part);

@@ -524,8 +524,6 @@ void dense_back_transform(const Launch& L, int n, long long ld, const double* Li
 int sytrd_ctas(int n);
 void launch_sytrd(const Launch& L, int n, const double* C, double* d, double* e, double* work, unsigned* bar);
 void launch_tridiag_eig(const Launch& L, int n, const double* d, const double* e, double* eig);
-void launch_symmetrize(const Launch& L, int n, double* A);
-void launch_trtri_leaf(const Launch& L, int n, const double* Lm, double* Li);
 // full-space eigenvector columns [c0, c0 + ncols) from the per-k blocks u (K m0 x m0 complex)
 void launch_reconstruct(const Launch& L, const Index* dims, Index m0, const double2* u, Index c0, Index ncols,
                         double2* out);
