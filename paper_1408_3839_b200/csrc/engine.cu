@@ -1342,31 +1342,49 @@ static void box_eig_device(lt_ctx* c, Index n, double* H, double* S, double* eig
         box_eig_tridiag(c, n, H, S, eig_dev, fail_dev);
         return;
     }
+    // eigenvectors (want_vectors) or N_b beyond the on-chip tridiagonalisation: the same device
+    // reduction A = L^-1 H L^-T (k_dense2.cu), the standard symmetric eigenproblem of A by the
+    // library (cusolverDnDsyevd), then the back-transform X = L^-T Z on DMMA (eigensolver.cpp:
+    // 29-32: llt.matrixU().solve(Z)); X^T S X = I.
+    box_factor(c, L, n, S, fail_dev);
+    box_transform(c, L, n, H, fail_dev);
+    unsigned long long fkey = ~0ull;
+    LT_CU(cudaMemcpyAsync(&fkey, fail_dev, sizeof(fkey), cudaMemcpyDeviceToHost, c->stream));
+    LT_CU(cudaStreamSynchronize(c->stream));
+    if (fkey != ~0ull)
+        fail(LT_EDEFINITE, "solve_box_dense: overlap matrix is not positive definite (near-linear-dependent basis?)");
     if (!c->solver) {
         if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS) fail(LT_ECUDA, "cusolverDnCreate failed");
     }
     cusolverDnSetStream(c->solver, c->stream);
     const cusolverEigMode_t mode = vec_dev ? CUSOLVER_EIG_MODE_VECTOR : CUSOLVER_EIG_MODE_NOVECTOR;
+    const int ni = static_cast<int>(n);
     int lwork = 0;
-    if (cusolverDnDsygvd_bufferSize(c->solver, CUSOLVER_EIG_TYPE_1, mode, CUBLAS_FILL_MODE_LOWER, static_cast<int>(n), H,
-                                    static_cast<int>(n), S, static_cast<int>(n), eig_dev,
-                                    &lwork) != CUSOLVER_STATUS_SUCCESS)
-        fail(LT_ECUDA, "cusolverDnDsygvd_bufferSize failed");
+    if (cusolverDnDsyevd_bufferSize(c->solver, mode, CUBLAS_FILL_MODE_LOWER, ni, H, ni, eig_dev, &lwork) !=
+        CUSOLVER_STATUS_SUCCESS)
+        fail(LT_ECUDA, "cusolverDnDsyevd_bufferSize failed");
     double* work = c->arena.get<double>("box.work", static_cast<size_t>(lwork) + 1);
     int* info = c->arena.get<int>("box.info", 1);
-    Stage st_(L, "sygvd");
-    if (cusolverDnDsygvd(c->solver, CUSOLVER_EIG_TYPE_1, mode, CUBLAS_FILL_MODE_LOWER, static_cast<int>(n), H,
-                         static_cast<int>(n), S, static_cast<int>(n), eig_dev, work, lwork,
-                         info) != CUSOLVER_STATUS_SUCCESS)
-        fail(LT_ECUDA, "cusolverDnDsygvd failed");
-    // map info > n (leading minor of S not positive) onto the failure key
+    {
+        Stage st_(L, "syevd");
+        if (cusolverDnDsyevd(c->solver, mode, CUBLAS_FILL_MODE_LOWER, ni, H, ni, eig_dev, work, lwork, info) !=
+            CUSOLVER_STATUS_SUCCESS)
+            fail(LT_ECUDA, "cusolverDnDsyevd failed");
+    }
     int hinfo = 0;
     LT_CU(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     LT_CU(cudaStreamSynchronize(c->stream));
-    if (hinfo > n) fail(LT_EDEFINITE, "solve_box_dense: overlap matrix is not positive definite (near-linear-dependent basis?)");
     if (hinfo != 0) fail(LT_EGENERIC, "solve_box_dense: eigensolver failed");
-    if (vec_dev)  // sygvd leaves the eigenvectors (X^T S X = I) in H
-        LT_CU(cudaMemcpyAsync(vec_dev, H, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, c->stream));
+    if (!vec_dev) return;
+    long long ld = 0;
+    const DenseReduceBufs b = box_bufs(c, n, &ld);
+    if (ld == n) {
+        dense_back_transform(L, ni, ld, b.Lic, H, vec_dev, fail_dev);
+    } else {  // odd n: TMA row pitches on padded copies
+        pad_copy(L, ni, n, H, ld, b.W);
+        dense_back_transform(L, ni, ld, b.Lic, b.W, b.T, fail_dev);
+        pad_copy(L, ni, ld, b.T, n, vec_dev);
+    }
 }
 
 // graph-cache key: everything the captured launches bake in (host-derived parameters of
