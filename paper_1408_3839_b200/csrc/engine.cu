@@ -1129,7 +1129,10 @@ static DftPrep prepare_dft(lt_ctx* c, const Index dims[3], Index m0, const std::
 
 // device part (kernels only: capturable). Transforms nops operators that share the
 // stored kidx (blocks[op] on device, std::map order); out[op] receives [K][mm] complex.
-static void launch_dft(lt_ctx* c, const DftPrep& P, int nops, const double* const* blocks, double2** out) {
+// With want_emajor, the fused multi-axis launch writes [mm][K] instead (entry-major, for the
+// one-thread-per-pencil kernel); returns whether it did.
+static bool launch_dft(lt_ctx* c, const DftPrep& P, int nops, const double* const* blocks, double2** out,
+                       bool want_emajor = false) {
     const Launch L = c->L();
     const Index mm = P.m0 * P.m0;
     double2* buf[2][2];
@@ -1155,8 +1158,9 @@ static void launch_dft(lt_ctx* c, const DftPrep& P, int nops, const double* cons
                 f.gen[op] = blocks[op];
                 f.out[op] = out[op] = buf[op][1];
             }
+            f.emajor = want_emajor ? 1 : 0;
             launch_dft_fused(L, f, nops);
-            return;
+            return want_emajor;
         }
     }
     DftAxisArgs a;
@@ -1198,6 +1202,7 @@ static void launch_dft(lt_ctx* c, const DftPrep& P, int nops, const double* cons
         cur = 1;
     }
     for (int op = 0; op < nops; ++op) out[op] = buf[op][cur];
+    return false;
 }
 
 static double2* block_diag_device(lt_ctx* c, const Index dims[3], Index m0,
@@ -1557,12 +1562,23 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
             } else {
                 const double* blocks[2] = {out.out0, out.out1};
                 double2* bd[2];
-                launch_dft(c, dp, 2, blocks, bd);
+                const Index nk = k_end - k_begin;
+                // the kernel choice depends on the whole lattice (not the shard): every k-point
+                // shard then reproduces the full solve bitwise
+                const bool lane = pencil_lane_supported(p.m0) &&
+                                  dp.dims[0] * dp.dims[1] * dp.dims[2] >= kPencilLaneMin;
+                const bool emajor = launch_dft(c, dp, 2, blocks, bd, lane);
                 double2* Hb = bd[0];
                 double2* Sb = bd[1];
-                if (k_begin < k_end)
-                    launch_pencil(c->L(), k_end - k_begin, p.m0, Hb + k_begin * mm, Sb + k_begin * mm,
+                if (lane && nk > 0) {
+                    const Index K = dp.dims[0] * dp.dims[1] * dp.dims[2];
+                    launch_pencil_lane(c->L(), nk, p.m0, Hb + k_begin * (emajor ? 1 : mm),
+                                       Sb + k_begin * (emajor ? 1 : mm), emajor ? 1 : mm, emajor ? K : 1,
+                                       eig_out + k_begin * p.m0, fk, rb);
+                } else if (!lane && nk > 0) {
+                    launch_pencil(c->L(), nk, p.m0, Hb + k_begin * mm, Sb + k_begin * mm,
                                   eig_out + k_begin * p.m0, fk, true, PencilDft{}, nullptr, rb);
+                }
             }
         } else if (box_split) {
             box_transform(c, c->L(), p.Nb, out.out0, fk);

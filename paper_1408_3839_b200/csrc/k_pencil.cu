@@ -339,18 +339,6 @@ __device__ void pencil_vectors(PSmem<NM>& sm, int n, int t, int slot, Index k, d
 
 }  // namespace
 
-// called once per finished pencil by its group leader (every exit path)
-__device__ __forceinline__ void group_done(const PencilReadback& rb, Index count) {
-    if (rb.done == nullptr) return;
-    __threadfence();  // this group's failure key update before its arrival
-    if (atomicAdd(rb.done, 1u) == static_cast<unsigned>(count - 1)) {
-        __threadfence();
-        const volatile int* src = rb.ret_dev;
-        for (int i = 0; i < 8; ++i) rb.ret_host[i] = src[i];
-        *rb.done = 0u;  // ready for the next launch or graph replay
-    }
-}
-
 // Threads of a group own matrix entries e = t + G*u (row e % NM, column e / NM); the
 // Householder mat-vec uses TPR = G / NM threads per row.
 template <int NM, int G, int BS, bool VEC, bool RE = false>

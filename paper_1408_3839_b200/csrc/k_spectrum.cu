@@ -113,7 +113,7 @@ void launch_dft_axis2(const Launch& L, const DftAxisArgs& a, int nops) {
 template <int AX>
 __device__ __forceinline__ void dft_pass(unsigned& n0, unsigned& n1, unsigned& n2, unsigned L, unsigned nc,
                                          const double2* __restrict__ t, const double2* in, double2* outs,
-                                         double2* __restrict__ outg, Index mm, Index e) {
+                                         double2* __restrict__ outg, Index sq, Index oe) {
     constexpr unsigned JT = 8;
     const unsigned o0 = AX == 0 ? L : n0, o1 = AX == 1 ? L : n1, o2 = AX == 2 ? L : n2;
     const unsigned uext = AX == 0 ? n1 : n0, wext = AX == 2 ? n1 : n2;
@@ -149,7 +149,7 @@ __device__ __forceinline__ void dft_pass(unsigned& n0, unsigned& n1, unsigned& n
         for (unsigned jj = 0; jj < JT; ++jj) {
             if (j0 + jj >= L) break;
             const unsigned q = bout + (j0 + jj) * sout;
-            if (outg) outg[static_cast<Index>(q) * mm + e] = acc[jj];
+            if (outg) outg[static_cast<Index>(q) * sq + oe] = acc[jj];
             else outs[q] = acc[jj];
         }
     }
@@ -165,7 +165,7 @@ __device__ __forceinline__ void dft_pass(unsigned& n0, unsigned& n1, unsigned& n
 template <int AX, int LOG>
 __device__ __forceinline__ void fft_pass(unsigned& n0, unsigned& n1, unsigned& n2, const int* __restrict__ cmap,
                                          const double2* __restrict__ tw, const double2* in, double2* outs,
-                                         double2* __restrict__ outg, Index mm, Index e) {
+                                         double2* __restrict__ outg, Index sq, Index oe) {
     constexpr unsigned L = 1u << LOG;
     const unsigned o0 = AX == 0 ? L : n0, o1 = AX == 1 ? L : n1, o2 = AX == 2 ? L : n2;
     const unsigned uext = AX == 0 ? n1 : n0, wext = AX == 2 ? n1 : n2;
@@ -211,7 +211,7 @@ __device__ __forceinline__ void fft_pass(unsigned& n0, unsigned& n1, unsigned& n
 #pragma unroll
             for (int bit = 0; bit < LOG; ++bit) r |= ((j >> bit) & 1u) << (LOG - 1 - bit);
             const unsigned q = bout + j * sout;
-            if (outg) outg[static_cast<Index>(q) * mm + e] = x[r];
+            if (outg) outg[static_cast<Index>(q) * sq + oe] = x[r];
             else outs[q] = x[r];
         }
     }
@@ -225,6 +225,9 @@ __global__ void __launch_bounds__(512) k_dft_fused(DftFusedArgs a) {
     const Index e = blockIdx.x;
     const int op = blockIdx.y;
     const Index mm = a.mm;
+    // output element (k, e): k-major [K][mm] (q mm + e), or entry-major [mm][K] (e K + q)
+    const Index osq = a.emajor ? 1 : mm;
+    const Index ooe = a.emajor ? e * (a.dims[0] * a.dims[1] * a.dims[2]) : e;
     // per wrapped axis in pass order: DFT twiddles (L x nc), or for power-of-two L <= 16 the
     // FFT twiddles (L/2) and the position -> compressed-index map (L ints, 8-byte slots);
     // then two cube buffers
@@ -298,9 +301,9 @@ __global__ void __launch_bounds__(512) k_dft_fused(DftFusedArgs a) {
             const int* cm = reinterpret_cast<const int*>(t + L / 2);
 #define LT_FFT_CASE(LG)                                                                            \
     case LG:                                                                                       \
-        if (ax == 0) fft_pass<0, LG>(n0, n1, n2, cm, t, cur, nxt, og, mm, e);                      \
-        else if (ax == 1) fft_pass<1, LG>(n0, n1, n2, cm, t, cur, nxt, og, mm, e);                 \
-        else fft_pass<2, LG>(n0, n1, n2, cm, t, cur, nxt, og, mm, e);                              \
+        if (ax == 0) fft_pass<0, LG>(n0, n1, n2, cm, t, cur, nxt, og, osq, ooe);                      \
+        else if (ax == 1) fft_pass<1, LG>(n0, n1, n2, cm, t, cur, nxt, og, osq, ooe);                 \
+        else fft_pass<2, LG>(n0, n1, n2, cm, t, cur, nxt, og, osq, ooe);                              \
         break;
             switch (lg) {
                 LT_FFT_CASE(1)
@@ -311,9 +314,9 @@ __global__ void __launch_bounds__(512) k_dft_fused(DftFusedArgs a) {
 #undef LT_FFT_CASE
             t += L / 2 + L;
         } else {
-            if (ax == 0) dft_pass<0>(n0, n1, n2, L, nc, t, cur, nxt, og, mm, e);
-            else if (ax == 1) dft_pass<1>(n0, n1, n2, L, nc, t, cur, nxt, og, mm, e);
-            else dft_pass<2>(n0, n1, n2, L, nc, t, cur, nxt, og, mm, e);
+            if (ax == 0) dft_pass<0>(n0, n1, n2, L, nc, t, cur, nxt, og, osq, ooe);
+            else if (ax == 1) dft_pass<1>(n0, n1, n2, L, nc, t, cur, nxt, og, osq, ooe);
+            else dft_pass<2>(n0, n1, n2, L, nc, t, cur, nxt, og, osq, ooe);
             t += L * nc;
         }
         double2* tmp = cur;

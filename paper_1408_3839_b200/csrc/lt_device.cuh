@@ -171,4 +171,18 @@ __device__ __forceinline__ void sturm3(const double* sd, const double* se2, int 
     for (; i < n; ++i) step(sd[i], se2[i - 1]);
 }
 
+// pencil kernels: called once per finished group (a group of threads per pencil, or a
+// warp of one-thread pencils) by its leader on every exit path; the last of `count` groups
+// copies the 8-int result block (L0 state, failure key) to pinned host memory
+__device__ __forceinline__ void group_done(const PencilReadback& rb, Index count) {
+    if (rb.done == nullptr) return;
+    __threadfence();  // this group's failure key update before its arrival
+    if (atomicAdd(rb.done, 1u) == static_cast<unsigned>(count - 1)) {
+        __threadfence();
+        const volatile int* src = rb.ret_dev;
+        for (int i = 0; i < 8; ++i) rb.ret_host[i] = src[i];
+        *rb.done = 0u;  // ready for the next launch or graph replay
+    }
+}
+
 }  // namespace lt

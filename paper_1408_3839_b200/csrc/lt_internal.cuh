@@ -450,6 +450,7 @@ struct DftFusedArgs {
     const int* slot2blk = nullptr;
     const double* gen[2] = {nullptr, nullptr};
     double2* out[2] = {nullptr, nullptr};
+    int emajor = 0;  // 1: out [mm][K] (entry-major, for the one-thread-per-pencil kernel)
 };
 // log2 L for the register FFT of power-of-two axes 2 <= L <= 16 (0: DFT pass); LT_DFT_NO_FFT
 // at compile time forces the DFT pass
@@ -554,6 +555,13 @@ void launch_pencil(const Launch& L, Index count, Index m0, const double2* H, con
                    unsigned long long* fail_key, bool periodic_checks, const PencilDft& dft = PencilDft{},
                    double2* vec = nullptr,  // vec: K m0 x m0 complex eigenvector blocks (vector mode)
                    const PencilReadback& rb = PencilReadback{}, bool real = false);
+
+// one thread per 8 x 8 pencil (k_pencil_lane.cu): blocks at H[k ks + e es], e = r + c m0
+bool pencil_lane_supported(Index m0);
+size_t pencil_lane_smem();
+constexpr Index kPencilLaneMin = 256;  // lattices below: the group-per-pencil kernel (DFT fused into its load)
+void launch_pencil_lane(const Launch& L, Index count, Index m0, const double2* H, const double2* S, Index ks, Index es,
+                        double* eig, unsigned long long* fail_key, const PencilReadback& rb = PencilReadback{});
 
 // combine (eigensolver.cpp:37-67) on device buffers with index maps
 void launch_axpby_map(const Launch& L, Index nout, Index mm, double wa, const double* a, const int64_t* ia, double wb,
