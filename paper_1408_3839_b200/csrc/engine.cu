@@ -187,7 +187,7 @@ struct lt_ctx {
     // side streams for independent branches of the assembly (captured into the same graph
     // as parallel branches) and the fork/join events between them
     cudaStream_t aux[3]{nullptr, nullptr, nullptr};  // 0, 1: assembly branches; 2: L0 check under speculation
-    cudaEvent_t ev[9]{};  // fork/join points of run_assembly (0-5), the L0 branch (6-7), external streams (8)
+    cudaEvent_t ev[11]{};  // fork/join points of run_assembly (0-5, 9-10), the L0 branch (6-7), external streams (8)
     // pinned staging for the small per-call host<->device copies (system, window starts,
     // DFT index maps, eigenvalue read-back): async copies instead of pageable round trips.
     // Valid between stage_begin() (stream idle) and the end of the API call.
@@ -318,6 +318,10 @@ static void run_cached(lt_ctx* c, GraphCache& g, K&& keyfn, F&& enqueue) {
         c->timer.owned = nullptr;
         LT_CU(cudaStreamEndCapture(c->stream, &graph));
         g.timing = c->timer.take_pending(p0);
+        if (const char* dp = std::getenv("LT_GRAPH_DOT")) {
+            static int ndot = 0;
+            cudaGraphDebugDotPrint(graph, (std::string(dp) + std::to_string(ndot++) + ".dot").c_str(), cudaGraphDebugDotFlagsVerbose);
+        }
         const cudaError_t e = cudaGraphInstantiate(&g.exec, graph, 0);
         cudaGraphDestroy(graph);
         LT_CU(e);
@@ -657,7 +661,8 @@ static void support_window(const HostSys& s, const Plan& p, int l, bool pwl, lon
 
 static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need, int mode, AsmOut out,
                          Work* wout = nullptr, const int64_t* s0_dev = nullptr, unsigned flags = 0,
-                         const CoreShard& shard = CoreShard{}, const BranchHook* s_hook = nullptr) {
+                         const CoreShard& shard = CoreShard{}, const BranchHook* s_hook = nullptr,
+                         const BranchHook* root_hook = nullptr) {
     // Three concurrent branches (parallel branches of the captured graph):
     //   main   : sinc -> potential of the 1st, 3rd distinct direction -> nuclear -> fill
     //   aux[1] : potential of the 2nd distinct direction (joins main before the nuclear part)
@@ -681,51 +686,13 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
     const int64_t* s0d = nullptr;
     const bool nuc = need & NEED_NUC, ms = need & NEED_MS;
     if (nuc) s0d = s0_dev ? s0_dev : upload_s0(c, p);
-    c->join(0, c->stream, c->aux[fi]);
-    c->join(1, c->stream, c->aux[pi]);
     // Trivial-direction panels could be evaluated inside k_triv_gemm (TrivJob.pot = null):
     // measured slower (erf pairs in the GEMM loader, repeated per N tile), so every panel is
     // materialised by the master-free window kernels.
     constexpr bool fused_nuc = false;
-    w.t = A.get<double>("sinc.t", RN);
-    w.w = A.get<double>("sinc.w", RN);
-    w.potw = A.get<double>("sinc.potw", Rtot);
-    // nodes and weights Z_v w_q on the side branch: the master kernels evaluate their nodes
-    // in place, the weights are first needed after the join before the nuclear part
-    launch_sinc(LP, p.M, sd->ds, w.t, w.w, w.potw, shard.r0, shard.r1);
-    if (nuc) {
-        int nth = 0;
-        for (int l = 0; l < 3; ++l) {
-            if (src[l] != l) {
-                w.pot[l] = w.pot[src[l]];
-                continue;
-            }
-            const DirPlan& d = p.d[l];
-            if (fused_nuc && d.L == 1) {  // consumed by k_triv_gemm straight from the master cells
-                w.pot[l] = nullptr;
-                continue;
-            }
-            const Launch& LL = (nth++ == 1) ? LP : L;
-            w.pot[l] = A.get<double>("pot.panel" + std::to_string(l), d.pot_rows * Rtot);
-            if ((d.nsum == 1 && p.nnuc == 1) || (d.nsum >= 32 && d.pot_rows <= d.n && p.nnuc <= 2)) {
-                // a single window copy of one nucleus: each master cell is read once, so it
-                // is evaluated in the copy kernel instead of being materialised first. The
-                // periodic cell window (one output per residue class) of <= 2 nuclei reads each
-                // cell at most twice: evaluating in place costs less than a serial master node
-                launch_potential_fused(LL, d.mrows, d.h, p.M, RN, p.nnuc, s0d + l * p.nnuc, d.nsum, d.n,
-                                       d.pot_rows, w.pot[l]);
-            } else {
-                // the master panel once (massively parallel), then the windows read it: a cell
-                // serves every nucleus and, for lattice sums, two running-sum updates
-                double* master = A.get<double>("pot.master" + std::to_string(l), d.mrows * RN);
-                launch_master(LL, d.mrows, d.h, RN, nullptr, master, p.M);
-                launch_window_sum(LL, master, d.mrows, RN, p.nnuc, s0d + l * p.nnuc, d.nsum, d.n, d.pot_rows,
-                                  w.pot[l]);
-            }
-        }
-    }
-    c->join(2, c->aux[pi], c->stream);
-    // profiles (galerkin.cpp:127-149), distinct directions only
+    // profiles (galerkin.cpp:127-149), distinct directions only. Every branch forks after one
+    // root kernel: measured on B200, a second root branch of this graph starts 7-11 us late
+    // (whichever is captured second), a branch forked after the root does not
     ProfileJob jobs[6];
     int nj = 0;
     for (int l = 0; l < 3; ++l) {
@@ -767,7 +734,57 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
             w.pwl_lo[l] = w.pwl_lo[src[l]];
             w.pwl_hi[l] = w.pwl_hi[src[l]];
         }
-    launch_profiles(LF, sd->ds, jobs, nj, 1e-280);
+    w.t = A.get<double>("sinc.t", RN);
+    w.w = A.get<double>("sinc.w", RN);
+    w.potw = A.get<double>("sinc.potw", Rtot);
+    // nodes and weights Z_v w_q: the graph's single root (the master kernels evaluate their
+    // nodes in place; the weights are first needed by the nuclear part)
+    // The graph's single root heads the longer chain: lattices with several wrapped axes spend
+    // longest in the FEM folds and the per-axis nuclear folds, both behind the profiles (c5:
+    // 148 vs 160 us with the sinc first); otherwise the potentials' masters are the long head
+    // (c4: 238 vs 250 us with the profiles first). Measured on B200 (tools/ab.sh).
+    int nwrap = 0;
+    for (int l = 0; l < 3; ++l) nwrap += p.d[l].L > 1;
+    const bool prof_root = p.periodic && nwrap >= 2;
+    if (prof_root) launch_profiles(L, sd->ds, jobs, nj, 1e-280);
+    else launch_sinc(L, p.M, sd->ds, w.t, w.w, w.potw, shard.r0, shard.r1);
+    c->join(0, c->stream, c->aux[fi]);
+    c->join(1, c->stream, c->aux[pi]);
+    if (root_hook) (*root_hook)(L);  // the L0 check under speculation: its own branch
+    if (prof_root) launch_sinc(LP, p.M, sd->ds, w.t, w.w, w.potw, shard.r0, shard.r1);
+    else launch_profiles(LF, sd->ds, jobs, nj, 1e-280);
+    if (nuc) {
+        int nth = 0;
+        for (int l = 0; l < 3; ++l) {
+            if (src[l] != l) {
+                w.pot[l] = w.pot[src[l]];
+                continue;
+            }
+            const DirPlan& d = p.d[l];
+            if (fused_nuc && d.L == 1) {  // consumed by k_triv_gemm straight from the master cells
+                w.pot[l] = nullptr;
+                continue;
+            }
+            const Launch& LL = (nth++ == 1) ? LP : L;
+            w.pot[l] = A.get<double>("pot.panel" + std::to_string(l), d.pot_rows * Rtot);
+            if ((d.nsum == 1 && p.nnuc == 1) || (d.nsum >= 32 && d.pot_rows <= d.n && p.nnuc <= 2)) {
+                // a single window copy of one nucleus: each master cell is read once, so it
+                // is evaluated in the copy kernel instead of being materialised first. The
+                // periodic cell window (one output per residue class) of <= 2 nuclei reads each
+                // cell at most twice: evaluating in place costs less than a serial master node
+                launch_potential_fused(LL, d.mrows, d.h, p.M, RN, p.nnuc, s0d + l * p.nnuc, d.nsum, d.n,
+                                       d.pot_rows, w.pot[l]);
+            } else {
+                // the master panel once (massively parallel), then the windows read it: a cell
+                // serves every nucleus and, for lattice sums, two running-sum updates
+                double* master = A.get<double>("pot.master" + std::to_string(l), d.mrows * RN);
+                launch_master(LL, d.mrows, d.h, RN, nullptr, master, p.M);
+                launch_window_sum(LL, master, d.mrows, RN, p.nnuc, s0d + l * p.nnuc, d.nsum, d.n, d.pot_rows,
+                                  w.pot[l]);
+            }
+        }
+    }
+    c->join(2, c->aux[pi], c->stream);
     c->join(3, c->aux[fi], c->stream);  // nuclear part needs the profiles
     if (ms) {
         // FEM-applied profiles (T v) for every distinct direction, then the tables as
@@ -940,12 +957,20 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
                 kr.Rtot = static_cast<int>(Rtot);
                 kr.W = W;
                 double* Tl[3] = {nullptr, nullptr, nullptr};
+                // the per-direction chains (fold -> fold GEMM) are independent: the second
+                // distinct direction runs on the potential side stream (idle by now)
+                int nchain = 0, ndist = 0;
+                for (int l = 0; l < 3; ++l) ndist += p.d[l].L > 1 && src[l] == l;
+                const bool forked = ndist >= 2 && !serial;
+                if (forked) c->join(9, c->stream, c->aux[pi]);  // fork before the first chain
                 for (int l = 0; l < 3; ++l) {
                     kr.width[l] = static_cast<int>(p.d[l].width);
                     kr.band[l] = static_cast<int>(p.d[l].band);
                     if (p.d[l].L == 1) continue;
                     const int s = src[l];
                     if (!Tl[s]) {
+                        const bool side = nchain++ == 1 && forked;
+                        const Launch& LC = side ? LP : L;
                         const DirPlan& d = p.d[s];
                         double* Qf = A.get<double>("nuc.Qf" + std::to_string(s), (d.band + 1) * mm * d.n);
                         Tl[s] = A.get<double>("nuc.T" + std::to_string(s), (d.band + 1) * Rtot * mm);
@@ -964,11 +989,12 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
                         f.slab = f.J <= kResfoldDirectJ ? nullptr : A.get<double>("nuc.slab" + std::to_string(s), resfold_slab_doubles(f));
                         f.sup_lo = w.pwc_lo[s];
                         f.sup_hi = w.pwc_hi[s];
-                        launch_resfold(L, f, false, false, "nuc_fold");
-                        launch_fgemm(L, static_cast<int>(m0), static_cast<int>(Rtot), d, w.pot[s], Qf, Tl[s]);
+                        launch_resfold(LC, f, false, false, "nuc_fold");
+                        launch_fgemm(LC, static_cast<int>(m0), static_cast<int>(Rtot), d, w.pot[s], Qf, Tl[s]);
                     }
                     kr.T[l] = Tl[s];
                 }
+                if (forked) c->join(10, c->aux[pi], c->stream);
                 w.N = A.get<double>("nuc.N", p.nblocks * mm);
                 kr.N = w.N;
                 launch_kr_combine(L, kr);
@@ -1511,8 +1537,15 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
         // under speculation the L0 check runs as its own branch beside the assembly (its
         // result is only read back at the end); it joins before the spectrum, whose
         // failure key it resets and whose read-back carries its state
+        // large box pencils (dense reduction on the device): the S side of the reduction runs
+        // on the FEM branch, overlapping the nuclear contraction
+        const bool box_split = graph_box && !small_box && phase == 0;
+        // with the assembly in this graph the check rides on its FEM branch (tail hook; not
+        // behind the box factorisation, whose failure key k_l0_init would reset)
+        // with the assembly in this graph the check forks after the assembly's root kernel
+        const bool fork_l0 = spec && !c->timer.on && phase != 2;
         const bool par_l0 = spec && !c->timer.on;
-        if (spec) {
+        if (spec && !fork_l0) {
             if (par_l0) {
                 c->join(6, c->stream, c->aux[2]);
                 l0w.enqueue(c->LA(2), 1, static_cast<int>(L0) + 3, true);
@@ -1520,13 +1553,14 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
                 l0w.enqueue(c->L(), 1, static_cast<int>(L0) + 3, true);
             }
         }
-        // large box pencils (dense reduction on the device): the S side of the reduction runs
-        // on the FEM branch, overlapping the nuclear contraction
-        const bool box_split = graph_box && !small_box && phase == 0;
+        const BranchHook l0_fork = [&](const Launch&) {
+            c->join(6, c->stream, c->aux[2]);
+            l0w.enqueue(c->LA(2), 1, static_cast<int>(L0) + 3, true);
+        };
         const BranchHook s_hook = [&](const Launch& LF) { box_factor(c, LF, p.Nb, out.out1, fk); };
         if (phase != 2)
             run_assembly(c, sd, p, NEED_MS | NEED_NUC, 0, out, nullptr, s0d, box_split ? AS_BOX_SPLIT : 0u, opt.shard,
-                         box_split ? &s_hook : nullptr);
+                         box_split ? &s_hook : nullptr, fork_l0 ? &l0_fork : nullptr);
         if (par_l0) c->join(7, c->aux[2], c->stream);
         if (phase == 2 && !periodic) {  // the box pencil factorises in place: work on copies
             LT_CU(cudaMemcpyAsync(out.out0, opt.H, sizeof(double) * ocount, cudaMemcpyDeviceToDevice, c->stream));
@@ -1916,9 +1950,9 @@ lt_status lt_create(int device, lt_ctx** out) {
         int prio_lo = 0, prio_hi = 0;
         LT_CU(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
         LT_CU(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi));
-        LT_CU(cudaStreamCreateWithPriority(&c->aux[0], cudaStreamNonBlocking, prio_lo));
+        LT_CU(cudaStreamCreateWithPriority(&c->aux[0], cudaStreamNonBlocking, prio_hi));
         LT_CU(cudaStreamCreateWithPriority(&c->aux[1], cudaStreamNonBlocking, prio_hi));
-        LT_CU(cudaStreamCreateWithPriority(&c->aux[2], cudaStreamNonBlocking, prio_lo));
+        LT_CU(cudaStreamCreateWithPriority(&c->aux[2], cudaStreamNonBlocking, prio_hi));
         for (auto& e : c->ev) LT_CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         LT_CU(cudaMalloc(&c->pencil_done, sizeof(unsigned)));
         LT_CU(cudaMemset(c->pencil_done, 0, sizeof(unsigned)));
