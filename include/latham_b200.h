@@ -110,6 +110,11 @@ lt_status lt_sys_upload(lt_ctx* ctx, const lt_system* sys, lt_sysdev** out);
 void lt_sys_free(lt_sysdev* s);
 lt_status lt_solve_core_dev(lt_ctx* ctx, const lt_sysdev* sys, int periodic, double* eig_dev, int64_t k_begin,
                             int64_t k_end, int64_t* info);
+/* lt_solve_core_dev ordered against a caller stream in one call (= lt_stream_wait(stream),
+ * lt_solve_core_dev, lt_stream_join(stream)): the low-latency form for callers that own a
+ * stream (a framework's current stream). */
+lt_status lt_solve_core_dev_on(lt_ctx* ctx, const lt_sysdev* sys, int periodic, double* eig_dev, int64_t k_begin,
+                               int64_t k_end, int64_t* info, void* stream);
 
 /* ---- several GPUs of one process (parallel.hpp:15-32) ------------------ *
  * lt_mctx: one lt_ctx per listed device and an in-process NCCL communicator over them

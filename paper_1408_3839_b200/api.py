@@ -562,6 +562,15 @@ class MultiContext:
         return out.reshape(sys.lattice_count, sys.m0) if periodic else out
 
 
+def _current_stream(device: int) -> int:
+    """Raw handle of torch's current CUDA stream on `device` (the cheap accessor when present)."""
+    import torch
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:
+        return raw(device)
+    return torch.cuda.current_stream(device).cuda_stream
+
+
 class DeviceSystem:
     """A LatticeSystem resident on the device (lt_sysdev) for the bench's device-timed leg."""
 
@@ -588,10 +597,13 @@ class DeviceSystem:
 
     def solve(self, periodic: bool, eig_dev_ptr: int, k_begin: int = 0, k_end: int = -1,
               info: Optional[np.ndarray] = None, stream: Optional[int] = None):
+        """Solve into eig_dev_ptr, ordered after `stream` (torch's current stream by default)
+        and before its later work, in one C-ABI call (lt_solve_core_dev_on)."""
         inf = np.zeros(8, dtype=np.int64) if info is None else info
-        with self._ordered(stream):
-            check(self.ctx.lib.lt_solve_core_dev(self.ctx.h, self.h, int(periodic), ctypes.c_void_p(eig_dev_ptr),
-                                                 k_begin, k_end, _i(inf)))
+        if stream is None:
+            stream = _current_stream(self.ctx.device)
+        check(self.ctx.lib.lt_solve_core_dev_on(self.ctx.h, self.h, int(periodic), eig_dev_ptr, k_begin, k_end,
+                                                _i(inf), stream))
         return inf
 
     # ---- multi-GPU assembly shards (lt_core_layout / lt_assemble_core_dev / lt_spectrum_dev)

@@ -2080,6 +2080,18 @@ lt_status lt_solve_core_dev(lt_ctx* c, const lt_sysdev* s, int periodic, double*
     });
 }
 
+lt_status lt_solve_core_dev_on(lt_ctx* c, const lt_sysdev* s, int periodic, double* eig_dev, int64_t k_begin,
+                               int64_t k_end, int64_t* info, void* stream) {
+    return guarded([&] {
+        LT_CU(cudaSetDevice(c->device));
+        const cudaStream_t ext = static_cast<cudaStream_t>(stream);
+        c->join(8, ext, c->stream);
+        StageScope ss(c, 1 << 20);
+        solve_core_dev(c, s, periodic != 0, eig_dev, k_begin, k_end, info);
+        c->join(8, c->stream, ext);
+    });
+}
+
 lt_status lt_core_layout(lt_ctx* c, const lt_sysdev* s, int periodic, int64_t* info, int64_t* kidx) {
     return guarded([&] {
         LT_CU(cudaSetDevice(c->device));

@@ -529,7 +529,14 @@ void launch_fgemm(const Launch& L, int m0, int Rtot, const DirPlan& d, const dou
 
 // Khatri-Rao combine: N[d0,d1,d2][e] = sum_r W[r][e] prod_{l wrapped} T_l[d_l][e][r]
 // (T_l stored for d >= 0 with r contiguous, so a CTA's table gathers are coalesced;
-// T_l[-d][(mu,nu)][r] = T_l[d][(nu,mu)][r]). CTA per (e, d0).
+// T_l[-d][(mu,nu)][r] = T_l[d][(nu,mu)][r]). CTA per (e, d0): u[d1][r] = W[r][e] T_0[d0][e][r]
+// T_1[d1][e][r] and t2[d2][r] = T_2[d2][e][r] in shared memory, then the (width1 x width2)
+// block N[d0][., .][e] = u t2^T as m8n8k4 DMMA tiles over r (one 8 x 8 tile per warp).
+__host__ __device__ inline int kr_ldk(int Rtot) {
+    const int kp = (Rtot + 3) & ~3;
+    return kp + (20 - kp % 16) % 16;  // = 4 (mod 16): conflict-free fragment reads
+}
+
 __global__ void k_kr_combine(KRArgs a) {
     extern __shared__ double sh[];
     const int e = blockIdx.x;
@@ -537,9 +544,12 @@ __global__ void k_kr_combine(KRArgs a) {
     const int mm = a.m0 * a.m0;
     const int mu = e % a.m0, nu = e / a.m0;
     const int eT = nu + mu * a.m0;
-    double* w0 = sh;                    // [Rtot]: W * T0[d0]
-    double* t1 = sh + a.Rtot;           // [width1][Rtot]
-    double* t2 = t1 + a.width[1] * a.Rtot;  // [width2][Rtot]
+    const int K = a.Rtot, Kp = (K + 3) & ~3, ldk = kr_ldk(K);
+    const int w1 = a.width[1], w2 = a.width[2];
+    const int W1p = (w1 + 7) & ~7, W2p = (w2 + 7) & ~7;
+    double* u = sh;                // [W1p][ldk]
+    double* t2 = u + W1p * ldk;    // [W2p][ldk]
+    double* w0 = t2 + W2p * ldk;   // [Kp]
     auto tab = [&](int l, int di, int r) -> double {
         if (!a.T[l]) return 1.0;
         const int d = di - a.band[l];
@@ -547,39 +557,55 @@ __global__ void k_kr_combine(KRArgs a) {
         const int ee = d < 0 ? eT : e;
         return a.T[l][(static_cast<long long>(ad) * mm + ee) * a.Rtot + r];  // [d][e][r]: r contiguous
     };
-    for (int r = threadIdx.x; r < a.Rtot; r += blockDim.x) w0[r] = a.W[r * mm + e] * tab(0, i0, r);
-    // the two table slabs, eight loads in flight per thread
-    auto gather = [&](int l, double* dst) {
-        const int tot = a.width[l] * a.Rtot;
+    for (int r = threadIdx.x; r < Kp; r += blockDim.x) w0[r] = r < K ? a.W[r * mm + e] * tab(0, i0, r) : 0.0;
+    __syncthreads();
+    // the two table slabs (zero padded), eight loads in flight per thread
+    auto gather = [&](int l, int w, int wp, double* dst, bool scale) {
+        const int tot = wp * Kp;
         for (int q0 = threadIdx.x; q0 < tot; q0 += 8 * blockDim.x) {
             double v[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int q = q0 + u * static_cast<int>(blockDim.x);
-                v[u] = q < tot ? tab(l, q / a.Rtot, q % a.Rtot) : 0.0;
+            for (int x = 0; x < 8; ++x) {
+                const int q = q0 + x * static_cast<int>(blockDim.x);
+                const int row = q / Kp, r = q % Kp;
+                v[x] = (q < tot && row < w && r < K) ? tab(l, row, r) : 0.0;
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int q = q0 + u * static_cast<int>(blockDim.x);
-                if (q < tot) dst[q] = v[u];
+            for (int x = 0; x < 8; ++x) {
+                const int q = q0 + x * static_cast<int>(blockDim.x);
+                if (q < tot) {
+                    const int row = q / Kp, r = q % Kp;
+                    dst[row * ldk + r] = scale ? v[x] * w0[r] : v[x];
+                }
             }
         }
     };
-    gather(1, t1);
-    gather(2, t2);
+    gather(1, w1, W1p, u, true);
+    gather(2, w2, W2p, t2, false);
     __syncthreads();
-    const int nout = a.width[1] * a.width[2];
-    for (int o = threadIdx.x; o < nout; o += blockDim.x) {
-        const int i1 = o / a.width[2], i2 = o % a.width[2];
-        double s = 0.0;
-        for (int r = 0; r < a.Rtot; ++r) s += w0[r] * t1[i1 * a.Rtot + r] * t2[i2 * a.Rtot + r];
-        const long long dlin = (static_cast<long long>(i0) * a.width[1] + i1) * a.width[2] + i2;
-        a.N[dlin * mm + e] = s;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int nt2 = W2p / 8, ntiles = (W1p / 8) * nt2;
+    for (int tile = warp; tile < ntiles; tile += nwarp) {
+        const int mt = tile / nt2, nt = tile % nt2;
+        double acc[2] = {0.0, 0.0};
+        const double* ua = u + (mt * 8 + g) * ldk + t;
+        const double* tb = t2 + (nt * 8 + g) * ldk + t;
+        for (int ks = 0; ks < Kp; ks += 4) dmma_m8n8k4(acc, ua[ks], tb[ks]);
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int i1 = mt * 8 + g, i2 = nt * 8 + 2 * t + i;
+            if (i1 < w1 && i2 < w2) {
+                const long long dlin = (static_cast<long long>(i0) * w1 + i1) * w2 + i2;
+                a.N[dlin * mm + e] = acc[i];
+            }
+        }
     }
 }
 
 void launch_kr_combine(const Launch& L, const KRArgs& a) {
-    const size_t smem = sizeof(double) * a.Rtot * (1 + a.width[1] + a.width[2]);
+    const int W1p = (a.width[1] + 7) & ~7, W2p = (a.width[2] + 7) & ~7;
+    const size_t smem = sizeof(double) * (static_cast<size_t>(W1p + W2p) * kr_ldk(a.Rtot) + ((a.Rtot + 3) & ~3));
     static size_t attr = 0;
     if (smem > 48 * 1024 && smem > attr) {
         LT_CU(cudaFuncSetAttribute(k_kr_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));

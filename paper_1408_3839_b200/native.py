@@ -86,6 +86,7 @@ def lib():
             "lt_sys_upload": ([_vp, _vp, _P(_vp)], ctypes.c_int),
             "lt_sys_free": ([_vp], None),
             "lt_solve_core_dev": ([_vp, _vp, ctypes.c_int, _vp, _i64, _i64, _ip], ctypes.c_int),
+            "lt_solve_core_dev_on": ([_vp, _vp, ctypes.c_int, _vp, _i64, _i64, _ip, _vp], ctypes.c_int),
             "lt_core_layout": ([_vp, _vp, ctypes.c_int, _ip, _ip], ctypes.c_int),
             "lt_assemble_core_dev": ([_vp, _vp, ctypes.c_int, _i64, _i64, ctypes.c_int, _vp, _vp], ctypes.c_int),
             "lt_spectrum_dev": ([_vp, _vp, ctypes.c_int, _vp, _vp, _vp, _i64, _i64], ctypes.c_int),
@@ -141,7 +142,7 @@ EXPORTS = (
     "lt_stage_count", "lt_stage_get", "lt_stage_timeline_count", "lt_stage_timeline_get",
     "lt_op_separable_count", "lt_op_separable", "lt_separable_residual", "lt_solve_periodic_factorized",
     "lt_solve_periodic_factorized_gen", "lt_factorized_block_diagonalize", "lt_box_circulant_defect", "lt_solve_core", "lt_sys_upload",
-    "lt_sys_free", "lt_solve_core_dev", "lt_core_layout", "lt_assemble_core_dev", "lt_spectrum_dev", "lt_assemble", "lt_assemble_core", "lt_combine", "lt_op_free", "lt_op_info",
+    "lt_sys_free", "lt_solve_core_dev", "lt_solve_core_dev_on", "lt_core_layout", "lt_assemble_core_dev", "lt_spectrum_dev", "lt_assemble", "lt_assemble_core", "lt_combine", "lt_op_free", "lt_op_info",
     "lt_op_dense", "lt_op_blocks", "lt_solve_periodic_ops", "lt_solve_periodic", "lt_block_diagonalize",
     "lt_solve_box_dense", "lt_pencil_eig", "lt_solve_box_dense_vectors", "lt_pencil_eigvec",
     "lt_solve_periodic_ops_vectors", "lt_solve_periodic_vectors", "lt_solve_periodic_factorized_vectors",
