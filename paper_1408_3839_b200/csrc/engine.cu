@@ -620,7 +620,9 @@ static int64_t* upload_s0(lt_ctx* c, const Plan& p) {
 
 // flags: AS_GENERAL_NUC forces the per-direction nuclear tables (w.T, the reference's
 // nucT layout) instead of the fused reassociations; AS_NO_FILL stops after the tables.
-enum AsmFlags : unsigned { AS_GENERAL_NUC = 1u, AS_NO_FILL = 2u, AS_BOX_SPLIT = 4u };
+// AS_EMAJOR (periodic, several wrapped axes, mode 0): the Khatri-Rao combine writes H, S
+// itself, entry-major ([mm][nblocks], for the fused lattice DFT), after the FEM join; no fill
+enum AsmFlags : unsigned { AS_GENERAL_NUC = 1u, AS_NO_FILL = 2u, AS_BOX_SPLIT = 4u, AS_EMAJOR = 8u };
 // AS_BOX_SPLIT (box, mode 0): S = Mass is filled on the FEM branch as soon as the mass tables
 // exist and `s_hook` runs right after it on that branch (the dense pencil's Cholesky and
 // L^-1 overlap the nuclear contraction); the main-stream fill writes H only.
@@ -842,6 +844,8 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
         }
     }
     // nuclear contraction: choose the reassociation (k_nuclear2.cu header)
+    KRArgs kr_fused;  // the combine deferred to the fill point (AS_EMAJOR)
+    bool kr_pending = false;
     int nuc_mode = 0, ndir = -1;
     const double* npart = nullptr;  // periodic single-direction fold partials (summed in fill)
     Index npart_res = 0, npart_nd = 0;
@@ -995,9 +999,14 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
                     kr.T[l] = Tl[s];
                 }
                 if (forked) c->join(10, c->aux[pi], c->stream);
-                w.N = A.get<double>("nuc.N", p.nblocks * mm);
-                kr.N = w.N;
-                launch_kr_combine(L, kr);
+                if ((flags & AS_EMAJOR) && p.periodic && mode == 0 && !(flags & AS_NO_FILL)) {
+                    kr_fused = kr;
+                    kr_pending = true;
+                } else {
+                    w.N = A.get<double>("nuc.N", p.nblocks * mm);
+                    kr.N = w.N;
+                    launch_kr_combine(L, kr);
+                }
             }
         } else {
             // general path: per-direction tables by direct contraction, combined in the fill
@@ -1042,6 +1051,22 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
     }
     c->join(4, c->aux[fi], c->stream);  // FEM tables (and the S branch) before the fill
     if (flags & AS_NO_FILL) {
+        if (wout) *wout = w;
+        return;
+    }
+    if (kr_pending) {
+        // Khatri-Rao combine + fill in one launch, H and S entry-major
+        for (int l = 0; l < 3; ++l) {
+            kr_fused.massT[l] = w.massT[l];
+            kr_fused.stiffT[l] = w.stiffT[l];
+            kr_fused.L[l] = p.d[l].L;
+        }
+        kr_fused.kin = shard.kin;
+        kr_fused.H = out.out0;
+        kr_fused.S = out.out1;
+        kr_fused.kidx = out.kidx;
+        kr_fused.nblocks = p.nblocks;
+        launch_kr_combine(L, kr_fused);
         if (wout) *wout = w;
         return;
     }
@@ -1153,12 +1178,25 @@ static DftPrep prepare_dft(lt_ctx* c, const Index dims[3], Index m0, const std::
     return P;
 }
 
+// the multi-axis transform runs as one fused launch (an entry's cube fits shared memory)
+static bool dft_fused_ok(const DftPrep& P) {
+    DftFusedArgs f;
+    f.mm = P.m0 * P.m0;
+    f.maxsz = P.maxsz;
+    for (int l = 0; l < 3; ++l) {
+        f.dims[l] = P.dims[l];
+        f.ncomp[l] = P.ncomp[l];
+        if (P.dims[l] > 1) f.axes[f.nax++] = l;
+    }
+    return f.nax >= 2 && dft_fused_smem(f) <= 200 * 1024;
+}
+
 // device part (kernels only: capturable). Transforms nops operators that share the
 // stored kidx (blocks[op] on device, std::map order); out[op] receives [K][mm] complex.
 // With want_emajor, the fused multi-axis launch writes [mm][K] instead (entry-major, for the
 // one-thread-per-pencil kernel); returns whether it did.
 static bool launch_dft(lt_ctx* c, const DftPrep& P, int nops, const double* const* blocks, double2** out,
-                       bool want_emajor = false) {
+                       bool want_emajor = false, bool gen_emajor = false) {
     const Launch L = c->L();
     const Index mm = P.m0 * P.m0;
     double2* buf[2][2];
@@ -1185,10 +1223,13 @@ static bool launch_dft(lt_ctx* c, const DftPrep& P, int nops, const double* cons
                 f.out[op] = out[op] = buf[op][1];
             }
             f.emajor = want_emajor ? 1 : 0;
+            f.gen_emajor = gen_emajor ? 1 : 0;
+            f.nblocks = P.nblk;
             launch_dft_fused(L, f, nops);
             return want_emajor;
         }
     }
+    if (gen_emajor) fail(LT_EGENERIC, "lattice DFT: entry-major generating blocks need the fused transform");
     DftAxisArgs a;
     a.mm = mm;
     for (int l = 0; l < 3; ++l) a.in[l] = P.ext[l];
@@ -1557,9 +1598,13 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
             c->join(6, c->stream, c->aux[2]);
             l0w.enqueue(c->LA(2), 1, static_cast<int>(L0) + 3, true);
         };
+        // generating blocks entry-major straight from the Khatri-Rao combine when the fused
+        // lattice DFT consumes them (the solve's internal buffers only)
+        const bool gen_emajor = periodic && phase == 0 && dft_fused_ok(dp) && p.m0 <= 32;
         const BranchHook s_hook = [&](const Launch& LF) { box_factor(c, LF, p.Nb, out.out1, fk); };
         if (phase != 2)
-            run_assembly(c, sd, p, NEED_MS | NEED_NUC, 0, out, nullptr, s0d, box_split ? AS_BOX_SPLIT : 0u, opt.shard,
+            run_assembly(c, sd, p, NEED_MS | NEED_NUC, 0, out, nullptr, s0d,
+                         (box_split ? AS_BOX_SPLIT : 0u) | (gen_emajor ? AS_EMAJOR : 0u), opt.shard,
                          box_split ? &s_hook : nullptr, fork_l0 ? &l0_fork : nullptr);
         if (par_l0) c->join(7, c->aux[2], c->stream);
         if (phase == 2 && !periodic) {  // the box pencil factorises in place: work on copies
@@ -1601,7 +1646,7 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
                 // shard then reproduces the full solve bitwise
                 const bool lane = pencil_lane_supported(p.m0) &&
                                   dp.dims[0] * dp.dims[1] * dp.dims[2] >= kPencilLaneMin;
-                const bool emajor = launch_dft(c, dp, 2, blocks, bd, lane);
+                const bool emajor = launch_dft(c, dp, 2, blocks, bd, lane, gen_emajor);
                 double2* Hb = bd[0];
                 double2* Sb = bd[1];
                 if (lane && nk > 0) {

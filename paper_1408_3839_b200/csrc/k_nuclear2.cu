@@ -493,16 +493,57 @@ void launch_hankel(const Launch& L, int m0, const DirPlan& d, const double* pwc,
 // ---------------------------------------------------------------------------
 // several wrapped directions: T[d][e][r] = sum_t P[r][t] Qf[d][e][t] (d >= 0), DMMA GEMM
 // ---------------------------------------------------------------------------
+constexpr int kFgemmK = 64;          // K (residues per cell) staged whole up to this
+constexpr int kFgemmLDA = kFgemmK + 4;  // conflict-free m16n8k4 fragment reads
+constexpr int kFgemmLDB = 64 + 8;
 __global__ void __launch_bounds__(256) k_fgemm(int mm, int Rtot, long long n, int ncols, const double* __restrict__ P,
                                                const double* __restrict__ Qf, double* __restrict__ T) {
-    __shared__ GemmSmem sm;
     const int r0 = blockIdx.y * kGBM;
     const int c0 = blockIdx.x * kGBN;  // column = d*mm + e
-    auto loadA = [&](int m, long long k) -> double { return r0 + m < Rtot ? P[(r0 + m) * n + k] : 0.0; };
-    // Qf layout [t][d][e] (k_resfold): column (d, e) of residue t at t*ncols + d*mm + e
-    auto loadB = [&](long long k, int nn) -> double { return c0 + nn < ncols ? Qf[k * ncols + c0 + nn] : 0.0; };
     double acc[4][4] = {};
-    cta_gemm_64x64(loadA, loadB, 0, n, acc, sm);
+    if (n <= kFgemmK) {
+        // the whole K range at once (one load latency instead of one per 16-deep stage):
+        // A[m][k] = P[r0+m][k], B[k][nn] = Qf[k][c0+nn] (Qf layout [t][d][e], k_resfold)
+        extern __shared__ double fsm[];
+        double* As = fsm;                  // [64][kFgemmLDA]
+        double* Bs = fsm + kGBM * kFgemmLDA;  // [kFgemmK][kFgemmLDB]
+        const int K = static_cast<int>(n);
+        {
+            // every element load in flight before the first store (16 + 16 per thread)
+            constexpr int kPer = kGBM * kFgemmK / 256;
+            double va[kPer], vb[kPer];
+#pragma unroll
+            for (int u = 0; u < kPer; ++u) {
+                const int e = threadIdx.x + 256 * u;
+                const int m = e / kFgemmK, k = e % kFgemmK;  // A: k fastest
+                va[u] = (k < K && r0 + m < Rtot) ? P[static_cast<long long>(r0 + m) * n + k] : 0.0;
+                const int kb = e / kGBN, nn = e % kGBN;      // B: n fastest
+                vb[u] = (kb < K && c0 + nn < ncols) ? Qf[static_cast<long long>(kb) * ncols + c0 + nn] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < kPer; ++u) {
+                const int e = threadIdx.x + 256 * u;
+                As[(e / kFgemmK) * kFgemmLDA + e % kFgemmK] = va[u];
+                Bs[(e / kGBN) * kFgemmLDB + e % kGBN] = vb[u];
+            }
+        }
+        const int Kp = (K + 3) & ~3;  // columns K .. Kp-1 were loaded as zeros
+        __syncthreads();
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const int wm = warp & 3, wn = warp >> 2;
+        const int g = lane >> 2, t = lane & 3;
+        for (int ks = 0; ks < Kp; ks += 4) {
+            const double a0 = As[(wm * 16 + g) * kFgemmLDA + ks + t];
+            const double a1 = As[(wm * 16 + g + 8) * kFgemmLDA + ks + t];
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) dmma_m16n8k4(acc[nt], a0, a1, Bs[(ks + t) * kFgemmLDB + wn * 32 + nt * 8 + g]);
+        }
+    } else {
+        __shared__ GemmSmem sm;
+        auto loadA = [&](int m, long long k) -> double { return r0 + m < Rtot ? P[(r0 + m) * n + k] : 0.0; };
+        auto loadB = [&](long long k, int nn) -> double { return c0 + nn < ncols ? Qf[k * ncols + c0 + nn] : 0.0; };
+        cta_gemm_64x64(loadA, loadB, 0, n, acc, sm);
+    }
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
@@ -521,8 +562,14 @@ void launch_fgemm(const Launch& L, int m0, int Rtot, const DirPlan& d, const dou
     const int mm = m0 * m0;
     const int ncols = static_cast<int>(d.band + 1) * mm;
     dim3 grid((ncols + kGBN - 1) / kGBN, (Rtot + kGBM - 1) / kGBM);
+    const size_t smem = d.n <= kFgemmK ? sizeof(double) * (kGBM * kFgemmLDA + kFgemmK * kFgemmLDB) : 0;
+    static bool attr = false;
+    if (smem && !attr) {
+        LT_CU(cudaFuncSetAttribute(k_fgemm, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        attr = true;
+    }
     Stage st_(L, "fold_gemm");
-    k_fgemm<<<grid, 256, 0, L.st>>>(mm, Rtot, d.n, ncols, P, Qf, T);
+    k_fgemm<<<grid, 256, smem, L.st>>>(mm, Rtot, d.n, ncols, P, Qf, T);
     LT_CU(cudaGetLastError());
     L.tick();
 }
@@ -596,8 +643,36 @@ __global__ void k_kr_combine(KRArgs a) {
         for (int i = 0; i < 2; ++i) {
             const int i1 = mt * 8 + g, i2 = nt * 8 + 2 * t + i;
             if (i1 < w1 && i2 < w2) {
-                const long long dlin = (static_cast<long long>(i0) * w1 + i1) * w2 + i2;
-                a.N[dlin * mm + e] = acc[i];
+                if (!a.H) {
+                    const long long dlin = (static_cast<long long>(i0) * w1 + i1) * w2 + i2;
+                    a.N[dlin * mm + e] = acc[i];
+                    continue;
+                }
+                // k_fill's combine for this block (the same rounded products and sums, so
+                // the blocks equal the two-kernel form bit for bit), entry-major
+                const int ii[3] = {i0, i1, i2};
+                double M[3], St[3];
+                long long slot = 0;
+#pragma unroll
+                for (int l = 0; l < 3; ++l) {
+                    M[l] = a.massT[l][static_cast<long long>(ii[l]) * mm + e];
+                    St[l] = a.stiffT[l][static_cast<long long>(ii[l]) * mm + e];
+                    const int d = ii[l] - a.band[l];
+                    slot = slot * a.width[l] + (d >= 0 ? d : a.width[l] + d);
+                }
+                const double mass = __dmul_rn(__dmul_rn(M[0], M[1]), M[2]);
+                const double t0 = __dmul_rn(__dmul_rn(St[0], M[1]), M[2]);
+                const double t1 = __dmul_rn(__dmul_rn(M[0], St[1]), M[2]);
+                const double t2 = __dmul_rn(__dmul_rn(M[0], M[1]), St[2]);
+                const double lap = __dadd_rn(__dadd_rn(t0, t1), t2);
+                a.H[e * a.nblocks + slot] = __dadd_rn(__dmul_rn(a.kin, lap), __dmul_rn(-1.0, acc[i]));
+                a.S[e * a.nblocks + slot] = mass;
+                if (e == 0)
+#pragma unroll
+                    for (int l = 0; l < 3; ++l) {
+                        const long long d = ii[l] - a.band[l];
+                        a.kidx[3 * slot + l] = ((d % a.L[l]) + a.L[l]) % a.L[l];
+                    }
             }
         }
     }

@@ -275,7 +275,8 @@ __global__ void __launch_bounds__(512) k_dft_fused(DftFusedArgs a) {
             }
             double v[U];
 #pragma unroll
-            for (unsigned u = 0; u < U; ++u) v[u] = bi[u] >= 0 ? gen[static_cast<Index>(bi[u]) * mm + e] : 0.0;
+            for (unsigned u = 0; u < U; ++u)
+                v[u] = bi[u] >= 0 ? gen[a.gen_emajor ? e * a.nblocks + bi[u] : static_cast<Index>(bi[u]) * mm + e] : 0.0;
 #pragma unroll
             for (unsigned u = 0; u < U; ++u) {
                 const unsigned q = q0 + u * blockDim.x;

@@ -278,6 +278,16 @@ struct KRArgs {
     const double* T[3] = {nullptr, nullptr, nullptr};  // [d>=0][r][e] per wrapped direction
     const double* W = nullptr;
     double* N = nullptr;
+    // fused fill (the periodic spectrum path): H = kin Lap - N and S = Mass of every block
+    // written entry-major, H[e][slot] (slot = k_fill's periodic slot), with kidx; N unused
+    double* H = nullptr;
+    double* S = nullptr;
+    int64_t* kidx = nullptr;
+    const double* massT[3] = {nullptr, nullptr, nullptr};
+    const double* stiffT[3] = {nullptr, nullptr, nullptr};
+    double kin = 0.5;
+    long long L[3] = {1, 1, 1};
+    long long nblocks = 0;
 };
 void launch_triv_tables(const Launch& L, const TrivJobs& jobs, int njobs, const WSpec& ws, int m0, int Rtot,
                         const double* potw, double* part, int splits, double* W, double* Tout, bool async = false);
@@ -450,7 +460,9 @@ struct DftFusedArgs {
     const int* slot2blk = nullptr;
     const double* gen[2] = {nullptr, nullptr};
     double2* out[2] = {nullptr, nullptr};
-    int emajor = 0;  // 1: out [mm][K] (entry-major, for the one-thread-per-pencil kernel)
+    int emajor = 0;     // 1: out [mm][K] (entry-major, for the one-thread-per-pencil kernel)
+    int gen_emajor = 0;  // 1: gen [mm][nblocks] (entry-major generating blocks, k_kr_combine's fused fill)
+    Index nblocks = 0;
 };
 // log2 L for the register FFT of power-of-two axes 2 <= L <= 16 (0: DFT pass); LT_DFT_NO_FFT
 // at compile time forces the DFT pass
