@@ -20,13 +20,13 @@ for c in c1 c2 c3 c4 c5; do
     timeout 300 python tools/cupti_timeline.py $c 3 > $O/${R}_${c}_timeline.txt 2>&1
 done
 # full sections for the top kernels (after warm-up launches)
-timeout 900 ncu --set full --import-source on -k regex:"k_pencil|k_fgemm|k_resfold|k_dft_fused|k_kr_combine|k_fill|k_window" \
-    -s 60 -c 10 -o $O/${R}_c5_full python bench.py --workload c5 --secondary '' --no-sweep --steps 3 --warmup 3 \
+timeout 900 ncu --set full --import-source on -k regex:"k_pencil_lane|k_fgemm|k_resfold|k_dft_fused|k_kr_combine|k_window|k_profiles" \
+    -s 60 -c 12 -o $O/${R}_c5_full python bench.py --workload c5 --secondary '' --no-sweep --steps 3 --warmup 3 \
     --no-cpu-baseline > $O/${R}_c5_full.log 2>&1
 timeout 900 ncu --set full --import-source on -k regex:"k_pencil|k_l0|k_triv_gemm|k_hankel|k_window|k_fill" \
     -s 40 -c 8 -o $O/${R}_c1_full python bench.py --workload c1 --secondary '' --no-sweep --steps 3 --warmup 3 \
     --no-cpu-baseline > $O/${R}_c1_full.log 2>&1
 timeout 900 ncu --set full --import-source on -k regex:"k_sytrd|k_tridiag_eig3|k_hankel|k_dgemm|k_potf|k_window" \
-    -s 10 -c 8 -o $O/${R}_c3_full python bench.py --workload c3 --secondary '' --no-sweep --steps 3 --warmup 3 \
+    -s 40 -c 12 -o $O/${R}_c3_full python bench.py --workload c3 --secondary '' --no-sweep --steps 3 --warmup 3 \
     --no-cpu-baseline > $O/${R}_c3_full.log 2>&1
 ls -la $O
