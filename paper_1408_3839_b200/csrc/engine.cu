@@ -458,6 +458,7 @@ struct L0Work {
     int act_peak[3] = {0, 0, 0}, act_scan[3] = {0, 0, 0};
     bool any_peak = false, any_scan = false;
     OverlapBufs b;
+    void init(const Launch& L) const { launch_overlap_init(L, b, m0); }
     void enqueue(const Launch& L, int s_begin, int s_end, bool first) const {
         if (first) launch_overlap_init(L, b, m0);
         if (any_scan) {
@@ -1506,7 +1507,10 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
     // from the previous call, the post-L0 graph is launched right behind the L0 graph
     // (no host round trip) and the device-computed L0 is checked after the final sync.
     std::vector<int64_t> skey = graph_key(sd->hs, Plan{}, periodic, -2, -2, nullptr, sd->mem, 0);
-    const bool spec_ok_path = periodic || sd->hs.m0() * sd->hs.cells() <= 32;  // no host sync inside
+    // no host sync inside the post-L0 work: periodic systems, and box pencils solved on the
+    // device (the batched pencil, or the dense reduction + on-chip tridiagonalisation)
+    const Index nb_box = sd->hs.m0() * sd->hs.cells();
+    const bool spec_ok_path = periodic || nb_box <= 32 || sytrd_ctas(static_cast<int>(nb_box)) > 0;
     const bool spec = allow_spec && spec_ok_path && c->graphs && !c->timer.on && c->spec_L0 >= 0 &&
                       c->spec_L0 <= 14 && skey == c->spec_key;
     Index L0;
@@ -1574,16 +1578,13 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
     if (kernel_readback) rb = PencilReadback{ret, rpin, c->pencil_done};
     auto enqueue = [&]() {
         // k_l0_init resets the failure key: in front of this graph under speculation, else in
-        // the L0 graph that just ran
-        // under speculation the L0 check runs as its own branch beside the assembly (its
-        // result is only read back at the end); it joins before the spectrum, whose
-        // failure key it resets and whose read-back carries its state
-        // large box pencils (dense reduction on the device): the S side of the reduction runs
-        // on the FEM branch, overlapping the nuclear contraction
+        // the L0 graph that just ran. Under speculation the L0 check runs as its own branch
+        // forked after the assembly's root kernel (its result is only read back at the end)
+        // and joins before the spectrum, whose failure key it resets and whose read-back
+        // carries its state. Large box pencils factor S on the FEM branch (the S side of the
+        // dense reduction overlaps the nuclear contraction) and write the failure key there:
+        // then k_l0_init goes first, ahead of every branch, and only the checks fork.
         const bool box_split = graph_box && !small_box && phase == 0;
-        // with the assembly in this graph the check rides on its FEM branch (tail hook; not
-        // behind the box factorisation, whose failure key k_l0_init would reset)
-        // with the assembly in this graph the check forks after the assembly's root kernel
         const bool fork_l0 = spec && !c->timer.on && phase != 2;
         const bool par_l0 = spec && !c->timer.on;
         if (spec && !fork_l0) {
@@ -1594,9 +1595,11 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
                 l0w.enqueue(c->L(), 1, static_cast<int>(L0) + 3, true);
             }
         }
+        const bool init_first = fork_l0 && box_split;
+        if (init_first) l0w.init(c->L());
         const BranchHook l0_fork = [&](const Launch&) {
             c->join(6, c->stream, c->aux[2]);
-            l0w.enqueue(c->LA(2), 1, static_cast<int>(L0) + 3, true);
+            l0w.enqueue(c->LA(2), 1, static_cast<int>(L0) + 3, !init_first);
         };
         // generating blocks entry-major straight from the Khatri-Rao combine when the fused
         // lattice DFT consumes them (the solve's internal buffers only)

@@ -153,7 +153,7 @@ def main():
     for cfg in ("c1", "c2", "c3", "c4", "c5"):
         launches(cfg, R)
     traffic = {}
-    for cfg in ("c2", "c3", "c4"):
+    for cfg in ("c1", "c2", "c3", "c4", "c5"):
         full(cfg, R, traffic)
     # per stage: mean DRAM bytes per launch
     agg = {cfg: {st: {"dram_bytes_per_launch": sum(x["dram_bytes"] for x in v) / len(v), "launches": len(v),
