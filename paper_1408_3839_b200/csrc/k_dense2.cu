@@ -16,6 +16,7 @@
 //      exactly symmetric, which is what 0.5 (A + A^T) produces from a rounding-symmetric A.
 // The triangular operands' zero parts are skipped at tile granularity (L^-1 row n has
 // k <= n only).
+#include "dmma.cuh"
 #include "lt_internal.cuh"
 
 namespace lt {
@@ -31,14 +32,16 @@ __device__ __forceinline__ double leaf_rsqrt(double x) {  // 1/sqrt(x) within an
     return y * fma(-hx * y, y, 1.5);
 }
 
-// Cholesky + inverse of diagonal block j (rows/cols b0 .. b0 + m) of the row-major S, in
-// shared memory, blocked by 8 columns (8 steps of three barriers instead of 64 of one):
-//   A. one warp factors the 8 x 8 diagonal block (lane per row, shuffles; Eigen's pivot
-//      test x <= 0 -> not positive definite) and inverts it;
-//   B. the panel below: L_r = A_r D^-T;
-//   C. the trailing lower part: A_rc -= sum_t L_rt L_ct (t in the block).
-// Then X = L^-1 by blocked column elimination: X_b <- D_b^-1 X_b, X_r -= L_rb X_b (r below).
+// Cholesky + inverse of diagonal block j (rows/cols b0 .. b0 + m) of the row-major S in shared
+// memory (padded to 64 with the identity), blocked by 8 columns:
+//   A. lanes 0-7 of warp 0 factor the 8 x 8 diagonal block, a row per lane (shuffles; Eigen's
+//      pivot test x <= 0 -> not positive definite), then invert it, a column per lane;
+//   B. the panel below, L_r = A_r D^-T, a row per thread (reads and writes its own row only);
+//   C. the trailing lower part A -= L_p L_p^T as m8n8k4 DMMA tiles spread over the warps.
+// Then X = L^-1 from the eight 8 x 8 inverses by recursive doubling, X21 = -X22 (L21 X11),
+// block pairs of 8, 16 and 32 as DMMA tiles.
 constexpr int kLB = 8;
+constexpr int kLL = 65;  // smem row stride
 
 #ifdef LT_LEAF_PROFILE
 __device__ long long lt_leaf_prof[64];
@@ -48,186 +51,176 @@ __device__ long long lt_leaf_prof[64];
 #define LPROF(i)
 #endif
 
-// one thread: Cholesky of the mb x mb (mb <= 8) diagonal block at (c0, c0) in registers, its
-// inverse, both written back (factor into sA's lower part, inverse into sD)
-__device__ __forceinline__ void leaf_chol8(double (*sA)[65], double (*sD)[9], int c0, int mb,
-                                           unsigned long long* fail, int* bad) {
-    double a[kLB][kLB];
-#pragma unroll
-    for (int r = 0; r < kLB; ++r)
-#pragma unroll
-        for (int c = 0; c < kLB; ++c) a[r][c] = (r < mb && c <= r) ? sA[c0 + r][c0 + c] : (r == c ? 1.0 : 0.0);
-    int ok = 1;
-    double rd[kLB];
-#pragma unroll
-    for (int t = 0; t < kLB; ++t) {
-        const double x = a[t][t];
-        if (t < mb && !(x > 0.0)) ok = 0;
-        const double is = leaf_rsqrt(x);
-        rd[t] = is;
-        a[t][t] = x * is;  // sqrt(x)
-#pragma unroll
-        for (int r = t + 1; r < kLB; ++r) a[r][t] *= is;
-#pragma unroll
-        for (int c = t + 1; c < kLB; ++c)
-#pragma unroll
-            for (int r = c; r < kLB; ++r) a[r][c] = fma(-a[r][t], a[c][t], a[r][c]);
-    }
-    // X = L^-1 by forward substitution (1 / L_rr = rd[r])
-    double x[kLB][kLB];
-#pragma unroll
-    for (int c = 0; c < kLB; ++c)
-#pragma unroll
-        for (int r = 0; r < kLB; ++r) {
-            if (r < c) {
-                x[r][c] = 0.0;
-                continue;
-            }
-            double acc = r == c ? 1.0 : 0.0;
-#pragma unroll
-            for (int k = c; k < r; ++k) acc = fma(-a[r][k], x[k][c], acc);
-            x[r][c] = acc * rd[r];
-        }
-    if (!ok) {
-        atomicMin(fail, 2ull);
-        *bad = 1;
-    }
-#pragma unroll
-    for (int r = 0; r < kLB; ++r)
-#pragma unroll
-        for (int c = 0; c < kLB; ++c) {
-            if (r < mb && c <= r) sA[c0 + r][c0 + c] = a[r][c];
-            sD[r][c] = (c <= r) ? x[r][c] : 0.0;
-        }
+// C (tile rows r0.., cols c0..) += sgn * A(r0.., k0..k0+K) B(c0.., k0..k0+K)^T as one m8n8k4 tile
+// (A, B, C in row-major smem with stride kLL); acc initialised from C when `acc_from_c`
+__device__ __forceinline__ void leaf_tile(const double* A, int ar0, int ak0, const double* B, int br0, int bk0, int K,
+                                          double* C, int cr0, int cc0, double sgn, bool acc_from_c) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    double acc[2];
+    acc[0] = acc_from_c ? C[(cr0 + g) * kLL + cc0 + 2 * t] : 0.0;
+    acc[1] = acc_from_c ? C[(cr0 + g) * kLL + cc0 + 2 * t + 1] : 0.0;
+    for (int ks = 0; ks < K; ks += 4)
+        dmma_m8n8k4(acc, sgn * A[(ar0 + g) * kLL + ak0 + ks + t], B[(br0 + g) * kLL + bk0 + ks + t]);
+    C[(cr0 + g) * kLL + cc0 + 2 * t] = acc[0];
+    C[(cr0 + g) * kLL + cc0 + 2 * t + 1] = acc[1];
 }
 
 __global__ void __launch_bounds__(256) k_potf_leaf(int n, long long ld, double* __restrict__ S, double* __restrict__ Li,
                                                    double* __restrict__ Lic, int j, unsigned long long* fail) {
     extern __shared__ double leaf_smem[];
-    double(*sA)[65] = reinterpret_cast<double(*)[65]>(leaf_smem);            // the block: lower part -> L
-    double(*sX)[65] = reinterpret_cast<double(*)[65]>(leaf_smem + 64 * 65);  // X = L^-1
-    double(*sDall)[kLB][9] = reinterpret_cast<double(*)[kLB][9]>(leaf_smem + 2 * 64 * 65);  // 8 x 8 inverses
+    double* sA = leaf_smem;                    // [64][kLL]: the block -> L (lower)
+    double* sX = leaf_smem + 64 * kLL;         // [64][kLL]: X = L^-1 (lower)
+    double* sT = leaf_smem + 2 * 64 * kLL;     // [64][kLL]: X^T staging / merge temporaries
+    __shared__ double srd[64];                 // 1 / L_rr
     __shared__ int bad;
     if (*fail != ~0ull) return;
     const int b0 = j * kLeaf, m = min(kLeaf, n - b0);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int idx = tid; idx < 64 * 64; idx += 256) {
         const int r = idx >> 6, c = idx & 63;
-        sA[r][c] = (r < m && c <= r) ? S[static_cast<long long>(b0 + r) * ld + b0 + c] : 0.0;
-        sX[r][c] = (r == c && r < m) ? 1.0 : 0.0;
+        sA[r * kLL + c] = (r < m && c <= r) ? S[static_cast<long long>(b0 + r) * ld + b0 + c] : (r == c ? 1.0 : 0.0);
+        sX[r * kLL + c] = 0.0;
     }
     if (tid == 0) bad = 0;
-    __syncthreads();
     LPROF(0);
-    const int nb = (m + kLB - 1) / kLB;
-    for (int kb = 0; kb < nb; ++kb) {
-        const int c0 = kb * kLB, mb = min(kLB, m - c0), r1 = c0 + mb;
-        double (*sD)[9] = sDall[kb];
-        LPROF(1 + 4 * kb);
-        if (tid == 0) leaf_chol8(sA, sD, c0, mb, fail, &bad);
-        __syncthreads();
-        LPROF(2 + 4 * kb);
-        if (bad) return;
-        // B: panel rows r >= r1: L_r,. = A_r,. D^-T (8 columns of the block); results held in
-        // registers until every thread has read the block's rows
-        double pv[2] = {0.0, 0.0};
-        int cnt = 0;
-        for (int idx = tid; idx < (m - r1) * kLB; idx += 256, ++cnt) {
-            const int r = r1 + idx / kLB, c = idx % kLB;
-            double acc = 0.0;
+    __syncthreads();
+    LPROF(1);
+    for (int kb = 0; kb < 64 / kLB; ++kb) {
+        const int c0 = kb * kLB, r1 = c0 + kLB;
+        // A: 8 x 8 factor (row per lane) and its inverse (column per lane)
+        if (warp == 0) {
+            double a[kLB];
+            const int rl = lane & 7;
 #pragma unroll
-            for (int t = 0; t < kLB; ++t)
-                if (t <= c && c < mb) acc = fma(sA[r][c0 + t], sD[c][t], acc);
-            pv[cnt] = acc;
-        }
-        __syncthreads();
-        cnt = 0;
-        for (int idx = tid; idx < (m - r1) * kLB; idx += 256, ++cnt) {
-            const int r = r1 + idx / kLB, c = idx % kLB;
-            sA[r][c0 + c] = pv[cnt];
-        }
-        __syncthreads();
-        // C: trailing lower part A_rc -= sum_t L_rt L_ct, r >= c >= r1
-        {
-            const int ty = tid >> 4, tx = tid & 15;  // 16 x 16 threads over the trailing square
-            double lc[4][kLB];
+            for (int q = 0; q < kLB; ++q) a[q] = q <= rl ? sA[(c0 + rl) * kLL + c0 + q] : 0.0;
+            int ok = 1;
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
-                const int c = r1 + tx + 16 * v;
+            for (int q = 0; q < kLB; ++q) {
+                const double piv = __shfl_sync(0xffffffffu, a[q], q);
+                if (!(piv > 0.0)) ok = 0;
+                const double rs = leaf_rsqrt(piv > 0.0 ? piv : 1.0);
+                if (rl == q) {
+                    a[q] = piv * rs;
+                    srd[c0 + q] = rs;
+                } else if (rl > q) {
+                    a[q] *= rs;
+                }
 #pragma unroll
-                for (int t = 0; t < kLB; ++t) lc[v][t] = c < m ? sA[c][c0 + t] : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int r = r1 + ty + 16 * u;
-                if (r >= m) break;
-                double lr[kLB];
-#pragma unroll
-                for (int t = 0; t < kLB; ++t) lr[t] = sA[r][c0 + t];
-#pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                    const int c = r1 + tx + 16 * v;
-                    if (c > r) continue;
-                    double acc = sA[r][c];
-#pragma unroll
-                    for (int t = 0; t < kLB; ++t) acc = fma(-lr[t], lc[v][t], acc);
-                    sA[r][c] = acc;
+                for (int c = q + 1; c < kLB; ++c) {
+                    const double lc = __shfl_sync(0xffffffffu, a[q], c);  // L[c][q]
+                    if (rl >= c) a[c] = fma(-a[q], lc, a[c]);
                 }
             }
-        }
-        __syncthreads();
-        LPROF(3 + 4 * kb);
-    }
-    LPROF(40);
-    // X = L^-1: for each 8-block b: X_b <- D_b^-1 X_b (rows of block b), then X_r -= L_rb X_b
-    for (int kb = 0; kb < nb; ++kb) {
-        const int c0 = kb * kLB, mb = min(kLB, m - c0), r1 = c0 + mb;
-        const double (*sD)[9] = sDall[kb];
-        // rows of block b: X_b,c = sum_t Dinv[r][t] X_{c0+t},c  (c <= r: columns up to r1)
-        double xb[2] = {0.0, 0.0};
-        int cnt = 0;
-        for (int idx = tid; idx < mb * r1; idx += 256, ++cnt) {
-            const int r = idx / r1, c = idx % r1;
-            double acc = 0.0;
+            if (lane < kLB)
 #pragma unroll
-            for (int t = 0; t < kLB; ++t)
-                if (t <= r) acc = fma(sD[r][t], sX[c0 + t][c], acc);
-            xb[cnt] = acc;
-        }
-        __syncthreads();
-        cnt = 0;
-        for (int idx = tid; idx < mb * r1; idx += 256, ++cnt) {
-            const int r = idx / r1, c = idx % r1;
-            sX[c0 + r][c] = xb[cnt];
-        }
-        __syncthreads();
-        // rows below: X_r,c -= sum_t L[r][c0+t] X[c0+t][c]
-        const int rows = m - r1;
-        for (int idx = tid; idx < rows * r1; idx += 256) {
-            const int r = r1 + idx / r1, c = idx % r1;
-            double acc = sX[r][c];
+                for (int q = 0; q < kLB; ++q)
+                    if (q <= lane) sA[(c0 + lane) * kLL + c0 + q] = a[q];
+            if (!ok && lane == 0) {
+                atomicMin(fail, 2ull);
+                bad = 1;
+            }
+            __syncwarp();
+            if (lane < kLB) {  // column `lane` of D^-1 by forward substitution
+                double x[kLB];
 #pragma unroll
-            for (int t = 0; t < kLB; ++t)
-                if (t < mb) acc = fma(-sA[r][c0 + t], sX[c0 + t][c], acc);
-            sX[r][c] = acc;
+                for (int r = 0; r < kLB; ++r) {
+                    if (r < lane) {
+                        x[r] = 0.0;
+                        continue;
+                    }
+                    double acc = r == lane ? 1.0 : 0.0;
+#pragma unroll
+                    for (int k = 0; k < r; ++k)
+                        if (k >= lane) acc = fma(-sA[(c0 + r) * kLL + c0 + k], x[k], acc);
+                    x[r] = acc * srd[c0 + r];
+                }
+#pragma unroll
+                for (int r = 0; r < kLB; ++r) sX[(c0 + r) * kLL + c0 + lane] = x[r];
+            }
+        }
+        __syncthreads();
+        LPROF(2 + 3 * kb);
+        if (bad) return;
+        // B: panel rows r1 .. 63, one row per thread: L[r][c0+q] = sum_{t <= q} A[r][c0+t] Dinv[q][t]
+        if (tid < 64 - r1) {
+            const int r = r1 + tid;
+            double ar[kLB], lr[kLB];
+#pragma unroll
+            for (int t = 0; t < kLB; ++t) ar[t] = sA[r * kLL + c0 + t];
+#pragma unroll
+            for (int q = 0; q < kLB; ++q) {
+                double acc = 0.0;
+#pragma unroll
+                for (int t = 0; t <= q; ++t) acc = fma(ar[t], sX[(c0 + q) * kLL + c0 + t], acc);
+                lr[q] = acc;
+            }
+#pragma unroll
+            for (int q = 0; q < kLB; ++q) sA[r * kLL + c0 + q] = lr[q];
+        }
+        __syncthreads();
+        LPROF(3 + 3 * kb);
+        // C: trailing lower part rows/cols >= r1: A -= L_p L_p^T (K = 8), 8 x 8 tiles on the warps
+        {
+            const int nt = (64 - r1) / 8;
+            const int ntiles = nt * (nt + 1) / 2;
+            for (int tile = warp; tile < ntiles; tile += 8) {
+                int ti = 0, rem = tile;  // lower-triangular tile (ti, tj), tj <= ti
+                while (rem > ti) {
+                    rem -= ti + 1;
+                    ++ti;
+                }
+                const int tj = rem;
+                leaf_tile(sA, r1 + 8 * ti, c0, sA, r1 + 8 * tj, c0, kLB, sA, r1 + 8 * ti, r1 + 8 * tj, -1.0, true);
+            }
+        }
+        __syncthreads();
+        LPROF(4 + 3 * kb);
+    }
+    // X = L^-1 by recursive doubling: X21 = -X22 (L21 X11) for block pairs of size s = 8, 16, 32
+    for (int sz = kLB; sz < 64; sz *= 2) {
+        const int npair = 64 / (2 * sz), tpb = (sz / 8) * (sz / 8);  // 8 x 8 tiles per s x s block
+        // T = L21 X11 -> sT rows o+s.., cols o.. (X11 lower: k >= col tile start)
+        for (int w = warp; w < npair * tpb; w += 8) {
+            const int pr = w / tpb, tt = w % tpb, o = pr * 2 * sz;
+            const int ti = tt / (sz / 8), tj = tt % (sz / 8);
+            // T[i][jj] = sum_k L[o+s+i][o+k] X[o+k][o+jj]: B operand rows = X^T -> use X11^T staged
+            // in sT's upper area? X11[k][jj] read as B(jj, k) = X11^T[jj][k]: a strided read of sX
+            const int lane2 = lane, g = lane2 >> 2, t = lane2 & 3;
+            double acc[2] = {0.0, 0.0};
+            for (int ks = 8 * tj; ks < sz; ks += 4)  // X11[k][jj] = 0 for k < jj (tile granularity)
+                dmma_m8n8k4(acc, sA[(o + sz + 8 * ti + g) * kLL + o + ks + t], sX[(o + ks + t) * kLL + o + 8 * tj + g]);
+            sT[(o + sz + 8 * ti + g) * kLL + o + 8 * tj + 2 * t] = acc[0];
+            sT[(o + sz + 8 * ti + g) * kLL + o + 8 * tj + 2 * t + 1] = acc[1];
+        }
+        __syncthreads();
+        // X21 = -X22 T (X22 lower: k <= row tile end)
+        for (int w = warp; w < npair * tpb; w += 8) {
+            const int pr = w / tpb, tt = w % tpb, o = pr * 2 * sz;
+            const int ti = tt / (sz / 8), tj = tt % (sz / 8);
+            const int g = lane >> 2, t = lane & 3;
+            double acc[2] = {0.0, 0.0};
+            for (int ks = 0; ks < 8 * (ti + 1); ks += 4)
+                dmma_m8n8k4(acc, -sX[(o + sz + 8 * ti + g) * kLL + o + sz + ks + t], sT[(o + sz + ks + t) * kLL + o + 8 * tj + g]);
+            sX[(o + sz + 8 * ti + g) * kLL + o + 8 * tj + 2 * t] = acc[0];
+            sX[(o + sz + 8 * ti + g) * kLL + o + 8 * tj + 2 * t + 1] = acc[1];
         }
         __syncthreads();
     }
-    LPROF(41);
+    LPROF(30);
     for (int idx = tid; idx < 64 * 64; idx += 256) {
         const int r = idx >> 6, c = idx & 63;  // consecutive threads: consecutive columns (row-major)
         if (r < m && c < m) {
-            Li[static_cast<long long>(b0 + r) * ld + b0 + c] = r >= c ? sX[r][c] : 0.0;
-            if (c <= r) S[static_cast<long long>(b0 + r) * ld + b0 + c] = sA[r][c];
+            Li[static_cast<long long>(b0 + r) * ld + b0 + c] = r >= c ? sX[r * kLL + c] : 0.0;
+            if (c <= r) S[static_cast<long long>(b0 + r) * ld + b0 + c] = sA[r * kLL + c];
         }
         const int cc = idx >> 6, rr = idx & 63;  // column-major: consecutive rows
-        if (rr < m && cc < m) Lic[static_cast<long long>(b0 + cc) * ld + b0 + rr] = rr >= cc ? sX[rr][cc] : 0.0;
+        if (rr < m && cc < m) Lic[static_cast<long long>(b0 + cc) * ld + b0 + rr] = rr >= cc ? sX[rr * kLL + cc] : 0.0;
     }
 }
 
 static void launch_potf_leaf(const Launch& L, int n, long long ld, double* S, double* Li, double* Lic, int j,
                              unsigned long long* fail) {
-    const int smem = static_cast<int>(sizeof(double) * (2 * 64 * 65 + (kLeaf / kLB) * kLB * 9));
+    const int smem = static_cast<int>(sizeof(double) * 3 * 64 * kLL);
     static bool attr = false;
     if (!attr) {
         LT_CU(cudaFuncSetAttribute(k_potf_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

@@ -89,7 +89,7 @@ int main() {
         long long pr[64];
         cudaMemcpyFromSymbol(pr, lt_leaf_prof, sizeof(pr));
         std::printf("leaf phases (cycles from start):");
-        for (int i = 1; i <= 41; ++i) std::printf(" %d:%lld", i, pr[i] - pr[0]);
+        for (int i = 1; i <= 30; ++i) std::printf(" %d:%lld", i, pr[i] - pr[0]);
         std::printf("\n");
     }
 #endif
