@@ -606,24 +606,28 @@ __global__ void k_kr_combine(KRArgs a) {
     };
     for (int r = threadIdx.x; r < Kp; r += blockDim.x) w0[r] = r < K ? a.W[r * mm + e] * tab(0, i0, r) : 0.0;
     __syncthreads();
-    // the two table slabs (zero padded), eight loads in flight per thread
+    // the two table slabs (zero padded): rows split over the warps, r over the lanes (no
+    // index division), the row's d sign and transposed entry resolved once per row
     auto gather = [&](int l, int w, int wp, double* dst, bool scale) {
-        const int tot = wp * Kp;
-        for (int q0 = threadIdx.x; q0 < tot; q0 += 8 * blockDim.x) {
-            double v[8];
+        const int nw = static_cast<int>(blockDim.x) >> 5, wl = static_cast<int>(threadIdx.x) >> 5;
+        const int ln = static_cast<int>(threadIdx.x) & 31;
+        for (int row = wl; row < wp; row += nw) {
+            const double* src = nullptr;
+            if (row < w && a.T[l]) {
+                const int d = row - a.band[l];
+                const int ad = d < 0 ? -d : d;
+                src = a.T[l] + (static_cast<long long>(ad) * mm + (d < 0 ? eT : e)) * a.Rtot;
+            }
+            double v[4];
 #pragma unroll
-            for (int x = 0; x < 8; ++x) {
-                const int q = q0 + x * static_cast<int>(blockDim.x);
-                const int row = q / Kp, r = q % Kp;
-                v[x] = (q < tot && row < w && r < K) ? tab(l, row, r) : 0.0;
+            for (int x = 0; x < 4; ++x) {
+                const int r = ln + 32 * x;
+                v[x] = r < K ? (src ? src[r] : (row < w ? 1.0 : 0.0)) : 0.0;
             }
 #pragma unroll
-            for (int x = 0; x < 8; ++x) {
-                const int q = q0 + x * static_cast<int>(blockDim.x);
-                if (q < tot) {
-                    const int row = q / Kp, r = q % Kp;
-                    dst[row * ldk + r] = scale ? v[x] * w0[r] : v[x];
-                }
+            for (int x = 0; x < 4; ++x) {
+                const int r = ln + 32 * x;
+                if (r < Kp) dst[row * ldk + r] = scale ? v[x] * w0[r] : v[x];
             }
         }
     };
@@ -679,6 +683,7 @@ __global__ void k_kr_combine(KRArgs a) {
 }
 
 void launch_kr_combine(const Launch& L, const KRArgs& a) {
+    if (a.Rtot > 128) fail(LT_EGENERIC, "kr_combine: more than 128 rank terms");
     const int W1p = (a.width[1] + 7) & ~7, W2p = (a.width[2] + 7) & ~7;
     const size_t smem = sizeof(double) * (static_cast<size_t>(W1p + W2p) * kr_ldk(a.Rtot) + ((a.Rtot + 3) & ~3));
     static size_t attr = 0;
