@@ -1,0 +1,96 @@
+"""GPU coverage of paths the BASELINE configs do not reach on their own.
+
+* ``lt_assembled_window_sum`` called directly (canonical_tensor.cpp:123-164) in each of its
+  device forms: the running sum of a uniform shift progression (the reference's recurrence,
+  bit-identical), the periodic cell window (size <= step, >= 32 shifts: warp-parallel
+  K-term sums, 1e-13 relative), the single-shift copy; and its BoundsError.
+* The dense box pencil beyond the on-chip tridiagonalisation (N_b = 2048: the device
+  reduction, the library eigensolver on A), eigensolver.cpp:12-35, against scipy.
+* A BASELINE-size periodic system (c2's lattice and grids) whose basis carries p-type
+  functions, so the L0 search runs its sampled scan (k_l0_sample + k_l0_scan) instead of the
+  s-type peak windows, against Oracle-X (entries, L0, eigenvalues).
+"""
+import numpy as np
+import pytest
+
+from conftest import eig_tolerance, entries_close
+from paper_1408_3839_b200.native import BoundsError
+from paper_1408_3839_b200.system import LatticeSystem, make_config
+
+pytestmark = pytest.mark.gpu
+
+
+def _direct_window_sum(m, shifts, size):
+    return sum(m[s:s + size] for s in shifts)
+
+
+def test_window_sum_running_uniform_bitwise(ctx, oracle):
+    rng = np.random.default_rng(11)
+    m = rng.uniform(0.05, 1.0, size=(900, 7))
+    for shifts, size in (([10 + 16 * k for k in range(24)], 400), ([3, 67, 131], 700), ([0, 1], 899)):
+        got = ctx.assembled_window_sum(m, shifts, size)
+        ref = oracle.assembled_window_sum(m, shifts, size)  # the reference's running sum
+        assert got.shape == ref.shape
+        assert np.array_equal(got, ref), (shifts[:3], size)
+        assert np.max(np.abs(got - _direct_window_sum(m, shifts, size))) <= 1e-12 * np.max(np.abs(got))
+
+
+def test_window_sum_cell_window_and_copy(ctx, oracle):
+    rng = np.random.default_rng(12)
+    m = rng.uniform(0.05, 1.0, size=(64 * 40 + 64, 5))
+    shifts = [64 * k for k in range(40)]  # 40 cells of 64 points, one output per residue
+    got = ctx.assembled_window_sum(m, shifts, 64)
+    ref = oracle.assembled_window_sum(m, shifts, 64)
+    assert np.max(np.abs(got - ref) / np.abs(ref)) < 1e-13
+    one = ctx.assembled_window_sum(m, [77], 300)
+    assert np.array_equal(one, m[77:377])
+
+
+def test_window_sum_bounds(ctx):
+    m = np.ones((100, 3))
+    with pytest.raises(BoundsError):
+        ctx.assembled_window_sum(m, [90], 20)
+
+
+def test_dense_pencil_beyond_onchip_tridiagonalisation(ctx):
+    scipy_linalg = pytest.importorskip("scipy.linalg")
+    n = 2048  # above the register/shared-memory resident one-stage reduction (~1900)
+    rng = np.random.default_rng(13)
+    B = rng.standard_normal((n, n)) / np.sqrt(n)
+    S = B @ B.T + np.eye(n)
+    A = rng.standard_normal((n, n))
+    H = 0.5 * (A + A.T)
+    ev = ctx.solve_box_dense(H, S)
+    ref = scipy_linalg.eigh(H, S, eigvals_only=True)
+    scale = np.max(np.abs(ref))
+    assert np.all(np.diff(ev) >= 0)
+    assert np.max(np.abs(ev - ref)) <= 1e-11 * scale
+
+
+def _with_p_functions(sys: LatticeSystem) -> LatticeSystem:
+    # p_x (along the lattice) on the two steepest functions, p_y on the fourth steepest: both
+    # the wrapped and a transverse direction take the sampled L0 scan; the overlap stays
+    # positive definite at every k-point (other placements make S_0 numerically singular)
+    deg = np.zeros((len(sys.bf_alpha), 3), dtype=np.int32)
+    order = np.argsort(sys.bf_alpha)
+    deg[order[-2:], 0] = 1
+    deg[order[-4], 1] = 1
+    return LatticeSystem(b=sys.b, L=tuple(sys.L), n=tuple(sys.n), nbar=tuple(sys.nbar), quad_M=sys.quad_M,
+                         nuc_pos=sys.nuc_pos, nuc_charge=sys.nuc_charge, bf_center=sys.bf_center,
+                         bf_alpha=sys.bf_alpha, bf_deg=deg, eps_ov=sys.eps_ov, name="c2_p")
+
+
+def test_baseline_size_with_p_functions(ctx, oracle):
+    sys = _with_p_functions(make_config("c2"))
+    oH, oS = oracle.assemble_core(sys, True)
+    info = np.zeros(8, dtype=np.int64)
+    ev = ctx.solve_core(sys, True, info)
+    assert info[0] == oH.L0
+    H, S = ctx.assemble_core(sys, True)
+    ok, worst = entries_close(H.blocks()[1], oH.blocks)
+    assert ok, worst
+    ok, worst = entries_close(S.blocks()[1], oS.blocks)
+    assert ok, worst
+    oev = oracle.solve_periodic_ops(oH, oS)
+    tol = eig_tolerance(oracle, True, oH, oS, oev)
+    assert np.all(np.abs(ev - oev) <= tol), np.max(np.abs(ev - oev) / tol)
