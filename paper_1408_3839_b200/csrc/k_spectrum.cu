@@ -220,7 +220,7 @@ __device__ __forceinline__ void fft_pass(unsigned& n0, unsigned& n1, unsigned& n
     n2 = o2;
 }
 
-__global__ void __launch_bounds__(512) k_dft_fused(DftFusedArgs a) {
+__global__ void __launch_bounds__(256) k_dft_fused(DftFusedArgs a) {
     extern __shared__ double2 fsm[];
     const Index e = blockIdx.x;
     const int op = blockIdx.y;
@@ -344,7 +344,7 @@ void launch_dft_fused(const Launch& L, const DftFusedArgs& a, int nops) {
         attr = smem;
     }
     Stage st_(L, "dft_fused");
-    k_dft_fused<<<dim3(static_cast<unsigned>(a.mm), nops), 512, smem, L.st>>>(a);
+    k_dft_fused<<<dim3(static_cast<unsigned>(a.mm), nops), 256, smem, L.st>>>(a);
     LT_CU(cudaGetLastError());
     L.tick();
 }
