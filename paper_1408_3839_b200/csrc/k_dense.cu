@@ -436,8 +436,9 @@ __global__ void __launch_bounds__(NT) k_sytrd_reg(int n, int P, const double* __
 #undef SYPROF
 }
 
-// G lanes per eigenvalue, Q shifts per lane; T scaled by 2^-s (max |d|, |e| < 1) internally
-template <int Q, int G, int BS>
+// G lanes per eigenvalue, Q shifts per lane; T scaled by 2^-s (max |d|, |e| < 1) internally;
+// GUARD: lt_device.cuh's sturm3 guard mode
+template <int Q, int G, int BS, int GUARD = 0>
 __global__ void __launch_bounds__(BS) k_tridiag_eig3(int n, const double* __restrict__ d, const double* __restrict__ e,
                                                      double* __restrict__ eig) {
     extern __shared__ __align__(16) double ts[];
@@ -503,7 +504,7 @@ __global__ void __launch_bounds__(BS) k_tridiag_eig3(int n, const double* __rest
 #pragma unroll
         for (int j = 0; j < Q; ++j) x[j] = a + (bnd - a) * (static_cast<double>(sub * Q + j + 1) * inv_pts);
         if (active) {
-            sturm3<Q, false>(sd, se2, n, x, cnt);
+            sturm3<Q, GUARD>(sd, se2, n, x, cnt);
         } else {
 #pragma unroll
             for (int j = 0; j < Q; ++j) cnt[j] = 0;
@@ -600,21 +601,24 @@ void launch_sytrd(const Launch& L, int n, const double* C, double* d, double* e,
     }
 }
 
-template <int Q, int G, int BS>
+template <int Q, int G, int BS, int GUARD>
 static void run_eig3(const Launch& L, int n, const double* d, const double* e, double* eig, size_t smem) {
-    LT_CU(cudaFuncSetAttribute(k_tridiag_eig3<Q, G, BS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    LT_CU(cudaFuncSetAttribute(k_tridiag_eig3<Q, G, BS, GUARD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(smem)));
     const unsigned blocks = static_cast<unsigned>((static_cast<size_t>(n) * G + BS - 1) / BS);
-    k_tridiag_eig3<Q, G, BS><<<blocks, BS, smem, L.st>>>(n, d, e, eig);
+    k_tridiag_eig3<Q, G, BS, GUARD><<<blocks, BS, smem, L.st>>>(n, d, e, eig);
 }
 
 void launch_tridiag_eig(const Launch& L, int n, const double* d, const double* e, double* eig) {
     const size_t smem = sizeof(double) * 2 * static_cast<size_t>(n);
     Stage st_(L, "tridiag_eig");
-    // 16 lanes x 2 shifts per eigenvalue (33-fold bracket shrink per round) in 64-thread
-    // CTAs: measured best on B200 for n = 1024 (the chain is issue-bound; more shifts per
-    // round cost more than the rounds they save; the LDL^T-ratio counts were slower)
-    run_eig3<2, 16, 64>(L, n, d, e, eig, smem);
+    // 32 lanes x 1 shift per eigenvalue (33-fold bracket shrink per round) in 64-thread CTAs,
+    // the three-term counts without the per-step guard (sturm3 GUARD 2: one FMA per step on
+    // the chain; the power-of-two rescale every 4 steps keeps it normal, |p_i| <= 4.3^i
+    // between rescales): n = 1024 415 -> 249 us on B200 (tools/eig3_probe.cu: the guard's
+    // compare/select on the chain, not the counts, set the round time; 2 shifts per lane,
+    // fewer lanes and the LDL^T-ratio counts were slower)
+    run_eig3<1, 32, 64, 2>(L, n, d, e, eig, smem);
     LT_CU(cudaGetLastError());
     L.tick();
 }
