@@ -53,6 +53,32 @@ __device__ __forceinline__ double fast_rcp(double q) {
     return fma(r, t, r);
 }
 
+// dlarfg coefficients from alpha = a0 and sigma = |x|^2 (sigma != 0): beta, tau and
+// 1 / (a0 - beta), on the step's dependent chain: MUFU reciprocal square root / reciprocal
+// with one cubic correction each (within an ulp or two) in the normal range, IEEE otherwise
+__device__ __forceinline__ void house_coeffs(double a0, double sigma, double& beta, double& tau, double& scal) {
+    const double q = fma(a0, a0, sigma);
+    if (q >= 1e-290 && q <= 1e290) {
+        double y;
+        asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(q));
+        const double ey = fma(-q * y, y, 1.0);
+        y = fma(y * ey, fma(ey, 0.375, 0.5), y);  // 1 / nrm
+        const double nrm = q * y;
+        beta = a0 >= 0.0 ? -nrm : nrm;
+        tau = (beta - a0) * (a0 >= 0.0 ? -y : y);  // (beta - a0) / beta
+        const double dn = a0 - beta;                // |a0| + nrm: no cancellation
+        double r;
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(dn));
+        const double er = fma(-dn, r, 1.0);
+        scal = fma(r, fma(er, er, er), r);
+    } else {
+        const double nrm = sqrt(q);
+        beta = a0 >= 0.0 ? -nrm : nrm;
+        tau = (beta - a0) / beta;
+        scal = 1.0 / (a0 - beta);
+    }
+}
+
 }  // namespace
 
 // smem: A[cols][n] (own columns j = b + s P), v[2][n] (ping-pong reflectors), w[n], c[n],
@@ -188,12 +214,7 @@ __global__ void __launch_bounds__(NT) k_sytrd(int n, int P, int cols, const doub
         if (r0 + 1 < n) {
             const double a0 = sc[r0 + 1];
             double beta = a0, scal = 0.0;
-            if (sigma != 0.0) {
-                const double nrm = sqrt(a0 * a0 + sigma);
-                beta = a0 >= 0.0 ? -nrm : nrm;
-                taun = (beta - a0) / beta;
-                scal = 1.0 / (a0 - beta);
-            }
+            if (sigma != 0.0) house_coeffs(a0, sigma, beta, taun, scal);
             for (int i = r0 + 1 + threadIdx.x; i < n; i += NT) svn[i] = (i == r0 + 1) ? 1.0 : sc[i] * scal;
             if (b == 0 && threadIdx.x == 0) e[r0] = beta;
         }
@@ -388,12 +409,7 @@ __global__ void __launch_bounds__(NT) k_sytrd_reg(int n, int P, const double* __
         if (r0 + 1 < n) {
             const double a0 = sc[r0 + 1];
             double beta = a0, scal = 0.0;
-            if (sigma != 0.0) {
-                const double nrm = sqrt(a0 * a0 + sigma);
-                beta = a0 >= 0.0 ? -nrm : nrm;
-                taun = (beta - a0) / beta;
-                scal = 1.0 / (a0 - beta);
-            }
+            if (sigma != 0.0) house_coeffs(a0, sigma, beta, taun, scal);
             for (int i = r0 + 1 + threadIdx.x; i < n; i += NT) svn[i] = (i == r0 + 1) ? 1.0 : sc[i] * scal;
             if (b == 0 && threadIdx.x == 0) e[r0] = beta;
         }
