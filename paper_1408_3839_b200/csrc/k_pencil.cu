@@ -30,6 +30,7 @@
 // clock64() at phase boundaries into lt_pencil_prof[k][0..7].
 #ifdef LT_PENCIL_PROFILE
 __device__ long long lt_pencil_prof[8192][8];
+__device__ long long lt_ms_prof[2];  // multisection of pencil 0, thread 0: cycles in Sturm counts, rounds
 #define PPROF(i) \
     if (t == 0 && k < 8192) lt_pencil_prof[k][i] = clock64();
 #else
@@ -77,6 +78,38 @@ template <bool RE> __device__ __forceinline__ double cabs2_(double2 a) {
 }
 template <bool RE> __device__ __forceinline__ double cabsr_(double2 a) {
     if constexpr (RE) return fabs(a.x); else return cabs_(a);
+}
+
+// Fused lattice DFT of one entry (single wrapped axis): F = sum_c w_c G[blk[c]] at offset
+// `off` of the m0 x m0 generating blocks, c ascending (k_dft_axis2's first-axis sum); block
+// indices from shared memory and eight (H, S) loads in flight per batch.
+template <bool RE>
+__device__ __forceinline__ void fused_dft_entry(const PencilDft& dft, const double2* tw, const int* blk, int mm,
+                                                Index off, double2& ah, double2& as) {
+    ah = make_double2(0.0, 0.0);
+    as = make_double2(0.0, 0.0);
+    int q = 0;
+    for (; q + 7 < dft.nc; q += 8) {
+        double vh[8], vs[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int b = blk[q + u];
+            vh[u] = b >= 0 ? dft.GH[static_cast<Index>(b) * mm + off] : 0.0;
+            vs[u] = b >= 0 ? dft.GS[static_cast<Index>(b) * mm + off] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            ah = cadd_<RE>(ah, cmul_<RE>(tw[q + u], make_double2(vh[u], 0.0)));
+            as = cadd_<RE>(as, cmul_<RE>(tw[q + u], make_double2(vs[u], 0.0)));
+        }
+    }
+    for (; q < dft.nc; ++q) {
+        const int b = blk[q];
+        const double vh = b >= 0 ? dft.GH[static_cast<Index>(b) * mm + off] : 0.0;
+        const double vs = b >= 0 ? dft.GS[static_cast<Index>(b) * mm + off] : 0.0;
+        ah = cadd_<RE>(ah, cmul_<RE>(tw[q], make_double2(vh, 0.0)));
+        as = cadd_<RE>(as, cmul_<RE>(tw[q], make_double2(vs, 0.0)));
+    }
 }
 
 template <int G>
@@ -146,6 +179,19 @@ __device__ __forceinline__ double fast_rcp(double q) {
     r = fma(r, t, r);
     t = fma(-q, r, 1.0);
     return fma(r, t, r);
+}
+// 1/sqrt(x), 1/q: MUFU seed (2^-20) and one cubic correction, for normal arguments
+__device__ __forceinline__ double pencil_rsqrt(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double e = fma(-x * y, y, 1.0);
+    return fma(y * e, fma(e, 0.375, 0.5), y);
+}
+__device__ __forceinline__ double pencil_rcp(double q) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+    const double e = fma(-q, r, 1.0);
+    return fma(r, fma(e, e, e), r);
 }
 __device__ __forceinline__ double safe_rcp(double q) {
     const double a = fabs(q);
@@ -337,6 +383,179 @@ __device__ void pencil_vectors(PSmem<NM>& sm, int n, int t, int slot, Index k, d
     for (int i = t; i < n; i += G) eig[k * n + i] = sm.d[i];
 }
 
+// Tridiagonal T (d, e) of an n x n pencil (n <= 32) -> the multisection's inputs, in place,
+// one entry per lane of a full warp: exact power-of-two scale (max |d|, |e| in [0.5, 1)) for
+// the three-term Sturm counts (the eigenvalues are unscaled exactly), e2 = e^2, the widened
+// Gershgorin bracket scal[0..1], 1/scale in scal[2] and the absolute tolerance
+// ulp * ||T|| (LAPACK dstebz's default ABSTOL) in scal[3]. Max / min reductions are exact,
+// so the values equal those of a serial sweep.
+__device__ void tridiag_prepare_warp(double* d, double* e, double* e2, double* scal, int n, int lane) {
+    const bool in = lane < n, ine = lane + 1 < n;
+    double dc = in ? d[lane] : 0.0, ec = ine ? e[lane] : 0.0;
+    double mx = in ? fmax(fabs(dc), fabs(ec)) : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    int ex = mx > 0.0 ? static_cast<int>((__double_as_longlong(mx) >> 52) & 0x7ff) - 1022 : 0;
+    ex = max(-1000, min(1000, ex));
+    const double sc = __longlong_as_double(static_cast<long long>(1023 - ex) << 52);
+    dc *= sc;
+    ec *= sc;
+    const double eprev = __shfl_up_sync(0xffffffffu, ec, 1);
+    const double rad = (lane > 0 ? fabs(eprev) : 0.0) + (ine ? fabs(ec) : 0.0);
+    double lo = in ? dc - rad : 1e300, hi = in ? dc + rad : -1e300;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    __syncwarp();
+    if (in) d[lane] = dc;
+    if (ine) {
+        e[lane] = ec;
+        e2[lane] = ec * ec;
+    }
+    if (lane == 0) {
+        const double wid = fmax(hi - lo, fmax(fabs(lo), fabs(hi))) * 4.4e-16 * n + 1e-300;
+        scal[0] = lo - wid;
+        scal[1] = hi + wid;
+        scal[2] = __longlong_as_double(static_cast<long long>(1023 + ex) << 52);  // 1 / sc
+        scal[3] = 2.2e-16 * fmax(fabs(lo), fabs(hi));
+    }
+}
+
+// Sturm counts of the scaled tridiagonal at Q shifts: sturm3<Q, 2>'s three-term recurrence
+// p_{i+1} = (d_i - x) p_i - e2_{i-1} p_{i-1}, unrolled over the compile-time bound NM <= 32
+// (steps i >= n run on padding and are masked out). The signs of p_1 .. p_n go into a bit
+// mask and the sign changes are counted once per chain (tools/sturm_probe.cu: an integer
+// count update per step costs more than the recurrence itself).
+template <int Q, int NM>
+__device__ __forceinline__ void sturm_fixed(const double* sd, const double* se2, int n, const double (&x)[Q],
+                                            int (&cnt)[Q]) {
+    static_assert(NM <= 32, "sign mask");
+    double pv[Q], cv[Q];
+    unsigned sg[Q];
+#pragma unroll
+    for (int j = 0; j < Q; ++j) {
+        pv[j] = 1.0;
+        cv[j] = sd[0] - x[j];
+        sg[j] = static_cast<unsigned>(__double2hiint(cv[j])) >> 31;
+    }
+#pragma unroll
+    for (int i = 1; i < NM; ++i) {
+        const double di = sd[i], ei = se2[i - 1];
+#pragma unroll
+        for (int j = 0; j < Q; ++j) {
+            const double nx = fma(di - x[j], cv[j], -ei * pv[j]);
+            sg[j] |= (static_cast<unsigned>(__double2hiint(nx)) >> 31) << i;
+            pv[j] = cv[j];
+            cv[j] = nx;
+        }
+        if ((i & 3) == 0) {
+#pragma unroll
+            for (int j = 0; j < Q; ++j) {
+                const int ex = ((__double2hiint(cv[j]) >> 20) & 0x7ff) - 1023;
+                if (ex > 400 || ex < -400) {  // rare: exact power-of-two rescale of (cur, prev)
+                    const double scl = __longlong_as_double(static_cast<long long>(1023 - ex) << 52);
+                    cv[j] *= scl;
+                    pv[j] *= scl;
+                }
+            }
+        }
+    }
+    // bit b of sg: sign of p_{b+1}; sign changes of p_0 = 1, p_1, ..., p_n
+    const unsigned live = n >= 32 ? 0xffffffffu : ((1u << n) - 1u);
+#pragma unroll
+    for (int j = 0; j < Q; ++j) cnt[j] = __popc((sg[j] ^ (sg[j] << 1)) & live);
+}
+
+// Parallel multisection over the G threads of a pencil group (t = 0 .. G-1, contiguous
+// lanes): all n eigenvalues of the prepared tridiagonal, ascending, into eig[k m0 + i].
+template <int G, int NM>
+__device__ void pencil_multisection(const double* d, const double* e2, const double* scal, int n, int t, Index k,
+                                    int m0, double* __restrict__ eig) {
+    // 5. parallel multisection: P threads (contiguous lanes) x Q shifts per thread and
+    //    eigenvalue; the bracket shrinks (P Q + 1)-fold per round.
+#ifndef LT_PENCIL_Q
+#define LT_PENCIL_Q 2  // shifts per thread: measured best (Q = 1, 4, 8 slower on the FP64 pipe)
+#endif
+    constexpr int Q = LT_PENCIL_Q;
+    int P = 1;
+    while (P * 2 <= 32 && P * 2 * n <= G) P *= 2;
+    const double unscale = scal[2];
+    const double atol = scal[3];
+    const int per_round = G / P;  // eigenvalues handled concurrently
+    const double inv_pts = 1.0 / static_cast<double>(P * Q + 1);
+    for (int base = 0; base < n; base += per_round) {
+        const int mi = base + t / P;  // eigenvalue index of this thread
+        const int sub = t % P;
+        const bool active = mi < n;
+        double a = scal[0], b = scal[1];
+        const unsigned lane = threadIdx.x & 31;
+        const int gb = static_cast<int>(lane & ~static_cast<unsigned>(P - 1));
+        const unsigned gmask = (P == 32) ? 0xffffffffu : (((1u << P) - 1u) << gb);
+        for (int it = 0; it < 80; ++it) {
+            double x[Q];
+            int cnt[Q];
+#pragma unroll
+            for (int j = 0; j < Q; ++j) x[j] = a + (b - a) * (static_cast<double>(sub * Q + j + 1) * inv_pts);
+#ifdef LT_PENCIL_PROFILE
+            const long long c0 = clock64();
+#endif
+            if (active) {
+                sturm_fixed<Q, NM>(d, e2, n, x, cnt);
+            } else {
+#pragma unroll
+                for (int j = 0; j < Q; ++j) cnt[j] = 0;
+            }
+#ifdef LT_PENCIL_PROFILE
+            if (t == 0 && k == 0) {
+                long long c1;
+                asm volatile("mov.u64 %0, %%clock64;" : "=l"(c1) : "r"(cnt[0]), "r"(cnt[Q - 1]) : "memory");
+                lt_ms_prof[0] += c1 - c0;
+                lt_ms_prof[1] += 1;
+            }
+#endif
+            // first shift (in group order sub*Q + j, increasing x) whose count exceeds mi
+            int fq = Q;
+#pragma unroll
+            for (int j = Q - 1; j >= 0; --j)
+                if (cnt[j] > mi) fq = j;
+            // candidate bracket if this thread holds the first such shift
+            const double prev_last = __shfl_up_sync(0xffffffffu, x[Q - 1], 1);
+            double clo = (sub > 0) ? prev_last : a, chi = x[0];
+#pragma unroll
+            for (int j = 1; j < Q; ++j)
+                if (fq == j) {
+                    clo = x[j - 1];
+                    chi = x[j];
+                }
+            const unsigned bal = __ballot_sync(0xffffffffu, active && fq < Q) & gmask;
+            const int src = bal ? (__ffs(bal) - 1) : (gb + P - 1);
+            const double slo = __shfl_sync(0xffffffffu, clo, src);
+            const double shi = __shfl_sync(0xffffffffu, chi, src);
+            const double last = __shfl_sync(0xffffffffu, x[Q - 1], gb + P - 1);
+            double na, nb;
+            if (bal) {
+                na = slo;
+                nb = shi;
+            } else {
+                na = last;  // every shift is below the eigenvalue
+                nb = b;
+            }
+            const bool done = !(nb - na > 2.2e-16 * fmax(fabs(na), fabs(nb)) + atol) || (na == a && nb == b);
+            a = na;
+            b = nb;
+            if (__all_sync(0xffffffffu, done || !active)) {
+#ifdef LT_PENCIL_PROFILE
+                if (t == 0 && k < 8192) lt_pencil_prof[k][7] = it + 1;  // multisection rounds
+#endif
+                break;
+            }
+        }
+        if (active && sub == 0) eig[k * m0 + mi] = 0.5 * (a + b) * unscale;
+    }
+}
+
 }  // namespace
 
 // Threads of a group own matrix entries e = t + G*u (row e % NM, column e / NM); the
@@ -350,6 +569,7 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
     constexpr int EPT = (NM * NM + G - 1) / G;  // matrix entries per thread
     constexpr int TPR = G / NM;                 // mat-vec threads per row
     static_assert(TPR >= 1 && TPR <= 32 && (TPR & (TPR - 1)) == 0, "row split");
+    static_assert(G >= 32, "the tridiagonal preparation runs on the first warp of the group");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PSmem<NM>* all = reinterpret_cast<PSmem<NM>*>(smem_raw);
     const int slot = threadIdx.x / G;
@@ -383,32 +603,8 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
             const int r = e % NM, c = e / NM;
             if (r < m0 && c < m0) {
                 if (dft.nc > 0) {
-                    // block indices from shared memory and eight (H, S) loads in flight per
-                    // batch; the sums stay in ascending q
-                    double2 ah = make_double2(0.0, 0.0), as = make_double2(0.0, 0.0);
-                    const Index off = r + c * m0;
-                    int q = 0;
-                    for (; q + 7 < dft.nc; q += 8) {
-                        double vh[8], vs[8];
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            const int b = sm.blk[q + u];
-                            vh[u] = b >= 0 ? dft.GH[static_cast<Index>(b) * mm + off] : 0.0;
-                            vs[u] = b >= 0 ? dft.GS[static_cast<Index>(b) * mm + off] : 0.0;
-                        }
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            ah = cadd_<RE>(ah, cmul_<RE>(sm.tw[q + u], make_double2(vh[u], 0.0)));
-                            as = cadd_<RE>(as, cmul_<RE>(sm.tw[q + u], make_double2(vs[u], 0.0)));
-                        }
-                    }
-                    for (; q < dft.nc; ++q) {
-                        const int b = sm.blk[q];
-                        const double vh = b >= 0 ? dft.GH[static_cast<Index>(b) * mm + off] : 0.0;
-                        const double vs = b >= 0 ? dft.GS[static_cast<Index>(b) * mm + off] : 0.0;
-                        ah = cadd_<RE>(ah, cmul_<RE>(sm.tw[q], make_double2(vh, 0.0)));
-                        as = cadd_<RE>(as, cmul_<RE>(sm.tw[q], make_double2(vs, 0.0)));
-                    }
+                    double2 ah, as;
+                    fused_dft_entry<RE>(dft, sm.tw, sm.blk, mm, r + c * m0, ah, as);
                     A[r][c] = ah;
                     B[r][c] = as;
                 } else {
@@ -569,12 +765,18 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
             beta = x0.x;
             scal = make_double2(0.0, 0.0);
         } else {
-            const double nrm = sqrt(x0.x * x0.x + x0.y * x0.y + xn2);
+            // 1/nrm and 1/|x0 - beta|^2 from the MUFU seeds with one cubic correction each
+            // (the step's dependent chain; IEEE sqrt / division outside the normal range)
+            const double q = fma(x0.x, x0.x, fma(x0.y, x0.y, xn2));
+            const bool nq = q >= 1e-290 && q <= 1e290;
+            const double rq = nq ? pencil_rsqrt(q) : 1.0 / sqrt(q);
+            const double nrm = q * rq;
             beta = x0.x >= 0.0 ? -nrm : nrm;
-            const double ib = safe_rcp(beta);
+            const double ib = x0.x >= 0.0 ? -rq : rq;  // 1 / beta
             tau = make_double2((beta - x0.x) * ib, -x0.y * ib);
             const double2 den = make_double2(x0.x - beta, x0.y);
-            const double id = safe_rcp(den.x * den.x + den.y * den.y);
+            const double dq = fma(den.x, den.x, den.y * den.y);
+            const double id = nq ? pencil_rcp(dq) : 1.0 / dq;
             scal = make_double2(den.x * id, -den.y * id);
         }
         // v (index 0 <-> row kk+1)
@@ -614,112 +816,12 @@ __global__ void __launch_bounds__(BS) k_pencil(Index count, int m0, const double
         }
         gsync<G>(slot);
     }
-    if (t == 0) {
-        sm.d[n - 1] = A[n - 1][n - 1].x;
-        // exact power-of-two scale (max |d|, |e| in [0.5, 1)) for the three-term Sturm counts;
-        // the multisection runs on the scaled T and the eigenvalues are unscaled exactly
-        double mx = 0.0;
-        for (int i = 0; i < n; ++i) mx = fmax(mx, fmax(fabs(sm.d[i]), i + 1 < n ? fabs(sm.e[i]) : 0.0));
-        int ex = mx > 0.0 ? static_cast<int>((__double_as_longlong(mx) >> 52) & 0x7ff) - 1022 : 0;
-        ex = max(-1000, min(1000, ex));
-        const double sc = __longlong_as_double(static_cast<long long>(1023 - ex) << 52);
-        sm.scal[2] = __longlong_as_double(static_cast<long long>(1023 + ex) << 52);  // 1 / sc
-        for (int i = 0; i < n; ++i) {
-            sm.d[i] *= sc;
-            if (i + 1 < n) sm.e[i] *= sc;
-        }
-        double emax = 0.0;
-        for (int i = 0; i + 1 < n; ++i) {
-            sm.e2[i] = sm.e[i] * sm.e[i];
-            emax = fmax(emax, sm.e2[i]);
-        }
-        // Gershgorin bracket, widened, and LAPACK's pivmin = safmin * max(1, max e^2)
-        double lo = 1e300, hi = -1e300;
-        for (int i = 0; i < n; ++i) {
-            const double r = (i > 0 ? fabs(sm.e[i - 1]) : 0.0) + (i + 1 < n ? fabs(sm.e[i]) : 0.0);
-            lo = fmin(lo, sm.d[i] - r);
-            hi = fmax(hi, sm.d[i] + r);
-        }
-        const double wid = fmax(hi - lo, fmax(fabs(lo), fabs(hi))) * 4.4e-16 * n + 1e-300;
-        sm.scal[0] = lo - wid;
-        sm.scal[1] = hi + wid;
-        (void)emax;
-        // absolute tolerance ulp * ||T|| (LAPACK dstebz's default ABSTOL): eigenvalues near
-        // zero stop at the normwise-backward-stable accuracy instead of chasing relative ulps
-        sm.scal[3] = 2.2e-16 * fmax(fabs(lo), fabs(hi));
-    }
+    if (t == 0) sm.d[n - 1] = A[n - 1][n - 1].x;
+    gsync<G>(slot);
+    if (t < 32) tridiag_prepare_warp(sm.d, sm.e, sm.e2, sm.scal, n, t);
     gsync<G>(slot);
     PPROF(5);
-    // 5. parallel multisection: P threads (contiguous lanes) x Q shifts per thread and
-    //    eigenvalue; the bracket shrinks (P Q + 1)-fold per round.
-#ifndef LT_PENCIL_Q
-#define LT_PENCIL_Q 2  // shifts per thread: measured best (Q = 1, 4, 8 slower on the FP64 pipe)
-#endif
-    constexpr int Q = LT_PENCIL_Q;
-    int P = 1;
-    while (P * 2 <= 32 && P * 2 * n <= G) P *= 2;
-    const double unscale = sm.scal[2];
-    const double atol = sm.scal[3];
-    const int per_round = G / P;  // eigenvalues handled concurrently
-    const double inv_pts = 1.0 / static_cast<double>(P * Q + 1);
-    for (int base = 0; base < n; base += per_round) {
-        const int mi = base + t / P;  // eigenvalue index of this thread
-        const int sub = t % P;
-        const bool active = mi < n;
-        double a = sm.scal[0], b = sm.scal[1];
-        const unsigned lane = threadIdx.x & 31;
-        const int gb = static_cast<int>(lane & ~static_cast<unsigned>(P - 1));
-        const unsigned gmask = (P == 32) ? 0xffffffffu : (((1u << P) - 1u) << gb);
-        for (int it = 0; it < 80; ++it) {
-            double x[Q];
-            int cnt[Q];
-#pragma unroll
-            for (int j = 0; j < Q; ++j) x[j] = a + (b - a) * (static_cast<double>(sub * Q + j + 1) * inv_pts);
-            if (active) {
-                sturm3<Q, 2>(sm.d, sm.e2, n, x, cnt);
-            } else {
-#pragma unroll
-                for (int j = 0; j < Q; ++j) cnt[j] = 0;
-            }
-            // first shift (in group order sub*Q + j, increasing x) whose count exceeds mi
-            int fq = Q;
-#pragma unroll
-            for (int j = Q - 1; j >= 0; --j)
-                if (cnt[j] > mi) fq = j;
-            // candidate bracket if this thread holds the first such shift
-            const double prev_last = __shfl_up_sync(0xffffffffu, x[Q - 1], 1);
-            double clo = (sub > 0) ? prev_last : a, chi = x[0];
-#pragma unroll
-            for (int j = 1; j < Q; ++j)
-                if (fq == j) {
-                    clo = x[j - 1];
-                    chi = x[j];
-                }
-            const unsigned bal = __ballot_sync(0xffffffffu, active && fq < Q) & gmask;
-            const int src = bal ? (__ffs(bal) - 1) : (gb + P - 1);
-            const double slo = __shfl_sync(0xffffffffu, clo, src);
-            const double shi = __shfl_sync(0xffffffffu, chi, src);
-            const double last = __shfl_sync(0xffffffffu, x[Q - 1], gb + P - 1);
-            double na, nb;
-            if (bal) {
-                na = slo;
-                nb = shi;
-            } else {
-                na = last;  // every shift is below the eigenvalue
-                nb = b;
-            }
-            const bool done = !(nb - na > 2.2e-16 * fmax(fabs(na), fabs(nb)) + atol) || (na == a && nb == b);
-            a = na;
-            b = nb;
-            if (__all_sync(0xffffffffu, done || !active)) {
-#ifdef LT_PENCIL_PROFILE
-                if (t == 0 && k < 8192) lt_pencil_prof[k][7] = it + 1;  // multisection rounds
-#endif
-                break;
-            }
-        }
-        if (active && sub == 0) eig[k * m0 + mi] = 0.5 * (a + b) * unscale;
-    }
+    pencil_multisection<G, NM>(sm.d, sm.e2, sm.scal, n, t, k, m0, eig);
     PPROF(6);
     if (t == 0) group_done(rb, count);
 }

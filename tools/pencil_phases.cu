@@ -57,6 +57,10 @@ static void run(int count, int m0, int reps) {
     cudaEventCreate(&e1);
     float best = 1e30f;
     for (int r = 0; r < reps; ++r) {
+        {
+            long long z[2] = {0, 0};
+            cudaMemcpyToSymbol(lt_ms_prof, z, sizeof(z));
+        }
         cudaMemset(fk, 0xff, sizeof(unsigned long long));
         cudaEventRecord(e0);
         lt::k_pencil<NM, G, BS, VEC, RE><<<blocks, BS, smem>>>(count, m0, dH, dS, de, fk, 1, lt::PencilDft{}, dv,
@@ -74,6 +78,9 @@ static void run(int count, int m0, int reps) {
     for (int k = 0; k < nk; ++k)
         for (int i = 0; i < 6; ++i) ph[i] += static_cast<double>(prof[k * 8 + i + 1] - prof[k * 8 + i]) / nk;
     for (int k = 0; k < nk; ++k) rounds += static_cast<double>(prof[k * 8 + 7]) / nk;
+    long long ms[2];
+    cudaMemcpyFromSymbol(ms, lt_ms_prof, sizeof(ms));
+    std::printf("   multisection of pencil 0: %.0f cycles per Sturm call over %lld calls\n", ms[1] ? double(ms[0]) / ms[1] : 0.0, ms[1]);
     std::printf("%s count %5d m0 %2d NM %2d G %4d BS %4d: kernel %8.1f us | cycles load %7.0f herm %7.0f chol %7.0f "
                 "reduce %7.0f hh %7.0f bisect %7.0f rounds %4.1f | err %s\n",
                 VEC ? "vec" : (RE ? "real" : "val"), count, m0, NM, G, BS, best * 1e3, ph[0], ph[1], ph[2], ph[3], ph[4], ph[5], rounds,
@@ -85,7 +92,7 @@ static void run(int count, int m0, int reps) {
 }
 
 int main() {
-    run<8, 32, 32>(32, 8, 5);
+    run<8, 32, 64>(32, 8, 5);
     run<8, 64, 64>(32, 8, 5);
     run<8, 128, 128>(32, 8, 5);
     run<8, 32, 64>(4096, 8, 5);
