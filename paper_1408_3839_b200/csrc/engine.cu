@@ -186,8 +186,10 @@ struct lt_ctx {
     int* pinned = nullptr;  // small pinned read-back buffer
     // side streams for independent branches of the assembly (captured into the same graph
     // as parallel branches) and the fork/join events between them
-    cudaStream_t aux[3]{nullptr, nullptr, nullptr};  // 0, 1: assembly branches; 2: L0 check under speculation
-    cudaEvent_t ev[11]{};  // fork/join points of run_assembly (0-5, 9-10), the L0 branch (6-7), external streams (8)
+    // 0, 1: assembly branches; 2: L0 check under speculation; 3: second FEM fold
+    cudaStream_t aux[4]{nullptr, nullptr, nullptr, nullptr};
+    // fork/join points of run_assembly (0-5, 9-12), the L0 branch (6-7), external streams (8)
+    cudaEvent_t ev[13]{};
     // pinned staging for the small per-call host<->device copies (system, window starts,
     // DFT index maps, eigenvalue read-back): async copies instead of pageable round trips.
     // Valid between stage_begin() (stream idle) and the end of the API call.
@@ -808,12 +810,19 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
             J.ws = wsf[l] = A.get<double>("fem.ws" + std::to_string(l), m0 * (d.Gbar + 2));
         }
         launch_fem_apply(LF, fj, nfj, static_cast<int>(m0));
+        // the distinct directions' folds are independent: the second runs on its own branch
+        // (c5: the two folds were the longest chain before the Khatri-Rao combine)
+        const bool fem_fork = nfj >= 2 && !serial;
+        const Launch LF2 = fem_fork ? c->LA(3) : LF;
+        if (fem_fork) c->join(11, c->aux[fi], c->aux[3]);
+        int nfold = 0;
         for (int l = 0; l < 3; ++l) {
             if (src[l] != l) {
                 w.massT[l] = w.massT[src[l]];
                 w.stiffT[l] = w.stiffT[src[l]];
                 continue;
             }
+            const Launch& LFd = nfold++ == 1 ? LF2 : LF;
             const DirPlan& d = p.d[l];
             w.massT[l] = A.get<double>("fem.mass" + std::to_string(l), d.width * mm);
             w.stiffT[l] = A.get<double>("fem.stiff" + std::to_string(l), d.width * mm);
@@ -841,8 +850,9 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
             f.sup_lo = w.pwl_lo[l];  // b = T v: one point wider on each side
             f.sup_hi = w.pwl_hi[l];
             f.bwiden = 1;
-            launch_resfold(LF, f, true, true, "fem_fold");
+            launch_resfold(LFd, f, true, true, "fem_fold");
         }
+        if (fem_fork) c->join(12, c->aux[3], c->aux[fi]);
     }
     // nuclear contraction: choose the reassociation (k_nuclear2.cu header)
     KRArgs kr_fused;  // the combine deferred to the fill point (AS_EMAJOR)
@@ -2001,6 +2011,7 @@ lt_status lt_create(int device, lt_ctx** out) {
         LT_CU(cudaStreamCreateWithPriority(&c->aux[0], cudaStreamNonBlocking, prio_hi));
         LT_CU(cudaStreamCreateWithPriority(&c->aux[1], cudaStreamNonBlocking, prio_hi));
         LT_CU(cudaStreamCreateWithPriority(&c->aux[2], cudaStreamNonBlocking, prio_hi));
+        LT_CU(cudaStreamCreateWithPriority(&c->aux[3], cudaStreamNonBlocking, prio_hi));
         for (auto& e : c->ev) LT_CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         LT_CU(cudaMalloc(&c->pencil_done, sizeof(unsigned)));
         LT_CU(cudaMemset(c->pencil_done, 0, sizeof(unsigned)));

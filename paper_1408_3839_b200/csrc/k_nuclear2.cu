@@ -558,9 +558,73 @@ __global__ void __launch_bounds__(256) k_fgemm(int mm, int Rtot, long long n, in
         }
 }
 
+// K <= kFgemmK (residues per cell): 32 x 32 output tiles on 128 threads (4 warps of 16 x 16),
+// the whole K staged at once. At c5 (Rtot ~ 100, 7 x 64 columns) the 64 x 64 tiles make only
+// 14 CTAs, each walking 64 x 64 x K on DMMA; the quarter tiles spread the same work over 4x
+// the SMs and finish in roughly a quarter of the time.
+constexpr int kFsBM = 32, kFsBN = 32;
+constexpr int kFsLDA = kFgemmK + 4;  // conflict-free m16n8k4 A-fragment reads
+constexpr int kFsLDB = kFsBN + 8;    // conflict-free B-fragment reads
+__global__ void __launch_bounds__(128) k_fgemm_s(int mm, int Rtot, int K, int ncols, const double* __restrict__ P,
+                                                 const double* __restrict__ Qf, double* __restrict__ T) {
+    __shared__ double As[kFsBM * kFsLDA];    // [m][k]
+    __shared__ double Bs[kFgemmK * kFsLDB];  // [k][n]
+    const int r0 = blockIdx.y * kFsBM;
+    const int c0 = blockIdx.x * kFsBN;
+    {
+        constexpr int kPer = kFsBM * kFgemmK / 128;
+        double va[kPer], vb[kPer];
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            const int e = threadIdx.x + 128 * u;
+            const int m = e / kFgemmK, k = e % kFgemmK;  // A: k fastest
+            va[u] = (k < K && r0 + m < Rtot) ? P[static_cast<long long>(r0 + m) * K + k] : 0.0;
+            const int kb = e / kFsBN, nn = e % kFsBN;  // B: n fastest
+            vb[u] = (kb < K && c0 + nn < ncols) ? Qf[static_cast<long long>(kb) * ncols + c0 + nn] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            const int e = threadIdx.x + 128 * u;
+            As[(e / kFgemmK) * kFsLDA + e % kFgemmK] = va[u];
+            Bs[(e / kFsBN) * kFsLDB + e % kFsBN] = vb[u];
+        }
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wm = warp & 1, wn = warp >> 1;
+    const int g = lane >> 2, t = lane & 3;
+    double acc[2][4] = {};
+    const int Kp = (K + 3) & ~3;  // columns K .. Kp-1 were loaded as zeros
+    for (int ks = 0; ks < Kp; ks += 4) {
+        const double a0 = As[(wm * 16 + g) * kFsLDA + ks + t];
+        const double a1 = As[(wm * 16 + g + 8) * kFsLDA + ks + t];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) dmma_m16n8k4(acc[nt], a0, a1, Bs[(ks + t) * kFsLDB + wn * 16 + nt * 8 + g]);
+    }
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int m = wm * 16 + g + 8 * (i >> 1), nn = wn * 16 + nt * 8 + 2 * t + (i & 1);
+            if (r0 + m < Rtot && c0 + nn < ncols) {
+                const int col = c0 + nn;
+                const int dd = col / mm, e = col % mm;
+                T[(static_cast<long long>(dd) * mm + e) * Rtot + r0 + m] = acc[nt][i];  // [d][e][r]
+            }
+        }
+}
+
 void launch_fgemm(const Launch& L, int m0, int Rtot, const DirPlan& d, const double* P, const double* Qf, double* T) {
     const int mm = m0 * m0;
     const int ncols = static_cast<int>(d.band + 1) * mm;
+    if (d.n <= kFgemmK) {
+        Stage st_(L, "fold_gemm");
+        k_fgemm_s<<<dim3((ncols + kFsBN - 1) / kFsBN, (Rtot + kFsBM - 1) / kFsBM), 128, 0, L.st>>>(
+            mm, Rtot, static_cast<int>(d.n), ncols, P, Qf, T);
+        LT_CU(cudaGetLastError());
+        L.tick();
+        return;
+    }
     dim3 grid((ncols + kGBN - 1) / kGBN, (Rtot + kGBM - 1) / kGBM);
     const size_t smem = d.n <= kFgemmK ? sizeof(double) * (kGBM * kFgemmLDA + kFgemmK * kFgemmLDB) : 0;
     static bool attr = false;
