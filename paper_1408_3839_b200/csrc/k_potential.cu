@@ -3,9 +3,14 @@
 //   launch_master      newton_kernel.cpp:22-45: f(i,q) = sqrt(pi)/(2 t_q) (erf(t_q x_{i+1}) - erf(t_q x_i))
 //                      on the centred cell grid x_i = -n h/2 + i h (grid.hpp:28-38)
 //   launch_window_sum  canonical_tensor.cpp:123-164: out[i] = sum_k m[s0 + i + k*step] over the
-//                      lattice shifts; uniform progressions use the reference's running sum
-//                      out[i] = out[i-step] + m[s0+i+(K-1)step] - m[s0+i-step] (same
-//                      recurrence, same rounding), one thread per residue class.
+//                      lattice shifts. Uniform progressions (k_window_sum_staged): a CTA bulk-copies
+//                      (cp.async.bulk + mbarrier) the master range its output chunk reads into
+//                      shared memory once, then every residue class of the chunk is cut into
+//                      segments: the segment head is a direct K-term sum, the rest follows by the
+//                      reference's recurrence out[i] = out[i-step] + m[s0+i+(K-1)step] - m[s0+i-step]
+//                      (restarted every segment, so the rounding differs from the reference's one
+//                      long chain by a few ulps of the largest term). Ranges that do not fit shared
+//                      memory keep one thread per residue class (k_window_sum_uniform).
 //
 // Window kernels read the master panel (MasterArray) or, where every cell would be read
 // exactly once (one nucleus, one window), evaluate the cells in place (MasterFused, the
@@ -15,6 +20,9 @@
 // of the concatenated lattice tensor = v*R_N + q (nucleus-major, canonical_tensor.cpp:166-187).
 #include "lt_device.cuh"
 #include "lt_internal.cuh"
+#include "tma.cuh"
+
+#include <type_traits>
 
 namespace lt {
 
@@ -85,6 +93,73 @@ __global__ void k_window_sum_uniform(Src src, Index RN, Index nnuc, const Index*
     }
 }
 
+// uniform progression staged through shared memory: CTA = (output chunk [i0, i0 + chunk), column
+// v*RN + q). Lanes run along the residue r (coalesced stores, conflict-free shared loads),
+// segments of Tl consecutive lattice steps along the rest of the CTA.
+constexpr int kWsNT = 512;
+constexpr Index kWsMaxSpan = 26000;  // doubles of master range per CTA (208 KB)
+__global__ void __launch_bounds__(kWsNT) k_window_sum_staged(const double* __restrict__ m, Index mrows, Index RN,
+                                                             const Index* __restrict__ s0v, int K, int step, Index size,
+                                                             int chunk, int Tl, double* __restrict__ out) {
+    extern __shared__ __align__(16) double ws_sm[];
+    __shared__ uint64_t bar;
+    const Index col = blockIdx.y;
+    const Index v = col / RN, q = col % RN;
+    const Index i0 = static_cast<Index>(blockIdx.x) * chunk;
+    const int cnt = static_cast<int>(min(static_cast<Index>(chunk), size - i0));
+    const int span = cnt + (K - 1) * step;
+    const Index A0 = q * mrows + s0v[v] + i0;  // first master element of this CTA
+    double* s = ws_sm + (A0 & 1);               // s[j] = m[A0 + j]; even master elements 16-byte aligned
+    const Index Ab = (A0 + 1) & ~static_cast<Index>(1), Ae = (A0 + span) & ~static_cast<Index>(1);
+    const bool bulk = Ae > Ab;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && bulk) {
+        mbar_arrive_expect_tx(&bar, static_cast<unsigned>((Ae - Ab) * 8));
+        for (Index a = Ab; a < Ae; a += 4096) {
+            const Index nb = min(static_cast<Index>(4096), Ae - a);
+            tma_bulk_1d(s + (a - A0), m + a, static_cast<unsigned>(nb * 8), &bar);
+        }
+    }
+    // the odd ends of the range (the bulk copy moves 16-byte units)
+    if (threadIdx.x == 32 && (A0 & 1)) s[0] = m[A0];
+    if (threadIdx.x == 64 && ((A0 + span) & 1)) s[span - 1] = m[A0 + span - 1];
+    if (bulk) mbar_wait(&bar, 0);
+    __syncthreads();
+    const int nres = min(step, cnt);
+    const int T = (cnt + step - 1) / step;
+    const int S = (T + Tl - 1) / Tl;
+    double* o = out + col * size + i0;
+    for (int item = threadIdx.x; item < nres * S; item += kWsNT) {
+        const int r = item % nres, seg = item / nres;
+        const int t0 = seg * Tl, t1 = min(T, t0 + Tl);
+        const double* p = s + r + static_cast<size_t>(t0) * step;
+        int i = r + t0 * step;
+        if (i >= cnt) continue;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int k = 0;
+        for (; k + 3 < K; k += 4) {
+            a0 += p[static_cast<size_t>(k) * step];
+            a1 += p[static_cast<size_t>(k + 1) * step];
+            a2 += p[static_cast<size_t>(k + 2) * step];
+            a3 += p[static_cast<size_t>(k + 3) * step];
+        }
+        for (; k < K; ++k) a0 += p[static_cast<size_t>(k) * step];
+        double acc = (a0 + a1) + (a2 + a3);
+        o[i] = acc;
+        for (int t = t0 + 1; t < t1; ++t) {
+            i += step;
+            if (i >= cnt) break;
+            const int u = t - t0;
+            acc = __dsub_rn(__dadd_rn(acc, p[static_cast<size_t>(u + K - 1) * step]), p[static_cast<size_t>(u - 1) * step]);
+            o[i] = acc;
+        }
+    }
+}
+
 // size <= step (the periodic cell window: every residue class holds one output): no
 // running-sum recurrence. CTA = 8 warps over 32 consecutive outputs r (coalesced reads
 // along r); warp w sums the k-slice k = w, w+8, ...; the 8 slice sums are added in warp
@@ -132,6 +207,36 @@ static void window_sum(const Launch& L, const Src& src, Index RN, Index nnuc, co
         k_window_sum_short<<<static_cast<unsigned>(blocks), 256, 0, L.st>>>(src, RN, nnuc, s0_dev, nsum, step, size,
                                                                               out);
     } else if (nsum >= 2) {
+        if constexpr (std::is_same_v<Src, MasterArray>) {
+            const Index ov = (nsum - 1) * step;
+            if (ov + std::min(size, step) + 2 <= kWsMaxSpan && nsum < (1 << 20) && step < (1 << 20)) {
+                // chunks of whole lattice steps: enough CTAs for two per SM, at least four steps each
+                const Index cols = nnuc * RN;
+                const Index want = std::max<Index>(1, (296 + cols - 1) / cols);
+                Index chunk = ((size + want - 1) / want + step - 1) / step * step;
+                chunk = std::max(chunk, std::min(size, 4 * step));
+                chunk = std::min(chunk, std::max<Index>(1, (kWsMaxSpan - ov - 2) / step) * step);
+                if (size <= step) chunk = size;
+                const Index nchunks = (size + chunk - 1) / chunk;
+                const Index T = (chunk + step - 1) / step, nres = std::min(step, chunk);
+                const Index S = std::max<Index>(1, std::min(T, kWsNT / std::max<Index>(1, std::min<Index>(nres, kWsNT))));
+                const Index Tl = (T + S - 1) / S;
+                const size_t smem = sizeof(double) * static_cast<size_t>(chunk + ov + 2);
+                static bool attr = false;
+                if (!attr) {
+                    LT_CU(cudaFuncSetAttribute(k_window_sum_staged, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(sizeof(double) * (kWsMaxSpan + 2))));
+                    attr = true;
+                }
+                dim3 grid(static_cast<unsigned>(nchunks), static_cast<unsigned>(cols));
+                k_window_sum_staged<<<grid, kWsNT, smem, L.st>>>(src.m, src.mrows, RN, s0_dev, static_cast<int>(nsum),
+                                                                  static_cast<int>(step), size, static_cast<int>(chunk),
+                                                                  static_cast<int>(Tl), out);
+                LT_CU(cudaGetLastError());
+                L.tick();
+                return;
+            }
+        }
         const Index nres = std::min(step, size);
         const Index threads = nnuc * RN * nres;
         k_window_sum_uniform<<<static_cast<unsigned>((threads + 127) / 128), 128, 0, L.st>>>(src, RN, nnuc, s0_dev,
