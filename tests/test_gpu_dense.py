@@ -38,7 +38,7 @@ def test_tridiagonal_eigenvalues(ctx, n):
         assert np.all(np.diff(ev) >= 0), name
 
 
-@pytest.mark.parametrize("n", [40, 129, 300, 512, 1024])
+@pytest.mark.parametrize("n", [40, 129, 300, 512, 513, 777, 1024])
 def test_dense_pencil_reduction(ctx, oracle, n):
     rng = np.random.default_rng(7 + n)
     A = rng.uniform(-1, 1, (n, n))
