@@ -335,13 +335,24 @@ __global__ void __launch_bounds__(NT) k_sytrd_reg(int n, int P, const double* __
                         if (i >= rnext && i < n) cdst[i] = a[u][s];
                     }
         }
+        // warp transpose-reduction: CM - 1 exchanges leave lane l with column l % CM summed over
+        // its CM-lane group, the remaining offsets add the groups (instead of 5 CM shuffles)
+        double pt[CM];
 #pragma unroll
-        for (int s = 0; s < CM; ++s) {
-            double v = part[s];
+        for (int s = 0; s < CM; ++s) pt[s] = part[s];
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            if (lane == 0) cred[warp][s] = v;
+        for (int off = CM / 2; off >= 1; off >>= 1) {
+            const bool up = (lane & off) != 0;
+#pragma unroll
+            for (int i = 0; i < off; ++i) {
+                const double send = up ? pt[i] : pt[i + off];
+                const double keep = up ? pt[i + off] : pt[i];
+                pt[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+            }
         }
+#pragma unroll
+        for (int o = CM; o < 32; o <<= 1) pt[0] += __shfl_xor_sync(0xffffffffu, pt[0], o);
+        if (lane < CM) cred[warp][lane] = pt[0];
         __syncthreads();
         if (static_cast<int>(threadIdx.x) < CM) {
             const int s = threadIdx.x;
@@ -426,17 +437,33 @@ __global__ void __launch_bounds__(NT) k_sytrd_reg(int n, int P, const double* __
             vni[u] = (i > r0 && i < n) ? svn[i] : 0.0;
         }
         double cp[CM];
+        // groups of 4 columns: a group whose columns are all reduced is skipped (uniform branch);
+        // inside a group the arithmetic is branch-free (reduced columns get w_j = v_j = 0), so the
+        // shared-memory loads and the FP64 chains of the columns overlap
 #pragma unroll
-        for (int s = 0; s < CM; ++s) {
-            cp[s] = 0.0;
-            const int j = b + s * P;
-            if (j > r0 && j < n) {
-                const double wj = sw[j], vj = sv[j];
+        for (int g4 = 0; g4 < CM; g4 += 4) {
+            if (b + (g4 + 3) * P > r0) {
+                double wj[4], vj[4];
 #pragma unroll
-                for (int u = 0; u < R; ++u) {
-                    a[u][s] -= fma(vi[u], wj, wi[u] * vj);  // rows < r0 carry v = w = 0
-                    cp[s] = fma(a[u][s], vni[u], cp[s]);
+                for (int s = 0; s < 4; ++s) {
+                    const int j = b + (g4 + s) * P;
+                    const bool ok = j > r0 && j < n;
+                    wj[s] = ok ? sw[j] : 0.0;
+                    vj[s] = ok ? sv[j] : 0.0;
                 }
+#pragma unroll
+                for (int s = 0; s < 4; ++s) {
+                    double c0 = 0.0;
+#pragma unroll
+                    for (int u = 0; u < R; ++u) {
+                        a[u][g4 + s] -= fma(vi[u], wj[s], wi[u] * vj[s]);  // rows < r0 carry v = w = 0
+                        c0 = fma(a[u][g4 + s], vni[u], c0);
+                    }
+                    cp[g4 + s] = c0;
+                }
+            } else {
+#pragma unroll
+                for (int s = 0; s < 4; ++s) cp[g4 + s] = 0.0;
             }
         }
         SYPROF(0);
