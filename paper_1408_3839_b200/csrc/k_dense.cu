@@ -587,6 +587,9 @@ __global__ void __launch_bounds__(BS) k_tridiag_eig3(int n, const double* __rest
 
 // A = 0.5 (A + A^T) in place: CTA per tile pair (bi >= bj), 32 x 32 tiles
 
+#ifdef LT_SYTRD_PROF
+long long* lt_sytrd_prof_ptr = nullptr;
+#endif
 static size_t sytrd_smem(int n, int cols) {
     return sizeof(double) * (static_cast<size_t>(cols) * n + 4 * static_cast<size_t>(n) + cols);
 }
@@ -624,7 +627,10 @@ void launch_sytrd(const Launch& L, int n, const double* C, double* d, double* e,
     constexpr int NT = 256;
     const int P = sytrd_ctas(n);
     if (P == 0) fail(LT_EGENERIC, "sytrd: matrix too large for the shared-memory resident reduction");
-    long long* pp = nullptr;  // per-phase cycle counters (tools/ probes only)
+    long long* pp = nullptr;  // per-phase cycle counters (tools/sytrd_phases.cu only)
+#ifdef LT_SYTRD_PROF
+    pp = lt_sytrd_prof_ptr;
+#endif
     // own columns in registers when they fit (n <= 256 R, ceil(n / P) <= CM), else in shared memory
     const bool reg = (try_sytrd_reg<256, 2, 4>(L, n, P, C, d, e, work, bar, pp) ||
                                     try_sytrd_reg<256, 4, 8>(L, n, P, C, d, e, work, bar, pp));

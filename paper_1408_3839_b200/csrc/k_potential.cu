@@ -133,6 +133,21 @@ __global__ void __launch_bounds__(kWsNT) k_window_sum_staged(const double* __res
     const int T = (cnt + step - 1) / step;
     const int S = (T + Tl - 1) / Tl;
     double* o = out + col * size + i0;
+    // block sums over Tl consecutive lattice steps (one shared load per staged element): a
+    // segment head is then K / Tl block sums plus the K mod Tl remaining terms
+    const int nfull = Tl >= 2 ? K / Tl : 0;
+    double* bs = ws_sm + ((span + 3) & ~1);  // [NB][nres]
+    if (nfull > 0) {
+        const int NB = (T + K - 1 + Tl - 1) / Tl;
+        for (int item = threadIdx.x; item < nres * NB; item += kWsNT) {
+            const int r = item % nres, c = item / nres;
+            int j = r + c * Tl * step;
+            double a0 = 0.0;
+            for (int u = 0; u < Tl && j < span; ++u, j += step) a0 += s[j];  // past the span: no output reads it
+            bs[item] = a0;
+        }
+        __syncthreads();
+    }
     for (int item = threadIdx.x; item < nres * S; item += kWsNT) {
         const int r = item % nres, seg = item / nres;
         const int t0 = seg * Tl, t1 = min(T, t0 + Tl);
@@ -140,7 +155,18 @@ __global__ void __launch_bounds__(kWsNT) k_window_sum_staged(const double* __res
         int i = r + t0 * step;
         if (i >= cnt) continue;
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        int k = 0;
+        {
+            const double* b = bs + static_cast<size_t>(seg) * nres + r;
+            int c = 0;
+            for (; c + 3 < nfull; c += 4) {
+                a0 += b[static_cast<size_t>(c) * nres];
+                a1 += b[static_cast<size_t>(c + 1) * nres];
+                a2 += b[static_cast<size_t>(c + 2) * nres];
+                a3 += b[static_cast<size_t>(c + 3) * nres];
+            }
+            for (; c < nfull; ++c) a0 += b[static_cast<size_t>(c) * nres];
+        }
+        int k = nfull * Tl;
         for (; k + 3 < K; k += 4) {
             a0 += p[static_cast<size_t>(k) * step];
             a1 += p[static_cast<size_t>(k + 1) * step];
@@ -209,23 +235,31 @@ static void window_sum(const Launch& L, const Src& src, Index RN, Index nnuc, co
     } else if (nsum >= 2) {
         if constexpr (std::is_same_v<Src, MasterArray>) {
             const Index ov = (nsum - 1) * step;
-            if (ov + std::min(size, step) + 2 <= kWsMaxSpan && nsum < (1 << 20) && step < (1 << 20)) {
-                // chunks of whole lattice steps: enough CTAs for two per SM, at least four steps each
+            if (ov + std::min(size, step) + 8 <= kWsMaxSpan && nsum < (1 << 20) && step < (1 << 20)) {
+                // chunks of whole lattice steps: about one CTA per SM (every chunk re-reads the
+                // (K - 1) step halo, so fewer, larger chunks move less), segments of Tl steps with
+                // Tl ~ sqrt(K / 2) balancing the K / Tl block sums of a head against its 2 Tl updates
                 const Index cols = nnuc * RN;
-                const Index want = std::max<Index>(1, (296 + cols - 1) / cols);
-                Index chunk = ((size + want - 1) / want + step - 1) / step * step;
-                chunk = std::max(chunk, std::min(size, 4 * step));
-                chunk = std::min(chunk, std::max<Index>(1, (kWsMaxSpan - ov - 2) / step) * step);
-                if (size <= step) chunk = size;
-                const Index nchunks = (size + chunk - 1) / chunk;
-                const Index T = (chunk + step - 1) / step, nres = std::min(step, chunk);
-                const Index S = std::max<Index>(1, std::min(T, kWsNT / std::max<Index>(1, std::min<Index>(nres, kWsNT))));
-                const Index Tl = (T + S - 1) / S;
-                const size_t smem = sizeof(double) * static_cast<size_t>(chunk + ov + 2);
+                Index nchunks = std::max<Index>(1, std::min<Index>(148 / std::max<Index>(cols, 1), (size + 4 * step - 1) / (4 * step)));
+                Index chunk = size, Tl = 1;
+                size_t smem = 0;
+                for (;; ++nchunks) {
+                    chunk = size <= step ? size : ((size + nchunks - 1) / nchunks + step - 1) / step * step;
+                    const Index T = (chunk + step - 1) / step, nres = std::min(step, chunk);
+                    const Index S = std::max<Index>(1, std::min<Index>(T, kWsNT / std::min<Index>(nres, kWsNT)));
+                    Index root = 1;
+                    while (2 * (root + 1) * (root + 1) <= nsum) ++root;
+                    Tl = std::max((T + S - 1) / S, std::min(T, root));
+                    const Index NB = Tl >= 2 ? (T + nsum - 1 + Tl - 1) / Tl : 0;
+                    smem = sizeof(double) * static_cast<size_t>(chunk + ov + 6 + NB * nres);
+                    if (smem <= sizeof(double) * (kWsMaxSpan + 2) || chunk <= step) break;
+                }
+                if (smem > sizeof(double) * (kWsMaxSpan + 2)) Tl = 1, smem = sizeof(double) * static_cast<size_t>(chunk + ov + 6);
+                nchunks = (size + chunk - 1) / chunk;
                 static bool attr = false;
                 if (!attr) {
                     LT_CU(cudaFuncSetAttribute(k_window_sum_staged, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               static_cast<int>(sizeof(double) * (kWsMaxSpan + 2))));
+                                               static_cast<int>(sizeof(double) * (kWsMaxSpan + 8))));
                     attr = true;
                 }
                 dim3 grid(static_cast<unsigned>(nchunks), static_cast<unsigned>(cols));
