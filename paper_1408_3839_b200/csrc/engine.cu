@@ -711,7 +711,9 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
             j.step = d.h;
             j.align = 0.5;
             j.dir = l;
-            j.values = w.pwc[l] = A.get<double>("prof.pwc" + std::to_string(l), m0 * d.G);
+            // slack on both sides: the Toeplitz TMA view of the resident Hankel kernel
+            const Index pad = d.band * d.n, padb = (d.band + 260) * d.n;
+            j.values = w.pwc[l] = A.get<double>("prof.pwc" + std::to_string(l), m0 * d.G + pad + padb) + pad;
             j.lo = w.pwc_lo[l] = A.get<unsigned long long>("prof.pwc_lo" + std::to_string(l), m0);
             j.hi = w.pwc_hi[l] = A.get<unsigned long long>("prof.pwc_hi" + std::to_string(l), m0);
             jobs[nj++] = j;
@@ -917,16 +919,17 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
                 const DirPlan& d = p.d[ndir];
                 double* V = nullptr;
                 if (!p.periodic) {  // periodic: V is formed per residue inside the fold
-                    V = A.get<double>("nuc.V", mm * d.pot_rows);
+                    V = A.get<double>("nuc.V", mm * d.pot_rows + (d.L + 260) * d.n);  // + the Hankel TMA view's slack
                     launch_vgemm(L, static_cast<int>(mm), static_cast<int>(Rtot), d.pot_rows, W, w.pot[ndir], V);
                 }
                 w.N = A.get<double>("nuc.N", d.L * d.width * mm);
                 if (!p.periodic) {
                     const int nt = static_cast<int>(((d.L + 63) / 64) * ((d.width + 63) / 64) * mm);
-                    const int sp = splits_for(nt, d.G);
+                    const int rs = d.pot_rows == d.G ? hankel_res_splits(d) : 0;  // the resident kernel's quota slots
+                    const int sp = rs > 0 ? rs : splits_for(nt, d.G);
                     double* hp = A.get<double>("nuc.hpart", static_cast<size_t>(sp) * mm * d.L * d.width);
                     launch_hankel(L, static_cast<int>(m0), d, w.pwc[ndir], w.pwc_lo[ndir], w.pwc_hi[ndir], V, hp, w.N,
-                                  sp);
+                                  sp, d.pot_rows == d.G);
                 } else {
                     ResFold f;
                     f.m0 = static_cast<int>(m0);

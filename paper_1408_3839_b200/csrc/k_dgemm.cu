@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kThreads) k_dgemm_tn(const __grid_constant__ C
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
-CUtensorMap tma_map_2d(const double* base, long long rows, long long cols, long long ld, int box_rows) {
+bool tma_try_map_2d(CUtensorMap* out, const double* base, long long rows, long long cols, long long ld, int box_rows) {
     static std::mutex mu;
     static std::map<std::tuple<const double*, long long, long long, long long, int, int>, CUtensorMap> cache;
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
@@ -153,7 +153,10 @@ CUtensorMap tma_map_2d(const double* base, long long rows, long long cols, long 
     std::lock_guard<std::mutex> lk(mu);
     const auto key = std::make_tuple(base, rows, cols, ld, box_rows, dev);
     auto it = cache.find(key);
-    if (it != cache.end()) return it->second;
+    if (it != cache.end()) {
+        *out = it->second;
+        return true;
+    }
     if (!encode) {
         cudaDriverEntryPointQueryResult q;
         void* fn = nullptr;
@@ -161,8 +164,7 @@ CUtensorMap tma_map_2d(const double* base, long long rows, long long cols, long 
         if (q != cudaDriverEntryPointSuccess || !fn) fail(LT_ECUDA, "cuTensorMapEncodeTiled unavailable");
         encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     }
-    if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld * 8) % 16)
-        fail(LT_EGENERIC, "tma_map_2d: base must be 16-byte aligned and the row pitch a multiple of 16 bytes");
+    if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld * 8) % 16) return false;
     CUtensorMap m;
     std::memset(&m, 0, sizeof(m));
     const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
@@ -172,9 +174,18 @@ CUtensorMap tma_map_2d(const double* base, long long rows, long long cols, long 
     const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), gdim, gstride, box,
                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) fail(LT_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+    if (r != CUDA_SUCCESS) return false;
     if (cache.size() > 4096) cache.clear();
     cache.emplace(key, m);
+    *out = m;
+    return true;
+}
+
+CUtensorMap tma_map_2d(const double* base, long long rows, long long cols, long long ld, int box_rows) {
+    CUtensorMap m;
+    if (!tma_try_map_2d(&m, base, rows, cols, ld, box_rows))
+        fail(LT_EGENERIC, "tma_map_2d: base must be 16-byte aligned, the row pitch a multiple of 16 bytes and the "
+                          "shape encodable (cuTensorMapEncodeTiled)");
     return m;
 }
 

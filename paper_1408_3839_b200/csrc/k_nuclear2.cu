@@ -20,6 +20,7 @@
 #include "dmma.cuh"
 #include "lt_device.cuh"
 #include "lt_internal.cuh"
+#include "tma.cuh"
 
 namespace lt {
 
@@ -462,6 +463,198 @@ __global__ void __launch_bounds__(256) k_hankel(int m0, long long Lc, long long 
         }
 }
 
+// The same product with the operands RESIDENT in shared memory. As per-stage tiles,
+// A(k, j) = V_e[j + k n] re-reads every element of V_e once per cell k (128-fold at c3; measured:
+// tile loads by TMA boxes or by plain loads both run at the L2 -> SM rate, 141-145 us at c3).
+// Here a CTA loads the part of V_e its (cell tile, j range) touches ONCE, as the row-major
+// [rows][n] reshaping of the vector: n / 16 TMA box loads (cp.async.bulk.tensor, SWIZZLE_128B
+// boxes of 16 columns x RV rows) through a tensor map of pitch n over the flat array, and the
+// same for the Toeplitz view of the profile b_nu (rows reversed so the pitch is positive):
+//   A(k, jj)   = Vt[k + jj / n][jj % n]            Vt[r][c] = V_e[jA + (k0 + r) n + c]
+//   B(rho, jj) = bt[rho - rho0 + jj / n][jj % n]   bt[r][c] = b_nu[jA + (rho0 + r - band) n + c]
+// times a_mu[jA + jj] (a plain shared array) in registers; rho = width - 1 - (d + band). Every
+// DMMA fragment is a conflict-free read of a swizzled box; no barrier inside the j loop.
+// Elements a view reads outside [0, G) of its function (the next pair's V, a neighbouring
+// profile, the slack the caller leaves around the arrays) are masked by per-thread j limits.
+// CTA = 8 warps, warp w owns cells 16 w .. 16 w + 15 of the 128-cell tile and NBLK 8-offset
+// blocks; a CTA covers a fixed quota of `per` grid points of one pair's support overlap.
+namespace {
+constexpr int kHkM = 128, kHkN = 64;
+struct HankelShape {
+    int per_max = 0;    // j quota of one CTA (multiple of 16)
+    int RV = 0, RB = 0; // box rows of the V and profile tiles (multiples of 8, <= 256)
+    size_t smem = 0;    // bytes (incl. 1 KB alignment slack)
+};
+// shared-memory plan for row length n, `live` offsets per tile; per_max = 0 when nothing fits
+HankelShape hankel_shape(long long n, int live) {
+    HankelShape h;
+    if (n % 16 != 0 || n > 1024) return h;
+    const int nblk = (live + 7) / 8;
+    // the longest quota with two CTAs per SM (<= 110 KB each), else the longest that fits one
+    for (const size_t cap : {110u * 1024u, 200u * 1024u})
+        for (const int per : {640, 512, 384, 256, 128}) {
+            const long long RV = (kHkM + (per + n - 1) / n + 1 + 7) / 8 * 8;
+            const long long RB = (8 * nblk + (per + n - 1) / n + 1 + 7) / 8 * 8;
+            const size_t bytes = sizeof(double) * static_cast<size_t>((RV + RB) * n + per + 24) + 1024 + 64;
+            if (RV <= 256 && RB <= 256 && bytes <= cap) {
+                h.per_max = per;
+                h.RV = static_cast<int>(RV);
+                h.RB = static_cast<int>(RB);
+                h.smem = bytes;
+                return h;
+            }
+        }
+    return h;
+}
+}  // namespace
+
+#ifdef LT_HK_PROF
+__device__ unsigned long long lt_hk_prof[8];
+extern "C" void lt_debug_hk_prof(unsigned long long* out) {
+    cudaMemcpyFromSymbol(out, lt_hk_prof, sizeof(lt_hk_prof));
+    unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(lt_hk_prof, z, sizeof(z));
+}
+#endif
+template <int NBLK>  // live 8-offset blocks of the tile, ceil(live / 8)
+__global__ void __launch_bounds__(256) k_hankel_res(const __grid_constant__ CUtensorMap tv,
+                                                    const __grid_constant__ CUtensorMap tb, int m0, long long Lc, int n,
+                                                    int band, long long G, const double* __restrict__ pwc,
+                                                    const unsigned long long* __restrict__ plo,
+                                                    const unsigned long long* __restrict__ phi,
+                                                    double* __restrict__ part, int per, int RV, int RB) {
+    extern __shared__ __align__(1024) unsigned char hk_raw[];
+    double* hk_sm = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(hk_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    __shared__ uint64_t bar;
+    const int width = 2 * band + 1;
+    const int nkt = static_cast<int>((Lc + kHkM - 1) / kHkM);
+    const int kt = blockIdx.x % nkt, dt = blockIdx.x / nkt;
+    const int e = blockIdx.y, split = blockIdx.z;
+    const int mu = e % m0, nu = e / m0;
+    const long long k0c = static_cast<long long>(kt) * kHkM;
+    const int rho0 = dt * kHkN;
+    const int live = min(kHkN, width - rho0);
+    const long long dmax = width - 1 - rho0 - band, dmin = width - 1 - (rho0 + live - 1) - band;
+    const long long alo = static_cast<long long>(plo[mu]), ahi = static_cast<long long>(phi[mu]);
+    const long long blo = static_cast<long long>(plo[nu]), bhi = static_cast<long long>(phi[nu]);
+    const long long jlo = max(alo, blo + dmin * n), jhi = min(ahi, bhi + dmax * n);
+    // fixed quota of `per` grid points per CTA: a pair with a long support overlap takes more
+    // CTAs (splits = ceil(G / per) slots exist; the unused ones only write zeros)
+    const long long j0 = jlo + static_cast<long long>(split) * per, j1 = min(jhi, j0 + per);
+    const long long jA = j0 & ~1LL;  // box columns start on 16-byte boundaries
+    const int Lj = j1 > j0 ? static_cast<int>(j1 - jA) : 0;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int nbox = n / 16;
+    double* Vs = hk_sm;                                      // [nbox][RV][16] swizzled
+    double* bs = Vs + static_cast<size_t>(nbox) * RV * 16;   // [nbox][RB][16] swizzled
+    double* as = bs + static_cast<size_t>(nbox) * RB * 16;   // [per + 24]
+    double acc[NBLK][4];
+#pragma unroll
+    for (int j = 0; j < NBLK; ++j)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[j][q] = 0.0;
+#ifdef LT_HK_PROF
+    const long long tp0 = clock64();
+    long long tp1 = tp0;
+#endif
+    if (Lj > 0) {
+        if (threadIdx.x == 0) {
+            mbar_init(&bar, 1);
+            mbar_fence_init();
+            mbar_arrive_expect_tx(&bar, static_cast<unsigned>((RV + RB) * n * 8));
+            for (int b = 0; b < nbox; ++b) {
+                tma_load_2d(Vs + static_cast<size_t>(b) * RV * 16, &tv, &bar, static_cast<int>(e * G + jA + 16 * b),
+                            static_cast<int>(k0c));
+                tma_load_2d(bs + static_cast<size_t>(b) * RB * 16, &tb, &bar, static_cast<int>(nu * G + jA + 16 * b), rho0);
+            }
+        }
+        {
+            const double* am = pwc + static_cast<long long>(mu) * G;
+            for (int x = threadIdx.x; x < Lj + 16; x += 256) {
+                const long long j = jA + x;
+                as[x] = (j >= j0 && j < j1) ? am[j] : 0.0;  // trims the range to [j0, j1); zero tail
+            }
+        }
+        __syncthreads();  // the barrier is initialised, as[] written
+        mbar_wait(&bar, 0);
+#ifdef LT_HK_PROF
+        tp1 = clock64();
+#endif
+        if (k0c + warp * 16 < Lc) {
+            // per-thread j limits (relative to jA) inside which the views read their own function
+            auto clampi = [](long long v) { return static_cast<int>(max(-(1LL << 30), min(1LL << 30, v))); };
+            const int rA = warp * 16 + g;
+            const int limA0 = clampi(G - jA - (k0c + rA) * n), limA1 = clampi(G - jA - (k0c + rA + 8) * n);
+            int loB[NBLK], hiB[NBLK];
+#pragma unroll
+            for (int jn = 0; jn < NBLK; ++jn) {
+                const long long o = jA + static_cast<long long>(rho0 + jn * 8 + g - band) * n;  // b index at jj = 0
+                loB[jn] = clampi(-o);
+                hiB[jn] = clampi(G - o);
+            }
+            const int nrow = (Lj + n - 1) / n;
+            for (int row = 0; row < nrow; ++row) {
+                const int rsw = (g + row) & 7;  // the swizzle row phase, common to the A and B rows
+                int off[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) off[q] = ((((4 * q + t) >> 1) ^ rsw) << 1) + (t & 1);
+                const double* pa = Vs + (rA + row) * 16;
+                const double* pb = bs + (g + row) * 16;
+                const int xe = min(n, Lj - row * n);
+                for (int xb = 0; xb * 16 < xe; ++xb) {
+                    const double* pab = pa + static_cast<size_t>(xb) * RV * 16;
+                    const double* pbb = pb + static_cast<size_t>(xb) * RB * 16;
+                    const int jj0 = row * n + xb * 16 + t;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int jj = jj0 + 4 * q;
+                        const double aj = as[jj];  // zero outside [j0, j1)
+                        const double a0 = jj < limA0 ? pab[off[q]] : 0.0;
+                        const double a1 = jj < limA1 ? pab[off[q] + 128] : 0.0;
+#pragma unroll
+                        for (int jn = 0; jn < NBLK; ++jn) {
+                            const double b0 = (jj >= loB[jn] && jj < hiB[jn]) ? pbb[off[q] + jn * 128] * aj : 0.0;
+                            dmma_m16n8k4(acc[jn], a0, a1, b0);
+                        }
+                    }
+                }
+            }
+        }
+    }
+#ifdef LT_HK_PROF
+    if (threadIdx.x == 0 && Lj > 0) {
+        const long long tp2 = clock64();
+        atomicAdd(&lt_hk_prof[0], static_cast<unsigned long long>(tp1 - tp0));
+        atomicAdd(&lt_hk_prof[1], static_cast<unsigned long long>(tp2 - tp1));
+        atomicAdd(&lt_hk_prof[2], 1ull);
+        atomicAdd(&lt_hk_prof[3], static_cast<unsigned long long>(Lj));
+        atomicMax(&lt_hk_prof[4], static_cast<unsigned long long>(tp2 - tp0));
+    }
+#endif
+    if (k0c + warp * 16 >= Lc) return;
+    if (Lj == 0 && width <= kHkN) return;  // an unused quota slot: k_split_reduce_quota skips it
+    double* out = part + (static_cast<long long>(split) * m0 * m0 + e) * Lc * width;
+#pragma unroll
+    for (int jn = 0; jn < NBLK; ++jn)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const long long kc = k0c + warp * 16 + g + 8 * (q >> 1);
+            const int rl = jn * 8 + 2 * t + (q & 1);
+            const int di = width - 1 - rho0 - rl;
+            if (kc < Lc && rl < live) out[kc * width + di] = acc[jn][q];
+        }
+}
+
+// splits the resident kernel needs so that a CTA's j range fits its shared-memory plan (0: the
+// shape does not fit, the tile-loading k_hankel runs with the caller's splits)
+int hankel_res_splits(const DirPlan& d) {
+    if (d.L < 32) return 0;  // few cells: the 64-row tile kernel wastes less
+    const HankelShape h = hankel_shape(d.n, static_cast<int>(std::min<Index>(kHkN, d.width)));
+    if (h.per_max == 0) return 0;
+    return static_cast<int>((d.G + h.per_max - 1) / h.per_max);
+}
+
 // N[(k*width + d)][e] = sum_split part[split][e][k][d]
 __global__ void k_split_reduce(long long mm, long long kd, int splits, const double* __restrict__ part,
                                double* __restrict__ N) {
@@ -473,19 +666,83 @@ __global__ void k_split_reduce(long long mm, long long kd, int splits, const dou
     N[idx] = s;
 }
 
+// splits: hankel_res_splits(d) when that is non-zero (the resident kernel), else the caller's.
+// padded: band * n doubles of slack lie on both sides of pwc and L * n behind V (the TMA views
+// of the resident kernel touch them; their contents are never used).
+// the same for the resident kernel with one offset tile (width <= 64): pair e filled the first
+// ceil(len_e / per) quota slots (k_hankel_res's own range arithmetic), the rest were not written
+__global__ void k_split_reduce_quota(int m0, long long mm, long long kd, int splits, int per, long long n, int band,
+                                     const unsigned long long* __restrict__ plo,
+                                     const unsigned long long* __restrict__ phi, const double* __restrict__ part,
+                                     double* __restrict__ N) {
+    const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= mm * kd) return;
+    const long long e = idx % mm, q = idx / mm;
+    const int mu = static_cast<int>(e % m0), nu = static_cast<int>(e / m0);
+    const long long alo = static_cast<long long>(plo[mu]), ahi = static_cast<long long>(phi[mu]);
+    const long long blo = static_cast<long long>(plo[nu]), bhi = static_cast<long long>(phi[nu]);
+    const long long jlo = max(alo, blo - band * n), jhi = min(ahi, bhi + band * n);
+    const long long len = jhi > jlo ? jhi - jlo : 0;
+    const int used = static_cast<int>(min(static_cast<long long>(splits), (len + per - 1) / per));
+    double s = 0.0;
+    for (int sp = 0; sp < used; ++sp) s += part[(sp * mm + e) * kd + q];
+    N[idx] = s;
+}
+
 void launch_hankel(const Launch& L, int m0, const DirPlan& d, const double* pwc, const unsigned long long* lo,
-                   const unsigned long long* hi, const double* V, double* part, double* N, int splits) {
-    const int nkt = static_cast<int>((d.L + kGBM - 1) / kGBM);
-    const int ndt = static_cast<int>((d.width + kGBN - 1) / kGBN);
-    dim3 grid(nkt * ndt, m0 * m0, splits);
-    {
+                   const unsigned long long* hi, const double* V, double* part, double* N, int splits, bool padded) {
+    const long long mm = m0 * m0, kd = d.L * d.width;
+    const int rs = padded ? hankel_res_splits(d) : 0;
+    const HankelShape h = hankel_shape(d.n, static_cast<int>(std::min<Index>(kHkN, d.width)));
+    CUtensorMap tv, tb;
+    bool res = rs > 0 && rs == splits && mm * d.G + d.G < (1LL << 31);
+    // V as rows of pitch n over the flat array (row k, column e G + j -> V_e[j + k n]); the
+    // profiles as rows of pitch n starting band n before pwc (row rho, column nu G + j)
+    if (res)
+        res = tma_try_map_2d(&tv, V, d.L + h.RV, mm * d.G, d.n, h.RV) &&
+              tma_try_map_2d(&tb, pwc - d.band * d.n, d.width + h.RB, static_cast<long long>(m0) * d.G, d.n, h.RB);
+    if (res) {
+        const int nkt = static_cast<int>((d.L + kHkM - 1) / kHkM);
+        const int ndt = static_cast<int>((d.width + kHkN - 1) / kHkN);
+        dim3 grid(nkt * ndt, m0 * m0, splits);
+        Stage st_(L, "hankel_gemm");
+        // every offset tile of a launch runs the same instantiation: the block count of the
+        // fullest tile (tiles with fewer live offsets compute on masked rows)
+        const int nblk = static_cast<int>((std::min<Index>(kHkN, d.width) + 7) / 8);
+        auto run = [&](auto kern) {
+            static size_t attr = 0;
+            if (h.smem > attr) {
+                LT_CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(h.smem)));
+                attr = h.smem;
+            }
+            kern<<<grid, 256, h.smem, L.st>>>(tv, tb, m0, d.L, static_cast<int>(d.n), static_cast<int>(d.band), d.G, pwc, lo,
+                                              hi, part, h.per_max, h.RV, h.RB);
+        };
+        switch (nblk) {
+            case 1: run(k_hankel_res<1>); break;
+            case 2: run(k_hankel_res<2>); break;
+            case 3: run(k_hankel_res<3>); break;
+            case 4: run(k_hankel_res<4>); break;
+            case 5: run(k_hankel_res<5>); break;
+            case 6: run(k_hankel_res<6>); break;
+            case 7: run(k_hankel_res<7>); break;
+            default: run(k_hankel_res<8>); break;
+        }
+        LT_CU(cudaGetLastError());
+    } else {
+        const int nkt = static_cast<int>((d.L + kGBM - 1) / kGBM);
+        const int ndt = static_cast<int>((d.width + kGBN - 1) / kGBN);
+        dim3 grid(nkt * ndt, m0 * m0, splits);
         Stage st_(L, "hankel_gemm");
         k_hankel<<<grid, 256, 0, L.st>>>(m0, d.L, d.n, static_cast<int>(d.band), d.G, pwc, lo, hi, V, part, splits);
         LT_CU(cudaGetLastError());
     }
-    const long long mm = m0 * m0, kd = d.L * d.width;
     Stage st2_(L, "split_reduce");
-    k_split_reduce<<<static_cast<unsigned>((mm * kd + 255) / 256), 256, 0, L.st>>>(mm, kd, splits, part, N);
+    if (res && d.width <= kHkN)
+        k_split_reduce_quota<<<static_cast<unsigned>((mm * kd + 255) / 256), 256, 0, L.st>>>(
+            m0, mm, kd, splits, h.per_max, d.n, static_cast<int>(d.band), lo, hi, part, N);
+    else
+        k_split_reduce<<<static_cast<unsigned>((mm * kd + 255) / 256), 256, 0, L.st>>>(mm, kd, splits, part, N);
     LT_CU(cudaGetLastError());
     L.tick(2);
 }

@@ -295,7 +295,8 @@ void launch_triv_tables(const Launch& L, const TrivJobs& jobs, int njobs, const 
 void launch_vdot(const Launch& L, int mm, int Rtot, long long rows, const double* W, const double* P, double* V);
 void launch_vgemm(const Launch& L, int mm, int Rtot, long long rows, const double* W, const double* P, double* V);
 void launch_hankel(const Launch& L, int m0, const DirPlan& d, const double* pwc, const unsigned long long* lo,
-                   const unsigned long long* hi, const double* V, double* part, double* N, int splits);
+                   const unsigned long long* hi, const double* V, double* part, double* N, int splits, bool padded = false);
+int hankel_res_splits(const DirPlan& d);
 // ---- residue-class correlations on DMMA (k_fold.cu) ----
 struct FemApplyJob {
     const double* pwl = nullptr;  // [m0][Gbar]

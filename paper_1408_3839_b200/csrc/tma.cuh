@@ -76,5 +76,8 @@ __device__ __forceinline__ int swz128(int r, int c) { return r * 16 + ((((c >> 1
 // multiple of 16 and the base 16-byte aligned) with box {16 columns, box_rows rows},
 // SWIZZLE_128B, out-of-bounds elements read as zero. Cached by (base, rows, cols, ld, box).
 CUtensorMap tma_map_2d(const double* base, long long rows, long long cols, long long ld, int box_rows);
+// the same, returning false instead of failing when the driver rejects the shape (rows may
+// overlap: a pitch smaller than the row length gives the Hankel / Toeplitz views of k_hankel_tma)
+bool tma_try_map_2d(CUtensorMap* out, const double* base, long long rows, long long cols, long long ld, int box_rows);
 
 }  // namespace lt

@@ -107,3 +107,20 @@ def test_baseline_size_with_p_functions(ctx, oracle):
     oev = oracle.solve_periodic_ops(oH, oS)
     tol = eig_tolerance(oracle, True, oH, oS, oev)
     assert np.all(np.abs(ev - oev) <= tol), np.max(np.abs(ev - oev) / tol)
+
+
+@pytest.mark.parametrize("L,n", [(40, 16), (150, 16), (64, 32), (48, 24)])
+def test_box_chain_nuclear_hankel_shapes(ctx, oracle, L, n):
+    """The box-chain nuclear contraction (galerkin.cpp:224-247) across the shapes of the Hankel
+    kernels: a partly filled 128-cell tile (L = 40, 48, 64), two cell tiles (L = 150), rows of
+    16 and 32 points (the shared-memory resident TMA kernel) and of 24 points (not a multiple
+    of 16: the tile-loading kernel); H and S entries against Oracle-X."""
+    pos = [(-0.45, 0.1, 0.0), (0.5, 0.0, -0.2)]
+    sys = LatticeSystem(b=2.0, L=(L, 1, 1), n=(n, 8, 8), nbar=(n, 8, 8), quad_M=6, nuc_pos=pos, nuc_charge=[1.0, 2.0],
+                        bf_center=[pos[0], pos[1], pos[0], pos[1]], bf_alpha=[0.35, 2.5, 0.9, 6.0])
+    oH, oS = oracle.assemble_core(sys, False)
+    H, S = ctx.assemble_core(sys, False)
+    ok, worst = entries_close(H.dense(), oH.dense)
+    assert ok, worst
+    ok, worst = entries_close(S.dense(), oS.dense)
+    assert ok, worst
