@@ -758,7 +758,10 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
     c->join(0, c->stream, c->aux[fi]);
     c->join(1, c->stream, c->aux[pi]);
     if (root_hook) (*root_hook)(L);  // the L0 check under speculation: its own branch
-    if (prof_root) launch_sinc(LP, p.M, sd->ds, w.t, w.w, w.potw, shard.r0, shard.r1);
+    // (with the profiles as the root the sinc kernel goes ahead of the FEM chain, which has slack:
+    // on the second potential's stream it delayed that master and its lattice sum, the head of
+    // the nuclear chain, by its own 2 us)
+    if (prof_root) launch_sinc(LF, p.M, sd->ds, w.t, w.w, w.potw, shard.r0, shard.r1);
     else launch_profiles(LF, sd->ds, jobs, nj, 1e-280);
     if (nuc) {
         int nth = 0;
@@ -774,7 +777,7 @@ static void run_assembly(lt_ctx* c, const lt_sysdev* sd, const Plan& p, int need
             }
             const Launch& LL = (nth++ == 1) ? LP : L;
             w.pot[l] = A.get<double>("pot.panel" + std::to_string(l), d.pot_rows * Rtot);
-            if ((d.nsum == 1 && p.nnuc == 1) || (d.nsum >= 32 && d.pot_rows <= d.n && p.nnuc <= 2)) {
+            if ((d.nsum == 1 && p.nnuc == 1) || (d.nsum >= 8 && d.pot_rows <= d.n && p.nnuc <= 2)) {
                 // a single window copy of one nucleus: each master cell is read once, so it
                 // is evaluated in the copy kernel instead of being materialised first. The
                 // periodic cell window (one output per residue class) of <= 2 nuclei reads each

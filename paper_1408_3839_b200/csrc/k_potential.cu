@@ -228,7 +228,7 @@ template <class Src>
 static void window_sum(const Launch& L, const Src& src, Index RN, Index nnuc, const Index* s0_dev, Index nsum,
                        Index step, Index size, double* out) {
     Stage st_(L, "window_sum");
-    if (nsum >= 32 && size <= step) {
+    if (nsum >= 8 && size <= step) {
         const Index blocks = nnuc * RN * ((size + 31) / 32);
         k_window_sum_short<<<static_cast<unsigned>(blocks), 256, 0, L.st>>>(src, RN, nnuc, s0_dev, nsum, step, size,
                                                                               out);

@@ -9,7 +9,7 @@ O=gpurun_out/prof
 mkdir -p $O
 python bench.py > $O/${R}_bench.json 2> $O/${R}_bench.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 6000 --csv \
-    --log-file $O/${R}_c5_launches.csv python bench.py --steps 20 --warmup 3 --no-sweep --no-cpu-baseline \
+    --log-file $O/${R}_c5_launches.csv python bench.py --steps 20 --warmup 3 --secondary '' --no-sweep --no-cpu-baseline \
     > /dev/null 2>&1
 for c in c1 c2 c3 c4; do
     timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \

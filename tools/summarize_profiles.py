@@ -37,6 +37,7 @@ STAGE = {
     "k_vgemm": "vgemm", "k_real_to_complex": "r2c", "k_sytrd_reg": "sytrd", "k_sytrd": "sytrd",
     "k_tridiag_eig3": "tridiag_eig", "k_symmetrize": "symmetrize", "k_trtri_leaf": "trtri_leaf",
     "k_l0_peak": "l0_peak", "k_profiles": "profiles", "k_window_sum_short": "window_sum",
+    "k_window_sum_staged": "window_sum", "k_hankel_res": "hankel_gemm", "k_split_reduce_quota": "split_reduce",
     "k_pencil_lane": "pencil", "k_potf_leaf": "potf_leaf", "k_vdot": "vdot", "k_resfold": "nuc_fold",
 }
 
