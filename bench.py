@@ -310,9 +310,11 @@ class GpuArm:
         if stages:
             _, _, stage_tot = timed_region(True)
 
+        e2e_out = np.empty(count)  # the caller's result buffer, reused across calls (numpy's out=)
+
         def e2e_call(s):
             if world == 1:
-                return ctx.solve_core(s, periodic)
+                return ctx.solve_core(s, periodic, out=e2e_out)
             fn = solve_core_sharded if shard_bufs is not None else solve_core_distributed
             return fn(ctx, s, periodic).cpu().numpy()
 

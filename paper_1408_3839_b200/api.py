@@ -278,13 +278,19 @@ class Context:
         return self._wrap(h)
 
     # ------------------------------------------------------------------
-    def solve_core(self, sys: LatticeSystem, periodic: bool, info: Optional[np.ndarray] = None) -> np.ndarray:
-        """LatticeSystem -> eigenvalues on the host ([K, m0] periodic, [N_b] box)."""
+    def solve_core(self, sys: LatticeSystem, periodic: bool, info: Optional[np.ndarray] = None,
+                   out: Optional[np.ndarray] = None) -> np.ndarray:
+        """LatticeSystem -> eigenvalues on the host ([K, m0] periodic, [N_b] box). ``out``: a
+        C-contiguous float64 array of basis_count entries to receive them (numpy's ``out=``
+        convention: a buffer reused across calls skips the allocation and its page faults)."""
         c = sys.to_c()
-        out = np.zeros(sys.basis_count)
+        if out is None:
+            out = np.empty(sys.basis_count)
+        elif out.dtype != np.float64 or out.size != sys.basis_count or not out.flags.c_contiguous:
+            raise ValueError("solve_core: out must be a C-contiguous float64 array of basis_count entries")
         inf = np.zeros(8, dtype=np.int64) if info is None else info
         check(self.lib.lt_solve_core(self.h, ctypes.byref(c), int(periodic), _d(out), _i(inf)))
-        return out.reshape(sys.lattice_count, sys.m0) if periodic else out
+        return out.reshape(sys.lattice_count, sys.m0) if periodic else out.reshape(-1)
 
     def upload(self, sys: LatticeSystem) -> "DeviceSystem":
         return DeviceSystem(self, sys)

@@ -101,6 +101,19 @@ class LatticeSystem:
         return self.b / self.n[l]
 
     def to_c(self) -> LtSystem:
+        """The ``lt_system`` view of this object. The struct points at the numpy arrays (in-place
+        edits stay visible) and is rebuilt only when a field was re-assigned, so a call with
+        the same system does not pay the ctypes marshalling again."""
+        key = (self.b, self.L, self.n, self.nbar, self.quad_M, self.eps_ov, id(self.nuc_pos), id(self.nuc_charge),
+               id(self.bf_center), id(self.bf_alpha), id(self.bf_deg))
+        cached = self.__dict__.get("_c_cache")
+        if cached is not None and cached[0] == key:
+            return cached[1]
+        c = self._build_c()
+        self.__dict__["_c_cache"] = (key, c)
+        return c
+
+    def _build_c(self) -> LtSystem:
         c = LtSystem()
         c.b = self.b
         for l in range(3):
