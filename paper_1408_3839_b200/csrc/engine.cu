@@ -320,10 +320,6 @@ static void run_cached(lt_ctx* c, GraphCache& g, K&& keyfn, F&& enqueue) {
         c->timer.owned = nullptr;
         LT_CU(cudaStreamEndCapture(c->stream, &graph));
         g.timing = c->timer.take_pending(p0);
-        if (const char* dp = std::getenv("LT_GRAPH_DOT")) {
-            static int ndot = 0;
-            cudaGraphDebugDotPrint(graph, (std::string(dp) + std::to_string(ndot++) + ".dot").c_str(), cudaGraphDebugDotFlagsVerbose);
-        }
         const cudaError_t e = cudaGraphInstantiate(&g.exec, graph, 0);
         cudaGraphDestroy(graph);
         LT_CU(e);
