@@ -27,13 +27,29 @@
 namespace lt {
 
 // t == null: the node t_q is evaluated in place (sinc_node, k_sinc's arithmetic), so the
-// master does not wait for the sinc kernel
-__global__ void k_master(Index mrows, double h, Index RN, const double* __restrict__ t, int M,
-                         double* __restrict__ out) {
-    const Index j = static_cast<Index>(blockIdx.x) * blockDim.x + threadIdx.x;
+// master does not wait for the sinc kernel. A cell needs erf at its two edges and shares each
+// with a neighbour: a CTA evaluates the kMasterC * 256 + 1 edges of its cells once into shared
+// memory (one erf per cell instead of two; the extra edge by one warp) and differences them.
+constexpr int kMasterC = 4;
+__global__ void __launch_bounds__(256) k_master(Index mrows, double h, Index RN, const double* __restrict__ t, int M,
+                                                double* __restrict__ out) {
+    __shared__ double se[kMasterC * 256 + 1];
+    const Index j0 = static_cast<Index>(blockIdx.x) * (kMasterC * 256);
     const Index q = blockIdx.y;
-    if (j >= mrows) return;
-    out[q * mrows + j] = master_cell(j, mrows, h, t ? t[q] : sinc_node(static_cast<int>(q), M));
+    const double tq = t ? t[q] : sinc_node(static_cast<int>(q), M);
+    const int cells = static_cast<int>(min(static_cast<Index>(kMasterC * 256), mrows - j0));
+#pragma unroll
+    for (int u = 0; u < kMasterC; ++u) {
+        const int i = threadIdx.x + 256 * u;
+        if (i <= cells) se[i] = master_edge(j0 + i, mrows, h, tq);
+    }
+    if (threadIdx.x == 0 && cells == kMasterC * 256) se[cells] = master_edge(j0 + cells, mrows, h, tq);
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kMasterC; ++u) {
+        const int i = threadIdx.x + 256 * u;
+        if (i < cells) out[q * mrows + j0 + i] = master_from_edges(se[i], se[i + 1], tq);
+    }
 }
 
 // the sinc nodes alone (k_sinc's t_q), for the master panel of a long lattice sum
@@ -49,7 +65,7 @@ void launch_sinc_nodes(const Launch& L, Index M, double* t) {
 }
 
 void launch_master(const Launch& L, Index mrows, double h, Index RN, const double* t, double* out, Index M) {
-    dim3 grid(static_cast<unsigned>((mrows + 255) / 256), static_cast<unsigned>(RN));
+    dim3 grid(static_cast<unsigned>((mrows + kMasterC * 256 - 1) / (kMasterC * 256)), static_cast<unsigned>(RN));
     Stage st_(L, "master");
     k_master<<<grid, 256, 0, L.st>>>(mrows, h, RN, t, static_cast<int>(M), out);
     LT_CU(cudaGetLastError());

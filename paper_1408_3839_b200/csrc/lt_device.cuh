@@ -45,6 +45,17 @@ __device__ __forceinline__ double master_cell(Index j, Index mrows, double h, do
     return __dmul_rn(c, __dsub_rn(er, el));
 }
 
+// the two halves of master_cell: erf(t_q x_j) and the cell from its two edge values (the
+// same arithmetic, so cells assembled from shared edge values are bitwise master_cell's)
+__device__ __forceinline__ double master_edge(Index j, Index mrows, double h, double tq) {
+    const double origin = __dmul_rn(__dmul_rn(-0.5, static_cast<double>(mrows)), h);
+    return erf(__dmul_rn(tq, __dadd_rn(origin, __dmul_rn(static_cast<double>(j), h))));
+}
+__device__ __forceinline__ double master_from_edges(double el, double er, double tq) {
+    const double c = __ddiv_rn(sqrt(3.141592653589793), __dmul_rn(2.0, tq));
+    return __dmul_rn(c, __dsub_rn(er, el));
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
