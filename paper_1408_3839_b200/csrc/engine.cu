@@ -216,6 +216,15 @@ struct lt_ctx {
     // plan-table uploads (window starts, DFT maps) bump the epoch; solve_core_dev reuses
     // its uploaded tables while the epoch and the arena generation are unchanged
     uint64_t prep_epoch = 0;
+    // the last lattice-DFT index maps per buffer tag: they depend on the lattice and the stored
+    // offsets only (not on the basis exponents), so a scan over systems of one shape re-uses them
+    struct DftCache {
+        std::vector<std::array<Index, 3>> kidx;
+        Index dims[3] = {0, 0, 0}, m0 = 0;
+        uint64_t gen = 0;
+        DftPrep P;
+    };
+    std::map<std::string, DftCache> dft_cache;
     CorePrep prep;
     // speculation on L0: the last (system, L0) pair the device computed
     std::vector<int64_t> spec_key;
@@ -1147,6 +1156,15 @@ static std::vector<std::array<Index, 3>> periodic_kidx(const Plan& p) {
 // slot map, uploaded (not capturable, so done before any graph capture)
 static DftPrep prepare_dft(lt_ctx* c, const Index dims[3], Index m0, const std::vector<std::array<Index, 3>>& kidx,
                            const std::string& tag) {
+    {
+        auto it = c->dft_cache.find(tag);
+        if (it != c->dft_cache.end()) {
+            const lt_ctx::DftCache& e = it->second;
+            if (e.gen == c->arena.generation() && e.m0 == m0 && e.dims[0] == dims[0] && e.dims[1] == dims[1] &&
+                e.dims[2] == dims[2] && e.kidx == kidx)
+                return e.P;  // the device tables of this tag still hold exactly these maps
+        }
+    }
     DftPrep P;
     P.m0 = m0;
     P.tag = tag;
@@ -1188,6 +1206,12 @@ static DftPrep prepare_dft(lt_ctx* c, const Index dims[3], Index m0, const std::
         P.comp[a] = c->arena.get<int64_t>("dft.comp" + tag + std::to_string(a), comp[a].size());
         upload(c, P.comp[a], comp[a].data(), comp[a].size() * sizeof(int64_t));
     }
+    lt_ctx::DftCache& e = c->dft_cache[tag];
+    e.kidx = kidx;
+    for (int l = 0; l < 3; ++l) e.dims[l] = dims[l];
+    e.m0 = m0;
+    e.gen = c->arena.generation();  // after the allocations above (a grown arena is a new generation)
+    e.P = P;
     return P;
 }
 
@@ -1505,6 +1529,30 @@ static std::vector<int64_t> graph_key(const HostSys& h, const Plan& p, bool peri
     return k;
 }
 
+// the part of a system an exponent / geometry scan leaves unchanged (lattice, grids, counts,
+// polynomial degrees): systems of one shape are likely to share L0
+static std::vector<int64_t> shape_key(const HostSys& h, bool periodic) {
+    std::vector<int64_t> k;
+    auto put_d = [&](double v) {
+        int64_t b;
+        std::memcpy(&b, &v, sizeof(b));
+        k.push_back(b);
+    };
+    k.push_back(periodic);
+    put_d(h.b);
+    put_d(h.eps_ov);
+    k.push_back(h.quad_M);
+    for (int l = 0; l < 3; ++l) {
+        k.push_back(h.L[l]);
+        k.push_back(h.n[l]);
+        k.push_back(h.nbar[l]);
+    }
+    k.push_back(static_cast<int64_t>(h.Z.size()));
+    k.push_back(static_cast<int64_t>(h.alpha.size()));
+    for (int v : h.deg) k.push_back(v);
+    return k;
+}
+
 // full path on device; eigenvalues -> eig_dev (device)
 static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double* eig_dev, Index k_begin,
                            Index k_end, int64_t* info, double* eig_host = nullptr, bool allow_spec = true,
@@ -1515,10 +1563,11 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
     validate(sd->hs);
     c->phase_mark(0);
     c->timer.mark_ref(c->stream);
-    // L0 speculation: L0 is a function of the system alone; when this system's L0 is known
-    // from the previous call, the post-L0 graph is launched right behind the L0 graph
-    // (no host round trip) and the device-computed L0 is checked after the final sync.
-    std::vector<int64_t> skey = graph_key(sd->hs, Plan{}, periodic, -2, -2, nullptr, sd->mem, 0);
+    // L0 speculation: L0 is a function of the system alone; when the previous call solved this
+    // system — or another one of the same shape (an exponent or geometry scan) — its L0 is the
+    // prediction: the post-L0 work is launched right behind the L0 check (no host round trip)
+    // and the device-computed L0 is compared after the final sync (a miss redoes the solve).
+    std::vector<int64_t> skey = shape_key(sd->hs, periodic);
     // no host sync inside the post-L0 work: periodic systems, and box pencils solved on the
     // device (the batched pencil, or the dense reduction + on-chip tridiagonalisation)
     const Index nb_box = sd->hs.m0() * sd->hs.cells();
@@ -1537,7 +1586,7 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
         L0 = compute_L0(c, sd);
     }
     // plan products (host integer planning + small table uploads), reused while unchanged
-    std::vector<int64_t> pkey = skey;
+    std::vector<int64_t> pkey = graph_key(sd->hs, Plan{}, periodic, -2, -2, nullptr, sd->mem, 0);
     pkey.push_back(L0);
     CorePrep& cp = c->prep;
     if (!(cp.valid && cp.key == pkey && cp.epoch == c->prep_epoch && cp.gen == c->arena.generation())) {
