@@ -14,6 +14,7 @@ import numpy as np
 import pytest
 
 from conftest import eig_tolerance, entries_close
+from paper_1408_3839_b200.api import Context
 from paper_1408_3839_b200.native import BoundsError
 from paper_1408_3839_b200.system import LatticeSystem, make_config
 
@@ -124,3 +125,34 @@ def test_box_chain_nuclear_hankel_shapes(ctx, oracle, L, n):
     assert ok, worst
     ok, worst = entries_close(S.dense(), oS.dense)
     assert ok, worst
+
+
+@pytest.mark.parametrize("periodic", [True, False])
+def test_l0_prediction_across_systems_of_one_shape(periodic):
+    """L0 is predicted from the previous system of the same shape (exponent scans run without
+    the L0 host round trip); a system whose L0 differs must be detected on the device and
+    solved again: alternating two such systems on one context reproduces the spectra of fresh
+    contexts exactly, with the right L0 reported each time."""
+    pos = [(-0.5, 0.1, 0.0), (0.5, 0.0, -0.2)]
+
+    def system(scale):
+        return LatticeSystem(b=2.0, L=(12, 1, 1) if periodic else (6, 1, 1), n=(16, 8, 8), nbar=(16, 8, 8), quad_M=8,
+                             nuc_pos=pos, nuc_charge=[1.0, 2.0], bf_center=[pos[0], pos[1], pos[0], pos[1]],
+                             bf_alpha=[0.9 * scale, 2.5 * scale, 0.6 * scale, 4.0 * scale])
+
+    tight, diffuse = system(1.0), system(0.45)
+    ref = {}
+    for name, s in (("tight", tight), ("diffuse", diffuse)):
+        c = Context(0)
+        info = np.zeros(8, dtype=np.int64)
+        ref[name] = (c.solve_core(s, periodic, info).copy(), int(info[0]))
+        c.close()
+    assert ref["tight"][1] != ref["diffuse"][1], "the two systems must differ in L0 for this test"
+    c = Context(0)
+    for name, s in (("tight", tight), ("tight", tight), ("diffuse", diffuse), ("tight", tight), ("diffuse", diffuse),
+                    ("diffuse", diffuse), ("tight", tight)):
+        info = np.zeros(8, dtype=np.int64)
+        ev = c.solve_core(s, periodic, info)
+        assert int(info[0]) == ref[name][1], name
+        assert np.array_equal(ev, ref[name][0]), name
+    c.close()
