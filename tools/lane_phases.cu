@@ -10,6 +10,8 @@
 
 #include "../paper_1408_3839_b200/csrc/k_pencil.cu"
 #include "../paper_1408_3839_b200/csrc/k_pencil_lane.cu"
+void lt::StageTimer::begin(cudaStream_t, const char*) {}
+void lt::StageTimer::end(cudaStream_t) {}
 
 int main(int argc, char** argv) {
     const int count = argc > 1 ? std::atoi(argv[1]) : 4096;
