@@ -155,6 +155,7 @@ struct DftPrep {
     Index ncomp[3]{1, 1, 1};
     Index nblk = 0, m0 = 0, maxsz = 0;
     int* slot2blk = nullptr;  // compressed position -> stored block (-1: zero block)
+    bool ident = false;       // slot2blk[q] == q for every q
     int64_t* comp[3]{nullptr, nullptr, nullptr};
     std::string tag;
 };
@@ -1199,6 +1200,8 @@ static DftPrep prepare_dft(lt_ctx* c, const Index dims[3], Index m0, const std::
         if (dims[a] > 1) e2[a] = dims[a];
         P.maxsz = std::max(P.maxsz, e2[0] * e2[1] * e2[2]);
     }
+    P.ident = true;
+    for (size_t q = 0; q < slot2blk.size(); ++q) P.ident = P.ident && slot2blk[q] == static_cast<int>(q);
     ++c->prep_epoch;
     P.slot2blk = c->arena.get<int>("dft.slot" + tag, slot2blk.size());
     upload(c, P.slot2blk, slot2blk.data(), slot2blk.size() * sizeof(int));
@@ -1247,6 +1250,7 @@ static bool launch_dft(lt_ctx* c, const DftPrep& P, int nops, const double* cons
         f.mm = mm;
         f.maxsz = P.maxsz;
         f.slot2blk = P.slot2blk;
+        f.ident = P.ident ? 1 : 0;
         for (int l = 0; l < 3; ++l) {
             f.dims[l] = P.dims[l];
             f.ext[l] = P.ext[l];

@@ -262,7 +262,25 @@ __global__ void __launch_bounds__(256) k_dft_fused(DftFusedArgs a) {
     double2* buf1 = buf0 + a.maxsz;
     const double* gen = a.gen[op];
     const unsigned ncube = static_cast<unsigned>(a.ext[0] * a.ext[1] * a.ext[2]);
-    {
+    if (a.ident && a.gen_emajor) {
+        // every cube position stored, in order, entry-major: the entry's cube is one contiguous
+        // row; eight independent loads in flight per thread (one or two round trips in all)
+        const double* row = gen + e * a.nblocks;
+        constexpr unsigned U = 8;
+        for (unsigned q0 = threadIdx.x; q0 < ncube; q0 += U * blockDim.x) {
+            double v[U];
+#pragma unroll
+            for (unsigned u = 0; u < U; ++u) {
+                const unsigned q = q0 + u * blockDim.x;
+                v[u] = q < ncube ? row[q] : 0.0;
+            }
+#pragma unroll
+            for (unsigned u = 0; u < U; ++u) {
+                const unsigned q = q0 + u * blockDim.x;
+                if (q < ncube) buf0[q] = make_double2(v[u], 0.0);
+            }
+        }
+    } else {
         // gather the entry's stored values: block indices first, then the values, four
         // independent loads in flight per thread
         constexpr unsigned U = 4;

@@ -464,6 +464,7 @@ struct DftFusedArgs {
     int emajor = 0;     // 1: out [mm][K] (entry-major, for the one-thread-per-pencil kernel)
     int gen_emajor = 0;  // 1: gen [mm][nblocks] (entry-major generating blocks, k_kr_combine's fused fill)
     Index nblocks = 0;
+    int ident = 0;  // 1: slot2blk is the identity (every cube position stored, in order): no index loads
 };
 // log2 L for the register FFT of power-of-two axes 2 <= L <= 16 (0: DFT pass); LT_DFT_NO_FFT
 // at compile time forces the DFT pass
