@@ -121,6 +121,13 @@ __global__ void __launch_bounds__(256) k_resfold(ResFold f) {
     const double* Bs = sh + m0p * ldj;    // [NB][m0p][ldj], column j' + 1 for j' in [-1, J]
     const long long tot = static_cast<long long>(1 + NB) * m0p * ldj;
     double* Vs = sh + tot;                // fused weights V[e] for this residue (f.W set)
+    // the supports are needed after the staging below: their loads go first, so they share its
+    // round trip to L2 instead of adding one between two barriers
+    long long sup_l = 0, sup_h = 0;
+    if (f.sup_lo && threadIdx.x < f.m0) {
+        sup_l = static_cast<long long>(f.sup_lo[threadIdx.x]);
+        sup_h = static_cast<long long>(f.sup_hi[threadIdx.x]);
+    }
     if (f.slab) {
         const double2* srcp = reinterpret_cast<const double2*>(f.slab + t * tot);
         double2* dstp = reinterpret_cast<double2*>(sh);
@@ -208,7 +215,12 @@ __global__ void __launch_bounds__(256) k_resfold(ResFold f) {
             Vs[e] = v;
         }
     }
-    __syncthreads();
+    __shared__ long long slo[32], shi[32];
+    if (f.sup_lo && threadIdx.x < f.m0) {
+        slo[threadIdx.x] = sup_l;
+        shi[threadIdx.x] = sup_h;
+    }
+    __syncthreads();  // the staged rows, V and the supports
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, tq = lane & 3;
     const int ntile = m0p / 8;
@@ -222,12 +234,6 @@ __global__ void __launch_bounds__(256) k_resfold(ResFold f) {
     // per 8-function tile: the j range of residue t where some function of the tile is
     // non-zero (a side: t + j n in [lo, hi); b side: t + j' n in [lo - w, hi + w))
     __shared__ int tja[2][4], tjb[2][4];
-    __shared__ long long slo[32], shi[32];
-    if (f.sup_lo && threadIdx.x < f.m0) {  // all supports in one round of loads
-        slo[threadIdx.x] = static_cast<long long>(f.sup_lo[threadIdx.x]);
-        shi[threadIdx.x] = static_cast<long long>(f.sup_hi[threadIdx.x]);
-    }
-    __syncthreads();
     if (threadIdx.x < 2 * ntile && threadIdx.x < 8) {
         const int side = threadIdx.x / ntile, tile = threadIdx.x % ntile;
         int jl = 1 << 30, jh = -(1 << 30);
