@@ -230,6 +230,7 @@ struct lt_ctx {
     // speculation on L0: the last (system, L0) pair the device computed
     std::vector<int64_t> spec_key;
     Index spec_L0 = -1;
+    bool spec_active = false;  // the running solve uses a predicted L0
     // optional host-side timestamps (lt_set_diagnostics LT_DIAG_HOST_TIMING): enter / launched / synced / exit
     bool host_timing = false;
     double host_acc[4] = {0, 0, 0, 0};
@@ -1557,10 +1558,30 @@ static std::vector<int64_t> shape_key(const HostSys& h, bool periodic) {
     return k;
 }
 
-// full path on device; eigenvalues -> eig_dev (device)
+static void solve_core_dev_body(lt_ctx* c, const lt_sysdev* sd, bool periodic, double* eig_dev, Index k_begin,
+                                Index k_end, int64_t* info, double* eig_host, bool allow_spec, const CoreOpts& opt);
+
+// full path on device; eigenvalues -> eig_dev (device). An error raised while the solve ran on
+// a PREDICTED L0 may be the prediction's (a too large L0 trips the alias guard of a valid
+// system): the solve is repeated without the prediction, which then decides.
 static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double* eig_dev, Index k_begin,
                            Index k_end, int64_t* info, double* eig_host = nullptr, bool allow_spec = true,
                            const CoreOpts& opt = CoreOpts{}) {
+    c->spec_active = false;
+    try {
+        solve_core_dev_body(c, sd, periodic, eig_dev, k_begin, k_end, info, eig_host, allow_spec, opt);
+    } catch (const lt::Error&) {
+        if (!c->spec_active) throw;
+        c->spec_active = false;
+        c->spec_L0 = -1;
+        c->prep.valid = false;
+        cudaStreamSynchronize(c->stream);
+        solve_core_dev_body(c, sd, periodic, eig_dev, k_begin, k_end, info, eig_host, false, opt);
+    }
+}
+
+static void solve_core_dev_body(lt_ctx* c, const lt_sysdev* sd, bool periodic, double* eig_dev, Index k_begin,
+                                Index k_end, int64_t* info, double* eig_host, bool allow_spec, const CoreOpts& opt) {
     const int phase = opt.phase;
     if (phase != 0) allow_spec = false;
     c->host_mark(0);
@@ -1580,6 +1601,7 @@ static void solve_core_dev(lt_ctx* c, const lt_sysdev* sd, bool periodic, double
                       c->spec_L0 <= 14 && skey == c->spec_key;
     Index L0;
     L0Work l0w;
+    c->spec_active = spec;
     if (spec) {
         // L0 runs inside the same graph as the rest (shifts 1 .. L0 + 2, exactly those the
         // rule needs to confirm the prediction); its state is read back with the results
