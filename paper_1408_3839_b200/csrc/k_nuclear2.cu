@@ -925,8 +925,19 @@ __global__ void k_kr_combine(KRArgs a) {
         const int ee = d < 0 ? eT : e;
         return a.T[l][(static_cast<long long>(ad) * mm + ee) * a.Rtot + r];  // [d][e][r]: r contiguous
     };
-    for (int r = threadIdx.x; r < Kp; r += blockDim.x) w0[r] = r < K ? a.W[r * mm + e] * tab(0, i0, r) : 0.0;
-    __syncthreads();
+    // w0[r] = W[r][e] T_0[d0][e][r] of this lane's ranks r = lane + 32 x in registers (the same
+    // rounded product every row is scaled by): no shared staging, so the loads of both slabs
+    // below are in flight together with these (one round trip to L2 for the whole prologue)
+    (void)w0;
+    double w0r[4];
+    {
+        const int ln = static_cast<int>(threadIdx.x) & 31;
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+            const int r = ln + 32 * x;
+            w0r[x] = r < K ? a.W[r * mm + e] * tab(0, i0, r) : 0.0;
+        }
+    }
     // the two table slabs (zero padded): rows split over the warps, r over the lanes (no
     // index division), the row's d sign and transposed entry resolved once per row
     auto gather = [&](int l, int w, int wp, double* dst, bool scale) {
@@ -948,7 +959,7 @@ __global__ void k_kr_combine(KRArgs a) {
 #pragma unroll
             for (int x = 0; x < 4; ++x) {
                 const int r = ln + 32 * x;
-                if (r < Kp) dst[row * ldk + r] = scale ? v[x] * w0[r] : v[x];
+                if (r < Kp) dst[row * ldk + r] = scale ? v[x] * w0r[x] : v[x];
             }
         }
     };
@@ -963,6 +974,21 @@ __global__ void k_kr_combine(KRArgs a) {
         double acc[2] = {0.0, 0.0};
         const double* ua = u + (mt * 8 + g) * ldk + t;
         const double* tb = t2 + (nt * 8 + g) * ldk + t;
+        // the fill's FEM factors of this thread's two outputs: loaded ahead of the DMMA loop
+        double Mv[2][3] = {}, Sv[2][3] = {};
+        if (a.H) {
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int ii[3] = {i0, mt * 8 + g, nt * 8 + 2 * t + i};
+                if (ii[1] < w1 && ii[2] < w2) {
+#pragma unroll
+                    for (int l = 0; l < 3; ++l) {
+                        Mv[i][l] = a.massT[l][static_cast<long long>(ii[l]) * mm + e];
+                        Sv[i][l] = a.stiffT[l][static_cast<long long>(ii[l]) * mm + e];
+                    }
+                }
+            }
+        }
         for (int ks = 0; ks < Kp; ks += 4) dmma_m8n8k4(acc, ua[ks], tb[ks]);
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
@@ -980,8 +1006,8 @@ __global__ void k_kr_combine(KRArgs a) {
                 long long slot = 0;
 #pragma unroll
                 for (int l = 0; l < 3; ++l) {
-                    M[l] = a.massT[l][static_cast<long long>(ii[l]) * mm + e];
-                    St[l] = a.stiffT[l][static_cast<long long>(ii[l]) * mm + e];
+                    M[l] = Mv[i][l];
+                    St[l] = Sv[i][l];
                     const int d = ii[l] - a.band[l];
                     slot = slot * a.width[l] + (d >= 0 ? d : a.width[l] + d);
                 }
