@@ -48,3 +48,26 @@ def test_c2_c1_definite(oracle):
 def test_accepted_draw_indices():
     assert make_config("c3").notes["exponent_draw"] == C3_ACCEPTED_DRAW
     assert make_config("c4").notes["exponent_draw"] == C4_ACCEPTED_DRAW
+
+
+def test_lt_system_view_is_cached_until_a_field_is_reassigned():
+    """LatticeSystem.to_c(): the ctypes view of an unchanged system is built once (the host API
+    calls it on every solve); it points at the numpy arrays, so in-place edits stay visible, and
+    re-assigning a field rebuilds it."""
+    import numpy as np
+
+    from paper_1408_3839_b200.system import make_config
+
+    s = make_config("c2")
+    a = s.to_c()
+    assert s.to_c() is a
+    s.bf_alpha[0] *= 1.5  # in place: same struct, the new value is what the library reads
+    assert s.to_c() is a
+    assert a.bf_alpha[0] == s.bf_alpha[0]
+    s.bf_alpha = np.ascontiguousarray(s.bf_alpha * 2.0)  # re-assigned: a new view
+    b = s.to_c()
+    assert b is not a
+    assert b.bf_alpha[0] == s.bf_alpha[0]
+    s.quad_M += 1
+    assert s.to_c() is not b
+    assert s.to_c().quad_M == s.quad_M
