@@ -29,4 +29,8 @@ timeout 900 ncu --set full --import-source on -k regex:"k_pencil|k_l0|k_triv_gem
 timeout 900 ncu --set full --import-source on -k regex:"k_sytrd|k_tridiag_eig3|k_hankel|k_dgemm|k_potf|k_window" \
     -s 40 -c 12 -o $O/${R}_c3_full python bench.py --workload c3 --secondary '' --no-sweep --steps 3 --warmup 3 \
     --no-cpu-baseline > $O/${R}_c3_full.log 2>&1
+# c3 outside the Cholesky chain: lattice sum, contraction, tridiagonalisation, eigenvalues
+timeout 900 ncu --set full --import-source on -k regex:"k_hankel|k_window_sum_staged|k_sytrd|k_tridiag_eig3|k_master|k_vgemm|k_triv_gemm" \
+    -s 24 -c 8 -o $O/${R}_c3b_full python bench.py --workload c3 --secondary '' --no-sweep --steps 3 --warmup 3 \
+    --no-cpu-baseline > $O/${R}_c3b_full.log 2>&1
 ls -la $O

@@ -154,7 +154,7 @@ def main():
     for cfg in ("c1", "c2", "c3", "c4", "c5"):
         launches(cfg, R)
     traffic = {}
-    for cfg in ("c1", "c2", "c3", "c4", "c5"):
+    for cfg in ("c1", "c2", "c3", "c3b", "c4", "c5"):  # c3b: the c3 kernels outside the Cholesky chain
         full(cfg, R, traffic)
     # per stage: mean DRAM bytes per launch
     agg = {cfg: {st: {"dram_bytes_per_launch": sum(x["dram_bytes"] for x in v) / len(v), "launches": len(v),
