@@ -138,7 +138,7 @@ def full(cfg, R, traffic):
         except ValueError:
             tb = None
         if st and tb is not None:
-            traffic.setdefault(cfg, {}).setdefault(st, []).append({"kernel": rec["kernel"], "dram_bytes": tb})
+            traffic.setdefault(cfg[:2], {}).setdefault(st, []).append({"kernel": rec["kernel"], "dram_bytes": tb})  # c3b -> c3
     with open(os.path.join(DST, f"{R}_{cfg}_full_metrics.csv"), "w", newline="") as f:
         w = csv.DictWriter(f, fieldnames=["kernel"] + [lab for lab, _ in FULL_METRICS])
         w.writeheader()
